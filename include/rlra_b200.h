@@ -1,0 +1,111 @@
+/*
+ * rlra_b200 — C ABI of the B200-native PowerLU hot path (sm_100a).
+ *
+ * Plain C: no torch or C++ types cross this boundary.  Every function returns
+ * 0 on success and a negative status on failure; rlra_b200_last_error()
+ * returns a thread-local description of the last failure.  Matrices are
+ * column-major float64 with an explicit leading dimension (the reference's
+ * canonical layout, rlra/core.py:25-30); permutations are int64 index vectors.
+ * `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ * Device-pointer entry points are asynchronous on `stream`; the caller owns
+ * every buffer and workspace (size queries are provided) and the library never
+ * allocates on those paths.
+ *
+ * Reference interfaces replaced (paths under /root/reference/pkg/src/rlra):
+ *   rlra_b200_plu_inplace      backend.plu_inplace            backend.py:32
+ *                              -> _lu_cython.plu_inplace      _lu_cython.pyx:14-55
+ *   rlra_b200_getrf            same kernel on device buffers  (kernels.plu, kernels.py:37-54)
+ *   rlra_b200_lu_basis         rangefinder._lu_basis          rangefinder.py:73-77
+ *                              (core.apply_inv_row_perm       core.py:103-109)
+ *   rlra_b200_lu_extract       L/U extraction of kernels.plu  kernels.py:50-53
+ *   rlra_b200_dgemm            DenseAccessor.matmul/rmatmul   accessors.py:27-31
+ *                              and the assembly products      fixedrank.py:145-146, kernels.py:96
+ *   rlra_b200_geqrf/_orgqr     kernels.eqr (np.linalg.qr)     kernels.py:57-61, :73
+ *   rlra_b200_trsm_rt          solve_triangular(trans='T')    kernels.py:95
+ *   rlra_b200_diag_absmin      pinv_factor rank test          kernels.py:75-79
+ *   rlra_b200_sumsq            DenseAccessor.fro_norm()**2    accessors.py:33-34, fixedprec.py:72
+ *   rlra_b200_colsumsq         per-column energies of G       fixedprec.py:75-80, :105-107
+ *   rlra_b200_transpose        U = L2^T                       fixedrank.py:146
+ */
+#ifndef RLRA_B200_H
+#define RLRA_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RLRA_B200_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define RLRA_B200_API __attribute__((visibility("default")))
+#else
+#define RLRA_B200_API
+#endif
+
+RLRA_B200_API int rlra_b200_abi_version(void);
+RLRA_B200_API const char* rlra_b200_last_error(void);
+RLRA_B200_API int rlra_b200_device_count(int* out);
+
+/* ---- host seam: drop-in for backend.plu_inplace(lu, piv) ---------------
+ * lu: HOST F-contiguous float64 m x n (ld = m), overwritten with packed L\U;
+ * piv: HOST int64[m], caller-preloaded (0..m-1) and permuted in place.
+ * Bit-identical to the reference kernel.  Synchronous; runs on the current
+ * CUDA device. */
+RLRA_B200_API int rlra_b200_plu_inplace(double* lu, int64_t m, int64_t n, int64_t* piv);
+
+/* ---- K3: GEPP on device buffers ---------------------------------------- */
+RLRA_B200_API size_t rlra_b200_getrf_workspace(int64_t m, int64_t n);
+/* nonzero_diag (device int64*, nullable) receives count_nonzero(diag(U)) */
+RLRA_B200_API int rlra_b200_getrf(double* a, int64_t lda, int64_t m, int64_t n, int64_t* piv,
+                    int64_t* nonzero_diag, void* ws, size_t ws_bytes, void* stream);
+RLRA_B200_API int rlra_b200_iota(int64_t* p, int64_t m, void* stream);
+/* count_nonzero(diag(a)) over the leading r x r block -> device int64 *out
+ * (rangefinder._check_width, rangefinder.py:55-64) */
+RLRA_B200_API int rlra_b200_count_nonzero_diag(const double* a, int64_t lda, int64_t r, int64_t* out,
+                                 void* stream);
+/* W (m x k) = P^T L: row-unpermuted unit-lower factor; pinv_ws: int64[m] */
+RLRA_B200_API int rlra_b200_lu_basis(const double* lu, int64_t ldlu, int64_t m, int64_t k, const int64_t* piv,
+                       int64_t* pinv_ws, double* w, int64_t ldw, void* stream);
+/* L (m x r, unit lower) and/or U (r x n, upper) of a packed LU; either may be NULL */
+RLRA_B200_API int rlra_b200_lu_extract(const double* lu, int64_t ldlu, int64_t m, int64_t n, double* l,
+                         int64_t ldl, double* u, int64_t ldu, void* stream);
+
+/* ---- K1/K2/K5: FP64 DMMA GEMM  C = alpha op(A) op(B) + beta C ---------- */
+RLRA_B200_API size_t rlra_b200_gemm_workspace(int64_t m, int64_t n, int64_t k);
+RLRA_B200_API int rlra_b200_dgemm(int transa, int transb, int64_t m, int64_t n, int64_t k, double alpha,
+                    const double* a, int64_t lda, const double* b, int64_t ldb, double beta,
+                    double* c, int64_t ldc, void* ws, size_t ws_bytes, void* stream);
+
+/* ---- K4: Householder QR (m >= n) + explicit thin Q --------------------- */
+RLRA_B200_API size_t rlra_b200_geqrf_workspace(int64_t m, int64_t n);
+RLRA_B200_API int rlra_b200_geqrf(double* a, int64_t lda, int64_t m, int64_t n, double* tau, void* ws,
+                    size_t ws_bytes, void* stream);
+/* must receive geqrf's workspace, untouched since the geqrf call */
+RLRA_B200_API int rlra_b200_orgqr(const double* a, int64_t lda, int64_t m, int64_t n, double* q, int64_t ldq,
+                    void* ws, size_t ws_bytes, void* stream);
+
+/* ---- K6: X = R^{-T} B in place over B (R upper l x l) ------------------- */
+RLRA_B200_API size_t rlra_b200_trsm_workspace(int64_t l, int64_t ncols);
+RLRA_B200_API int rlra_b200_trsm_rt(const double* r, int64_t ldr, int64_t l, double* x, int64_t ldx,
+                      int64_t ncols, void* ws, size_t ws_bytes, void* stream);
+RLRA_B200_API int rlra_b200_diag_absmin(const double* a, int64_t lda, int64_t r, double* out, void* stream);
+
+/* ---- K8 / K2b: compensated deterministic energies ----------------------- */
+RLRA_B200_API size_t rlra_b200_sumsq_workspace(int64_t m, int64_t n);
+RLRA_B200_API int rlra_b200_sumsq(const double* a, int64_t lda, int64_t m, int64_t n, double* out, void* ws,
+                    size_t ws_bytes, void* stream);
+RLRA_B200_API int rlra_b200_colsumsq(const double* a, int64_t lda, int64_t m, int64_t n, double* out,
+                       void* stream);
+
+/* ---- layout helper ------------------------------------------------------ */
+RLRA_B200_API int rlra_b200_transpose(const double* in, int64_t ldi, int64_t m, int64_t n, double* out,
+                        int64_t ldo, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* RLRA_B200_H */

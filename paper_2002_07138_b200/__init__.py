@@ -1,0 +1,53 @@
+"""B200-native PowerLU hot path (arXiv 2002.07138), drop-in for the reference
+package ``rlra``'s PowerLU / PowerLU_FP / single-pass API.
+
+All factorization arithmetic runs in hand-written sm_100a kernels in
+librlra_b200.so (FP64 DMMA GEMMs, bit-exact GEPP, Householder QR, TRSM,
+compensated reductions) called through its C ABI (include/rlra_b200.h).
+There is no CPU fallback: without the library or a CUDA device every entry
+point raises NativeUnavailable.
+"""
+
+from .backend import BACKEND, plu_inplace
+from .core import gaussian, set_omega_cache
+from .device import (
+    DenseColumnStream,
+    DeviceColumnStream,
+    DeviceMatrix,
+    InstrumentedAccessor,
+    as_accessor,
+)
+from .errors import (
+    DeviceError,
+    IllConditionedSolve,
+    IllPosedPseudoinverse,
+    NativeUnavailable,
+    NotConverged,
+    RankCollapse,
+    RlraError,
+    Unsatisfiable,
+)
+from .fixedprec import (
+    AdaptiveOutcome,
+    PrecisionParams,
+    adaptive_rank,
+    default_width,
+    powerlu_fp,
+    refine_rank,
+    restart_policy,
+)
+from .fixedrank import LowRankLU, lu_from_projection, powerlu, reconstruct
+from .rangefinder import RangeBasis, general_power_basis_v, power_basis_v
+from .singlepass import SketchPair, single_pass_lu, stream_sketch
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "BACKEND", "AdaptiveOutcome", "DenseColumnStream", "DeviceColumnStream", "DeviceError",
+    "DeviceMatrix", "IllConditionedSolve", "IllPosedPseudoinverse", "InstrumentedAccessor",
+    "LowRankLU", "NativeUnavailable", "NotConverged", "PrecisionParams", "RangeBasis",
+    "RankCollapse", "RlraError", "SketchPair", "Unsatisfiable", "adaptive_rank", "as_accessor",
+    "default_width", "gaussian", "general_power_basis_v", "lu_from_projection", "plu_inplace",
+    "power_basis_v", "powerlu", "powerlu_fp", "reconstruct", "refine_rank", "restart_policy",
+    "set_omega_cache", "single_pass_lu", "stream_sketch",
+]

@@ -1,0 +1,104 @@
+"""Synthetic workloads C1-C5 (BASELINE.json ``configs``; SURVEY.md §8(d) and
+Appendix A recipes).  Host-side input generation for tests and bench.py — not
+part of the factorization path.
+
+C1 is exactly ``rlra.matgen.gen_decay("custom", 2000, 2000, seed=1, sigma)``
+(rlra/matgen.py:36-58).  C2-C5 are ``A = X diag(sigma) Y^T + noise N(0,1)``
+with X, Y QR-orthonormalised seeded Gaussians drawn from ONE default_rng
+stream in the order X, Y, noise (noise filled column-major), as the survey's
+recipe states.  The reference measured its numbers on
+these recipes, so the seeds are fixed here.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+
+def _gaussian_from(rng, m, n):
+    # rlra/core.py:46-48 — the F-order fill order is part of the contract
+    return rng.standard_normal(m * n).reshape((m, n), order="F")
+
+
+@dataclass(frozen=True)
+class Workload:
+    name: str
+    m: int
+    n: int
+    k: int
+    q_os: int
+    v: int
+    seed: int = 0  # driver seed for Omega
+    kind: str = "powerlu"  # powerlu | powerlu_fp | single_pass
+    eps: float = 0.0
+    b: int = 0
+
+
+def gen_c1():
+    """C1: 2000x2000 log-uniform decay 1 -> 1e-4 (seed 1)."""
+    sigma = 10.0 ** (-4.0 * np.arange(2000) / 1999)
+    rng = np.random.default_rng(1)
+    u, _ = np.linalg.qr(_gaussian_from(rng, 2000, 2000))
+    v, _ = np.linalg.qr(_gaussian_from(rng, 2000, 2000))
+    return np.asfortranarray((u * sigma) @ v.T)
+
+
+def gen_lowrank_plus_noise(m, n, r, sigma, noise, seed):
+    """A = X diag(sigma) Y^T + noise * N(0,1); X, Y, noise from one stream."""
+    rng = np.random.default_rng(seed)
+    x, _ = np.linalg.qr(_gaussian_from(rng, m, r))
+    y, _ = np.linalg.qr(_gaussian_from(rng, n, r))
+    a = np.asfortranarray((x * sigma) @ y.T)
+    if noise:
+        a += noise * _gaussian_from(rng, m, n)
+    return a
+
+
+def gen_c2(m=20000, n=10000):
+    """C2: rank-400 i^-2 spectrum + 1e-8 noise (seed 2)."""
+    return gen_lowrank_plus_noise(m, n, 400, 1.0 / np.arange(1, 401) ** 2, 1e-8, 2)
+
+
+def gen_c3(n=16384):
+    """C3: width-1024 exp(-i/60) spectrum, no noise (seed 3)."""
+    return gen_lowrank_plus_noise(n, n, 1024, np.exp(-np.arange(1, 1025) / 60.0), 0.0, 3)
+
+
+def gen_c4(n=50000):
+    """C4: rank-300 i^-1.5 spectrum + 1e-6 noise (seed 4)."""
+    return gen_lowrank_plus_noise(n, n, 300, np.arange(1, 301) ** -1.5, 1e-6, 4)
+
+
+def gen_c5(m=262144, n=32768):
+    """C5: width-640 log-uniform 1 -> 1e-8 spectrum + 1e-10 noise (seed 5)."""
+    return gen_lowrank_plus_noise(m, n, 640, 10.0 ** (-8.0 * np.arange(640) / 639), 1e-10, 5)
+
+
+WORKLOADS = {
+    "C1": Workload("C1", 2000, 2000, 50, 10, 3),
+    "C2": Workload("C2", 20000, 10000, 200, 20, 4),
+    "C3": Workload("C3", 16384, 16384, 0, 0, 3, kind="powerlu_fp", eps=1e-6, b=64),
+    "C4": Workload("C4", 50000, 50000, 360, 360, 1, kind="single_pass"),
+    "C5": Workload("C5", 262144, 32768, 512, 32, 4),
+}
+
+
+def powerlu_flops(m, n, k, l, v):
+    """Algorithmic flops of one powerlu.
+
+    Passes 2mn[(v-1)l + k]; GEPP a x b = ab^2 - b^3/3; Householder QR with
+    explicit Q of a x b = 4ab^2 - 4b^3/3; assembly GEMMs 2nk^2 + 2mk^2.
+    """
+    gepp = lambda a, b: a * b * b - b ** 3 / 3.0
+    qr = lambda a, b: 4.0 * a * b * b - 4.0 * b ** 3 / 3.0
+    passes = 2.0 * m * n * ((v - 1) * l + k)
+    fact = qr(n, l) + gepp(m, k) + gepp(n, k) + 2.0 * n * k * k + 2.0 * m * k * k
+    if v % 2:
+        h = (v - 1) // 2
+        fact += h * gepp(m, l) + (h - 1) * gepp(n, l)
+    elif v >= 4:
+        h = (v - 2) // 2
+        fact += h * (gepp(m, l) + gepp(n, l))
+    return passes, fact

@@ -1,0 +1,202 @@
+// extern "C" boundary of librlra_b200.so (declared in include/rlra_b200.h).
+#include <cstdarg>
+#include <mutex>
+#include <vector>
+
+#include "../../include/rlra_b200.h"
+#include "common.cuh"
+
+namespace rlra {
+
+static thread_local char g_err[1024] = {0};
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+const char* last_error() { return g_err; }
+
+const DeviceInfo& device_info() {
+  static std::mutex mu;
+  static std::vector<DeviceInfo> cache;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lock(mu);
+  if ((int)cache.size() <= dev) cache.resize(dev + 1);
+  DeviceInfo& d = cache[dev];
+  if (d.sm_count == 0) {
+    cudaDeviceGetAttribute(&d.sm_count, cudaDevAttrMultiProcessorCount, dev);
+    cudaDeviceGetAttribute(&d.max_smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    if (d.sm_count <= 0) d.sm_count = 148;
+  }
+  return d;
+}
+
+// implemented in the kernel translation units
+int gemm(bool ta, bool tb, int64_t M, int64_t N, int64_t K, double alpha, const double* A,
+         int64_t lda, const double* B, int64_t ldb, double beta, double* C, int64_t ldc,
+         void* ws, size_t ws_bytes, cudaStream_t st);
+size_t gemm_workspace_bytes(int64_t M, int64_t N, int64_t K);
+size_t getrf_workspace_bytes(int64_t m, int64_t n);
+int getrf(double* a, int64_t lda, int64_t m, int64_t n, int64_t* piv, int64_t* nonzero_diag_dev,
+          int* zflag_out, void* ws, size_t ws_bytes, cudaStream_t st);
+int fill_iota(int64_t* p, int64_t m, cudaStream_t st);
+int count_nonzero_diag(const double* a, int64_t lda, int64_t r, int64_t* out_dev, cudaStream_t st);
+int lu_basis(const double* lu, int64_t ldlu, int64_t m, int64_t k, const int64_t* piv,
+             int64_t* pinv_ws, double* w, int64_t ldw, cudaStream_t st);
+int extract_l(const double* lu, int64_t ldlu, int64_t m, int64_t k, double* l, int64_t ldl,
+              cudaStream_t st);
+int extract_u(const double* lu, int64_t ldlu, int64_t k, int64_t n, double* u, int64_t ldu,
+              cudaStream_t st);
+size_t geqrf_workspace_bytes(int64_t m, int64_t n);
+int geqrf(double* a, int64_t lda, int64_t m, int64_t n, double* tau, void* ws, size_t ws_bytes,
+          cudaStream_t st);
+int orgqr(const double* a, int64_t lda, int64_t m, int64_t n, double* q, int64_t ldq, void* ws,
+          size_t ws_bytes, cudaStream_t st);
+int trsm_rt(const double* r, int64_t ldr, int64_t l, double* x, int64_t ldx, int64_t ncols,
+            void* ws, size_t ws_bytes, cudaStream_t st);
+int diag_absmin(const double* a, int64_t lda, int64_t r, double* out_dev, cudaStream_t st);
+size_t sumsq_workspace_bytes(int64_t m, int64_t n);
+int sumsq(const double* a, int64_t lda, int64_t m, int64_t n, double* out_dev, void* ws,
+          size_t ws_bytes, cudaStream_t st);
+int colsumsq(const double* a, int64_t lda, int64_t m, int64_t n, double* out_dev, cudaStream_t st);
+int transpose(const double* in, int64_t ldi, int64_t m, int64_t n, double* out, int64_t ldo,
+              cudaStream_t st);
+
+}  // namespace rlra
+
+using namespace rlra;
+
+static cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+extern "C" {
+
+int rlra_b200_abi_version(void) { return RLRA_B200_ABI_VERSION; }
+const char* rlra_b200_last_error(void) { return last_error(); }
+
+int rlra_b200_device_count(int* out) {
+  RLRA_CHECK_CUDA(cudaGetDeviceCount(out));
+  return 0;
+}
+
+int rlra_b200_plu_inplace(double* lu, int64_t m, int64_t n, int64_t* piv) {
+  RLRA_REQUIRE(lu != nullptr && piv != nullptr, "plu_inplace: null buffer");
+  RLRA_REQUIRE(m >= 0 && n >= 0, "plu_inplace: negative shape");
+  if (m == 0 || n == 0) return 0;
+  cudaStream_t st;
+  RLRA_CHECK_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  const size_t abytes = (size_t)m * n * sizeof(double), pbytes = (size_t)m * sizeof(int64_t);
+  const size_t wbytes = getrf_workspace_bytes(m, n);
+  char* dev = nullptr;
+  int rc = 0;
+  cudaError_t e = cudaMallocAsync(&dev, abytes + pbytes + wbytes + 512, st);
+  if (e != cudaSuccess) {
+    set_error("plu_inplace: device allocation failed: %s", cudaGetErrorString(e));
+    cudaStreamDestroy(st);
+    return -1;
+  }
+  double* da = reinterpret_cast<double*>(dev);
+  int64_t* dp = reinterpret_cast<int64_t*>(dev + ((abytes + 255) & ~(size_t)255));
+  void* dw = dev + ((abytes + 255) & ~(size_t)255) + ((pbytes + 255) & ~(size_t)255);
+  do {
+    if ((e = cudaMemcpyAsync(da, lu, abytes, cudaMemcpyHostToDevice, st)) != cudaSuccess) break;
+    if ((e = cudaMemcpyAsync(dp, piv, pbytes, cudaMemcpyHostToDevice, st)) != cudaSuccess) break;
+    rc = getrf(da, m, m, n, dp, nullptr, nullptr, dw, wbytes, st);
+    if (rc) break;
+    if ((e = cudaMemcpyAsync(lu, da, abytes, cudaMemcpyDeviceToHost, st)) != cudaSuccess) break;
+    if ((e = cudaMemcpyAsync(piv, dp, pbytes, cudaMemcpyDeviceToHost, st)) != cudaSuccess) break;
+    e = cudaStreamSynchronize(st);
+  } while (0);
+  cudaFreeAsync(dev, st);
+  cudaStreamSynchronize(st);
+  cudaStreamDestroy(st);
+  if (rc) return rc;
+  if (e != cudaSuccess) {
+    set_error("plu_inplace: %s", cudaGetErrorString(e));
+    return -1;
+  }
+  return 0;
+}
+
+size_t rlra_b200_getrf_workspace(int64_t m, int64_t n) { return getrf_workspace_bytes(m, n); }
+
+int rlra_b200_getrf(double* a, int64_t lda, int64_t m, int64_t n, int64_t* piv,
+                    int64_t* nonzero_diag, void* ws, size_t ws_bytes, void* stream) {
+  return getrf(a, lda, m, n, piv, nonzero_diag, nullptr, ws, ws_bytes, S(stream));
+}
+
+int rlra_b200_iota(int64_t* p, int64_t m, void* stream) { return fill_iota(p, m, S(stream)); }
+
+int rlra_b200_count_nonzero_diag(const double* a, int64_t lda, int64_t r, int64_t* out,
+                                 void* stream) {
+  return count_nonzero_diag(a, lda, r, out, S(stream));
+}
+
+int rlra_b200_lu_basis(const double* lu, int64_t ldlu, int64_t m, int64_t k, const int64_t* piv,
+                       int64_t* pinv_ws, double* w, int64_t ldw, void* stream) {
+  return lu_basis(lu, ldlu, m, k, piv, pinv_ws, w, ldw, S(stream));
+}
+
+int rlra_b200_lu_extract(const double* lu, int64_t ldlu, int64_t m, int64_t n, double* l,
+                         int64_t ldl, double* u, int64_t ldu, void* stream) {
+  const int64_t r = m < n ? m : n;
+  if (l && extract_l(lu, ldlu, m, r, l, ldl, S(stream))) return -1;
+  if (u && extract_u(lu, ldlu, r, n, u, ldu, S(stream))) return -1;
+  return 0;
+}
+
+size_t rlra_b200_gemm_workspace(int64_t m, int64_t n, int64_t k) { return gemm_workspace_bytes(m, n, k); }
+
+int rlra_b200_dgemm(int transa, int transb, int64_t m, int64_t n, int64_t k, double alpha,
+                    const double* a, int64_t lda, const double* b, int64_t ldb, double beta,
+                    double* c, int64_t ldc, void* ws, size_t ws_bytes, void* stream) {
+  return gemm(transa != 0, transb != 0, m, n, k, alpha, a, lda, b, ldb, beta, c, ldc, ws, ws_bytes,
+              S(stream));
+}
+
+size_t rlra_b200_geqrf_workspace(int64_t m, int64_t n) { return geqrf_workspace_bytes(m, n); }
+
+int rlra_b200_geqrf(double* a, int64_t lda, int64_t m, int64_t n, double* tau, void* ws,
+                    size_t ws_bytes, void* stream) {
+  return geqrf(a, lda, m, n, tau, ws, ws_bytes, S(stream));
+}
+
+int rlra_b200_orgqr(const double* a, int64_t lda, int64_t m, int64_t n, double* q, int64_t ldq,
+                    void* ws, size_t ws_bytes, void* stream) {
+  return orgqr(a, lda, m, n, q, ldq, ws, ws_bytes, S(stream));
+}
+
+size_t rlra_b200_trsm_workspace(int64_t l, int64_t ncols) {
+  (void)l;
+  return (size_t)16 * 32 * (ncols > 0 ? ncols : 1) * sizeof(double);
+}
+
+int rlra_b200_trsm_rt(const double* r, int64_t ldr, int64_t l, double* x, int64_t ldx,
+                      int64_t ncols, void* ws, size_t ws_bytes, void* stream) {
+  return trsm_rt(r, ldr, l, x, ldx, ncols, ws, ws_bytes, S(stream));
+}
+
+int rlra_b200_diag_absmin(const double* a, int64_t lda, int64_t r, double* out, void* stream) {
+  return diag_absmin(a, lda, r, out, S(stream));
+}
+
+size_t rlra_b200_sumsq_workspace(int64_t m, int64_t n) { return sumsq_workspace_bytes(m, n); }
+
+int rlra_b200_sumsq(const double* a, int64_t lda, int64_t m, int64_t n, double* out, void* ws,
+                    size_t ws_bytes, void* stream) {
+  return sumsq(a, lda, m, n, out, ws, ws_bytes, S(stream));
+}
+
+int rlra_b200_colsumsq(const double* a, int64_t lda, int64_t m, int64_t n, double* out,
+                       void* stream) {
+  return colsumsq(a, lda, m, n, out, S(stream));
+}
+
+int rlra_b200_transpose(const double* in, int64_t ldi, int64_t m, int64_t n, double* out,
+                        int64_t ldo, void* stream) {
+  return transpose(in, ldi, m, n, out, ldo, S(stream));
+}
+
+}  // extern "C"

@@ -1,0 +1,80 @@
+// Shared helpers for the rlra_b200 sm_100a kernels: error plumbing behind the
+// C ABI, column-major indexing, a deterministic grid barrier for the
+// cooperative panel kernels, and small warp utilities.
+#pragma once
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <cuda_runtime.h>
+
+namespace rlra {
+
+// thread-local last error string for rlra_b200_last_error()
+void set_error(const char* fmt, ...);
+const char* last_error();
+
+#define RLRA_CHECK_CUDA(expr)                                                   \
+  do {                                                                          \
+    cudaError_t _e = (expr);                                                    \
+    if (_e != cudaSuccess) {                                                    \
+      ::rlra::set_error("%s failed at %s:%d: %s", #expr, __FILE__, __LINE__,    \
+                        cudaGetErrorString(_e));                                \
+      return -1;                                                                \
+    }                                                                           \
+  } while (0)
+
+#define RLRA_REQUIRE(cond, ...)                                                 \
+  do {                                                                          \
+    if (!(cond)) {                                                              \
+      ::rlra::set_error(__VA_ARGS__);                                           \
+      return -2;                                                                \
+    }                                                                           \
+  } while (0)
+
+struct DeviceInfo {
+  int sm_count = 0;
+  int max_smem_optin = 0;
+};
+const DeviceInfo& device_info();
+
+// Column-major element access, 64-bit indices throughout (C5 A is 8.6e9 elems).
+__host__ __device__ __forceinline__ int64_t cm(int64_t i, int64_t j, int64_t ld) {
+  return i + j * ld;
+}
+
+__host__ __device__ __forceinline__ int64_t ceil_div(int64_t a, int64_t b) {
+  return (a + b - 1) / b;
+}
+
+// Non-contracted multiply-then-subtract: a - l*u rounded twice, exactly like the
+// reference's `lu[i, jj] - lu[i, j] * ujj` built with -ffp-contract=off
+// (rlra/_lu_cython.pyx:52-55, pkg/setup.py:25-27).
+__device__ __forceinline__ double sub_mul_nofma(double a, double l, double u) {
+  return __dsub_rn(a, __dmul_rn(l, u));
+}
+
+// Sense-reversing grid barrier over global memory for cooperative launches.
+// `bar[0]` = arrival counter, `bar[1]` = generation.  All CTAs of the grid must
+// be co-resident (launched with cudaLaunchCooperativeKernel).
+__device__ __forceinline__ void grid_barrier(unsigned int* bar, unsigned int nblocks) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile unsigned int* vgen = bar + 1;
+    unsigned int gen = *vgen;
+    __threadfence();
+    unsigned int arrived = atomicAdd(bar, 1u);
+    if (arrived == nblocks - 1) {
+      bar[0] = 0;
+      __threadfence();
+      atomicAdd(bar + 1, 1u);
+    } else {
+      while (*vgen == gen) {
+        __nanosleep(20);
+      }
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+}  // namespace rlra

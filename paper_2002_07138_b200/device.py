@@ -1,0 +1,212 @@
+"""Device operands: the reference's accessor protocol (rlra/accessors.py:17-100)
+and column-stream protocol (rlra/singlepass.py:27-57) over HBM-resident data.
+
+A ``DeviceMatrix`` holds A column-major in HBM (one upload); ``matmul`` and
+``rmatmul`` are one pass over A each on the DMMA GEMM (K1/K2), ``fro_norm`` is
+the compensated K2b reduction.  Host ndarrays handed to the drivers are wrapped
+in a DeviceMatrix; duck-typed host accessors are adapted so their products feed
+the device pipeline (their own products run wherever they run).
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import torch
+
+from . import ops
+
+DEFAULT_PANEL = 256  # rlra/singlepass.py:19
+
+
+class DeviceMatrix:
+    """HBM-resident dense operand (rlra/accessors.py:17-37 on device)."""
+
+    is_device_accessor = True
+
+    def __init__(self, a, device=None):
+        dev = ops.check_device(device)
+        if isinstance(a, torch.Tensor):
+            if a.dim() != 2:
+                raise ValueError(f"expected a 2-d array, got ndim={a.dim()}")
+            t = a.to(device=dev, dtype=torch.float64)
+            self._a = ops.as_fmat(t)
+        else:
+            self._a = ops.from_numpy(a, dev)
+        self._fro = None
+
+    @property
+    def shape(self):
+        return tuple(self._a.shape)
+
+    @property
+    def tensor(self):
+        return self._a
+
+    @property
+    def device(self):
+        return self._a.device
+
+    def matmul(self, x):
+        """A @ X, one pass over A (rlra/accessors.py:27-28)."""
+        return ops.matmul(self._a, _dev(x, self.device))
+
+    def rmatmul(self, x):
+        """A^T @ X, one pass over A (rlra/accessors.py:30-31)."""
+        return ops.matmul(self._a, _dev(x, self.device), ta=True)
+
+    def fro_norm_sq_device(self):
+        """Compensated ||A||_F^2 as a device scalar (no host sync)."""
+        return ops.sumsq(self._a)
+
+    def fro_norm(self):
+        """||A||_F (rlra/accessors.py:33-34)."""
+        return math.sqrt(float(self.fro_norm_sq_device().item()))
+
+    def to_dense(self):
+        return ops.to_numpy(self._a)
+
+
+class HostAccessorAdapter:
+    """Adapts a duck-typed host accessor (anything with shape/matmul/rmatmul,
+    rlra/accessors.py:94-100) to device operands: products are computed by the
+    wrapped object and uploaded."""
+
+    is_device_accessor = True
+
+    def __init__(self, inner, device=None):
+        self.inner = inner
+        self._dev = ops.check_device(device)
+
+    @property
+    def shape(self):
+        return tuple(self.inner.shape)
+
+    @property
+    def device(self):
+        return self._dev
+
+    def matmul(self, x):
+        return ops.from_numpy(np.asarray(self.inner.matmul(ops.to_numpy(x))), self._dev)
+
+    def rmatmul(self, x):
+        return ops.from_numpy(np.asarray(self.inner.rmatmul(ops.to_numpy(x))), self._dev)
+
+    def fro_norm(self):
+        return float(self.inner.fro_norm())
+
+    def fro_norm_sq_device(self):
+        return torch.tensor([self.fro_norm() ** 2], dtype=torch.float64, device=self._dev)
+
+
+class InstrumentedAccessor:
+    """Counts product invocations (passes) like rlra/accessors.py:67-91."""
+
+    is_device_accessor = True
+
+    def __init__(self, inner):
+        self.inner = as_accessor(inner)
+        self.product_count = 0
+
+    @property
+    def shape(self):
+        return self.inner.shape
+
+    @property
+    def device(self):
+        return self.inner.device
+
+    def matmul(self, x):
+        self.product_count += 1
+        return self.inner.matmul(x)
+
+    def rmatmul(self, x):
+        self.product_count += 1
+        return self.inner.rmatmul(x)
+
+    def fro_norm(self):
+        # a norm query is not a product (rlra/accessors.py:86-88)
+        return self.inner.fro_norm()
+
+    def fro_norm_sq_device(self):
+        return self.inner.fro_norm_sq_device()
+
+    def to_dense(self):
+        return self.inner.to_dense()
+
+
+def as_accessor(a, device=None):
+    """Device analogue of rlra/accessors.py:94-100."""
+    if getattr(a, "is_device_accessor", False):
+        return a
+    if hasattr(a, "matmul") and hasattr(a, "rmatmul") and hasattr(a, "shape"):
+        return HostAccessorAdapter(a, device)
+    try:
+        import scipy.sparse as sp
+
+        if sp.issparse(a):
+            raise TypeError("sparse operands are outside the B200 path (SURVEY.md §8(f) row 4)")
+    except ImportError:  # pragma: no cover
+        pass
+    return DeviceMatrix(a, device)
+
+
+def _dev(x, device):
+    if isinstance(x, torch.Tensor):
+        if x.device != device:
+            x = x.to(device)
+        return ops.as_fmat(x.to(torch.float64))
+    return ops.from_numpy(x, device)
+
+
+# ---------------------------------------------------------------- column streams
+class _StreamBase:
+    """Single-use pull interface (rlra/singlepass.py:27-46)."""
+
+    def __init__(self, shape):
+        self.shape = shape
+        self.columns_pulled = 0
+        self._spent = False
+
+    def panels(self, width=DEFAULT_PANEL):
+        if self._spent:
+            raise RuntimeError("stream already consumed; columns are single-use")
+        if width < 1:
+            raise ValueError("panel width must be >= 1")
+        self._spent = True
+        n = self.shape[1]
+        for j0 in range(0, n, width):
+            j1 = min(j0 + width, n)
+            block = self._panel(j0, j1)
+            self.columns_pulled += j1 - j0
+            yield j0, block
+
+
+class DeviceColumnStream(_StreamBase):
+    """Streams an HBM-resident matrix by column panels (views, no copies)."""
+
+    def __init__(self, a, device=None):
+        self._m = a if isinstance(a, DeviceMatrix) else DeviceMatrix(a, device)
+        super().__init__(self._m.shape)
+
+    @property
+    def device(self):
+        return self._m.device
+
+    def _panel(self, j0, j1):
+        return self._m.tensor[:, j0:j1]
+
+
+class DenseColumnStream(_StreamBase):
+    """Streams an in-memory HOST matrix (rlra/singlepass.py:49-57); each panel
+    is uploaded when pulled (out-of-core style)."""
+
+    def __init__(self, a):
+        self._a = np.asfortranarray(np.asarray(a, dtype=np.float64))
+        if self._a.ndim != 2:
+            raise ValueError(f"expected a 2-d array, got ndim={self._a.ndim}")
+        super().__init__(self._a.shape)
+
+    def _panel(self, j0, j1):
+        return self._a[:, j0:j1]

@@ -1,0 +1,72 @@
+"""Device versions of the reference's dense factorization kernels
+(rlra/kernels.py:20-117): pivoted LU, economy QR, pseudoinverse solve.
+All arithmetic runs in librlra_b200.so; nothing here computes on the host.
+"""
+
+from __future__ import annotations
+
+from typing import NamedTuple
+
+import torch
+
+from . import ops
+from .errors import IllPosedPseudoinverse
+
+PINV_RTOL = 1e-12  # rlra/kernels.py:17
+
+
+class PivotedLU(NamedTuple):
+    L: torch.Tensor  # m x r unit-lower
+    U: torch.Tensor  # r x n upper
+    p: torch.Tensor  # row permutation: A[p, :] = L @ U
+    nonzero_diag: torch.Tensor  # device int64[1]: count_nonzero(diag(U))
+
+
+def plu_(a, want_l=True, want_u=True):
+    """kernels.plu (rlra/kernels.py:37-54) on a device matrix, factoring `a` IN
+    PLACE (callers pass a scratch copy when they still need the input)."""
+    piv, cnt = ops.getrf_(a)
+    l, u = ops.lu_extract(a, want_l, want_u)
+    return PivotedLU(l, u, piv, cnt)
+
+
+def plu(a):
+    """Non-destructive kernels.plu."""
+    return plu_(_copy(a))
+
+
+def _copy(a):
+    out = ops.fmat(a.shape[0], a.shape[1], a.device)
+    out.copy_(a)
+    return out
+
+
+def eqr_(a):
+    """kernels.eqr (rlra/kernels.py:57-61), destroying `a`: returns (Q, QR)."""
+    qr = ops.QR(a)
+    return qr.q(), qr
+
+
+def pinv_factor_(l):
+    """kernels.pinv_factor (rlra/kernels.py:64-79) on a scratch copy of `l`.
+
+    Raises IllPosedPseudoinverse when min |R_ii| <= PINV_RTOL * ||L||_F."""
+    m, n = l.shape
+    if m < n:
+        raise ValueError(f"need a tall matrix, got {(m, n)}")
+    fro2 = ops.sumsq(l)
+    work = _copy(l)
+    qr = ops.QR(work)
+    dmin = ops.diag_absmin(qr.r_view())
+    vals = torch.cat([dmin, fro2]).cpu()
+    if float(vals[0]) <= PINV_RTOL * float(vals[1]) ** 0.5:
+        raise IllPosedPseudoinverse(f"matrix of shape {(m, n)} is numerically rank-deficient")
+    return qr
+
+
+def pinv_transpose_apply(l, m_):
+    """(L^T)^+ M = Q R^{-T} M (rlra/kernels.py:92-96)."""
+    qr = pinv_factor_(l)
+    x = _copy(m_)
+    ops.trsm_rt_(qr.r_view(), x)
+    return ops.matmul(qr.q(), x)

@@ -1,0 +1,111 @@
+"""Power-iteration row-space basis for any pass budget v >= 2 on device
+(rlra/rangefinder.py:20-176, the paper's Alg. 7 generalised to any v).
+
+Same control flow, Omega shapes and pass accounting as the reference: even v
+draws Omega m x l and starts with A^T Omega, odd v draws Omega n x l; interior
+renormalisations are the row-unpermuted L of a partial-pivot LU (bit-exact
+GEPP, K3); the last step is a Householder QR (K4).  The exact-zero-diagonal
+RankCollapse checks (rlra/rangefinder.py:55-64) are evaluated on device and
+raised when the basis is handed back, with the reference's attributes.
+"""
+
+from __future__ import annotations
+
+from typing import NamedTuple
+
+import torch
+
+from . import core, ops
+from .device import as_accessor
+from .errors import RankCollapse
+
+
+class RangeBasis(NamedTuple):
+    V: torch.Tensor  # n x l, orthonormal columns (device)
+    passes_used: int
+
+
+class RankChecks:
+    """Deferred _check_width calls: (device nonzero-count, requested) pairs,
+    resolved with a single host sync in call order."""
+
+    def __init__(self):
+        self._items = []
+
+    def add(self, count, requested):
+        self._items.append((count, int(requested)))
+
+    def raise_if_collapsed(self):
+        if not self._items:
+            return
+        counts = torch.cat([c for c, _ in self._items]).cpu().tolist()
+        items = self._items
+        self._items = []
+        for achieved, (_, requested) in zip(counts, items):
+            if achieved < requested:
+                raise RankCollapse(int(achieved), requested)
+
+
+def _validate(a, l, lower=1):
+    """rlra/rangefinder.py:80-83."""
+    m, n = a.shape
+    if not lower <= l <= min(m, n):
+        raise ValueError(f"sketch width l={l} outside {lower}..min{(m, n)}")
+
+
+def qr_basis_(x, checks):
+    """rlra/rangefinder.py:67-70 (destroys x)."""
+    qr = ops.QR(x)
+    checks.add(ops.count_nonzero_diag(qr.r_view()), x.shape[1])
+    return qr.q()
+
+
+def lu_basis_(x, checks):
+    """rlra/rangefinder.py:73-77: row-unpermuted L of lu(x) (destroys x)."""
+    piv, cnt = ops.getrf_(x)
+    checks.add(cnt, x.shape[1])
+    return ops.lu_basis(x, piv)
+
+
+def general_power_basis_v(a, l, v, seed, *, _checks=None):
+    """rlra/rangefinder.py:144-176; consumes exactly v - 1 passes."""
+    a = as_accessor(a)
+    _validate(a, l)
+    if v < 2:
+        raise ValueError("pass budget v must be >= 2")
+    checks = _checks if _checks is not None else RankChecks()
+    m, n = a.shape
+    dev = a.device
+    passes = 0
+    basis = None
+    if v % 2 == 0:
+        om = core.omega(seed, m, l, dev)
+        x = a.rmatmul(om)
+        passes += 1
+        if v == 2:
+            basis = qr_basis_(x, checks)
+            if _checks is None:
+                checks.raise_if_collapsed()
+            return RangeBasis(basis, passes)
+        w = lu_basis_(x, checks)
+    else:
+        w = core.omega(seed, n, l, dev)
+    half = (v - 1) // 2
+    for i in range(1, half + 1):
+        w = lu_basis_(a.matmul(w), checks)
+        passes += 1
+        if i == half:
+            basis = qr_basis_(a.rmatmul(w), checks)
+        else:
+            w = lu_basis_(a.rmatmul(w), checks)
+        passes += 1
+    if _checks is None:
+        checks.raise_if_collapsed()
+    return RangeBasis(basis, passes)
+
+
+def power_basis_v(a, l, p, seed):
+    """rlra/rangefinder.py:137-141: odd pass budget 2p + 1."""
+    if p < 1:
+        raise ValueError("p must be >= 1: no products means no basis")
+    return general_power_basis_v(a, l, 2 * p + 1, seed)

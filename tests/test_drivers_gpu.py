@@ -1,0 +1,227 @@
+"""End-to-end parity of the drop-in drivers against the reference's golden
+outputs (tests/golden/, produced by the unmodified reference) and the oracle.
+
+Bar (BASELINE.json north_star): identical pivot sequences p, q and rank;
+relative Frobenius reconstruction error within 1e-10 of the reference's."""
+
+import hashlib
+import json
+import os
+
+import numpy as np
+import pytest
+
+from oracle import rlra_oracle as O
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+GOLD = os.path.join(HERE, "golden")
+META = json.load(open(os.path.join(GOLD, "golden.json")))
+DRV = np.load(os.path.join(GOLD, "drivers.npz"))
+
+pytestmark = pytest.mark.gpu
+
+REL_ERR_TOL = 1e-10  # |rel_err_gpu - rel_err_ref|, BASELINE.json north_star
+
+
+def sha_i64(a):
+    return hashlib.sha256(np.ascontiguousarray(a, dtype=np.int64).tobytes()).hexdigest()
+
+
+def lu_structure_ok(f):
+    return np.count_nonzero(np.triu(f.L, 1)) == 0 and np.count_nonzero(np.tril(f.U, -1)) == 0
+
+
+@pytest.mark.parametrize("v", [2, 3, 4, 5, 6])
+def test_powerlu_matches_reference(cuda_dev, v):
+    import paper_2002_07138_b200 as P
+
+    a = DRV["pl_a"]
+    f = P.powerlu(a, 30, q_os=10, v=v, seed=1)
+    assert isinstance(f.L, np.ndarray)
+    assert np.array_equal(f.p, DRV[f"pl_v{v}/p"])
+    assert np.array_equal(f.q, DRV[f"pl_v{v}/q"])
+    err = O.rel_fro_error_factor(a, f)
+    assert abs(err - META["drivers"][f"pl_v{v}"]["rel_err"]) <= REL_ERR_TOL
+    assert lu_structure_ok(f)
+    np.testing.assert_allclose(f.L, DRV[f"pl_v{v}/L"], rtol=0, atol=1e-9)
+
+
+@pytest.mark.parametrize("v", [2, 3, 4, 5])
+def test_powerlu_exact_rank_all_parities(cuda_dev, v):
+    import paper_2002_07138_b200 as P
+
+    a = DRV["exact_a"]
+    f = P.powerlu(a, 8, q_os=4, v=v, seed=0)
+    assert O.rel_fro_error_factor(a, f) < 1e-12  # pkg/tests/test_fixedrank.py:50-56
+    assert np.array_equal(f.p, DRV[f"exact_v{v}/p"]) and np.array_equal(f.q, DRV[f"exact_v{v}/q"])
+
+
+def test_basis_v2_is_qr_of_transpose_sketch(cuda_dev):
+    import paper_2002_07138_b200 as P
+
+    b = P.general_power_basis_v(P.DeviceMatrix(DRV["pl_a"]), 40, 2, 9)
+    from paper_2002_07138_b200 import ops
+
+    V = ops.to_numpy(b.V)
+    assert b.passes_used == 1
+    np.testing.assert_allclose(V, DRV["basis_v2/V"], rtol=0, atol=1e-12)
+    b = P.general_power_basis_v(P.DeviceMatrix(DRV["pl_a"]), 40, 5, 9)
+    assert b.passes_used == 4
+    np.testing.assert_allclose(ops.to_numpy(b.V), DRV["basis_v5/V"], rtol=0, atol=1e-9)
+
+
+def test_pass_budgets_exact(cuda_dev):
+    import paper_2002_07138_b200 as P
+
+    a = O.gaussian(10, 60, 45)
+    for v in (2, 3, 4, 5, 6):
+        acc = P.InstrumentedAccessor(a)
+        P.powerlu(acc, 8, q_os=4, v=v, seed=0)
+        assert acc.product_count == v
+        acc = P.InstrumentedAccessor(a)
+        P.adaptive_rank(acc, P.PrecisionParams(1e-3, 5, 20, v), seed=0)
+        assert acc.product_count == v
+
+
+def test_adaptive_rank_matches_reference(cuda_dev):
+    import paper_2002_07138_b200 as P
+
+    ref = META["drivers"]["fp"]
+    o = P.adaptive_rank(DRV["fp_a"], P.PrecisionParams(1e-3, 5, 60, 4), seed=0)
+    assert o.converged and o.rank == ref["rank"]
+    assert abs(o.residual_energy - ref["residual"]) <= 1e-9 * O.fro_norm(DRV["fp_a"]) ** 2
+    np.testing.assert_allclose(np.abs(o.V), np.abs(DRV["fp/V"]), atol=1e-9)
+    fac, o2 = P.powerlu_fp(DRV["fp_a"], P.PrecisionParams(1e-3, 5, 60, 4), seed=0)
+    assert fac.rank == o2.rank == META["drivers"]["fpfac"]["rank"]
+    assert np.array_equal(fac.p, DRV["fpfac/p"]) and np.array_equal(fac.q, DRV["fpfac/q"])
+    assert abs(O.rel_fro_error_factor(DRV["fp_a"], fac) - META["drivers"]["fpfac"]["rel_err"]) <= REL_ERR_TOL
+
+
+def test_adaptive_rank_not_converged(cuda_dev):
+    import paper_2002_07138_b200 as P
+
+    params = P.PrecisionParams(1e-6, 10, 20, 4)
+    o = P.adaptive_rank(DRV["fp_nc_a"], params, seed=0)
+    assert not o.converged and o.rank == 20 and o.V.shape == (120, 20)
+    assert abs(o.residual_energy - META["drivers"]["fp_nc"]["residual"]) <= 1e-12
+    with pytest.raises(P.NotConverged) as exc:
+        P.powerlu_fp(DRV["fp_nc_a"], params, seed=0)
+    assert exc.value.outcome.rank == 20 and not exc.value.outcome.converged
+
+
+def test_eps_one_stops_immediately(cuda_dev):
+    import paper_2002_07138_b200 as P
+
+    a = O.gaussian(3, 60, 60)
+    o = P.adaptive_rank(a, P.PrecisionParams(1.0, 5, 20, 4), seed=0)
+    assert o.converged and o.rank == 1
+
+
+def test_single_pass_matches_reference(cuda_dev):
+    import paper_2002_07138_b200 as P
+
+    f = P.single_pass_lu(P.DenseColumnStream(DRV["sp_a"]), 20, seed=0, q_os=5)
+    assert f.L.shape == (120, 20) and f.U.shape == (20, 100)
+    assert np.array_equal(f.p, DRV["sp/p"]) and np.array_equal(f.q, DRV["sp/q"])
+    assert abs(O.rel_fro_error_factor(DRV["sp_a"], f) - META["drivers"]["sp"]["rel_err"]) <= REL_ERR_TOL
+    s = P.DeviceColumnStream(DRV["sp_a"])
+    g, h = P.stream_sketch(s, 25, 3, panel=16)
+    from paper_2002_07138_b200 import ops
+
+    assert s.columns_pulled == 100
+    np.testing.assert_allclose(ops.to_numpy(g), DRV["sk/G"], rtol=0, atol=1e-12)
+    np.testing.assert_allclose(ops.to_numpy(h), DRV["sk/H"], rtol=0, atol=1e-11)
+
+
+def test_identity_stream_sketch_is_the_draw(cuda_dev):
+    import paper_2002_07138_b200 as P
+    from paper_2002_07138_b200 import ops
+
+    g, h = P.stream_sketch(P.DeviceColumnStream(np.eye(30)), 6, seed=3, panel=7)
+    om = O.gaussian(3, 30, 6)
+    assert np.array_equal(ops.to_numpy(g), om) and np.array_equal(ops.to_numpy(h), om)
+
+
+def test_single_pass_rejects_rank_above_numerical_rank(cuda_dev):
+    import paper_2002_07138_b200 as P
+
+    rng = np.random.default_rng(10)
+    a = O.gaussian_from(rng, 80, 5) @ O.gaussian_from(rng, 5, 60)
+    with pytest.raises(P.IllPosedPseudoinverse):
+        P.single_pass_lu(P.DenseColumnStream(a), 8, seed=0)
+
+
+def test_stream_single_use_and_length(cuda_dev):
+    import paper_2002_07138_b200 as P
+
+    s = P.DeviceColumnStream(np.eye(5))
+    list(s.panels(2))
+    with pytest.raises(RuntimeError, match="single-use"):
+        list(s.panels(2))
+
+
+def test_rank_collapse_from_duplicated_rows(cuda_dev):
+    import paper_2002_07138_b200 as P
+
+    base = O.gaussian(17, 5, 30)
+    a = np.vstack([base] * 8)  # pkg/tests/test_fixedrank.py:159-167
+    with pytest.raises(P.RankCollapse):
+        P.powerlu(a, 10, q_os=5, v=4, seed=0)
+
+
+def test_rank_collapse_reports_achieved_width(cuda_dev):
+    import paper_2002_07138_b200 as P
+
+    a = np.diag([1.0, 1.0, 1.0, 0.0, 0.0, 0.0, 0.0, 0.0])
+    with pytest.raises(P.RankCollapse) as exc:
+        P.general_power_basis_v(a, 5, 2, seed=0)
+    assert exc.value.achieved == 3 and exc.value.requested == 5
+
+
+def test_validation_errors(cuda_dev):
+    import paper_2002_07138_b200 as P
+
+    a = O.gaussian(18, 20, 10)
+    for args in [(0, 2, 3), (8, 5, 3), (4, 2, 1)]:
+        with pytest.raises(ValueError):
+            P.powerlu(a, args[0], q_os=args[1], v=args[2], seed=0)
+    with pytest.raises(ValueError, match="width"):
+        P.adaptive_rank(O.gaussian(11, 30, 25), P.PrecisionParams(1e-2, 10, 30, 4), seed=0)
+
+
+def test_c1_config_matches_reference(cuda_dev):
+    import paper_2002_07138_b200 as P
+    from paper_2002_07138_b200 import configs
+
+    a = configs.gen_c1()
+    f = P.powerlu(a, 50, 10, 3, 0)
+    ref = META["configs"]["C1"]
+    assert sha_i64(f.p) == ref["p_sha"] and sha_i64(f.q) == ref["q_sha"]
+    assert abs(O.rel_fro_error_factor(a, f) - ref["rel_err"]) <= REL_ERR_TOL
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("v", [2, 3, 4, 5, 6])
+def test_c2_config_matches_reference(cuda_dev, v):
+    import paper_2002_07138_b200 as P
+    from paper_2002_07138_b200 import configs
+
+    a = _c2()
+    dm = P.DeviceMatrix(a)
+    f = P.powerlu(dm, 200, 20, v, 0).to_numpy()
+    ref = META["configs"][f"C2_v{v}"]
+    pq = np.load(os.path.join(GOLD, "c2_pq.npz"))
+    assert np.array_equal(f.p, pq[f"v{v}_p"]), "row pivots differ from the reference"
+    assert np.array_equal(f.q, pq[f"v{v}_q"]), "column pivots differ from the reference"
+    assert abs(O.rel_fro_error_factor(a, f) - ref["rel_err"]) <= REL_ERR_TOL
+
+
+_C2 = {}
+
+
+def _c2():
+    from paper_2002_07138_b200 import configs
+
+    if "a" not in _C2:
+        _C2["a"] = configs.gen_c2()
+    return _C2["a"]

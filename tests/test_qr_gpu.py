@@ -1,0 +1,52 @@
+"""K4 numerics: device Householder QR + explicit Q against LAPACK
+(np.linalg.qr, what the reference calls at rlra/kernels.py:60).  Same sign
+convention, so Q matches entrywise to ~cond * eps; orthogonality to 1e-13."""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def dev_qr(x):
+    from paper_2002_07138_b200 import ops
+
+    dev = ops.check_device()
+    d = ops.from_numpy(x, dev)
+    qr = ops.QR(d)
+    q = ops.to_numpy(qr.q())
+    r = np.triu(ops.to_numpy(qr.r_view()))
+    cnt = int(ops.count_nonzero_diag(qr.r_view()).item())
+    return q, r, cnt
+
+
+@pytest.mark.parametrize("m,n", [(30, 8), (2000, 60), (10000, 220), (3000, 97), (512, 512), (33, 33)])
+def test_qr_matches_lapack(cuda_dev, m, n):
+    x = np.random.default_rng(m + n).standard_normal((m, n))
+    q, r, cnt = dev_qr(x)
+    q_ref, r_ref = np.linalg.qr(x)
+    assert cnt == n
+    assert np.allclose(q.T @ q, np.eye(n), atol=1e-13)
+    assert np.allclose(q @ r, x, atol=1e-12 * np.linalg.norm(x))
+    np.testing.assert_allclose(np.diag(r), np.diag(r_ref), rtol=1e-11)
+    np.testing.assert_allclose(q, q_ref, rtol=0, atol=1e-11)
+
+
+def test_qr_exact_zero_diagonal_on_structural_deficiency(cuda_dev):
+    # rows 3..7 of A^T Omega vanish exactly (pkg/tests/test_rangefinder.py:102-107)
+    a = np.diag([1.0, 1.0, 1.0, 0, 0, 0, 0, 0])
+    om = np.random.default_rng(0).standard_normal((8, 5))
+    x = a.T @ om
+    _, r, cnt = dev_qr(x)
+    r_ref = np.linalg.qr(x)[1]
+    assert cnt == int(np.count_nonzero(np.diag(r_ref))) == 3
+
+
+def test_qr_ill_conditioned_orthogonality(cuda_dev):
+    rng = np.random.default_rng(1)
+    u, _ = np.linalg.qr(rng.standard_normal((5000, 300)))
+    v, _ = np.linalg.qr(rng.standard_normal((300, 300)))
+    x = (u * np.logspace(0, -9, 300)) @ v.T
+    q, r, _ = dev_qr(x)
+    assert np.abs(q.T @ q - np.eye(300)).max() < 1e-13
+    assert np.allclose(q @ r, x, atol=1e-13 * np.linalg.norm(x))
