@@ -1,0 +1,328 @@
+#!/usr/bin/env python
+"""PowerLU FP64 benchmark (BASELINE.json metric) on B200.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--config C2|C1|C3|C5] [--v 4] [--breakdown]
+
+One step = one complete factorization of the workload (default C2:
+powerlu(A 20000x10000, k=200, q_os=20, v=4, seed=0), BASELINE.json configs[1]).
+
+Our arm prints ONE JSON line with:
+  value      algorithmic GFLOP/s (SURVEY.md Appendix B flop count) with A and
+             Omega resident in HBM, outputs left in HBM; CUDA events, K steps
+  e2e        the same metric through the public API with HOST inputs (pinned
+             NumPy A), Omega drawn on the host each step, factors returned to
+             the host: H2D/D2H inside the timed region
+  roofline   the pass GEMM (DMMA) against the measured FP64 DMMA peak
+  cpu_baseline  the unmodified reference (oracle/_ref, rlra 0.1.0) on the box's
+             host cores, same call, best of a bounded sample
+`--impl reference` times the reference's own CPU implementation (oracle/_ref).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+FP64_PEAK_TFLOPS = 37.1  # measured DMMA m8n8k4 sustained, profiles/fp64_peak_r01.log
+FP64_PEAK_SRC = "measured: tools/fp64_peak.cu on this pool's B200 (profiles/fp64_peak_r01.log); MEASURED_PEAKS.json has no FP64 entry"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", default="C2")
+    ap.add_argument("--v", type=int, default=None)
+    ap.add_argument("--breakdown", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def workload(args):
+    from paper_2002_07138_b200 import configs
+
+    w = configs.WORKLOADS[args.config]
+    v = args.v if args.v is not None else w.v
+    if w.kind != "powerlu":
+        raise SystemExit(f"bench supports the fixed-rank powerlu configs (C1, C2, C5); got {args.config}")
+    gen = {"C1": configs.gen_c1, "C2": configs.gen_c2, "C5": configs.gen_c5}[w.name]
+    passes, fact = configs.powerlu_flops(w.m, w.n, w.k, w.k + w.q_os, v)
+    desc = (f"{w.name}: powerlu(A {w.m}x{w.n} float64, k={w.k}, q_os={w.q_os}, v={v}, seed={w.seed})")
+    return w, v, gen, passes, fact, desc
+
+
+def ref_module():
+    """The unmodified reference (oracle/_ref), else the oracle port."""
+    ref = os.path.join(REPO, "oracle", "_ref")
+    if os.path.isdir(os.path.join(ref, "rlra")):
+        sys.path.insert(0, ref)
+        os.environ.setdefault("RLRA_BACKEND", "compiled")
+        import rlra
+
+        return rlra, "reference"
+    from oracle import rlra_oracle
+
+    return rlra_oracle, "port"
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md recipe)."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.15)
+        self.proc.terminate()
+        self.proc.wait()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax.append(float(parts[2]))
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[5:9]):
+                if val.lower() == "active":
+                    reasons.add(nm)
+        os.unlink(self.path)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        loaded = [s for s in sm if s > 0.5 * max(sm)] or sm
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": max(smax), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    w, v, gen, passes, fact, desc = workload(args)
+    mod, kind = ref_module()
+    a = gen()
+    flops = passes + fact
+    for _ in range(args.warmup):
+        mod.powerlu(a, w.k, w.q_os, v, w.seed)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        mod.powerlu(a, w.k, w.q_os, v, w.seed)
+        times.append(time.perf_counter() - t0)
+    sec = sum(times) / len(times)
+    val = flops / sec / 1e9
+    cores = os.cpu_count()
+    line = {
+        "impl": "reference", "metric": f"PowerLU FP64 GFLOP/s ({w.name}, v={v})", "value": val,
+        "unit": "GFLOP/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": sec * 1e3, "s_per_factorization": sec, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": desc, "m": w.m, "n": w.n, "k": w.k, "l": w.k + w.q_os, "v": v},
+        "cpu_baseline": {"value": val, "unit": "GFLOP/s", "cores": cores, "kind": kind,
+                         "sample": f"{args.steps} full factorizations (mean), rlra {getattr(mod, '__version__', 'port')} "
+                                   f"backend={getattr(mod, 'BACKEND', 'c-oracle')}, OpenBLAS threads=all"},
+        "e2e": {"value": val, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def cpu_baseline(a, w, v, flops, budget_s=30.0):
+    mod, kind = ref_module()
+    times, f = [], None
+    t_start = time.perf_counter()
+    while True:
+        t0 = time.perf_counter()
+        f = mod.powerlu(a, w.k, w.q_os, v, w.seed)
+        times.append(time.perf_counter() - t0)
+        if len(times) >= 3 or time.perf_counter() - t_start + times[-1] > budget_s:
+            break
+    best = min(times)
+    return {"value": flops / best / 1e9, "unit": "GFLOP/s", "cores": os.cpu_count(), "kind": kind,
+            "sample": f"{len(times)} full {w.name} factorizations (best of), same A and seed; "
+                      f"s/factorization {best:.3f}"}, f
+
+
+def our_arm(args):
+    import numpy as np
+    import torch
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        from paper_2002_07138_b200 import distributed as D
+
+        return D.bench_main(args)
+    torch.cuda.set_device(local)
+    import paper_2002_07138_b200 as P
+    from paper_2002_07138_b200 import _native, ops
+
+    w, v, gen, passes, fact, desc = workload(args)
+    flops = passes + fact
+    t0 = time.perf_counter()
+    a = gen()
+    gen_s = time.perf_counter() - t0
+    dev = torch.device("cuda", local)
+    t0 = time.perf_counter()
+    dm = P.DeviceMatrix(a, local)
+    torch.cuda.synchronize()
+    upload_s = time.perf_counter() - t0
+    P.set_omega_cache(True)
+    st = torch.cuda.current_stream(dev)
+    for _ in range(args.warmup):
+        P.powerlu(dm, w.k, w.q_os, v, w.seed)
+    torch.cuda.synchronize()
+
+    # ---- timed region: device-resident inputs and outputs
+    lib = _native.load()
+    clocks = Clocks(local)
+    clocks.start()
+    l0 = lib.rlra_b200_launch_count()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(st)
+    for _ in range(args.steps):
+        f = P.powerlu(dm, w.k, w.q_os, v, w.seed)
+    e1.record(st)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    launches = lib.rlra_b200_launch_count() - l0
+    clk = clocks.stop()
+    value = flops / (ms / 1e3) / 1e9
+
+    # ---- roofline of the dominant kernel (pass GEMMs), CUDA events per launch
+    ops.PROF.records.clear()
+    ops.PROF.on = True
+    for _ in range(max(1, min(args.steps, 3))):
+        P.powerlu(dm, w.k, w.q_os, v, w.seed)
+    summ = ops.PROF.summary()
+    ops.PROF.on = False
+    ops.PROF.records.clear()
+    pass_ms = sum(summ.get(k, (0.0, 0))[0] for k in ("pass_nn", "pass_tn"))
+    pass_cnt = sum(summ.get(k, (0.0, 0))[1] for k in ("pass_nn", "pass_tn"))
+    reps = max(1, min(args.steps, 3))
+    achieved = passes * reps / (pass_ms / 1e3) / 1e12 if pass_ms else None
+    total_prof_ms = sum(t for t, _ in summ.values())
+    traffic = None
+    tpath = os.path.join(REPO, "profiles", "ncu_pass_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get(f"{w.name}_v{v}")
+        except Exception:
+            traffic = None
+    roofline = {"bound": "tensor", "kernel": "dgemm_dmma_kernel (pass products A W / A^T W)",
+                "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                "frac": (achieved / FP64_PEAK_TFLOPS) if achieved else None, "traffic": traffic,
+                "peak_source": FP64_PEAK_SRC,
+                "pass_ms_per_step": pass_ms / reps, "pass_launches_per_step": pass_cnt / reps,
+                "pass_share_of_step": (pass_ms / total_prof_ms) if total_prof_ms else None,
+                "flops_per_unit": "2*m*n*w per pass of width w (SURVEY.md Appendix B)"}
+    if args.breakdown:
+        for k2, (t, c) in sorted(summ.items(), key=lambda kv: -kv[1][0]):
+            print(f"  {k2:32s} {t / reps:9.3f} ms/step  {c / reps:6.1f} calls/step", file=sys.stderr)
+
+    # ---- e2e through the public API with host buffers
+    e2e = None
+    if not args.no_e2e:
+        P.set_omega_cache(False)
+        pinned = torch.empty((w.n, w.m), dtype=torch.float64, pin_memory=True)
+        ah = pinned.numpy().T  # F-ordered m x n view of pinned memory
+        ah[...] = a
+        fh = P.powerlu(ah, w.k, w.q_os, v, w.seed)  # warm
+        ksteps = max(1, min(args.steps, 5))
+        torch.cuda.synchronize()
+        s0 = torch.cuda.Event(enable_timing=True)
+        s1 = torch.cuda.Event(enable_timing=True)
+        s0.record(torch.cuda.current_stream(dev))
+        for _ in range(ksteps):
+            fh = P.powerlu(ah, w.k, w.q_os, v, w.seed)
+        s1.record(torch.cuda.current_stream(dev))
+        torch.cuda.synchronize()
+        e2e_ms = s0.elapsed_time(s1) / ksteps
+        l_ = w.k + w.q_os
+        om_rows = w.m if v % 2 == 0 else w.n
+        h2d = a.nbytes + om_rows * l_ * 8
+        d2h = fh.L.nbytes + fh.U.nbytes + fh.p.nbytes + fh.q.nbytes
+        e2e = {"value": flops / (e2e_ms / 1e3) / 1e9, "unit": "GFLOP/s", "ms_per_step": e2e_ms,
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h), "steps": ksteps,
+               "path": "paper_2002_07138_b200.powerlu(pinned host ndarray) -> NumPy factors"}
+        P.set_omega_cache(True)
+
+    # ---- CPU baseline (reference on the host) + parity of this very call
+    cpu = None
+    parity = None
+    if not args.no_cpu_baseline:
+        cpu, fref = cpu_baseline(a, w, v, flops)
+        from oracle import rlra_oracle as O
+
+        fd = f.to_numpy()
+        parity = {"p_identical": bool(np.array_equal(fd.p, fref.p)),
+                  "q_identical": bool(np.array_equal(fd.q, fref.q))}
+        if w.m * w.n <= 5e8:
+            e_gpu = O.rel_fro_error_factor(a, fd)
+            e_ref = O.rel_fro_error_factor(a, fref)
+            parity.update({"rel_err_gpu": e_gpu, "rel_err_ref": e_ref, "abs_diff": abs(e_gpu - e_ref)})
+
+    line = {
+        "metric": f"PowerLU FP64 GFLOP/s ({w.name}, v={v})", "value": value, "unit": "GFLOP/s",
+        "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "s_per_factorization": ms / 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": desc, "m": w.m, "n": w.n, "k": w.k, "l": w.k + w.q_os, "v": v,
+                   "algorithmic_gflop": flops / 1e9, "pass_gflop": passes / 1e9,
+                   "l2": f"inputs larger than L2 (A = {a.nbytes / 1e9:.2f} GB > 126 MB L2)",
+                   "omega": "host NumPy PCG64 draw (bit-exact rlra.core.gaussian), device-cached for value",
+                   "parallelism": "single GPU"},
+        "gpu_launches": int(launches), "gpu_launches_per_step": launches / args.steps,
+        "clocks": clk, "roofline": roofline, "e2e": e2e, "cpu_baseline": cpu, "parity": parity,
+        "host_prep": {"generate_A_s": gen_s, "upload_A_s": upload_s},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return reference_arm(args)
+    return our_arm(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -48,6 +48,8 @@ extern "C" {
 RLRA_B200_API int rlra_b200_abi_version(void);
 RLRA_B200_API const char* rlra_b200_last_error(void);
 RLRA_B200_API int rlra_b200_device_count(int* out);
+/* number of kernels this library has launched in this process (instrumentation) */
+RLRA_B200_API long long rlra_b200_launch_count(void);
 
 /* ---- host seam: drop-in for backend.plu_inplace(lu, piv) ---------------
  * lu: HOST F-contiguous float64 m x n (ld = m), overwritten with packed L\U;

@@ -1,4 +1,5 @@
 // extern "C" boundary of librlra_b200.so (declared in include/rlra_b200.h).
+#include <atomic>
 #include <cstdarg>
 #include <mutex>
 #include <vector>
@@ -17,6 +18,9 @@ void set_error(const char* fmt, ...) {
   va_end(ap);
 }
 const char* last_error() { return g_err; }
+
+static std::atomic<long long> g_launches{0};
+void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 const DeviceInfo& device_info() {
   static std::mutex mu;
@@ -75,6 +79,8 @@ extern "C" {
 
 int rlra_b200_abi_version(void) { return RLRA_B200_ABI_VERSION; }
 const char* rlra_b200_last_error(void) { return last_error(); }
+
+long long rlra_b200_launch_count(void) { return g_launches.load(); }
 
 int rlra_b200_device_count(int* out) {
   RLRA_CHECK_CUDA(cudaGetDeviceCount(out));
@@ -170,7 +176,7 @@ int rlra_b200_orgqr(const double* a, int64_t lda, int64_t m, int64_t n, double* 
 
 size_t rlra_b200_trsm_workspace(int64_t l, int64_t ncols) {
   (void)l;
-  return (size_t)16 * 32 * (ncols > 0 ? ncols : 1) * sizeof(double);
+  return (size_t)32 * 32 * (ncols > 0 ? ncols : 1) * sizeof(double);
 }
 
 int rlra_b200_trsm_rt(const double* r, int64_t ldr, int64_t l, double* x, int64_t ldx,

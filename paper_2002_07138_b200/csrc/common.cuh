@@ -31,6 +31,15 @@ const char* last_error();
     }                                                                           \
   } while (0)
 
+// Process-wide count of kernels this library launched (bench.py's gpu_launches).
+void note_launch();
+
+#define RLRA_LAUNCHED()                                                          \
+  do {                                                                          \
+    ::rlra::note_launch();                                                      \
+    RLRA_CHECK_CUDA(cudaGetLastError());                                        \
+  } while (0)
+
 struct DeviceInfo {
   int sm_count = 0;
   int max_smem_optin = 0;

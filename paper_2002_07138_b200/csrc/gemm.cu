@@ -248,20 +248,25 @@ struct SplitPlan {
   int64_t ktiles_per_split;
 };
 
-static SplitPlan plan_splits(int64_t tiles, int64_t ktiles, int slots) {
+// Split-K plan from a simple time model (microseconds): waves x k-tiles per
+// split x the DMMA time of one BM x BN x 16 k-tile (64 FMA/clk/SM at ~1.9 GHz),
+// plus the fixed-order reduction (read s partials + write C at ~4 TB/s, and a
+// launch).  Deterministic for a given shape and SM count.
+static SplitPlan plan_splits(int64_t M, int64_t N, int bm, int bn, int64_t tiles, int64_t ktiles,
+                             int slots) {
+  const double t_ktile = (double)bm * bn * 16 / (64.0 * 1.9e3);
   SplitPlan best{1, ktiles};
-  double best_eff = 0.0;
-  for (int s = 1; s <= 16; s++) {
-    if (s > 1 && ktiles / s < 8) break;  // keep >= 8 k-tiles per split
+  double best_t = 1e300;
+  for (int s = 1; s <= 32; s++) {
     int64_t kps = ceil_div(ktiles, s);
+    if (s > 1 && kps < 4) break;
     int64_t real_s = ceil_div(ktiles, kps);
-    int64_t work = tiles * real_s;
-    int64_t waves = ceil_div(work, slots);
-    double eff = (double)work / (double)(waves * slots);
-    // small penalty per split for the partial traffic + reduce launch
-    double score = eff - 0.01 * (real_s - 1);
-    if (score > best_eff + 1e-9) {
-      best_eff = score;
+    if (real_s != s) continue;
+    double waves = (double)ceil_div(tiles * real_s, slots);
+    double t = waves * kps * t_ktile;
+    if (real_s > 1) t += 4.0 + (double)(real_s + 1) * M * N * 8 / 4e6;
+    if (t < best_t * 0.98) {  // prefer fewer splits unless clearly faster
+      best_t = t;
       best = SplitPlan{(int)real_s, kps};
     }
   }
@@ -283,7 +288,7 @@ static int launch_cfg(GemmArgs& a, cudaStream_t st) {
   }
   dim3 grid((unsigned)ceil_div(a.N, Cfg::BN), (unsigned)ceil_div(a.M, Cfg::BM), (unsigned)a.splits);
   kern<<<grid, Cfg::THREADS, Cfg::SMEM_BYTES, st>>>(a);
-  RLRA_CHECK_CUDA(cudaGetLastError());
+  RLRA_LAUNCHED();
   return 0;
 }
 
@@ -303,7 +308,7 @@ size_t gemm_workspace_bytes(int64_t M, int64_t N, int64_t K) {
   if (M <= 0 || N <= 0 || K <= 0) return 0;
   TileChoice tc = choose_tile(N);
   int64_t tiles = ceil_div(M, tc.bm) * ceil_div(N, tc.bn);
-  SplitPlan sp = plan_splits(tiles, ceil_div(K, 16), device_info().sm_count);
+  SplitPlan sp = plan_splits(M, N, tc.bm, tc.bn, tiles, ceil_div(K, 16), device_info().sm_count);
   return sp.splits > 1 ? (size_t)sp.splits * M * N * sizeof(double) : 0;
 }
 
@@ -317,7 +322,8 @@ int gemm(bool ta, bool tb, int64_t M, int64_t N, int64_t K, double alpha, const 
   TileChoice tc = choose_tile(N);
   int64_t tiles = ceil_div(M, tc.bm) * ceil_div(N, tc.bn);
   int64_t ktiles = ceil_div(K, 16);
-  SplitPlan sp = K > 0 ? plan_splits(tiles, ktiles, device_info().sm_count) : SplitPlan{1, 0};
+  SplitPlan sp = K > 0 ? plan_splits(M, N, tc.bm, tc.bn, tiles, ktiles, device_info().sm_count)
+                       : SplitPlan{1, 0};
   GemmArgs a{M, N, K, A, lda, B, ldb, C, ldc, alpha, beta, sp.ktiles_per_split, sp.splits, nullptr};
   if (sp.splits > 1) {
     size_t need = (size_t)sp.splits * M * N * sizeof(double);
@@ -339,7 +345,7 @@ int gemm(bool ta, bool tb, int64_t M, int64_t N, int64_t K, double alpha, const 
     int64_t total = M * N;
     int blocks = (int)std::min<int64_t>(ceil_div(total, 256), (int64_t)device_info().sm_count * 8);
     splitk_reduce_kernel<<<blocks, 256, 0, st>>>(a.partial, sp.splits, M, N, alpha, beta, C, ldc);
-    RLRA_CHECK_CUDA(cudaGetLastError());
+    RLRA_LAUNCHED();
   }
   return 0;
 }

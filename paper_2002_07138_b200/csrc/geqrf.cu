@@ -36,60 +36,69 @@ struct QrPanelArgs {
   unsigned* bar;
 };
 
-__global__ void __launch_bounds__(QR_THREADS) qr_panel_kernel(QrPanelArgs p) {
-  __shared__ double s_red[QR_THREADS / 32][QR_NB + 1];
-  __shared__ double s_w[QR_NB + 1];
+// Householder panel with the CTA's panel rows resident in SHARED MEMORY
+// (column-major s_a[c * R + r]).  Per column: the norm of x = a(j+1:, j) and the
+// dot products x . a_c (c > jj) are computed warp-per-value in a fixed order,
+// published, one grid barrier, a fixed-order cross-CTA sum (deterministic),
+// dlarfg on every CTA redundantly, and the rank-1 update of the own rows.
+template <int THREADS>
+__global__ void __launch_bounds__(THREADS, 1) qr_panel_smem_kernel(QrPanelArgs p) {
+  constexpr int NV = QR_NB + 1;
+  constexpr int NW = THREADS / 32;
+  constexpr int CH = THREADS / NV;  // chunks of the cross-CTA sum
+  extern __shared__ __align__(16) double s_a[];
+  __shared__ double s_chunk[CH][NV];
+  __shared__ double s_w[NV];
   __shared__ double s_row[QR_NB];
   __shared__ double s_scal, s_tau, s_beta;
-  const int G = gridDim.x, b = blockIdx.x;
+  const int G = gridDim.x, b = blockIdx.x, tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
   const int nb = p.nb;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t rb = min(p.m, p.j0 + (int64_t)b * p.rows_per_cta);
-  const int64_t re = min(p.m, rb + p.rows_per_cta);
+  const int64_t R = p.rows_per_cta;
+  const int64_t rb = min(p.m, p.j0 + (int64_t)b * R);
+  const int64_t re = min(p.m, rb + R);
+  const int nr = (int)(re - rb);
+
+  for (int c = 0; c < nb; c++)
+    for (int r = tid; r < nr; r += THREADS) s_a[c * R + r] = p.a[cm(rb + r, p.j0 + c, p.lda)];
+  __syncthreads();
 
   for (int jj = 0; jj < nb; jj++) {
     const int64_t j = p.j0 + jj;
     const int par = jj & 1;
-    // ---- partial sums over own rows i > j: x.x and x.a_c for c > jj
-    {
-      double acc[QR_NB + 1];
+    const int r0 = (int)max((int64_t)0, j + 1 - rb);  // local rows strictly below row j
+    const double* x = s_a + jj * R;
+    // value q: q == 0 -> ||x||^2, q >= 1 -> x . a_{jj+q}
+    const int cnt = nb - jj;
+    for (int q = warp; q < cnt; q += NW) {
+      const double* y = s_a + (q == 0 ? jj : jj + q) * R;
+      double acc = 0.0;
+      for (int r = r0 + lane; r < nr; r += 32) acc += x[r] * y[r];
 #pragma unroll
-      for (int c = 0; c <= QR_NB; c++) acc[c] = 0.0;
-      const double* colj = p.a + cm(0, j, p.lda);
-      for (int64_t i = max(rb, j + 1) + threadIdx.x; i < re; i += blockDim.x) {
-        double x = colj[i];
-        acc[0] += x * x;
-#pragma unroll
-        for (int c = 1; c < QR_NB; c++)
-          if (c > jj && c < nb) acc[c + 1] += x * p.a[cm(i, p.j0 + c, p.lda)];
-      }
-      // fixed-order tree: warp shuffles then warps in index order
-#pragma unroll
-      for (int c = 0; c <= QR_NB; c++) {
-        double v = acc[c];
-#pragma unroll
-        for (int off = 16; off; off >>= 1) v += __shfl_down_sync(0xffffffffu, v, off);
-        if (lane == 0) s_red[warp][c] = v;
-      }
-      __syncthreads();
-      if (threadIdx.x <= QR_NB) {
-        double v = 0.0;
-        for (int w = 0; w < QR_THREADS / 32; w++) v += s_red[w][threadIdx.x];
-        __stcg(p.part + ((int64_t)par * G + b) * (QR_NB + 1) + threadIdx.x, v);
-      }
-      if (j >= rb && j < re && threadIdx.x < nb)
-        __stcg(p.diag + par * QR_NB + threadIdx.x, p.a[cm(j, p.j0 + threadIdx.x, p.lda)]);
+      for (int off = 16; off; off >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, off);
+      if (lane == 0) __stcg(p.part + ((int64_t)par * G + b) * NV + (q == 0 ? 0 : jj + q + 1), acc);
     }
+    if (j >= rb && j < re && tid < nb) __stcg(p.diag + par * QR_NB + tid, s_a[tid * R + (j - rb)]);
     grid_barrier(p.bar, G);
-    // ---- every CTA reduces the partials in the same fixed order
-    if (threadIdx.x <= QR_NB) {
-      double v = 0.0;
-      for (int q = 0; q < G; q++) v += __ldcg(p.part + ((int64_t)par * G + q) * (QR_NB + 1) + threadIdx.x);
-      s_w[threadIdx.x] = v;
+    // ---- fixed-order cross-CTA reduction: CH chunks of CTAs, then chunks in order
+    if (tid < CH * NV) {
+      const int c = tid % NV, ch = tid / NV;
+      if (c == 0 || (c >= jj + 2 && c <= nb)) {
+        const int q0 = (int)(((int64_t)G * ch) / CH), q1 = (int)(((int64_t)G * (ch + 1)) / CH);
+        double v = 0.0;
+        for (int q = q0; q < q1; q++) v += __ldcg(p.part + ((int64_t)par * G + q) * NV + c);
+        s_chunk[ch][c] = v;
+      }
     }
-    if (threadIdx.x < nb) s_row[threadIdx.x] = __ldcg(p.diag + par * QR_NB + threadIdx.x);
+    if (tid < nb) s_row[tid] = __ldcg(p.diag + par * QR_NB + tid);
     __syncthreads();
-    if (threadIdx.x == 0) {
+    if (tid < NV && (tid == 0 || (tid >= jj + 2 && tid <= nb))) {
+      double v = 0.0;
+      for (int ch = 0; ch < CH; ch++) v += s_chunk[ch][tid];
+      s_w[tid] = v;
+    }
+    __syncthreads();
+    if (tid == 0) {
       // dlarfg: alpha = a(j,j), xnorm = ||a(j+1:m, j)||
       const double alpha = s_row[jj];
       const double xnorm = sqrt(s_w[0]);
@@ -108,27 +117,27 @@ __global__ void __launch_bounds__(QR_THREADS) qr_panel_kernel(QrPanelArgs p) {
     __syncthreads();
     const double tau = s_tau, scal = s_scal;
     if (tau != 0.0) {
-      // w_c = v^T a_c = a(j,c) + scal * sum_{i>j} x_i a_ic ; then a_c -= tau * w_c * v
-      if (threadIdx.x < nb && threadIdx.x > jj)
-        s_w[threadIdx.x + 1] = tau * (s_row[threadIdx.x] + scal * s_w[threadIdx.x + 1]);
+      // w_c = tau * v^T a_c = tau * (a(j,c) + scal * x . a_c) ; a_c -= w_c v
+      if (tid < nb && tid > jj) s_w[tid + 1] = tau * (s_row[tid] + scal * s_w[tid + 1]);
       __syncthreads();
-      for (int64_t i = max(rb, j + 1) + threadIdx.x; i < re; i += blockDim.x) {
-        double vi = p.a[cm(i, j, p.lda)] * scal;
-        p.a[cm(i, j, p.lda)] = vi;
-        for (int c = jj + 1; c < nb; c++) {
-          double* e = p.a + cm(i, p.j0 + c, p.lda);
-          *e = *e - s_w[c + 1] * vi;
-        }
+      double* xc = s_a + jj * R;
+      for (int r = r0 + tid; r < nr; r += THREADS) {
+        const double vi = xc[r] * scal;
+        xc[r] = vi;
+        for (int c = jj + 1; c < nb; c++) s_a[c * R + r] -= s_w[c + 1] * vi;
       }
-      if (j >= rb && j < re) {
-        if (threadIdx.x < nb && threadIdx.x > jj)
-          p.a[cm(j, p.j0 + threadIdx.x, p.lda)] = s_row[threadIdx.x] - s_w[threadIdx.x + 1];
-        if (threadIdx.x == 0) p.a[cm(j, j, p.lda)] = s_beta;
+      if (j >= rb && j < re && tid < nb) {
+        if (tid > jj) s_a[tid * R + (j - rb)] = s_row[tid] - s_w[tid + 1];
+        if (tid == jj) s_a[tid * R + (j - rb)] = s_beta;
       }
     }
     __syncthreads();
   }
+  for (int c = 0; c < nb; c++)
+    for (int r = tid; r < nr; r += THREADS) p.a[cm(rb + r, p.j0 + c, p.lda)] = s_a[c * R + r];
 }
+
+static constexpr int QR_PANEL_SMEM_BYTES = 200 * 1024;
 
 // Explicit V (rows j0..m-1 of the panel, unit diagonal, zeros above) for the GEMMs.
 __global__ void qr_make_v_kernel(const double* __restrict__ a, int64_t lda, int64_t j0, int64_t rows,
@@ -179,6 +188,15 @@ __global__ void set_identity_kernel(double* q, int64_t ldq, int64_t m, int64_t n
 // ------------------------------------------------------------------ host side
 static size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
 
+// Panel width for m rows (geqrf and orgqr must agree): 32 while a 32-column
+// panel of every row fits in one CTA's shared memory per SM, else 16 or 8.
+static int64_t qr_rows_cap(int pw) { return (int64_t)(QR_PANEL_SMEM_BYTES / (pw * 8)); }
+static int qr_pw(int64_t m, int sms) {
+  if (m <= sms * qr_rows_cap(32)) return 32;
+  if (m <= sms * qr_rows_cap(16)) return 16;
+  return 8;
+}
+
 struct QrLayout {
   size_t part, diag, bar, vbuf, gram, tblocks, wbuf, w2buf, gemm_ws, total;
 };
@@ -187,7 +205,7 @@ static QrLayout qr_layout(int64_t m, int64_t n, int G) {
   QrLayout L{};
   size_t o = 0;
   auto take = [&](size_t& off, size_t bytes) { off = o; o += al(bytes); };
-  const int64_t npan = ceil_div(n, QR_NB);
+  const int64_t npan = ceil_div(n, 8);  // smallest panel width is 8
   take(L.part, 2 * (size_t)G * (QR_NB + 1) * sizeof(double));
   take(L.diag, 2 * QR_NB * sizeof(double));
   take(L.bar, 2 * sizeof(unsigned));
@@ -196,8 +214,8 @@ static QrLayout qr_layout(int64_t m, int64_t n, int G) {
   take(L.tblocks, (size_t)npan * QR_NB * QR_NB * sizeof(double));
   take(L.wbuf, (size_t)QR_NB * n * sizeof(double));
   take(L.w2buf, (size_t)QR_NB * n * sizeof(double));
-  // split-K partials of the skinny (QR_NB-row) GEMMs: at most 16 splits
-  size_t g = (size_t)16 * QR_NB * std::max<int64_t>(n, QR_NB) * sizeof(double);
+  // split-K partials of the skinny (QR_NB-row) GEMMs: at most 32 splits
+  size_t g = (size_t)32 * QR_NB * std::max<int64_t>(n, QR_NB) * sizeof(double);
   g = std::max(g, gemm_workspace_bytes(m, n, QR_NB));
   take(L.gemm_ws, g);
   L.total = o;
@@ -232,22 +250,39 @@ int geqrf(double* a, int64_t lda, int64_t m, int64_t n, double* tau, void* ws, s
   void* gws = base + L.gemm_ws;
   const size_t gws_bytes = L.total - L.gemm_ws;
   RLRA_CHECK_CUDA(cudaMemsetAsync(bar, 0, 2 * sizeof(unsigned), st));
-  for (int64_t j0 = 0, pidx = 0; j0 < n; j0 += QR_NB, pidx++) {
-    const int nb = (int)std::min<int64_t>(QR_NB, n - j0);
+  const int pw = qr_pw(m, sms);
+  RLRA_REQUIRE(m <= sms * qr_rows_cap(8), "geqrf: m = %lld exceeds the panel capacity", (long long)m);
+  const void* kern = (const void*)qr_panel_smem_kernel<256>;
+  {
+    static unsigned attr_mask = 0;
+    int dev = 0;
+    RLRA_CHECK_CUDA(cudaGetDevice(&dev));
+    if (!(attr_mask & (1u << (dev & 31)))) {
+      RLRA_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           QR_PANEL_SMEM_BYTES));
+      attr_mask |= 1u << (dev & 31);
+    }
+  }
+  for (int64_t j0 = 0, pidx = 0; j0 < n; j0 += pw, pidx++) {
+    const int nb = (int)std::min<int64_t>(pw, n - j0);
     const int64_t rows = m - j0;
-    int G = (int)std::min<int64_t>(sms, std::max<int64_t>(1, ceil_div(rows, 128)));
+    const int64_t target = std::min<int64_t>(qr_rows_cap(pw), 256);
+    int G = (int)std::min<int64_t>(sms, ceil_div(rows, target));
+    G = (int)std::max<int64_t>(G, ceil_div(rows, qr_rows_cap(pw)));
     QrPanelArgs pa{a, lda, m, j0, nb, ceil_div(rows, G),
                    reinterpret_cast<double*>(base + L.part), reinterpret_cast<double*>(base + L.diag),
                    tau, bar};
+    const size_t smem = (size_t)pa.rows_per_cta * nb * sizeof(double);
     void* args[] = {&pa};
-    RLRA_CHECK_CUDA(cudaLaunchCooperativeKernel((void*)qr_panel_kernel, dim3(G), dim3(QR_THREADS), args, 0, st));
+    RLRA_CHECK_CUDA(cudaLaunchCooperativeKernel(kern, dim3(G), dim3(256), args, smem, st));
+    note_launch();
     // explicit V and the T factor of this panel
     qr_make_v_kernel<<<grid_for_q(rows * nb), 256, 0, st>>>(a, lda, j0, rows, nb, vbuf, rows);
-    RLRA_CHECK_CUDA(cudaGetLastError());
+    RLRA_LAUNCHED();
     if (gemm(true, false, nb, nb, rows, 1.0, vbuf, rows, vbuf, rows, 0.0, gram, nb, gws, gws_bytes, st)) return -1;
     double* T = tbl + pidx * QR_NB * QR_NB;
     qr_larft_kernel<<<1, 32, 0, st>>>(gram, nb, tau + j0, T);
-    RLRA_CHECK_CUDA(cudaGetLastError());
+    RLRA_LAUNCHED();
     // trailing update C = (I - V T^T V^T) C on columns [j0+nb, n)
     const int64_t nc = n - j0 - nb;
     if (nc > 0) {
@@ -276,15 +311,16 @@ int orgqr(const double* a, int64_t lda, int64_t m, int64_t n, double* q, int64_t
   void* gws = base + L.gemm_ws;
   const size_t gws_bytes = L.total - L.gemm_ws;
   set_identity_kernel<<<grid_for_q(m * n), 256, 0, st>>>(q, ldq, m, n);
-  RLRA_CHECK_CUDA(cudaGetLastError());
-  const int64_t npan = ceil_div(n, QR_NB);
+  RLRA_LAUNCHED();
+  const int pw = qr_pw(m, sms);
+  const int64_t npan = ceil_div(n, pw);
   for (int64_t pidx = npan - 1; pidx >= 0; pidx--) {
-    const int64_t j0 = pidx * QR_NB;
-    const int nb = (int)std::min<int64_t>(QR_NB, n - j0);
+    const int64_t j0 = pidx * pw;
+    const int nb = (int)std::min<int64_t>(pw, n - j0);
     const int64_t rows = m - j0;
     const int64_t nc = n - j0;
     qr_make_v_kernel<<<grid_for_q(rows * nb), 256, 0, st>>>(a, lda, j0, rows, nb, vbuf, rows);
-    RLRA_CHECK_CUDA(cudaGetLastError());
+    RLRA_LAUNCHED();
     const double* T = tbl + pidx * QR_NB * QR_NB;
     double* Qs = q + cm(j0, j0, ldq);
     // Qs = (I - V T V^T) Qs

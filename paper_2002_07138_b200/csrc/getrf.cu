@@ -20,20 +20,19 @@ namespace rlra {
 
 constexpr int LU_NB = 32;
 constexpr double ZERO_PIVOT_RTOL = 1e-14;  // rlra/_lu_cython.pyx:11
-constexpr int PANEL_THREADS = 256;
 
 struct LuWork {
   double* cand_val;    // [2][G]   local first-max |a| over own rows >= j (-1 if none)
   int64_t* cand_idx;   // [2][G]
   double* cand_cmax;   // [2][G]   local max |a| over own rows in [j0, j)
-  double* cand_row;    // [2][G][NB] panel row of the local argmax
-  double* diag_row;    // [2][NB]  current panel row j
-  double* above;       // [G][NB]  max |a| over rows < j0, per panel column
+  double* cand_row;    // [2][G][LU_NB] panel row of the local argmax
+  double* diag_row;    // [2][LU_NB]  current panel row j
+  double* above;       // [G][LU_NB]  max |a| over rows < j0, per panel column
   unsigned* bar;       // grid barrier (2 words)
   int64_t* ipiv;       // [r] pivot row chosen at step j (== j when no swap)
   int* zflag;          // [r] 1 when step j was a zero pivot
-  int64_t* perm_rows;  // [2*NB] rows touched by the panel's swaps
-  int64_t* perm_src;   // [2*NB] source row of each touched row after the swaps
+  int64_t* perm_rows;  // [2*LU_NB] rows touched by the panel's swaps
+  int64_t* perm_src;   // [2*LU_NB] source row of each touched row after the swaps
   int* perm_cnt;       // [1]
   int64_t* count;      // [1] nonzero diagonal count
 };
@@ -53,10 +52,7 @@ __device__ __forceinline__ bool better(double v, int64_t i, double bv, int64_t b
   return v > bv || (v == bv && i < bi);
 }
 
-// Block-wide reduction of (value, index) with first-max semantics; also max of cmax.
-__device__ void block_argmax(double& v, int64_t& idx, double& cmax, double* s_v, int64_t* s_i,
-                             double* s_c) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+__device__ __forceinline__ void warp_argmax(double& v, int64_t& idx, double& cmax) {
 #pragma unroll
   for (int off = 16; off; off >>= 1) {
     double ov = __shfl_down_sync(0xffffffffu, v, off);
@@ -65,6 +61,14 @@ __device__ void block_argmax(double& v, int64_t& idx, double& cmax, double* s_v,
     if (better(ov, oi, v, idx)) { v = ov; idx = oi; }
     if (oc > cmax) cmax = oc;
   }
+}
+
+// Block-wide (value, index) first-max reduction + max of cmax; result broadcast
+// to every thread through shared memory.
+__device__ void block_argmax_bcast(double& v, int64_t& idx, double& cmax, double* s_v,
+                                   int64_t* s_i, double* s_c) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  warp_argmax(v, idx, cmax);
   if (lane == 0) { s_v[warp] = v; s_i[warp] = idx; s_c[warp] = cmax; }
   __syncthreads();
   if (warp == 0) {
@@ -72,178 +76,190 @@ __device__ void block_argmax(double& v, int64_t& idx, double& cmax, double* s_v,
     v = lane < nw ? s_v[lane] : -1.0;
     idx = lane < nw ? s_i[lane] : INT64_MAX;
     cmax = lane < nw ? s_c[lane] : -1.0;
-#pragma unroll
-    for (int off = 16; off; off >>= 1) {
-      double ov = __shfl_down_sync(0xffffffffu, v, off);
-      long long oi = __shfl_down_sync(0xffffffffu, (long long)idx, off);
-      double oc = __shfl_down_sync(0xffffffffu, cmax, off);
-      if (better(ov, oi, v, idx)) { v = ov; idx = oi; }
-      if (oc > cmax) cmax = oc;
-    }
+    warp_argmax(v, idx, cmax);
+    if (lane == 0) { s_v[32] = v; s_i[32] = idx; s_c[32] = cmax; }
   }
+  __syncthreads();
+  v = s_v[32];
+  idx = s_i[32];
+  cmax = s_c[32];
   __syncthreads();
 }
 
-// Local candidate search for panel column c (step row j) over this CTA's rows,
-// then publish into buffer `par`.
-__device__ void publish_candidates(const PanelArgs& p, int c, int64_t j, int par, int64_t rb,
-                                   int64_t re, double* s_v, int64_t* s_i, double* s_c,
-                                   int64_t* s_best) {
-  const int G = gridDim.x, b = blockIdx.x;
-  const double* col = p.a + cm(0, p.j0 + c, p.lda);
-  double v = -1.0, cmax = -1.0;
-  int64_t idx = INT64_MAX;
-  for (int64_t i = rb + threadIdx.x; i < re; i += blockDim.x) {
-    double x = fabs(col[i]);
-    if (i >= j) {
-      if (better(x, i, v, idx)) { v = x; idx = i; }
-    } else if (x > cmax) {
-      cmax = x;  // rows in [j0, j): already pivoted, part of colmax
-    }
-  }
-  block_argmax(v, idx, cmax, s_v, s_i, s_c);
-  if (threadIdx.x == 0) {
-    __stcg(p.w.cand_val + par * G + b, v);
-    __stcg(p.w.cand_idx + par * G + b, idx);
-    __stcg(p.w.cand_cmax + par * G + b, cmax);
-    *s_best = (v >= 0.0) ? idx : -1;
-  }
-  __syncthreads();
-  const int64_t best = *s_best;
-  if (best >= 0 && threadIdx.x < p.nb)
-    __stcg(p.w.cand_row + ((int64_t)par * G + b) * LU_NB + threadIdx.x,
-           p.a[cm(best, p.j0 + threadIdx.x, p.lda)]);
-  if (j >= rb && j < re && threadIdx.x < p.nb)
-    __stcg(p.w.diag_row + par * LU_NB + threadIdx.x, p.a[cm(j, p.j0 + threadIdx.x, p.lda)]);
-}
-
-__global__ void __launch_bounds__(PANEL_THREADS)
-lu_panel_kernel(PanelArgs p) {
-  __shared__ double s_v[32], s_c[32];
-  __shared__ int64_t s_i[32];
-  __shared__ int64_t s_best;
-  __shared__ double s_above[LU_NB];
-  __shared__ double s_u[LU_NB];
+// Panel factorization with the CTA's panel rows resident in SHARED MEMORY
+// (column-major s_a[c * R + r], R = rows_per_cta), one grid barrier per column.
+// Thread t handles local rows t, t + THREADS, ...; every inner loop has a
+// runtime trip count (nb - jj), so no predicated full-width sweeps.
+template <int PW, int THREADS>
+__global__ void __launch_bounds__(THREADS, 1) lu_panel_smem_kernel(PanelArgs p) {
+  extern __shared__ __align__(16) double s_a[];
+  __shared__ double s_v[33], s_c[33];
+  __shared__ int64_t s_i[33];
+  __shared__ double s_above[PW];
+  __shared__ double s_u[PW];
+  __shared__ double s_part[THREADS / 32][PW];
   __shared__ int64_t s_prow;
   __shared__ int s_zero, s_winner;
 
-  const int G = gridDim.x, b = blockIdx.x;
+  const int G = gridDim.x, b = blockIdx.x, tid = threadIdx.x;
   const int nb = p.nb;
-  const int64_t rb = min(p.m, p.j0 + (int64_t)b * p.rows_per_cta);
-  const int64_t re = min(p.m, rb + p.rows_per_cta);
+  const int64_t R = p.rows_per_cta;
+  const int64_t rb = min(p.m, p.j0 + (int64_t)b * R);
+  const int64_t re = min(p.m, rb + R);
+  const int nr = (int)(re - rb);
 
-  // ---- prologue: colmax contribution of rows < j0 (final U rows), per panel column
+  // ---- prologue 1: max |a| over rows < j0 (final U rows), per panel column
   {
     const int64_t ab = min(p.j0, (int64_t)b * p.above_per_cta);
     const int64_t ae = min(p.j0, ab + p.above_per_cta);
-    for (int c = 0; c < nb; c++) {
-      const double* col = p.a + cm(0, p.j0 + c, p.lda);
-      double cmax = -1.0, v = -1.0;
-      int64_t idx = INT64_MAX;
-      for (int64_t i = ab + threadIdx.x; i < ae; i += blockDim.x) {
-        double x = fabs(col[i]);
-        if (x > cmax) cmax = x;
+    double mx[PW];
+#pragma unroll
+    for (int c = 0; c < PW; c++) mx[c] = -1.0;
+    for (int64_t i = ab + tid; i < ae; i += THREADS)
+#pragma unroll
+      for (int c = 0; c < PW; c++)
+        if (c < nb) {
+          double v = fabs(p.a[cm(i, p.j0 + c, p.lda)]);
+          if (v > mx[c]) mx[c] = v;
+        }
+#pragma unroll
+    for (int c = 0; c < PW; c++) {
+#pragma unroll
+      for (int off = 16; off; off >>= 1) {
+        double o = __shfl_down_sync(0xffffffffu, mx[c], off);
+        if (o > mx[c]) mx[c] = o;
       }
-      block_argmax(v, idx, cmax, s_v, s_i, s_c);
-      if (threadIdx.x == 0) __stcg(p.w.above + (int64_t)b * LU_NB + c, cmax);
+      if ((tid & 31) == 0) s_part[tid >> 5][c] = mx[c];
+    }
+    __syncthreads();
+    if (tid < nb) {
+      double m2 = -1.0;
+      for (int wv = 0; wv < THREADS / 32; wv++)
+        if (s_part[wv][tid] > m2) m2 = s_part[wv][tid];
+      __stcg(p.w.above + (int64_t)b * LU_NB + tid, m2);
     }
   }
-  publish_candidates(p, 0, p.j0, 0, rb, re, s_v, s_i, s_c, &s_best);
+  // ---- prologue 2: stage the panel rows in shared memory (coalesced)
+  for (int c = 0; c < nb; c++)
+    for (int r = tid; r < nr; r += THREADS) s_a[c * R + r] = p.a[cm(rb + r, p.j0 + c, p.lda)];
+  __syncthreads();
+
+  // local candidates of column c (step row j), published into buffer `par`
+  auto publish = [&](int c, int64_t j, int par) {
+    double v = -1.0, cmax = -1.0;
+    int64_t idx = INT64_MAX;
+    const double* col = s_a + c * R;
+    for (int r = tid; r < nr; r += THREADS) {
+      const int64_t i = rb + r;
+      const double xv = fabs(col[r]);
+      if (i >= j) {
+        if (better(xv, i, v, idx)) { v = xv; idx = i; }
+      } else if (xv > cmax) {
+        cmax = xv;  // rows in [j0, j): pivoted rows, part of colmax
+      }
+    }
+    block_argmax_bcast(v, idx, cmax, s_v, s_i, s_c);
+    if (tid == 0) {
+      __stcg(p.w.cand_val + par * G + b, v);
+      __stcg(p.w.cand_idx + par * G + b, idx);
+      __stcg(p.w.cand_cmax + par * G + b, cmax);
+    }
+    if (v >= 0.0 && tid < nb)
+      __stcg(p.w.cand_row + ((int64_t)par * G + b) * LU_NB + tid, s_a[tid * R + (idx - rb)]);
+    if (j >= rb && j < re && tid < nb)
+      __stcg(p.w.diag_row + par * LU_NB + tid, s_a[tid * R + (j - rb)]);
+  };
+
+  publish(0, p.j0, 0);
 
   for (int jj = 0; jj < nb; jj++) {
     const int64_t j = p.j0 + jj;
     const int par = jj & 1;
     grid_barrier(p.w.bar, G);
-    if (jj == 0) {
-      // reduce the rows-above maxima once per panel
-      if (threadIdx.x < nb) {
-        double mx = -1.0;
-        for (int q = 0; q < G; q++) {
-          double x = __ldcg(p.w.above + (int64_t)q * LU_NB + threadIdx.x);
-          if (x > mx) mx = x;
-        }
-        s_above[threadIdx.x] = mx;
+    if (jj == 0 && tid < nb) {
+      double mx = -1.0;
+      for (int q = 0; q < G; q++) {
+        double v = __ldcg(p.w.above + (int64_t)q * LU_NB + tid);
+        if (v > mx) mx = v;
       }
-      __syncthreads();
+      s_above[tid] = mx;
     }
-    // ---- global pivot decision (every CTA redundantly, same order -> same answer)
-    if (threadIdx.x < 32) {
+    // ---- global pivot decision: every CTA reduces the G candidates identically
+    {
       double v = -1.0, cmax = -1.0;
       int64_t idx = INT64_MAX;
-      int who = -1;
-      for (int q = threadIdx.x; q < G; q += 32) {
-        double qv = __ldcg(p.w.cand_val + par * G + q);
-        int64_t qi = __ldcg(p.w.cand_idx + par * G + q);
-        double qc = __ldcg(p.w.cand_cmax + par * G + q);
-        if (qv >= 0.0 && better(qv, qi, v, idx)) { v = qv; idx = qi; who = q; }
-        if (qc > cmax) cmax = qc;
+      if (tid < G) {
+        double qv = __ldcg(p.w.cand_val + par * G + tid);
+        if (qv >= 0.0) { v = qv; idx = __ldcg(p.w.cand_idx + par * G + tid); }
+        cmax = __ldcg(p.w.cand_cmax + par * G + tid);
       }
-#pragma unroll
-      for (int off = 16; off; off >>= 1) {
-        double ov = __shfl_down_sync(0xffffffffu, v, off);
-        long long oi = __shfl_down_sync(0xffffffffu, (long long)idx, off);
-        int ow = __shfl_down_sync(0xffffffffu, who, off);
-        double oc = __shfl_down_sync(0xffffffffu, cmax, off);
-        if (ow >= 0 && better(ov, oi, v, idx)) { v = ov; idx = oi; who = ow; }
-        if (oc > cmax) cmax = oc;
-      }
-      if (threadIdx.x == 0) {
-        // reference: amax = first max over rows >= j (or -1), colmax = amax then
-        // max over rows < j with strict '>' (rlra/_lu_cython.pyx:23-35)
-        double amax = v;  // -1 when every candidate is NaN / absent
-        double colmax = amax;
-        double ab = s_above[jj];
-        if (ab > colmax) colmax = ab;
+      block_argmax_bcast(v, idx, cmax, s_v, s_i, s_c);
+      if (tid == 0) {
+        // reference: amax = first max over rows >= j (or -1); colmax = amax,
+        // then max over rows < j with strict '>' (rlra/_lu_cython.pyx:23-35)
+        double amax = v, colmax = amax;
+        if (s_above[jj] > colmax) colmax = s_above[jj];
         if (cmax > colmax) colmax = cmax;
-        int zero = (amax <= ZERO_PIVOT_RTOL * colmax) ? 1 : 0;
+        const int zero = (amax <= ZERO_PIVOT_RTOL * colmax) ? 1 : 0;
         s_zero = zero;
         s_prow = zero ? j : idx;
-        s_winner = who;
+        // owner CTA of the winning row (rows are split in contiguous chunks)
+        s_winner = zero ? -1 : (int)((idx - p.j0) / R);
         if (b == 0) {
           p.w.zflag[j] = zero;
           p.w.ipiv[j] = zero ? j : idx;
+          if (!zero && idx != j) {
+            int64_t t = p.piv[j];
+            p.piv[j] = p.piv[idx];
+            p.piv[idx] = t;
+          }
         }
       }
+      __syncthreads();
     }
-    __syncthreads();
     const int zero = s_zero;
     const int64_t prow = s_prow;
-    if (zero) {
-      // zero the L column below the diagonal; no swap, no update (:36-39)
-      double* col = p.a + cm(0, j, p.lda);
-      for (int64_t i = max(rb, j + 1) + threadIdx.x; i < re; i += blockDim.x) col[i] = 0.0;
-    } else {
-      if (threadIdx.x < nb)
-        s_u[threadIdx.x] = __ldcg(p.w.cand_row + ((int64_t)par * G + s_winner) * LU_NB + threadIdx.x);
-      __syncthreads();
-      if (prow != j) {
-        if (j >= rb && j < re && threadIdx.x < nb)
-          p.a[cm(j, p.j0 + threadIdx.x, p.lda)] = s_u[threadIdx.x];
-        if (prow >= rb && prow < re && threadIdx.x < nb)
-          p.a[cm(prow, p.j0 + threadIdx.x, p.lda)] = __ldcg(p.w.diag_row + par * LU_NB + threadIdx.x);
-        if (b == 0 && threadIdx.x == 0) {
-          int64_t t = p.piv[j];
-          p.piv[j] = p.piv[prow];
-          p.piv[prow] = t;
+    const int r0 = (int)max((int64_t)0, j + 1 - rb);  // first local row below the diagonal
+    if (!zero) {
+      if (tid < nb) {
+        const double u = __ldcg(p.w.cand_row + ((int64_t)par * G + s_winner) * LU_NB + tid);
+        s_u[tid] = u;
+        // full-row swap inside the panel (:40-48)
+        if (prow != j) {
+          if (j >= rb && j < re) s_a[tid * R + (j - rb)] = u;
+          if (prow >= rb && prow < re)
+            s_a[tid * R + (prow - rb)] = __ldcg(p.w.diag_row + par * LU_NB + tid);
         }
       }
       __syncthreads();
       const double ujj = s_u[jj];
-      for (int64_t i = max(rb, j + 1) + threadIdx.x; i < re; i += blockDim.x) {
-        double l = p.a[cm(i, j, p.lda)] / ujj;  // IEEE division (:49-51)
-        p.a[cm(i, j, p.lda)] = l;
+      double* colj = s_a + jj * R;
+      // same thread->row mapping as publish(): each thread only touches its own
+      // rows, so the fused candidate scan below needs no extra barrier
+      for (int r = tid; r < nr; r += THREADS) {
+        if (r < r0) continue;
+        const double l = colj[r] / ujj;  // IEEE division (:49-51)
+        colj[r] = l;
         for (int c = jj + 1; c < nb; c++) {
-          double* e = p.a + cm(i, p.j0 + c, p.lda);
-          *e = sub_mul_nofma(*e, l, s_u[c]);  // (:52-55)
+          double* e = s_a + c * R + r;
+          *e = sub_mul_nofma(*e, l, s_u[c]);  // multiply then subtract (:52-55)
         }
       }
+    } else {
+      // zero pivot: zero the L column below the diagonal; no swap, no update (:36-39)
+      for (int r = tid; r < nr; r += THREADS)
+        if (r >= r0) s_a[jj * R + r] = 0.0;
     }
-    __syncthreads();
-    if (jj + 1 < nb) publish_candidates(p, jj + 1, j + 1, par ^ 1, rb, re, s_v, s_i, s_c, &s_best);
+    if (jj + 1 < nb) publish(jj + 1, j + 1, par ^ 1);
   }
 
+  // ---- write the panel back (coalesced)
+  __syncthreads();
+  for (int c = 0; c < nb; c++)
+    for (int r = tid; r < nr; r += THREADS) p.a[cm(rb + r, p.j0 + c, p.lda)] = s_a[c * R + r];
+
   // ---- net row permutation of this panel for the columns outside it (CTA 0)
-  if (b == 0 && threadIdx.x == 0) {
+  if (b == 0 && tid == 0) {
     int cnt = 0;
     int64_t* rows = p.w.perm_rows;
     int64_t* src = p.w.perm_src;
@@ -254,10 +270,10 @@ lu_panel_kernel(PanelArgs p) {
       src[cnt] = r;
       return cnt++;
     };
-    for (int jj = 0; jj < nb; jj++) {
-      int64_t j = p.j0 + jj, pr = p.w.ipiv[j];
-      if (pr == j) continue;
-      int ka = find(j), kb = find(pr);
+    for (int q = 0; q < nb; q++) {
+      int64_t jq = p.j0 + q, pr = p.w.ipiv[jq];
+      if (pr == jq) continue;
+      int ka = find(jq), kb = find(pr);
       int64_t t = src[ka];
       src[ka] = src[kb];
       src[kb] = t;
@@ -265,6 +281,8 @@ lu_panel_kernel(PanelArgs p) {
     *p.w.perm_cnt = cnt;
   }
 }
+
+static constexpr int LU_PANEL_SMEM_BYTES = 200 * 1024;
 
 // Apply the panel's net row permutation to columns [0, j0) and [j0+nb, n).
 // One warp per column: gather every touched row, then scatter.
@@ -448,7 +466,7 @@ static LuWork lu_work(void* ws, int64_t r, int G) {
 
 int count_nonzero_diag(const double* a, int64_t lda, int64_t r, int64_t* out_dev, cudaStream_t st) {
   count_nonzero_diag_kernel<<<1, 256, 0, st>>>(a, lda, r, out_dev);
-  RLRA_CHECK_CUDA(cudaGetLastError());
+  RLRA_LAUNCHED();
   return 0;
 }
 
@@ -456,7 +474,7 @@ int fill_iota(int64_t* p, int64_t m, cudaStream_t st) {
   if (m <= 0) return 0;
   int blocks = (int)std::min<int64_t>(ceil_div(m, 256), 4096);
   iota_kernel<<<blocks, 256, 0, st>>>(p, m);
-  RLRA_CHECK_CUDA(cudaGetLastError());
+  RLRA_LAUNCHED();
   return 0;
 }
 
@@ -475,41 +493,77 @@ int getrf(double* a, int64_t lda, int64_t m, int64_t n, int64_t* piv, int64_t* n
                ws_bytes, L.total);
   LuWork w = lu_work(ws, r, sms);
   RLRA_CHECK_CUDA(cudaMemsetAsync(w.bar, 0, 2 * sizeof(unsigned), st));
-  for (int64_t j0 = 0; j0 < r; j0 += LU_NB) {
-    const int nb = (int)std::min<int64_t>(LU_NB, r - j0);
-    const int64_t active = m - j0;
-    // enough rows per CTA to amortise the barrier; at most one CTA per SM
-    int G = (int)std::min<int64_t>(sms, std::max<int64_t>(1, ceil_div(active, 128)));
-    PanelArgs pa;
-    pa.a = a; pa.lda = lda; pa.m = m; pa.n = n; pa.j0 = j0; pa.nb = nb;
-    pa.rows_per_cta = ceil_div(active, G);
-    pa.above_per_cta = std::max<int64_t>(1, ceil_div(j0, G));
-    pa.piv = piv;
-    pa.w = w;
-    void* args[] = {&pa};
-    RLRA_CHECK_CUDA(cudaLaunchCooperativeKernel((void*)lu_panel_kernel, dim3(G), dim3(PANEL_THREADS),
-                                                args, 0, st));
-    if (n > nb) {
-      int64_t ncols = n - nb;
-      int blocks = (int)std::min<int64_t>(ceil_div(ncols * 32, 256), 2048);
-      lu_laswp_kernel<<<blocks, 256, 0, st>>>(a, lda, n, j0, nb, w.perm_rows, w.perm_src, w.perm_cnt);
-      RLRA_CHECK_CUDA(cudaGetLastError());
+  // Panel width: 32 when a 32-column panel of every active row fits in the
+  // shared memory of at most one CTA per SM, else 16 or 8 inner panels inside
+  // 32-wide outer blocks (same rounding sequence per element: still bit-exact).
+  auto rows_cap = [](int pw) { return (int64_t)(LU_PANEL_SMEM_BYTES / (pw * 8)); };
+  const int pw = (m <= sms * rows_cap(32)) ? 32 : (m <= sms * rows_cap(16) ? 16 : 8);
+  RLRA_REQUIRE(m <= sms * rows_cap(8), "getrf: m = %lld exceeds the panel capacity", (long long)m);
+  const void* kern = pw == 32 ? (const void*)lu_panel_smem_kernel<32, 512>
+                   : pw == 16 ? (const void*)lu_panel_smem_kernel<16, 512>
+                              : (const void*)lu_panel_smem_kernel<8, 512>;
+  {
+    static unsigned attr_mask[3] = {0, 0, 0};
+    const int slot = pw == 32 ? 0 : (pw == 16 ? 1 : 2);
+    int dev = 0;
+    RLRA_CHECK_CUDA(cudaGetDevice(&dev));
+    if (!(attr_mask[slot] & (1u << (dev & 31)))) {
+      RLRA_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           LU_PANEL_SMEM_BYTES));
+      attr_mask[slot] |= 1u << (dev & 31);
     }
-    const int64_t c0 = j0 + nb;
-    if (c0 < n) {
-      int blocks = (int)std::min<int64_t>(ceil_div(n - c0, 128), 1024);
-      lu_trsm_kernel<<<blocks, 128, 0, st>>>(a, lda, j0, nb, c0, n, w.zflag);
-      RLRA_CHECK_CUDA(cudaGetLastError());
-      if (c0 < m) {
-        dim3 grid((unsigned)ceil_div(m - c0, UPD_TM), (unsigned)ceil_div(n - c0, UPD_TN));
-        lu_update_kernel<<<grid, 256, 0, st>>>(a, lda, j0, nb, c0, m, c0, n, w.zflag);
-        RLRA_CHECK_CUDA(cudaGetLastError());
+  }
+  for (int64_t jo = 0; jo < r; jo += LU_NB) {
+    const int nbo = (int)std::min<int64_t>(LU_NB, r - jo);
+    const int64_t ce = jo + nbo;
+    for (int64_t j0 = jo; j0 < ce; j0 += pw) {
+      const int nb = (int)std::min<int64_t>(pw, ce - j0);
+      const int64_t active = m - j0;
+      PanelArgs pa;
+      pa.a = a; pa.lda = lda; pa.m = m; pa.n = n; pa.j0 = j0; pa.nb = nb;
+      pa.piv = piv;
+      pa.w = w;
+      // about one row per thread, never more rows than shared memory holds
+      const int64_t target = std::min<int64_t>(rows_cap(pw), 512);
+      int G = (int)std::min<int64_t>(sms, ceil_div(active, target));
+      G = (int)std::max<int64_t>(G, ceil_div(active, rows_cap(pw)));
+      pa.rows_per_cta = ceil_div(active, G);
+      pa.above_per_cta = std::max<int64_t>(1, ceil_div(j0, G));
+      const size_t smem = (size_t)pa.rows_per_cta * nb * sizeof(double);
+      void* args[] = {&pa};
+      RLRA_CHECK_CUDA(cudaLaunchCooperativeKernel(kern, dim3(G), dim3(512), args, smem, st));
+      note_launch();
+      if (n > nb) {
+        int64_t ncols = n - nb;
+        int blocks = (int)std::min<int64_t>(ceil_div(ncols * 32, 256), 2048);
+        lu_laswp_kernel<<<blocks, 256, 0, st>>>(a, lda, n, j0, nb, w.perm_rows, w.perm_src, w.perm_cnt);
+        RLRA_LAUNCHED();
+      }
+      const int64_t c0 = j0 + nb;
+      if (c0 < ce) {  // inner update, restricted to the outer block's columns
+        lu_trsm_kernel<<<1, 128, 0, st>>>(a, lda, j0, nb, c0, ce, w.zflag);
+        RLRA_LAUNCHED();
+        if (c0 < m) {
+          dim3 grid((unsigned)ceil_div(m - c0, UPD_TM), (unsigned)ceil_div(ce - c0, UPD_TN));
+          lu_update_kernel<<<grid, 256, 0, st>>>(a, lda, j0, nb, c0, m, c0, ce, w.zflag);
+          RLRA_LAUNCHED();
+        }
+      }
+    }
+    if (ce < n) {  // outer trailing update with the whole 32-column block
+      int blocks = (int)std::min<int64_t>(ceil_div(n - ce, 128), 1024);
+      lu_trsm_kernel<<<blocks, 128, 0, st>>>(a, lda, jo, nbo, ce, n, w.zflag);
+      RLRA_LAUNCHED();
+      if (ce < m) {
+        dim3 grid((unsigned)ceil_div(m - ce, UPD_TM), (unsigned)ceil_div(n - ce, UPD_TN));
+        lu_update_kernel<<<grid, 256, 0, st>>>(a, lda, jo, nbo, ce, m, ce, n, w.zflag);
+        RLRA_LAUNCHED();
       }
     }
   }
   if (nonzero_diag_dev) {
     count_nonzero_diag_kernel<<<1, 256, 0, st>>>(a, lda, r, nonzero_diag_dev);
-    RLRA_CHECK_CUDA(cudaGetLastError());
+    RLRA_LAUNCHED();
   }
   if (zflag_out && r > 0)
     RLRA_CHECK_CUDA(cudaMemcpyAsync(zflag_out, w.zflag, r * sizeof(int), cudaMemcpyDeviceToDevice, st));

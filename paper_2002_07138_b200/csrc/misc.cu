@@ -98,9 +98,9 @@ int sumsq(const double* a, int64_t lda, int64_t m, int64_t n, double* out_dev, v
   RLRA_REQUIRE(ws_bytes >= (size_t)parts * 2 * sizeof(double), "sumsq: workspace too small");
   double* partial = static_cast<double*>(ws);
   sumsq_partial_kernel<<<(unsigned)parts, 512, 0, st>>>(a, lda, m, n, cpb, partial);
-  RLRA_CHECK_CUDA(cudaGetLastError());
+  RLRA_LAUNCHED();
   dd_finish_kernel<<<1, 1024, 0, st>>>(partial, (int)parts, out_dev);
-  RLRA_CHECK_CUDA(cudaGetLastError());
+  RLRA_LAUNCHED();
   return 0;
 }
 
@@ -120,7 +120,7 @@ int colsumsq(const double* a, int64_t lda, int64_t m, int64_t n, double* out_dev
   if (n <= 0) return 0;
   int blocks = (int)std::min<int64_t>(n, 65535);
   colsumsq_kernel<<<blocks, 256, 0, st>>>(a, lda, m, n, out_dev);
-  RLRA_CHECK_CUDA(cudaGetLastError());
+  RLRA_LAUNCHED();
   return 0;
 }
 
@@ -188,7 +188,7 @@ static int grid_for(int64_t total) {
 int inv_perm(const int64_t* p, int64_t m, int64_t* pinv, cudaStream_t st) {
   if (m <= 0) return 0;
   inv_perm_kernel<<<grid_for(m), 256, 0, st>>>(p, m, pinv);
-  RLRA_CHECK_CUDA(cudaGetLastError());
+  RLRA_LAUNCHED();
   return 0;
 }
 
@@ -197,7 +197,7 @@ int lu_basis(const double* lu, int64_t ldlu, int64_t m, int64_t k, const int64_t
   if (m <= 0 || k <= 0) return 0;
   if (inv_perm(piv, m, pinv_ws, st)) return -1;
   lu_basis_kernel<<<grid_for(m * k), 256, 0, st>>>(lu, ldlu, m, k, pinv_ws, w, ldw);
-  RLRA_CHECK_CUDA(cudaGetLastError());
+  RLRA_LAUNCHED();
   return 0;
 }
 
@@ -205,7 +205,7 @@ int extract_l(const double* lu, int64_t ldlu, int64_t m, int64_t k, double* l, i
               cudaStream_t st) {
   if (m <= 0 || k <= 0) return 0;
   extract_l_kernel<<<grid_for(m * k), 256, 0, st>>>(lu, ldlu, m, k, l, ldl);
-  RLRA_CHECK_CUDA(cudaGetLastError());
+  RLRA_LAUNCHED();
   return 0;
 }
 
@@ -213,7 +213,7 @@ int extract_u(const double* lu, int64_t ldlu, int64_t k, int64_t n, double* u, i
               cudaStream_t st) {
   if (k <= 0 || n <= 0) return 0;
   extract_u_kernel<<<grid_for(k * n), 256, 0, st>>>(lu, ldlu, k, n, u, ldu);
-  RLRA_CHECK_CUDA(cudaGetLastError());
+  RLRA_LAUNCHED();
   return 0;
 }
 
@@ -222,7 +222,7 @@ int transpose(const double* in, int64_t ldi, int64_t m, int64_t n, double* out, 
   if (m <= 0 || n <= 0) return 0;
   dim3 grid((unsigned)ceil_div(m, 32), (unsigned)ceil_div(n, 32));
   transpose_kernel<<<grid, dim3(32, 8), 0, st>>>(in, ldi, m, n, out, ldo);
-  RLRA_CHECK_CUDA(cudaGetLastError());
+  RLRA_LAUNCHED();
   return 0;
 }
 

@@ -57,7 +57,7 @@ int trsm_rt(const double* r, int64_t ldr, int64_t l, double* x, int64_t ldx, int
     }
     int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(ncols, 64), 1024));
     trsm_rt_diag_kernel<<<blocks, 64, 0, st>>>(r, ldr, i0, nb, x, ldx, ncols);
-    RLRA_CHECK_CUDA(cudaGetLastError());
+    RLRA_LAUNCHED();
   }
   return 0;
 }
@@ -79,7 +79,7 @@ __global__ void diag_absmin_kernel(const double* a, int64_t lda, int64_t r, doub
 
 int diag_absmin(const double* a, int64_t lda, int64_t r, double* out_dev, cudaStream_t st) {
   diag_absmin_kernel<<<1, 256, 0, st>>>(a, lda, r, out_dev);
-  RLRA_CHECK_CUDA(cudaGetLastError());
+  RLRA_LAUNCHED();
   return 0;
 }
 

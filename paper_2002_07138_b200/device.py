@@ -50,11 +50,15 @@ class DeviceMatrix:
 
     def matmul(self, x):
         """A @ X, one pass over A (rlra/accessors.py:27-28)."""
-        return ops.matmul(self._a, _dev(x, self.device))
+        x = _dev(x, self.device)
+        with ops.label("pass_nn"):
+            return ops.matmul(self._a, x)
 
     def rmatmul(self, x):
         """A^T @ X, one pass over A (rlra/accessors.py:30-31)."""
-        return ops.matmul(self._a, _dev(x, self.device), ta=True)
+        x = _dev(x, self.device)
+        with ops.label("pass_tn"):
+            return ops.matmul(self._a, x, ta=True)
 
     def fro_norm_sq_device(self):
         """Compensated ||A||_F^2 as a device scalar (no host sync)."""

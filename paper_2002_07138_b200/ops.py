@@ -18,6 +18,57 @@ F64 = torch.float64
 I64 = torch.int64
 
 
+class _Profiler:
+    """Optional CUDA-event timing of every C-ABI call (bench.py breakdown and
+    the live roofline of the pass GEMMs).  Off by default: zero overhead."""
+
+    def __init__(self):
+        self.on = False
+        self.records = []  # (label, start_event, end_event)
+        self.label = None
+
+    def call(self, name, args, dev):
+        if not self.on:
+            return _native.call(name, *args)
+        st = torch.cuda.current_stream(dev)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        rc = _native.call(name, *args)
+        e1.record(st)
+        self.records.append((self.label or name, e0, e1))
+        return rc
+
+    def summary(self):
+        torch.cuda.synchronize()
+        out = {}
+        for lab, e0, e1 in self.records:
+            ms = e0.elapsed_time(e1)
+            tot, cnt = out.get(lab, (0.0, 0))
+            out[lab] = (tot + ms, cnt + 1)
+        return out
+
+
+PROF = _Profiler()
+
+
+class label:
+    """Tag the C-ABI calls issued inside the block (profiling only)."""
+
+    def __init__(self, name):
+        self.name = name
+
+    def __enter__(self):
+        self.prev, PROF.label = PROF.label, self.name
+
+    def __exit__(self, *exc):
+        PROF.label = self.prev
+
+
+def _call(name, dev, *args):
+    return PROF.call(name, args, dev)
+
+
 def _stream(dev):
     return ctypes_ptr(torch.cuda.current_stream(dev).cuda_stream)
 
@@ -99,7 +150,7 @@ def gemm(a, b, c, *, ta=False, tb=False, alpha=1.0, beta=0.0):
         raise ValueError(f"gemm shape mismatch: op(a) {tuple(a.shape)} ta={ta}, op(b) {tuple(b.shape)} tb={tb}, c {tuple(c.shape)}")
     wsb = _native.query("rlra_b200_gemm_workspace", m, n, k)
     ws = torch.empty(max(wsb, 8), dtype=torch.uint8, device=c.device) if wsb else None
-    _native.call("rlra_b200_dgemm", int(ta), int(tb), m, n, k, float(alpha), ptr(a), ld_of(a),
+    _call("rlra_b200_dgemm", c.device, int(ta), int(tb), m, n, k, float(alpha), ptr(a), ld_of(a),
                  ptr(b), ld_of(b), float(beta), ptr(c), ld_of(c), ptr(ws), wsb,
                  _stream(c.device))
     return c
@@ -115,7 +166,7 @@ def matmul(a, b, *, ta=False, tb=False):
 def iota(m, device):
     p = torch.empty(max(int(m), 1), dtype=I64, device=device)[: int(m)]
     if m:
-        _native.call("rlra_b200_iota", ptr(p), int(m), _stream(device))
+        _call("rlra_b200_iota", device, ptr(p), int(m), _stream(device))
     return p
 
 
@@ -129,7 +180,7 @@ def getrf_(a, piv=None):
     cnt = torch.zeros(1, dtype=I64, device=a.device)
     wsb = _native.query("rlra_b200_getrf_workspace", m, n)
     ws = torch.empty(max(wsb, 8), dtype=torch.uint8, device=a.device)
-    _native.call("rlra_b200_getrf", ptr(a), ld_of(a), m, n, ptr(piv), ptr(cnt), ptr(ws), wsb,
+    _call("rlra_b200_getrf", a.device, ptr(a), ld_of(a), m, n, ptr(piv), ptr(cnt), ptr(ws), wsb,
                  _stream(a.device))
     return piv, cnt
 
@@ -140,7 +191,7 @@ def lu_basis(lu, piv, k=None):
     k = min(m, n) if k is None else k
     w = fmat(m, k, lu.device)
     pinv = torch.empty(max(m, 1), dtype=I64, device=lu.device)
-    _native.call("rlra_b200_lu_basis", ptr(lu), ld_of(lu), m, k, ptr(piv), ptr(pinv), ptr(w),
+    _call("rlra_b200_lu_basis", lu.device, ptr(lu), ld_of(lu), m, k, ptr(piv), ptr(pinv), ptr(w),
                  ld_of(w), _stream(lu.device))
     return w
 
@@ -150,7 +201,7 @@ def lu_extract(lu, want_l=True, want_u=True):
     r = min(m, n)
     l = fmat(m, r, lu.device) if want_l else None
     u = fmat(r, n, lu.device) if want_u else None
-    _native.call("rlra_b200_lu_extract", ptr(lu), ld_of(lu), m, n, ptr(l),
+    _call("rlra_b200_lu_extract", lu.device, ptr(lu), ld_of(lu), m, n, ptr(l),
                  ld_of(l) if l is not None else 1, ptr(u), ld_of(u) if u is not None else 1,
                  _stream(lu.device))
     return l, u
@@ -159,7 +210,7 @@ def lu_extract(lu, want_l=True, want_u=True):
 def count_nonzero_diag(a, r=None):
     r = min(a.shape) if r is None else r
     cnt = torch.zeros(1, dtype=I64, device=a.device)
-    _native.call("rlra_b200_count_nonzero_diag", ptr(a), ld_of(a), r, ptr(cnt), _stream(a.device))
+    _call("rlra_b200_count_nonzero_diag", a.device, ptr(a), ld_of(a), r, ptr(cnt), _stream(a.device))
     return cnt
 
 
@@ -174,13 +225,13 @@ class QR:
         self.tau = torch.empty(max(n, 1), dtype=F64, device=a.device)
         self.wsb = _native.query("rlra_b200_geqrf_workspace", m, n)
         self.ws = torch.empty(max(self.wsb, 8), dtype=torch.uint8, device=a.device)
-        _native.call("rlra_b200_geqrf", ptr(a), ld_of(a), m, n, ptr(self.tau), ptr(self.ws),
+        _call("rlra_b200_geqrf", a.device, ptr(a), ld_of(a), m, n, ptr(self.tau), ptr(self.ws),
                      self.wsb, _stream(a.device))
 
     def q(self):
         m, n = self.a.shape
         q = fmat(m, n, self.a.device)
-        _native.call("rlra_b200_orgqr", ptr(self.a), ld_of(self.a), m, n, ptr(q), ld_of(q),
+        _call("rlra_b200_orgqr", self.a.device, ptr(self.a), ld_of(self.a), m, n, ptr(q), ld_of(q),
                      ptr(self.ws), self.wsb, _stream(self.a.device))
         return q
 
@@ -195,14 +246,14 @@ def trsm_rt_(r, x):
     ncols = x.shape[1]
     wsb = _native.query("rlra_b200_trsm_workspace", l, ncols)
     ws = torch.empty(max(wsb, 8), dtype=torch.uint8, device=x.device)
-    _native.call("rlra_b200_trsm_rt", ptr(r), ld_of(r), l, ptr(x), ld_of(x), ncols, ptr(ws), wsb,
+    _call("rlra_b200_trsm_rt", x.device, ptr(r), ld_of(r), l, ptr(x), ld_of(x), ncols, ptr(ws), wsb,
                  _stream(x.device))
     return x
 
 
 def diag_absmin(a):
     out = torch.empty(1, dtype=F64, device=a.device)
-    _native.call("rlra_b200_diag_absmin", ptr(a), ld_of(a), min(a.shape), ptr(out), _stream(a.device))
+    _call("rlra_b200_diag_absmin", a.device, ptr(a), ld_of(a), min(a.shape), ptr(out), _stream(a.device))
     return out
 
 
@@ -212,19 +263,19 @@ def sumsq(a):
     out = torch.zeros(1, dtype=F64, device=a.device)
     wsb = _native.query("rlra_b200_sumsq_workspace", m, n)
     ws = torch.empty(max(wsb, 8), dtype=torch.uint8, device=a.device)
-    _native.call("rlra_b200_sumsq", ptr(a), ld_of(a), m, n, ptr(out), ptr(ws), wsb, _stream(a.device))
+    _call("rlra_b200_sumsq", a.device, ptr(a), ld_of(a), m, n, ptr(out), ptr(ws), wsb, _stream(a.device))
     return out
 
 
 def colsumsq(a):
     m, n = a.shape
     out = torch.empty(max(n, 1), dtype=F64, device=a.device)[:n]
-    _native.call("rlra_b200_colsumsq", ptr(a), ld_of(a), m, n, ptr(out), _stream(a.device))
+    _call("rlra_b200_colsumsq", a.device, ptr(a), ld_of(a), m, n, ptr(out), _stream(a.device))
     return out
 
 
 def transpose(a):
     m, n = a.shape
     out = fmat(n, m, a.device)
-    _native.call("rlra_b200_transpose", ptr(a), ld_of(a), m, n, ptr(out), ld_of(out), _stream(a.device))
+    _call("rlra_b200_transpose", a.device, ptr(a), ld_of(a), m, n, ptr(out), ld_of(out), _stream(a.device))
     return out

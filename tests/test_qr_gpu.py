@@ -20,7 +20,8 @@ def dev_qr(x):
     return q, r, cnt
 
 
-@pytest.mark.parametrize("m,n", [(30, 8), (2000, 60), (10000, 220), (3000, 97), (512, 512), (33, 33)])
+@pytest.mark.parametrize("m,n", [(30, 8), (2000, 60), (10000, 220), (3000, 97), (512, 512), (33, 33),
+                                 (50000, 72), (120000, 40), (160000, 20)])
 def test_qr_matches_lapack(cuda_dev, m, n):
     x = np.random.default_rng(m + n).standard_normal((m, n))
     q, r, cnt = dev_qr(x)
