@@ -86,4 +86,21 @@ __device__ __forceinline__ void grid_barrier(unsigned int* bar, unsigned int nbl
   __syncthreads();
 }
 
+// Monotonic grid barrier: every CTA adds 1 (release), then waits until the
+// counter reaches `target` = (barriers so far) * gridDim (acquire).  The host
+// zeroes the counter once per factorization and tracks the running base.
+__device__ __forceinline__ void grid_barrier_mono(unsigned int* ctr, unsigned int target) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;\n" ::"l"(ctr) : "memory");
+    unsigned int v;
+    while (true) {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(ctr) : "memory");
+      if ((int)(v - target) >= 0) break;
+      __nanosleep(32);
+    }
+  }
+  __syncthreads();
+}
+
 }  // namespace rlra

@@ -304,12 +304,32 @@ static int launch_tile(int which, GemmArgs& a, cudaStream_t st) {
 
 static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
+bool tma_gemm_eligible(bool ta, bool tb, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda,
+                       const double* B, int64_t ldb);
+size_t tma_gemm_workspace_bytes(int64_t M, int64_t N, int64_t K);
+int tma_gemm(bool ta, int64_t M, int64_t N, int64_t K, double alpha, const double* A, int64_t lda,
+             const double* B, int64_t ldb, double beta, double* C, int64_t ldc, void* ws, size_t ws_bytes,
+             cudaStream_t st);
+
+int splitk_reduce(const double* partial, int splits, int64_t M, int64_t N, double alpha, double beta,
+                  double* C, int64_t ldc, cudaStream_t st) {
+  int64_t total = M * N;
+  int blocks = (int)std::min<int64_t>(ceil_div(total, 256), (int64_t)device_info().sm_count * 8);
+  splitk_reduce_kernel<<<blocks, 256, 0, st>>>(partial, splits, M, N, alpha, beta, C, ldc);
+  RLRA_LAUNCHED();
+  return 0;
+}
+
+// Upper bound over both mainloops (the TMA one needs aligned pointers, which a
+// size query cannot see).
 size_t gemm_workspace_bytes(int64_t M, int64_t N, int64_t K) {
   if (M <= 0 || N <= 0 || K <= 0) return 0;
+  const size_t tma = tma_gemm_workspace_bytes(M, N, K);
   TileChoice tc = choose_tile(N);
   int64_t tiles = ceil_div(M, tc.bm) * ceil_div(N, tc.bn);
   SplitPlan sp = plan_splits(M, N, tc.bm, tc.bn, tiles, ceil_div(K, 16), device_info().sm_count);
-  return sp.splits > 1 ? (size_t)sp.splits * M * N * sizeof(double) : 0;
+  const size_t legacy = sp.splits > 1 ? (size_t)sp.splits * M * N * sizeof(double) : 0;
+  return std::max(tma, legacy);
 }
 
 int gemm(bool ta, bool tb, int64_t M, int64_t N, int64_t K, double alpha, const double* A,
@@ -318,6 +338,8 @@ int gemm(bool ta, bool tb, int64_t M, int64_t N, int64_t K, double alpha, const 
   RLRA_REQUIRE(M >= 0 && N >= 0 && K >= 0, "gemm: negative dimension");
   if (M == 0 || N == 0) return 0;
   RLRA_REQUIRE(ldc >= M, "gemm: ldc < M");
+  if (tma_gemm_eligible(ta, tb, M, N, K, A, lda, B, ldb))
+    return tma_gemm(ta, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, ws, ws_bytes, st);
   // K == 0 runs one split with no k-tiles: the epilogue writes alpha*0 + beta*C.
   TileChoice tc = choose_tile(N);
   int64_t tiles = ceil_div(M, tc.bm) * ceil_div(N, tc.bn);
@@ -341,12 +363,7 @@ int gemm(bool ta, bool tb, int64_t M, int64_t N, int64_t K, double alpha, const 
   else if (!ta && tb) rc = vec ? launch_tile<false, true, 2>(tc.which, a, st) : launch_tile<false, true, 1>(tc.which, a, st);
   else rc = vec ? launch_tile<true, true, 2>(tc.which, a, st) : launch_tile<true, true, 1>(tc.which, a, st);
   if (rc) return rc;
-  if (sp.splits > 1) {
-    int64_t total = M * N;
-    int blocks = (int)std::min<int64_t>(ceil_div(total, 256), (int64_t)device_info().sm_count * 8);
-    splitk_reduce_kernel<<<blocks, 256, 0, st>>>(a.partial, sp.splits, M, N, alpha, beta, C, ldc);
-    RLRA_LAUNCHED();
-  }
+  if (sp.splits > 1) return splitk_reduce(a.partial, sp.splits, M, N, alpha, beta, C, ldc, st);
   return 0;
 }
 

@@ -34,6 +34,7 @@ struct QrPanelArgs {
   double* diag;      // [2][QR_NB] row j of the panel
   double* tau;       // [n]
   unsigned* bar;
+  unsigned bar_base;  // monotonic grid-barrier counter at kernel entry
 };
 
 // Householder panel with the CTA's panel rows resident in SHARED MEMORY
@@ -79,7 +80,7 @@ __global__ void __launch_bounds__(THREADS, 1) qr_panel_smem_kernel(QrPanelArgs p
       if (lane == 0) __stcg(p.part + ((int64_t)par * G + b) * NV + (q == 0 ? 0 : jj + q + 1), acc);
     }
     if (j >= rb && j < re && tid < nb) __stcg(p.diag + par * QR_NB + tid, s_a[tid * R + (j - rb)]);
-    grid_barrier(p.bar, G);
+    grid_barrier_mono(p.bar, p.bar_base + (unsigned)G * (jj + 1));
     // ---- fixed-order cross-CTA reduction: CH chunks of CTAs, then chunks in order
     if (tid < CH * NV) {
       const int c = tid % NV, ch = tid / NV;
@@ -263,6 +264,7 @@ int geqrf(double* a, int64_t lda, int64_t m, int64_t n, double* tau, void* ws, s
       attr_mask |= 1u << (dev & 31);
     }
   }
+  unsigned bar_base = 0;
   for (int64_t j0 = 0, pidx = 0; j0 < n; j0 += pw, pidx++) {
     const int nb = (int)std::min<int64_t>(pw, n - j0);
     const int64_t rows = m - j0;
@@ -271,7 +273,8 @@ int geqrf(double* a, int64_t lda, int64_t m, int64_t n, double* tau, void* ws, s
     G = (int)std::max<int64_t>(G, ceil_div(rows, qr_rows_cap(pw)));
     QrPanelArgs pa{a, lda, m, j0, nb, ceil_div(rows, G),
                    reinterpret_cast<double*>(base + L.part), reinterpret_cast<double*>(base + L.diag),
-                   tau, bar};
+                   tau, bar, bar_base};
+    bar_base += (unsigned)G * nb;
     const size_t smem = (size_t)pa.rows_per_cta * nb * sizeof(double);
     void* args[] = {&pa};
     RLRA_CHECK_CUDA(cudaLaunchCooperativeKernel(kern, dim3(G), dim3(256), args, smem, st));

@@ -14,6 +14,12 @@
 //   * pivot = first maximum (smallest row index among equal |values|).
 // Row swaps are full-row (the reference swaps all n columns, :40-48); columns
 // outside the panel are permuted after the panel by a gather/scatter kernel.
+#include <cooperative_groups.h>
+
+#include <mutex>
+#include <set>
+#include <utility>
+
 #include "common.cuh"
 
 namespace rlra {
@@ -45,6 +51,7 @@ struct PanelArgs {
   int64_t above_per_cta;  // rows [0, j0) split in contiguous chunks
   int64_t* piv;
   LuWork w;
+  unsigned bar_base;  // monotonic grid-barrier counter value at kernel entry
 };
 
 // strict-greater first-max merge: (v,i) replaces best when v > best or (v == best && i < besti)
@@ -86,6 +93,41 @@ __device__ void block_argmax_bcast(double& v, int64_t& idx, double& cmax, double
   __syncthreads();
 }
 
+// Net row permutation of one panel's swap sequence (j <-> ipiv[j], j ascending),
+// as (touched row, source row) pairs for the laswp gather/scatter.  Run by one
+// warp with the lookups done lane-parallel in shared memory (<= 2*LU_NB rows).
+__device__ int build_panel_perm(int64_t j0, int nb, const int64_t* s_ipiv, int64_t* s_rows,
+                                int64_t* s_src, const LuWork& w) {
+  const int lane = threadIdx.x & 31;
+  int cnt = 0;
+  auto find = [&](int64_t r) -> int {
+    bool hit0 = lane < cnt && s_rows[lane] == r;
+    bool hit1 = lane + 32 < cnt && s_rows[lane + 32] == r;
+    unsigned b0 = __ballot_sync(0xffffffffu, hit0), b1 = __ballot_sync(0xffffffffu, hit1);
+    if (b0) return __ffs(b0) - 1;
+    if (b1) return 32 + __ffs(b1) - 1;
+    if (lane == 0) { s_rows[cnt] = r; s_src[cnt] = r; }
+    __syncwarp();
+    return cnt++;
+  };
+  for (int q = 0; q < nb; q++) {
+    const int64_t jq = j0 + q, pr = s_ipiv[q];
+    if (pr == jq) continue;
+    const int ka = find(jq), kb = find(pr);
+    if (lane == 0) {
+      int64_t t = s_src[ka];
+      s_src[ka] = s_src[kb];
+      s_src[kb] = t;
+    }
+    __syncwarp();
+  }
+  if (lane < cnt) { w.perm_rows[lane] = s_rows[lane]; w.perm_src[lane] = s_src[lane]; }
+  if (lane + 32 < cnt) { w.perm_rows[lane + 32] = s_rows[lane + 32]; w.perm_src[lane + 32] = s_src[lane + 32]; }
+  if (lane == 0) *w.perm_cnt = cnt;
+  __syncwarp();
+  return cnt;
+}
+
 // Panel factorization with the CTA's panel rows resident in SHARED MEMORY
 // (column-major s_a[c * R + r], R = rows_per_cta), one grid barrier per column.
 // Thread t handles local rows t, t + THREADS, ...; every inner loop has a
@@ -100,6 +142,7 @@ __global__ void __launch_bounds__(THREADS, 1) lu_panel_smem_kernel(PanelArgs p) 
   __shared__ double s_part[THREADS / 32][PW];
   __shared__ int64_t s_prow;
   __shared__ int s_zero, s_winner;
+  __shared__ int64_t s_ipiv[PW], s_prow_rows[2 * PW], s_prow_src[2 * PW];
 
   const int G = gridDim.x, b = blockIdx.x, tid = threadIdx.x;
   const int nb = p.nb;
@@ -175,7 +218,7 @@ __global__ void __launch_bounds__(THREADS, 1) lu_panel_smem_kernel(PanelArgs p) 
   for (int jj = 0; jj < nb; jj++) {
     const int64_t j = p.j0 + jj;
     const int par = jj & 1;
-    grid_barrier(p.w.bar, G);
+    grid_barrier_mono(p.w.bar, p.bar_base + (unsigned)G * (jj + 1));
     if (jj == 0 && tid < nb) {
       double mx = -1.0;
       for (int q = 0; q < G; q++) {
@@ -203,6 +246,7 @@ __global__ void __launch_bounds__(THREADS, 1) lu_panel_smem_kernel(PanelArgs p) 
         const int zero = (amax <= ZERO_PIVOT_RTOL * colmax) ? 1 : 0;
         s_zero = zero;
         s_prow = zero ? j : idx;
+        s_ipiv[jj] = zero ? j : idx;
         // owner CTA of the winning row (rows are split in contiguous chunks)
         s_winner = zero ? -1 : (int)((idx - p.j0) / R);
         if (b == 0) {
@@ -258,28 +302,290 @@ __global__ void __launch_bounds__(THREADS, 1) lu_panel_smem_kernel(PanelArgs p) 
   for (int c = 0; c < nb; c++)
     for (int r = tid; r < nr; r += THREADS) p.a[cm(rb + r, p.j0 + c, p.lda)] = s_a[c * R + r];
 
-  // ---- net row permutation of this panel for the columns outside it (CTA 0)
-  if (b == 0 && tid == 0) {
-    int cnt = 0;
-    int64_t* rows = p.w.perm_rows;
-    int64_t* src = p.w.perm_src;
-    auto find = [&](int64_t r) {
-      for (int k = 0; k < cnt; k++)
-        if (rows[k] == r) return k;
-      rows[cnt] = r;
-      src[cnt] = r;
-      return cnt++;
-    };
-    for (int q = 0; q < nb; q++) {
-      int64_t jq = p.j0 + q, pr = p.w.ipiv[jq];
-      if (pr == jq) continue;
-      int ka = find(jq), kb = find(pr);
-      int64_t t = src[ka];
-      src[ka] = src[kb];
-      src[kb] = t;
-    }
-    *p.w.perm_cnt = cnt;
+  if (b == 0 && tid < 32) build_panel_perm(p.j0, nb, s_ipiv, s_prow_rows, s_prow_src, p.w);
+}
+
+// (value, index, cmax) first-max reduction over the whole block; every thread
+// ends with the result.  Two shuffle rounds, ONE __syncthreads; callers must
+// separate consecutive uses of the staging arrays by another block barrier.
+__device__ __forceinline__ void block_argmax_all(double& v, int64_t& idx, double& cmax, double* s_v,
+                                                 int64_t* s_i, double* s_c) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  warp_argmax(v, idx, cmax);
+  if (lane == 0) { s_v[warp] = v; s_i[warp] = idx; s_c[warp] = cmax; }
+  __syncthreads();
+  const int nw = blockDim.x >> 5;
+  v = lane < nw ? s_v[lane] : -1.0;
+  idx = lane < nw ? s_i[lane] : INT64_MAX;
+  cmax = lane < nw ? s_c[lane] : -1.0;
+  warp_argmax(v, idx, cmax);
+  v = __shfl_sync(0xffffffffu, v, 0);
+  idx = __shfl_sync(0xffffffffu, (long long)idx, 0);
+  cmax = __shfl_sync(0xffffffffu, cmax, 0);
+}
+
+// ---------------------------------------------------------------------------
+// Cluster-resident panel (B200 thread-block cluster, up to 16 CTAs on one GPC).
+// The panel rows live in the CTAs' shared memory.  Each column step, every CTA
+// PUSHES its pivot candidate record (|value|, row, colmax, full panel row) into
+// every peer's shared memory with a DSMEM bulk copy (cp.async.bulk, TMA engine)
+// that completes on the peer's local mbarrier; the owner of the next diagonal
+// row pushes that row the same way.  A CTA then only waits on its OWN
+// mbarrier and decides from local data: no cluster-wide barrier, no
+// MEMBAR.GPU, no remote loads on the critical path.  Records are double
+// buffered by step parity; the wait for step s+1's records is what makes it
+// safe to overwrite step s's slots (every peer has then finished reading).
+template <int PW>
+struct LuRec {
+  double val, idx, cmax, pad;  // idx is an int64 stored bit-for-bit
+  double row[PW];
+};
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ unsigned mapa_u32(unsigned addr, int rank) {
+  unsigned r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait_parity(uint64_t* bar, unsigned parity) {
+  const unsigned a = smem_u32(bar);
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(a), "r"(parity)
+      : "memory");
+}
+// local smem [src, src+bytes) -> peer smem dst (shared::cluster), completing
+// `bytes` of transactions on the peer's mbarrier
+__device__ __forceinline__ void bulk_push(unsigned dst_cluster, const void* src, unsigned bytes,
+                                          unsigned mbar_cluster) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+          dst_cluster),
+      "r"(smem_u32(src)), "r"(bytes), "r"(mbar_cluster)
+      : "memory");
+}
+
+template <int PW, int THREADS>
+__global__ void __launch_bounds__(THREADS, 1) lu_panel_cluster_kernel(PanelArgs p) {
+  namespace cg = cooperative_groups;
+  constexpr int MAXCS = 16;
+  cg::cluster_group cluster = cg::this_cluster();
+  extern __shared__ __align__(16) double s_a[];
+  __shared__ double s_v[32], s_c[32];
+  __shared__ int64_t s_i[32];
+  __shared__ __align__(16) LuRec<PW> recv[2][MAXCS];  // records from every peer
+  __shared__ __align__(16) double recv_diag[2][PW];   // current diagonal row
+  __shared__ __align__(16) LuRec<PW> mine[2];         // my outgoing record
+  __shared__ __align__(16) double mine_diag[2][PW];
+  __shared__ __align__(8) uint64_t mbar[2];
+  __shared__ double c_above[PW];
+  __shared__ double s_u[PW];
+  __shared__ double s_part[THREADS / 32][PW];
+  __shared__ int64_t s_prow;
+  __shared__ int s_zero;
+  __shared__ int64_t s_ipiv[PW], s_prow_rows[2 * PW], s_prow_src[2 * PW];
+  __shared__ int s_zf[PW];
+
+  const int CS = (int)cluster.num_blocks(), b = (int)cluster.block_rank(), tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  const int nb = p.nb;
+  const int64_t R = p.rows_per_cta;
+  const int64_t rb = min(p.m, p.j0 + (int64_t)b * R);
+  const int64_t re = min(p.m, rb + R);
+  const int nr = (int)(re - rb);
+  const unsigned rec_bytes = (unsigned)sizeof(LuRec<PW>);
+  const unsigned tx_bytes = CS * rec_bytes + PW * 8u;
+
+  if (tid == 0) {
+    mbar_init(&mbar[0], 1);
+    mbar_init(&mbar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
+
+  // ---- prologue 1: max |a| over rows < j0 (final U rows), per panel column
+  {
+    const int64_t ab = min(p.j0, (int64_t)b * p.above_per_cta);
+    const int64_t ae = min(p.j0, ab + p.above_per_cta);
+    double mx[PW];
+#pragma unroll
+    for (int c = 0; c < PW; c++) mx[c] = -1.0;
+    for (int64_t i = ab + tid; i < ae; i += THREADS)
+#pragma unroll
+      for (int c = 0; c < PW; c++)
+        if (c < nb) {
+          double v = fabs(p.a[cm(i, p.j0 + c, p.lda)]);
+          if (v > mx[c]) mx[c] = v;
+        }
+#pragma unroll
+    for (int c = 0; c < PW; c++) {
+#pragma unroll
+      for (int off = 16; off; off >>= 1) {
+        double o = __shfl_down_sync(0xffffffffu, mx[c], off);
+        if (o > mx[c]) mx[c] = o;
+      }
+      if (lane == 0) s_part[warp][c] = mx[c];
+    }
+  }
+  // ---- prologue 2: stage the panel rows
+  for (int c = 0; c < nb; c++)
+    for (int r = tid; r < nr; r += THREADS) s_a[c * R + r] = p.a[cm(rb + r, p.j0 + c, p.lda)];
+  __syncthreads();
+  if (tid < PW) {
+    double m2 = -1.0;
+    for (int wv = 0; wv < THREADS / 32; wv++)
+      if (s_part[wv][tid] > m2) m2 = s_part[wv][tid];
+    c_above[tid] = m2;
+  }
+  if (tid == 0) {  // arm both phases' expected bytes
+    mbar_arrive_expect_tx(&mbar[0], tx_bytes);
+    mbar_arrive_expect_tx(&mbar[1], tx_bytes);
+  }
+  cluster.sync();  // mbarrier inits + c_above visible cluster-wide (once per panel)
+  double above_mine = -1.0;  // warp 0, lane c: max |a| over rows < j0 of column c
+  if (warp == 0 && lane < nb)
+    for (int q = 0; q < CS; q++) {
+      double v = *cluster.map_shared_rank(&c_above[lane], q);
+      if (v > above_mine) above_mine = v;
+    }
+
+  // local candidates of panel column c for step row j -> push to every peer
+  auto publish = [&](int c, int64_t j, int par) {
+    double v = -1.0, cmax = -1.0;
+    int64_t idx = INT64_MAX;
+    const double* col = s_a + c * R;
+    for (int r = tid; r < nr; r += THREADS) {
+      const int64_t i = rb + r;
+      const double xv = fabs(col[r]);
+      if (i >= j) {
+        if (better(xv, i, v, idx)) { v = xv; idx = i; }
+      } else if (xv > cmax) {
+        cmax = xv;
+      }
+    }
+    block_argmax_all(v, idx, cmax, s_v, s_i, s_c);
+    const bool own_diag = (j >= rb && j < re);
+    if (warp == 0) {
+      // the bulk copies that read mine[par] two steps ago must have read it
+      if (lane < CS) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+      __syncwarp();
+      if (lane == 0) {
+        mine[par].val = v;
+        mine[par].idx = __longlong_as_double((long long)idx);
+        mine[par].cmax = cmax;
+        mine[par].pad = 0.0;
+      }
+      if (lane < PW) mine[par].row[lane] = (v >= 0.0 && lane < nb) ? s_a[lane * R + (idx - rb)] : 0.0;
+      if (own_diag && lane < PW) mine_diag[par][lane] = lane < nb ? s_a[lane * R + (j - rb)] : 0.0;
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      __syncwarp();
+      if (lane < CS) {
+        const unsigned bar_remote = mapa_u32(smem_u32(&mbar[par]), lane);
+        bulk_push(mapa_u32(smem_u32(&recv[par][b]), lane), &mine[par], rec_bytes, bar_remote);
+        if (own_diag) bulk_push(mapa_u32(smem_u32(&recv_diag[par][0]), lane), &mine_diag[par][0], PW * 8u, bar_remote);
+        asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+      }
+    }
+  };
+
+  publish(0, p.j0, 0);
+  unsigned phase_bits = 0u;  // bit k: phase parity of mbar[k]
+
+  for (int jj = 0; jj < nb; jj++) {
+    const int64_t j = p.j0 + jj;
+    const int par = jj & 1;
+    if (warp == 0) {
+      mbar_wait_parity(&mbar[par], (phase_bits >> par) & 1u);
+      // decide from local copies of every peer's record
+      double v = -1.0, cmax = -1.0;
+      int64_t idx = INT64_MAX;
+      if (lane < CS) {
+        const LuRec<PW>& rc = recv[par][lane];
+        if (rc.val >= 0.0) { v = rc.val; idx = (int64_t)__double_as_longlong(rc.idx); }
+        cmax = rc.cmax;
+      }
+      warp_argmax(v, idx, cmax);
+      v = __shfl_sync(0xffffffffu, v, 0);
+      idx = __shfl_sync(0xffffffffu, (long long)idx, 0);
+      cmax = __shfl_sync(0xffffffffu, cmax, 0);
+      const double ab = __shfl_sync(0xffffffffu, above_mine, jj);
+      // rlra/_lu_cython.pyx:23-39 (first max, whole-column colmax, zero pivot)
+      double colmax = v;
+      if (ab > colmax) colmax = ab;
+      if (cmax > colmax) colmax = cmax;
+      const int zero = (v <= ZERO_PIVOT_RTOL * colmax) ? 1 : 0;
+      const int64_t prow = zero ? j : idx;
+      if (lane == 0) {
+        s_zero = zero;
+        s_prow = prow;
+        s_ipiv[jj] = prow;
+        s_zf[jj] = zero;
+      }
+      if (!zero && lane < nb) {
+        const int winner = (int)((prow - p.j0) / R);
+        const double u = recv[par][winner].row[lane];
+        s_u[lane] = u;
+        if (prow != j) {  // full-row swap inside the panel (:40-48)
+          if (j >= rb && j < re) s_a[lane * R + (j - rb)] = u;
+          if (prow >= rb && prow < re) s_a[lane * R + (prow - rb)] = recv_diag[par][lane];
+        }
+      }
+      __syncwarp();
+      // slots of this parity are consumed: re-arm for step jj + 2
+      if (lane == 0) mbar_arrive_expect_tx(&mbar[par], tx_bytes);
+      phase_bits ^= 1u << par;
+    }
+    __syncthreads();
+    const int64_t r0 = j + 1 - rb;  // first local row strictly below the diagonal
+    if (!s_zero) {
+      const double ujj = s_u[jj];
+      double* colj = s_a + jj * R;
+      for (int r = tid; r < nr; r += THREADS) {
+        if (r < r0) continue;
+        const double l = colj[r] / ujj;  // IEEE division (:49-51)
+        colj[r] = l;
+        for (int c = jj + 1; c < nb; c++) {
+          double* e = s_a + c * R + r;
+          *e = sub_mul_nofma(*e, l, s_u[c]);  // (:52-55)
+        }
+      }
+    } else {
+      for (int r = tid; r < nr; r += THREADS)
+        if (r >= r0) s_a[jj * R + r] = 0.0;
+    }
+    if (jj + 1 < nb) publish(jj + 1, j + 1, par ^ 1);
+  }
+  __syncthreads();
+  for (int c = 0; c < nb; c++)
+    for (int r = tid; r < nr; r += THREADS) p.a[cm(rb + r, p.j0 + c, p.lda)] = s_a[c * R + r];
+  if (b == 0 && warp == 0) {
+    if (lane < nb) {
+      p.w.ipiv[p.j0 + lane] = s_ipiv[lane];
+      p.w.zflag[p.j0 + lane] = s_zf[lane];
+    }
+    const int cnt = build_panel_perm(p.j0, nb, s_ipiv, s_prow_rows, s_prow_src, p.w);
+    // the same net permutation applied to piv (rlra/_lu_cython.pyx:46-48)
+    int64_t v0 = 0, v1 = 0;
+    if (lane < cnt) v0 = p.piv[s_prow_src[lane]];
+    if (lane + 32 < cnt) v1 = p.piv[s_prow_src[lane + 32]];
+    __syncwarp();
+    if (lane < cnt) p.piv[s_prow_rows[lane]] = v0;
+    if (lane + 32 < cnt) p.piv[s_prow_rows[lane + 32]] = v1;
+  }
+  if (warp == 0 && lane < CS) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+  cluster.sync();  // every peer's pushes into this CTA have landed and been read
 }
 
 static constexpr int LU_PANEL_SMEM_BYTES = 200 * 1024;
@@ -478,6 +784,56 @@ int fill_iota(int64_t* p, int64_t m, cudaStream_t st) {
   return 0;
 }
 
+// Largest thread-block cluster (<= 16, non-portable above 8) that can hold one
+// 512-thread CTA with the full panel shared memory per SM; 1 if none.
+static int lu_max_cluster() {
+  static int cached[64];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 1;
+  if (cached[dev & 63]) return cached[dev & 63];
+  int best = 1;
+  const void* kern = (const void*)lu_panel_cluster_kernel<16, 512>;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, LU_PANEL_SMEM_BYTES) ==
+          cudaSuccess &&
+      cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess) {
+    for (int cs = 16; cs >= 2; cs /= 2) {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(cs);
+      cfg.blockDim = dim3(512);
+      cfg.dynamicSmemBytes = LU_PANEL_SMEM_BYTES;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = cs;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      int nclusters = 0;
+      if (cudaOccupancyMaxActiveClusters(&nclusters, kern, &cfg) == cudaSuccess && nclusters > 0) {
+        best = cs;
+        break;
+      }
+    }
+  }
+  cudaGetLastError();
+  cached[dev & 63] = best;
+  return best;
+}
+
+static int lu_prepare_kernel(const void* kern) {
+  static std::mutex mu;
+  static std::set<std::pair<int, const void*>> done;
+  int dev = 0;
+  RLRA_CHECK_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(mu);
+  if (done.count({dev, kern})) return 0;
+  RLRA_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, LU_PANEL_SMEM_BYTES));
+  cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  cudaGetLastError();
+  done.insert({dev, kern});
+  return 0;
+}
+
 // Packed in-place GEPP: on return `a` holds unit-L multipliers below the
 // diagonal and U on/above it, `piv` (caller-preloaded, typically 0..m-1) is
 // permuted like the reference's piv (rlra/_lu_cython.pyx:14, rlra/kernels.py:48),
@@ -493,26 +849,24 @@ int getrf(double* a, int64_t lda, int64_t m, int64_t n, int64_t* piv, int64_t* n
                ws_bytes, L.total);
   LuWork w = lu_work(ws, r, sms);
   RLRA_CHECK_CUDA(cudaMemsetAsync(w.bar, 0, 2 * sizeof(unsigned), st));
-  // Panel width: 32 when a 32-column panel of every active row fits in the
-  // shared memory of at most one CTA per SM, else 16 or 8 inner panels inside
-  // 32-wide outer blocks (same rounding sequence per element: still bit-exact).
+  // Panel placement.  Up to 16 x rows_cap rows: one thread-block cluster (DSMEM
+  // + hardware cluster barrier).  Beyond: one CTA per SM with a global-memory
+  // grid barrier.  Panel width 32 when every active row of a 32-wide panel fits
+  // in shared memory, else 16 / 8 inner panels inside 32-wide outer blocks
+  // (same rounding sequence per element: still bit-exact).
   auto rows_cap = [](int pw) { return (int64_t)(LU_PANEL_SMEM_BYTES / (pw * 8)); };
-  const int pw = (m <= sms * rows_cap(32)) ? 32 : (m <= sms * rows_cap(16) ? 16 : 8);
+  const int cmax = lu_max_cluster();
+  const bool use_cluster = cmax > 1 && m <= cmax * rows_cap(16);
+  int pw;
+  if (use_cluster) pw = (m <= cmax * rows_cap(32)) ? 32 : 16;
+  else pw = (m <= sms * rows_cap(32)) ? 32 : (m <= sms * rows_cap(16) ? 16 : 8);
   RLRA_REQUIRE(m <= sms * rows_cap(8), "getrf: m = %lld exceeds the panel capacity", (long long)m);
-  const void* kern = pw == 32 ? (const void*)lu_panel_smem_kernel<32, 512>
-                   : pw == 16 ? (const void*)lu_panel_smem_kernel<16, 512>
-                              : (const void*)lu_panel_smem_kernel<8, 512>;
-  {
-    static unsigned attr_mask[3] = {0, 0, 0};
-    const int slot = pw == 32 ? 0 : (pw == 16 ? 1 : 2);
-    int dev = 0;
-    RLRA_CHECK_CUDA(cudaGetDevice(&dev));
-    if (!(attr_mask[slot] & (1u << (dev & 31)))) {
-      RLRA_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           LU_PANEL_SMEM_BYTES));
-      attr_mask[slot] |= 1u << (dev & 31);
-    }
-  }
+  const void* kern = use_cluster
+      ? (pw == 32 ? (const void*)lu_panel_cluster_kernel<32, 512> : (const void*)lu_panel_cluster_kernel<16, 512>)
+      : (pw == 32 ? (const void*)lu_panel_smem_kernel<32, 512>
+                  : pw == 16 ? (const void*)lu_panel_smem_kernel<16, 512> : (const void*)lu_panel_smem_kernel<8, 512>);
+  if (lu_prepare_kernel(kern)) return -1;
+  unsigned bar_base = 0;
   for (int64_t jo = 0; jo < r; jo += LU_NB) {
     const int nbo = (int)std::min<int64_t>(LU_NB, r - jo);
     const int64_t ce = jo + nbo;
@@ -523,15 +877,34 @@ int getrf(double* a, int64_t lda, int64_t m, int64_t n, int64_t* piv, int64_t* n
       pa.a = a; pa.lda = lda; pa.m = m; pa.n = n; pa.j0 = j0; pa.nb = nb;
       pa.piv = piv;
       pa.w = w;
+      pa.bar_base = bar_base;
+      const int limit = use_cluster ? cmax : sms;
       // about one row per thread, never more rows than shared memory holds
       const int64_t target = std::min<int64_t>(rows_cap(pw), 512);
-      int G = (int)std::min<int64_t>(sms, ceil_div(active, target));
+      int G = (int)std::min<int64_t>(limit, ceil_div(active, target));
       G = (int)std::max<int64_t>(G, ceil_div(active, rows_cap(pw)));
       pa.rows_per_cta = ceil_div(active, G);
       pa.above_per_cta = std::max<int64_t>(1, ceil_div(j0, G));
       const size_t smem = (size_t)pa.rows_per_cta * nb * sizeof(double);
       void* args[] = {&pa};
-      RLRA_CHECK_CUDA(cudaLaunchCooperativeKernel(kern, dim3(G), dim3(512), args, smem, st));
+      if (use_cluster) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(G);
+        cfg.blockDim = dim3(512);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = G;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        RLRA_CHECK_CUDA(cudaLaunchKernelExC(&cfg, kern, args));
+      } else {
+        RLRA_CHECK_CUDA(cudaLaunchCooperativeKernel(kern, dim3(G), dim3(512), args, smem, st));
+        bar_base += (unsigned)G * nb;
+      }
       note_launch();
       if (n > nb) {
         int64_t ncols = n - nb;

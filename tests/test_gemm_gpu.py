@@ -38,7 +38,8 @@ def run(ta, tb, m, n, k, alpha=1.0, beta=0.0, seed=0, odd_ld=False):
 
 @pytest.mark.parametrize("ta,tb", [(False, False), (True, False), (False, True), (True, True)])
 @pytest.mark.parametrize("m,n,k", [(1000, 220, 700), (257, 61, 333), (33, 544, 1000), (4096, 512, 96),
-                                   (10000, 200, 16), (7, 9, 5), (128, 80, 2048)])
+                                   (10000, 200, 16), (7, 9, 5), (128, 80, 2048), (1024, 61, 700),
+                                   (132, 1000, 4), (2000, 544, 3000)])
 def test_gemm_matches_fp64_reference(cuda_dev, ta, tb, m, n, k):
     run(ta, tb, m, n, k)
 
