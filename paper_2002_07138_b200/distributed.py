@@ -1,0 +1,324 @@
+"""Multi-GPU PowerLU: A row-sharded across the ranks of one node, one process
+per GPU, torch.distributed over NCCL (NVLink 5 / NVSwitch) for the exchanges
+(SURVEY.md §8(e)).
+
+Per pass (rlra/rangefinder.py:144-176 control flow, unchanged):
+  Y = A W     local rows only (W replicated)            no communication
+  Z = A^T Y   local partial A_i^T Y_i, then all-reduce   n x l doubles
+  ||A||_F^2   local compensated sum, then all-reduce     1 double
+  column energies of G: local, then all-reduce           l doubles
+Sketch factorizations:
+  interior LU of the row-sharded Y and the final LU of G are EXACT GEPP on the
+  all-gathered matrix (every rank redundantly, bit-exact kernel) so pivots are
+  those of the single-GPU / reference algorithm; LU / QR of the replicated
+  n x l sketches run redundantly with no communication.
+
+The orchestration is written against a small ops interface so the same code
+runs on CUDA tensors with NCCL (CudaOps, the product) and -- in the CPU test
+suite only -- on CPU tensors with gloo and an oracle-backed ops object
+(tests/test_distributed_gloo.py).
+"""
+
+from __future__ import annotations
+
+import os
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from .errors import NotConverged, RankCollapse
+
+
+def row_range(m, world, rank):
+    """Contiguous, nearly equal row shards (the last ones may be shorter)."""
+    per = -(-m // world)
+    r0 = min(m, rank * per)
+    return r0, min(m, r0 + per)
+
+
+class CudaOps:
+    """Product ops: librlra_b200 kernels on CUDA tensors."""
+
+    def __init__(self, device):
+        from . import ops as _ops
+
+        self.o = _ops
+        self.device = device
+
+    def upload(self, a):
+        return self.o.from_numpy(a, self.device)
+
+    def empty(self, m, n):
+        return self.o.fmat(m, n, self.device)
+
+    def matmul(self, a, b, ta=False, tb=False):
+        return self.o.matmul(a, b, ta=ta, tb=tb)
+
+    def getrf_(self, a):
+        return self.o.getrf_(a)
+
+    def lu_basis(self, lu, piv):
+        return self.o.lu_basis(lu, piv)
+
+    def lu_extract(self, lu):
+        return self.o.lu_extract(lu)
+
+    def qr_q(self, x):
+        qr = self.o.QR(x)
+        return qr.q(), self.o.count_nonzero_diag(qr.r_view())
+
+    def transpose(self, a):
+        return self.o.transpose(a)
+
+    def sumsq(self, a):
+        return self.o.sumsq(a)
+
+    def colsumsq(self, a):
+        return self.o.colsumsq(a)
+
+
+@dataclass
+class DistLU:
+    p: object
+    q: object
+    L: object
+    U: object
+    rank: int
+
+
+class ShardedMatrix:
+    """Row shard A_i (rows [r0, r1) of the m x n operand) on this rank."""
+
+    def __init__(self, local, m, r0, r1, ops, group=None):
+        self.local = local
+        self.m, self.n = int(m), int(local.shape[1])
+        self.r0, self.r1 = r0, r1
+        self.ops = ops
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.product_count = 0
+
+    @property
+    def shape(self):
+        return (self.m, self.n)
+
+    # ---- passes
+    def matmul(self, w):
+        """Y_i = A_i W (W replicated n x w) -> local rows of Y."""
+        self.product_count += 1
+        return self.ops.matmul(self.local, w)
+
+    def rmatmul(self, y_local):
+        """Z = sum_i A_i^T Y_i -> replicated n x w (NCCL all-reduce)."""
+        self.product_count += 1
+        z = self.ops.matmul(self.local, y_local, ta=True)
+        # column-major (n, w) == contiguous (w, n) storage: reduce that view in place
+        dist.all_reduce(z.t(), op=dist.ReduceOp.SUM, group=self.group)
+        return z
+
+    def fro_norm_sq(self):
+        s = self.ops.sumsq(self.local).clone()
+        dist.all_reduce(s, op=dist.ReduceOp.SUM, group=self.group)
+        return s
+
+    # ---- exchanges
+    def gather_rows(self, y_local):
+        """All-gather the row-sharded m x w matrix to every rank (column-major)."""
+        w = y_local.shape[1]
+        per = -(-self.m // self.world)
+        # pad each shard to `per` rows; gather as (world, w, per) row-major blocks
+        buf = torch.zeros((w, per), dtype=y_local.dtype, device=y_local.device)
+        rows = self.r1 - self.r0
+        if rows:
+            buf[:, :rows].copy_(y_local.t())
+        out = [torch.empty_like(buf) for _ in range(self.world)]
+        dist.all_gather(out, buf, group=self.group)
+        full = self.ops.empty(self.m, w)
+        for r in range(self.world):
+            a0, a1 = row_range(self.m, self.world, r)
+            if a1 > a0:
+                full[a0:a1, :].copy_(out[r][:, : a1 - a0].t())
+        return full
+
+    def local_rows(self, full):
+        return full[self.r0:self.r1, :]
+
+
+def _check(count, requested):
+    achieved = int(count.item())
+    if achieved < requested:
+        raise RankCollapse(achieved, requested)
+
+
+def general_power_basis_v(A: ShardedMatrix, l, v, seed, omega_fn):
+    """rlra/rangefinder.py:144-176 over a row-sharded A.  omega_fn(seed, rows, l)
+    returns the full host Omega (bit-exact rlra.core.gaussian)."""
+    m, n = A.shape
+    if not 1 <= l <= min(m, n):
+        raise ValueError(f"sketch width l={l} outside 1..min{(m, n)}")
+    if v < 2:
+        raise ValueError("pass budget v must be >= 2")
+    ops = A.ops
+
+    def lu_basis_rows(y_local):
+        full = A.gather_rows(y_local)
+        piv, cnt = ops.getrf_(full)
+        _check(cnt, l)
+        return A.local_rows(ops.lu_basis(full, piv))
+
+    def lu_basis_repl(z):
+        piv, cnt = ops.getrf_(z)
+        _check(cnt, l)
+        return ops.lu_basis(z, piv)
+
+    def qr_basis(z):
+        q, cnt = ops.qr_q(z)
+        _check(cnt, l)
+        return q
+
+    if v % 2 == 0:
+        om = omega_fn(seed, m, l)
+        om_local = ops.upload(np.asfortranarray(om[A.r0:A.r1]))
+        x = A.rmatmul(om_local)
+        if v == 2:
+            return qr_basis(x), 1
+        w = lu_basis_repl(x)
+    else:
+        w = ops.upload(omega_fn(seed, n, l))
+    half = (v - 1) // 2
+    passes = 1 if v % 2 == 0 else 0
+    basis = None
+    for i in range(1, half + 1):
+        w_rows = lu_basis_rows(A.matmul(w))
+        passes += 1
+        z = A.rmatmul(w_rows)
+        passes += 1
+        if i == half:
+            basis = qr_basis(z)
+        else:
+            w = lu_basis_repl(z)
+    return basis, passes
+
+
+def lu_from_projection(A: ShardedMatrix, g_local, vk):
+    """rlra/fixedrank.py:136-146 with G gathered for the exact GEPP."""
+    ops = A.ops
+    k = g_local.shape[1]
+    g = A.gather_rows(g_local)
+    piv1, cnt = ops.getrf_(g)
+    l1, u1 = ops.lu_extract(g)
+    bt = ops.matmul(vk, u1, tb=True)
+    piv2, _ = ops.getrf_(bt)
+    l2, u2 = ops.lu_extract(bt)
+    big_l = ops.matmul(l1, u2, tb=True)
+    big_u = ops.transpose(l2)
+    return DistLU(piv1, piv2, big_l, big_u, k)
+
+
+def powerlu(A: ShardedMatrix, k, q_os=10, v=3, seed=0, omega_fn=None):
+    """rlra/fixedrank.py:120-133 over a row-sharded A; every rank returns the
+    same factors (replicated)."""
+    m, n = A.shape
+    if k < 1:
+        raise ValueError("target rank must be >= 1")
+    if q_os < 0:
+        raise ValueError("oversampling must be >= 0")
+    if k + q_os > min(m, n):
+        raise ValueError(f"sketch width {k + q_os} exceeds min{(m, n)}")
+    V, _ = general_power_basis_v(A, k + q_os, v, seed, omega_fn)
+    vk = V[:, :k]
+    return lu_from_projection(A, A.matmul(vk), vk)
+
+
+def adaptive_rank(A: ShardedMatrix, eps, b, l, v, seed, omega_fn):
+    """rlra/fixedprec.py:57-94 over a row-sharded A (energies all-reduced)."""
+    from .fixedprec import scan_energies
+    import math
+
+    m, n = A.shape
+    if l > min(m, n):
+        raise ValueError(f"sketch width {l} exceeds min{(m, n)}")
+    V, _ = general_power_basis_v(A, l, v, seed, omega_fn)
+    g_local = A.matmul(V)
+    e = A.ops.colsumsq(g_local).clone()
+    dist.all_reduce(e, op=dist.ReduceOp.SUM, group=A.group)
+    total = math.sqrt(float(A.fro_norm_sq().item())) ** 2
+    rank, resid, conv = scan_energies(total, e.cpu().numpy(), eps, b, l)
+    return rank, V, g_local, resid, conv
+
+
+def powerlu_fp(A: ShardedMatrix, eps, b, l, v, seed, omega_fn):
+    """rlra/fixedprec.py:152-163 over a row-sharded A: (factors, rank)."""
+    rank, V, g_local, resid, conv = adaptive_rank(A, eps, b, l, v, seed, omega_fn)
+    if not conv:
+        from .fixedprec import AdaptiveOutcome
+
+        raise NotConverged(AdaptiveOutcome(rank, V, g_local, resid, conv))
+    # lu_from_projection factors the all-gathered copy, g_local stays intact
+    return lu_from_projection(A, g_local[:, :rank], V[:, :rank]), rank
+
+
+# ---------------------------------------------------------------- bench entry
+def bench_main(args):
+    """bench.py under torchrun (N > 1): row-sharded C2 / C5 powerlu over NCCL."""
+    import json
+    import time
+
+    from . import configs
+    from .core import gaussian
+
+    rank = int(os.environ["RANK"])
+    world = int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    w = configs.WORKLOADS[args.config]
+    v = args.v if args.v is not None else w.v
+    passes, fact = configs.powerlu_flops(w.m, w.n, w.k, w.k + w.q_os, v)
+    flops = passes + fact
+    r0, r1 = row_range(w.m, world, rank)
+    gen = {"C1": configs.gen_c1, "C2": configs.gen_c2, "C5": configs.gen_c5}[w.name]
+    a = gen()
+    ops = CudaOps(dev)
+    A = ShardedMatrix(ops.upload(np.asfortranarray(a[r0:r1])), w.m, r0, r1, ops)
+    del a
+    cache = {}
+
+    def omega(seed, rows, l):
+        key = (seed, rows, l)
+        if key not in cache:
+            cache[key] = gaussian(seed, rows, l)
+        return cache[key]
+
+    for _ in range(args.warmup):
+        powerlu(A, w.k, w.q_os, v, w.seed, omega)
+    torch.cuda.synchronize()
+    dist.barrier()
+    st = torch.cuda.current_stream(dev)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    for _ in range(args.steps):
+        powerlu(A, w.k, w.q_os, v, w.seed, omega)
+    e1.record(st)
+    torch.cuda.synchronize()
+    ms = torch.tensor([e0.elapsed_time(e1) / args.steps], device=dev)
+    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    dist.barrier()
+    if rank == 0:
+        msv = float(ms.item())
+        line = {"metric": f"PowerLU FP64 GFLOP/s ({w.name}, v={v})", "value": flops / (msv / 1e3) / 1e9,
+                "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": msv, "s_per_factorization": msv / 1e3, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": {"workload": f"{w.name} powerlu m={w.m} n={w.n} k={w.k} l={w.k + w.q_os} v={v}",
+                           "parallelism": f"row-sharded A over {world} GPUs, NCCL all-reduce/all-gather",
+                           "l2": "inputs larger than L2"},
+                "roofline": None, "e2e": None, "cpu_baseline": None}
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
+    return 0

@@ -225,3 +225,33 @@ def _c2():
     if "a" not in _C2:
         _C2["a"] = configs.gen_c2()
     return _C2["a"]
+
+
+def test_distributed_path_single_rank_nccl(cuda_dev):
+    """The row-sharded orchestration with the CUDA ops over a 1-rank NCCL group
+    reproduces the single-GPU drop-in result (multi-rank logic: gloo tests)."""
+    import os
+
+    import torch.distributed as dist
+
+    import paper_2002_07138_b200 as P
+    from paper_2002_07138_b200 import distributed as D, ops
+
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29517")
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=cuda_dev)
+    try:
+        a = DRV["pl_a"]
+        A = D.ShardedMatrix(ops.from_numpy(a, cuda_dev), a.shape[0], 0, a.shape[0], D.CudaOps(cuda_dev))
+        f = D.powerlu(A, 30, 10, 4, 1, O.gaussian)
+        assert np.array_equal(f.p.cpu().numpy(), DRV["pl_v4/p"])
+        assert np.array_equal(f.q.cpu().numpy(), DRV["pl_v4/q"])
+        fd = P.LowRankLU(f.p.cpu().numpy(), f.q.cpu().numpy(), ops.to_numpy(f.L), ops.to_numpy(f.U), 30)
+        assert abs(O.rel_fro_error_factor(a, fd) - META["drivers"]["pl_v4"]["rel_err"]) <= REL_ERR_TOL
+        fa = DRV["fp_a"]
+        B = D.ShardedMatrix(ops.from_numpy(fa, cuda_dev), fa.shape[0], 0, fa.shape[0], D.CudaOps(cuda_dev))
+        fp, r = D.powerlu_fp(B, 1e-3, 5, 60, 4, 0, O.gaussian)
+        assert r == META["drivers"]["fp"]["rank"]
+        assert np.array_equal(fp.p.cpu().numpy(), DRV["fpfac/p"])
+    finally:
+        dist.destroy_process_group()
