@@ -26,6 +26,8 @@
  *   rlra_b200_sumsq            DenseAccessor.fro_norm()**2    accessors.py:33-34, fixedprec.py:72
  *   rlra_b200_colsumsq         per-column energies of G       fixedprec.py:75-80, :105-107
  *   rlra_b200_transpose        U = L2^T                       fixedrank.py:146
+ *   rlra_b200_normal_*         core.gaussian (NumPy PCG64     core.py:33-48
+ *                              + ziggurat standard_normal)
  */
 #ifndef RLRA_B200_H
 #define RLRA_B200_H
@@ -101,6 +103,27 @@ RLRA_B200_API int rlra_b200_sumsq(const double* a, int64_t lda, int64_t m, int64
                     size_t ws_bytes, void* stream);
 RLRA_B200_API int rlra_b200_colsumsq(const double* a, int64_t lda, int64_t m, int64_t n, double* out,
                        void* stream);
+
+/* ---- a1: Omega on the device, bit-identical to the reference's host draw
+ * np.random.default_rng(seed).standard_normal(n) (rlra/core.py:33-48): NumPy's
+ * PCG64 (state/inc from the seed) + its 256-layer ziggurat (tables ki/wi/fi).
+ * Two phases: begin() generates and classifies the word stream on the
+ * device; the caller resolves the rare tail draws (|x| > r; positions and the
+ * following words are exposed by views()) with the host libm log1p and passes
+ * them to finish(), which emits the n normals (flat == column-major order).
+ * status (device int64[2]): {normals produced (== n on success), flags}. */
+RLRA_B200_API size_t rlra_b200_normal_workspace(int64_t n);
+RLRA_B200_API int64_t rlra_b200_normal_stream_words(int64_t n);
+RLRA_B200_API int64_t rlra_b200_normal_tail_cap(int64_t n);
+RLRA_B200_API int rlra_b200_normal_begin(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi,
+                                         uint64_t inc_lo, int64_t n, const uint64_t* ki,
+                                         const double* wi, const double* fi, void* ws,
+                                         size_t ws_bytes, void* stream);
+RLRA_B200_API int rlra_b200_normal_views(int64_t n, void* ws, uint64_t** words, int64_t** tail_pos,
+                                         unsigned long long** ntail);
+RLRA_B200_API int rlra_b200_normal_finish(int64_t n, const int64_t* tail_pos, const int* tail_len,
+                                          const double* tail_val, int64_t ntail, double* out,
+                                          int64_t* status, void* ws, size_t ws_bytes, void* stream);
 
 /* ---- layout helper ------------------------------------------------------ */
 RLRA_B200_API int rlra_b200_transpose(const double* in, int64_t ldi, int64_t m, int64_t n, double* out,

@@ -48,6 +48,13 @@ SIGNATURES = {
     "rlra_b200_sumsq": (_c_i, [_c_p, _c_i64, _c_i64, _c_i64, _c_p, _c_p, _c_sz, _c_p]),
     "rlra_b200_colsumsq": (_c_i, [_c_p, _c_i64, _c_i64, _c_i64, _c_p, _c_p]),
     "rlra_b200_transpose": (_c_i, [_c_p, _c_i64, _c_i64, _c_i64, _c_p, _c_i64, _c_p]),
+    "rlra_b200_normal_workspace": (_c_sz, [_c_i64]),
+    "rlra_b200_normal_stream_words": (_c_i64, [_c_i64]),
+    "rlra_b200_normal_tail_cap": (_c_i64, [_c_i64]),
+    "rlra_b200_normal_begin": (_c_i, [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64,
+                                      _c_i64, _c_p, _c_p, _c_p, _c_p, _c_sz, _c_p]),
+    "rlra_b200_normal_views": (_c_i, [_c_i64, _c_p, _c_p, _c_p, _c_p]),
+    "rlra_b200_normal_finish": (_c_i, [_c_i64, _c_p, _c_p, _c_p, _c_i64, _c_p, _c_p, _c_p, _c_sz, _c_p]),
 }
 
 _lib = None

@@ -68,6 +68,15 @@ int sumsq(const double* a, int64_t lda, int64_t m, int64_t n, double* out_dev, v
 int colsumsq(const double* a, int64_t lda, int64_t m, int64_t n, double* out_dev, cudaStream_t st);
 int transpose(const double* in, int64_t ldi, int64_t m, int64_t n, double* out, int64_t ldo,
               cudaStream_t st);
+size_t normal_workspace_bytes(int64_t N);
+int64_t normal_stream_words(int64_t N);
+int64_t normal_tail_cap(int64_t N);
+int normal_phase1(uint64_t s_hi, uint64_t s_lo, uint64_t i_hi, uint64_t i_lo, int64_t N,
+                  const uint64_t* ki, const double* wi, const double* fi, void* ws, size_t ws_bytes,
+                  cudaStream_t st);
+int normal_views(int64_t N, void* ws, uint64_t** u, int64_t** tail_pos, unsigned long long** ntail);
+int normal_phase2(int64_t N, const int64_t* tpos, const int* tlen, const double* tval, int64_t ntail,
+                  double* out, int64_t* status_dev, void* ws, size_t ws_bytes, cudaStream_t st);
 
 }  // namespace rlra
 
@@ -203,6 +212,29 @@ int rlra_b200_colsumsq(const double* a, int64_t lda, int64_t m, int64_t n, doubl
 int rlra_b200_transpose(const double* in, int64_t ldi, int64_t m, int64_t n, double* out,
                         int64_t ldo, void* stream) {
   return transpose(in, ldi, m, n, out, ldo, S(stream));
+}
+
+size_t rlra_b200_normal_workspace(int64_t n) { return normal_workspace_bytes(n); }
+
+int64_t rlra_b200_normal_stream_words(int64_t n) { return normal_stream_words(n); }
+
+int64_t rlra_b200_normal_tail_cap(int64_t n) { return normal_tail_cap(n); }
+
+int rlra_b200_normal_begin(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo,
+                           int64_t n, const uint64_t* ki, const double* wi, const double* fi, void* ws,
+                           size_t ws_bytes, void* stream) {
+  return normal_phase1(state_hi, state_lo, inc_hi, inc_lo, n, ki, wi, fi, ws, ws_bytes, S(stream));
+}
+
+int rlra_b200_normal_views(int64_t n, void* ws, uint64_t** words, int64_t** tail_pos,
+                           unsigned long long** ntail) {
+  return normal_views(n, ws, words, tail_pos, ntail);
+}
+
+int rlra_b200_normal_finish(int64_t n, const int64_t* tail_pos, const int* tail_len,
+                            const double* tail_val, int64_t ntail, double* out, int64_t* status,
+                            void* ws, size_t ws_bytes, void* stream) {
+  return normal_phase2(n, tail_pos, tail_len, tail_val, ntail, out, status, ws, ws_bytes, S(stream));
 }
 
 }  // extern "C"
