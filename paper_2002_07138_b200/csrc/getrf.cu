@@ -41,6 +41,7 @@ struct LuWork {
   int64_t* perm_src;   // [2*LU_NB] source row of each touched row after the swaps
   int* perm_cnt;       // [1]
   int64_t* count;      // [1] nonzero diagonal count
+  double* recg;        // cluster panel: [2][16][2+LU_NB] records + [2][LU_NB] diagonal rows (global staging for the multicast)
 };
 
 struct PanelArgs {
@@ -52,7 +53,22 @@ struct PanelArgs {
   int64_t* piv;
   LuWork w;
   unsigned bar_base;  // monotonic grid-barrier counter value at kernel entry
+  unsigned long long* trace;  // RLRA_LU_TRACE builds only: [CTA][128] globaltimer stamps
 };
+
+// x / d correctly rounded (IEEE round-to-nearest, like C's `/`), given the
+// correctly rounded reciprocal rcp = RN(1/d): Markstein's theorem -- q0 = RN(x*rcp),
+// rem = x - d*q0 exactly (FMA), RN(q0 + rem*rcp) == RN(x/d) -- valid away from
+// overflow / underflow; other operands take the hardware division path.
+__device__ __forceinline__ double ieee_div_by(double x, double d, double rcp) {
+  const double ax = fabs(x), ad = fabs(d);
+  if (ax > 0x1p-960 && ax < 0x1p+960 && ad > 0x1p-960 && ad < 0x1p+960) {
+    const double q0 = __dmul_rn(x, rcp);
+    const double rem = fma(-d, q0, x);
+    return fma(rem, rcp, q0);
+  }
+  return x / d;
+}
 
 // strict-greater first-max merge: (v,i) replaces best when v > best or (v == best && i < besti)
 __device__ __forceinline__ bool better(double v, int64_t i, double bv, int64_t bi) {
@@ -306,22 +322,36 @@ __global__ void __launch_bounds__(THREADS, 1) lu_panel_smem_kernel(PanelArgs p) 
 }
 
 // (value, index, cmax) first-max reduction over the whole block; every thread
-// ends with the result.  Two shuffle rounds, ONE __syncthreads; callers must
-// separate consecutive uses of the staging arrays by another block barrier.
+// ends with the result.  Values are |a| >= 0 (or -1 for "no row"); the max is
+// found with fmax shuffles (NaN never wins, like the reference's strict '>'),
+// the smallest row index holding it with one redux.min, so ties keep the
+// first maximum.  ONE __syncthreads; callers must separate consecutive uses of
+// the staging arrays by another block barrier.  `base` is subtracted from the
+// row indices so they fit the 32-bit redux.
 __device__ __forceinline__ void block_argmax_all(double& v, int64_t& idx, double& cmax, double* s_v,
-                                                 int64_t* s_i, double* s_c) {
+                                                 int64_t* s_i, double* s_c, int64_t base = 0) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  warp_argmax(v, idx, cmax);
+  auto warp_reduce = [&](double& vv, int64_t& ii, double& cc) {
+    double vm = vv, cm2 = cc;
+#pragma unroll
+    for (int off = 16; off; off >>= 1) {
+      vm = fmax(vm, __shfl_xor_sync(0xffffffffu, vm, off));
+      cm2 = fmax(cm2, __shfl_xor_sync(0xffffffffu, cm2, off));
+    }
+    const unsigned key = (vv == vm && vm >= 0.0 && ii != INT64_MAX) ? (unsigned)(ii - base) : 0xffffffffu;
+    const unsigned kmin = __reduce_min_sync(0xffffffffu, key);
+    vv = vm;
+    cc = cm2;
+    ii = (kmin == 0xffffffffu) ? INT64_MAX : (int64_t)kmin + base;
+  };
+  warp_reduce(v, idx, cmax);
   if (lane == 0) { s_v[warp] = v; s_i[warp] = idx; s_c[warp] = cmax; }
   __syncthreads();
   const int nw = blockDim.x >> 5;
   v = lane < nw ? s_v[lane] : -1.0;
   idx = lane < nw ? s_i[lane] : INT64_MAX;
   cmax = lane < nw ? s_c[lane] : -1.0;
-  warp_argmax(v, idx, cmax);
-  v = __shfl_sync(0xffffffffu, v, 0);
-  idx = __shfl_sync(0xffffffffu, (long long)idx, 0);
-  cmax = __shfl_sync(0xffffffffu, cmax, 0);
+  warp_reduce(v, idx, cmax);
 }
 
 // ---------------------------------------------------------------------------
@@ -382,40 +412,70 @@ template <int PW, int THREADS>
 __global__ void __launch_bounds__(THREADS, 1) lu_panel_cluster_kernel(PanelArgs p) {
   namespace cg = cooperative_groups;
   constexpr int MAXCS = 16;
+  constexpr int RECD = 2 + PW;  // record doubles: {|value|, row index bits, row[PW]}
+  static_assert(RECD % 2 == 0, "records are pushed as 16-byte pairs");
   cg::cluster_group cluster = cg::this_cluster();
   extern __shared__ __align__(16) double s_a[];
-  __shared__ double s_v[32], s_c[32];
+  __shared__ double s_v[32];
   __shared__ int64_t s_i[32];
-  __shared__ __align__(16) LuRec<PW> recv[2][MAXCS];  // records from every peer
-  __shared__ __align__(16) double recv_diag[2][PW];   // current diagonal row
-  __shared__ __align__(16) LuRec<PW> mine[2];         // my outgoing record
-  __shared__ __align__(16) double mine_diag[2][PW];
+  __shared__ double s_c[32];
+  __shared__ __align__(16) double recv[2][MAXCS][RECD];  // pushed by every peer
+  __shared__ __align__(16) double recv_diag[2][PW];      // current diagonal row (pre-swap)
   __shared__ __align__(8) uint64_t mbar[2];
+  __shared__ __align__(8) uint64_t ldbar;
   __shared__ double c_above[PW];
-  __shared__ double s_u[PW];
+  __shared__ double s_u[2][PW];   // pivot row of the step, double-buffered by parity
+  __shared__ double s_rcp[2];
   __shared__ double s_part[THREADS / 32][PW];
-  __shared__ int64_t s_prow;
-  __shared__ int s_zero;
+  __shared__ int64_t s_prow[2];
+  __shared__ int s_zero[2];
   __shared__ int64_t s_ipiv[PW], s_prow_rows[2 * PW], s_prow_src[2 * PW];
   __shared__ int s_zf[PW];
 
   const int CS = (int)cluster.num_blocks(), b = (int)cluster.block_rank(), tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
+#ifdef RLRA_LU_TRACE
+  auto trace = [&](int slot) {
+    if (lane == 0 && warp == 0 && p.trace && slot < 128) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      p.trace[(int64_t)b * 128 + slot] = t;
+    }
+  };
+#else
+  auto trace = [&](int) {};
+#endif
+  trace(0);
   const int nb = p.nb;
   const int64_t R = p.rows_per_cta;
   const int64_t rb = min(p.m, p.j0 + (int64_t)b * R);
   const int64_t re = min(p.m, rb + R);
   const int nr = (int)(re - rb);
-  const unsigned rec_bytes = (unsigned)sizeof(LuRec<PW>);
-  const unsigned tx_bytes = CS * rec_bytes + PW * 8u;
+  const int Ri = (int)R;  // 32-bit shared-memory indexing
+  const unsigned tx_bytes = CS * RECD * 8u + PW * 8u;
 
   if (tid == 0) {
     mbar_init(&mbar[0], 1);
     mbar_init(&mbar[1], 1);
+    mbar_init(&ldbar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
+  __syncthreads();
 
-  // ---- prologue 1: max |a| over rows < j0 (final U rows), per panel column
+  // ---- prologue 1: stage the panel rows -- one TMA bulk copy per column
+  // (16-byte aligned when R, rb and lda are even; an odd last row is loaded directly)
+  const bool bulk_ok = ((R & 1) == 0) && ((p.lda & 1) == 0) && ((rb & 1) == 0);
+  const int nr_bulk = bulk_ok ? (nr & ~1) : 0;
+  if (nr_bulk > 0 && tid == 0) {
+    mbar_arrive_expect_tx(&ldbar, (unsigned)(nb * nr_bulk * 8));
+    for (int c = 0; c < nb; c++)
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+              smem_u32(s_a + c * R)),
+          "l"(p.a + cm(rb, p.j0 + c, p.lda)), "r"((unsigned)(nr_bulk * 8)), "r"(smem_u32(&ldbar))
+          : "memory");
+  }
+  // ---- prologue 2 (overlaps the copies): max |a| over rows < j0 (final U rows)
   {
     const int64_t ab = min(p.j0, (int64_t)b * p.above_per_cta);
     const int64_t ae = min(p.j0, ab + p.above_per_cta);
@@ -439,9 +499,9 @@ __global__ void __launch_bounds__(THREADS, 1) lu_panel_cluster_kernel(PanelArgs 
       if (lane == 0) s_part[warp][c] = mx[c];
     }
   }
-  // ---- prologue 2: stage the panel rows
   for (int c = 0; c < nb; c++)
-    for (int r = tid; r < nr; r += THREADS) s_a[c * R + r] = p.a[cm(rb + r, p.j0 + c, p.lda)];
+    for (int r = nr_bulk + tid; r < nr; r += THREADS) s_a[c * R + r] = p.a[cm(rb + r, p.j0 + c, p.lda)];
+  if (nr_bulk > 0) mbar_wait_parity(&ldbar, 0);
   __syncthreads();
   if (tid < PW) {
     double m2 = -1.0;
@@ -453,124 +513,226 @@ __global__ void __launch_bounds__(THREADS, 1) lu_panel_cluster_kernel(PanelArgs 
     mbar_arrive_expect_tx(&mbar[0], tx_bytes);
     mbar_arrive_expect_tx(&mbar[1], tx_bytes);
   }
+  trace(1);
   cluster.sync();  // mbarrier inits + c_above visible cluster-wide (once per panel)
-  double above_mine = -1.0;  // warp 0, lane c: max |a| over rows < j0 of column c
+  trace(2);
+  // warp 0, lane c: running colmax of column c = max(|a| over rows < j0,
+  // |pivot row value| over this panel's earlier steps) -- the reference's
+  // "whole column" colmax without a second reduction (rlra/_lu_cython.pyx:31-35)
+  double colmax_mine = -1.0;
   if (warp == 0 && lane < nb)
     for (int q = 0; q < CS; q++) {
       double v = *cluster.map_shared_rank(&c_above[lane], q);
-      if (v > above_mine) above_mine = v;
+      if (v > colmax_mine) colmax_mine = v;
     }
 
-  // local candidates of panel column c for step row j -> push to every peer
-  auto publish = [&](int c, int64_t j, int par) {
-    double v = -1.0, cmax = -1.0;
+  // Local first-max candidate of panel column c (rows >= j), then warp 0
+  // finishes the look-ahead remainder (columns > c, multipliers in column c-1)
+  // of the two rows that leave this CTA -- candidate row and next diagonal row
+  // -- and pushes record + diagonal row into every peer with st.async, which
+  // completes on the peer's mbarrier (no proxy fence, no source buffer).
+  auto publish = [&](int c, int64_t j, int par, bool owe, int upar) {
+    double v = -1.0, dummy = -1.0;
     int64_t idx = INT64_MAX;
     const double* col = s_a + c * R;
     for (int r = tid; r < nr; r += THREADS) {
       const int64_t i = rb + r;
-      const double xv = fabs(col[r]);
       if (i >= j) {
+        const double xv = fabs(col[r]);
         if (better(xv, i, v, idx)) { v = xv; idx = i; }
-      } else if (xv > cmax) {
-        cmax = xv;
       }
     }
-    block_argmax_all(v, idx, cmax, s_v, s_i, s_c);
+    block_argmax_all(v, idx, dummy, s_v, s_i, s_c, rb);
+    if (c <= 12) trace(8 + 8 * (c - 1) + 4);
     const bool own_diag = (j >= rb && j < re);
     if (warp == 0) {
-      // the bulk copies that read mine[par] two steps ago must have read it
-      if (lane < CS) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+      const double* u = s_u[upar];
+      if (owe) {
+        const double* lcol = s_a + (c - 1) * R;
+        if (lane > c && lane < nb) {
+          if (v >= 0.0) {
+            const int r = (int)(idx - rb);
+            s_a[lane * R + r] = sub_mul_nofma(s_a[lane * R + r], lcol[r], u[lane]);
+          }
+          if (own_diag && j != idx) {
+            const int r = (int)(j - rb);
+            s_a[lane * R + r] = sub_mul_nofma(s_a[lane * R + r], lcol[r], u[lane]);
+          }
+        }
+        __syncwarp();
+      }
+      // Record {v, idx, row[PW]} (and the next diagonal row) are staged in a
+      // per-CTA global slot, then ONE multicast bulk copy (TMA engine) writes
+      // them into every peer's shared memory at the same offset and completes
+      // on every peer's mbarrier.  Slots are reused two steps later, after this
+      // CTA has received the step's multicast (so the read is done).
+      const int rr = (int)(idx - rb);
+      double* slot = p.w.recg + ((int64_t)par * 16 + b) * RECD;
+      double* dslot = p.w.recg + 2 * 16 * RECD + par * PW;
+      for (int pr = lane; pr < RECD / 2; pr += 32) {
+        double x0, x1;
+        if (pr == 0) {
+          x0 = v;
+          x1 = __longlong_as_double((long long)idx);
+        } else {
+          const int c0 = 2 * pr - 2;
+          x0 = (v >= 0.0 && c0 < nb) ? s_a[c0 * Ri + rr] : 0.0;
+          x1 = (v >= 0.0 && c0 + 1 < nb) ? s_a[(c0 + 1) * Ri + rr] : 0.0;
+        }
+        reinterpret_cast<double2*>(slot)[pr] = make_double2(x0, x1);
+      }
+      if (own_diag && lane < PW / 2) {
+        const int rj = (int)(j - rb);
+        const double x0 = 2 * lane < nb ? s_a[(2 * lane) * Ri + rj] : 0.0;
+        const double x1 = 2 * lane + 1 < nb ? s_a[(2 * lane + 1) * Ri + rj] : 0.0;
+        reinterpret_cast<double2*>(dslot)[lane] = make_double2(x0, x1);
+      }
+      asm volatile("fence.proxy.async.global;\n" ::: "memory");
       __syncwarp();
       if (lane == 0) {
-        mine[par].val = v;
-        mine[par].idx = __longlong_as_double((long long)idx);
-        mine[par].cmax = cmax;
-        mine[par].pad = 0.0;
-      }
-      if (lane < PW) mine[par].row[lane] = (v >= 0.0 && lane < nb) ? s_a[lane * R + (idx - rb)] : 0.0;
-      if (own_diag && lane < PW) mine_diag[par][lane] = lane < nb ? s_a[lane * R + (j - rb)] : 0.0;
-      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-      __syncwarp();
-      if (lane < CS) {
-        const unsigned bar_remote = mapa_u32(smem_u32(&mbar[par]), lane);
-        bulk_push(mapa_u32(smem_u32(&recv[par][b]), lane), &mine[par], rec_bytes, bar_remote);
-        if (own_diag) bulk_push(mapa_u32(smem_u32(&recv_diag[par][0]), lane), &mine_diag[par][0], PW * 8u, bar_remote);
-        asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+        const unsigned short mask = (unsigned short)((1u << CS) - 1u);
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1], %2, [%3], %4;\n" ::"r"(
+                smem_u32(&recv[par][b][0])),
+            "l"(slot), "r"((unsigned)(RECD * 8)), "r"(smem_u32(&mbar[par])), "h"(mask)
+            : "memory");
+        if (own_diag)
+          asm volatile(
+              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1], %2, [%3], %4;\n" ::"r"(
+                  smem_u32(&recv_diag[par][0])),
+              "l"(dslot), "r"((unsigned)(PW * 8)), "r"(smem_u32(&mbar[par])), "h"(mask)
+              : "memory");
       }
     }
+    if (c <= 12) trace(8 + 8 * (c - 1) + 5);
+    return idx;  // the CTA's candidate row (or INT64_MAX)
   };
 
-  publish(0, p.j0, 0);
+  publish(0, p.j0, 0, false, 0);
   unsigned phase_bits = 0u;  // bit k: phase parity of mbar[k]
 
   for (int jj = 0; jj < nb; jj++) {
     const int64_t j = p.j0 + jj;
     const int par = jj & 1;
     if (warp == 0) {
+      if (jj < 12) trace(8 + 8 * jj + 0);
       mbar_wait_parity(&mbar[par], (phase_bits >> par) & 1u);
-      // decide from local copies of every peer's record
-      double v = -1.0, cmax = -1.0;
+      if (jj < 12) trace(8 + 8 * jj + 1);
+      // decide from the local copies of every peer's record
+      double v = -1.0, dummy = -1.0;
       int64_t idx = INT64_MAX;
       if (lane < CS) {
-        const LuRec<PW>& rc = recv[par][lane];
-        if (rc.val >= 0.0) { v = rc.val; idx = (int64_t)__double_as_longlong(rc.idx); }
-        cmax = rc.cmax;
+        const double rv = recv[par][lane][0];
+        if (rv >= 0.0) { v = rv; idx = (int64_t)__double_as_longlong(recv[par][lane][1]); }
       }
-      warp_argmax(v, idx, cmax);
+      warp_argmax(v, idx, dummy);
       v = __shfl_sync(0xffffffffu, v, 0);
       idx = __shfl_sync(0xffffffffu, (long long)idx, 0);
-      cmax = __shfl_sync(0xffffffffu, cmax, 0);
-      const double ab = __shfl_sync(0xffffffffu, above_mine, jj);
-      // rlra/_lu_cython.pyx:23-39 (first max, whole-column colmax, zero pivot)
+      // rlra/_lu_cython.pyx:23-39: first max, whole-column colmax, zero pivot
       double colmax = v;
-      if (ab > colmax) colmax = ab;
-      if (cmax > colmax) colmax = cmax;
+      const double cm_j = __shfl_sync(0xffffffffu, colmax_mine, jj);
+      if (cm_j > colmax) colmax = cm_j;
       const int zero = (v <= ZERO_PIVOT_RTOL * colmax) ? 1 : 0;
       const int64_t prow = zero ? j : idx;
+      // pivot row (post-swap row j): the winner's record, or row j itself
+      double u = 0.0;
+      if (lane < nb) u = zero ? recv_diag[par][lane] : recv[par][(int)((prow - p.j0) / R)][2 + lane];
+      if (lane < PW) s_u[par][lane] = u;
+      if (lane > jj && lane < nb && fabs(u) > colmax_mine) colmax_mine = fabs(u);
       if (lane == 0) {
-        s_zero = zero;
-        s_prow = prow;
+        s_zero[par] = zero;
+        s_prow[par] = prow;
         s_ipiv[jj] = prow;
         s_zf[jj] = zero;
       }
-      if (!zero && lane < nb) {
-        const int winner = (int)((prow - p.j0) / R);
-        const double u = recv[par][winner].row[lane];
-        s_u[lane] = u;
-        if (prow != j) {  // full-row swap inside the panel (:40-48)
-          if (j >= rb && j < re) s_a[lane * R + (j - rb)] = u;
-          if (prow >= rb && prow < re) s_a[lane * R + (prow - rb)] = recv_diag[par][lane];
-        }
-      }
+      if (lane == jj) s_rcp[par] = zero ? 0.0 : __drcp_rn(u);
       __syncwarp();
-      // slots of this parity are consumed: re-arm for step jj + 2
-      if (lane == 0) mbar_arrive_expect_tx(&mbar[par], tx_bytes);
+      if (lane == 0) mbar_arrive_expect_tx(&mbar[par], tx_bytes);  // re-arm for step jj + 2
       phase_bits ^= 1u << par;
     }
+    // all warps: previous step's bulk update done; decision visible
     __syncthreads();
+    if (jj < 12) trace(8 + 8 * jj + 2);
+    const int zero = s_zero[par];
+    const int64_t prow = s_prow[par];
+    const double* u = s_u[par];
     const int64_t r0 = j + 1 - rb;  // first local row strictly below the diagonal
-    if (!s_zero) {
-      const double ujj = s_u[jj];
-      double* colj = s_a + jj * R;
+    const bool last = (jj + 1 >= nb);
+    // full-row swap (:40-48), lane-parallel in the warps that own rows j / prow
+    // (the owner thread then updates that row, so __syncwarp is enough)
+    if (!zero && prow != j) {
+      if (j >= rb && j < re && (((int)(j - rb) % THREADS) >> 5) == warp && lane < nb)
+        s_a[lane * Ri + (int)(j - rb)] = u[lane];
+      if (prow >= rb && prow < re && (((int)(prow - rb) % THREADS) >> 5) == warp && lane < nb)
+        s_a[lane * Ri + (int)(prow - rb)] = recv_diag[par][lane];
+      __syncwarp();
+    }
+    if (!zero) {
+      // look-ahead: multipliers and the NEXT column only
+      const double ujj = u[jj], rcp = s_rcp[par];
+      const double unext = last ? 0.0 : u[jj + 1];
+      double* colj = s_a + jj * Ri;
+      double* coln = s_a + (jj + 1) * Ri;
       for (int r = tid; r < nr; r += THREADS) {
         if (r < r0) continue;
-        const double l = colj[r] / ujj;  // IEEE division (:49-51)
+        const double l = ieee_div_by(colj[r], ujj, rcp);  // IEEE division (:49-51)
         colj[r] = l;
-        for (int c = jj + 1; c < nb; c++) {
-          double* e = s_a + c * R + r;
-          *e = sub_mul_nofma(*e, l, s_u[c]);  // (:52-55)
-        }
+        if (!last) coln[r] = sub_mul_nofma(coln[r], l, unext);  // (:52-55), column jj+1
       }
     } else {
+      // zero pivot: zero the L column below the diagonal; no swap, no update (:36-39)
       for (int r = tid; r < nr; r += THREADS)
         if (r >= r0) s_a[jj * R + r] = 0.0;
     }
-    if (jj + 1 < nb) publish(jj + 1, j + 1, par ^ 1);
+    if (jj < 12) trace(8 + 8 * jj + 3);
+    if (!last) {
+      const int64_t cand = publish(jj + 1, j + 1, par ^ 1, !zero, par);
+      if (!zero) {
+        // bulk of the step's update (columns jj+2 ..) by warps 1.., overlapping
+        // the exchange -- warp 0 goes straight to the next decision; the two
+        // rows published above were finished by warp 0
+        const double* colj = s_a + jj * Ri;
+        if (warp > 0) {
+          for (int r = tid - 32; r < nr; r += THREADS - 32) {
+            if (r < r0) continue;
+            const int64_t i = rb + r;
+            if (i == cand || i == j + 1) continue;
+            const double l = colj[r];
+            int c = jj + 2;
+            for (; c + 8 <= nb; c += 8) {  // 8 independent chains per batch (ILP)
+              double vv[8];
+#pragma unroll
+              for (int q = 0; q < 8; q++) vv[q] = s_a[(c + q) * Ri + r];
+#pragma unroll
+              for (int q = 0; q < 8; q++) vv[q] = sub_mul_nofma(vv[q], l, u[c + q]);  // (:52-55)
+#pragma unroll
+              for (int q = 0; q < 8; q++) s_a[(c + q) * Ri + r] = vv[q];
+            }
+            for (; c < nb; c++) {
+              double* e = s_a + c * Ri + r;
+              *e = sub_mul_nofma(*e, l, u[c]);
+            }
+          }
+        }
+      }
+    }
   }
   __syncthreads();
+  // ---- write the panel back (bulk copies; an odd last row directly)
+  if (nr_bulk > 0) {
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    __syncthreads();
+    if (tid < nb) {
+      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(
+                       p.a + cm(rb, p.j0 + tid, p.lda)),
+                   "r"(smem_u32(s_a + tid * R)), "r"((unsigned)(nr_bulk * 8))
+                   : "memory");
+      asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+    }
+  }
   for (int c = 0; c < nb; c++)
-    for (int r = tid; r < nr; r += THREADS) p.a[cm(rb + r, p.j0 + c, p.lda)] = s_a[c * R + r];
-  if (b == 0 && warp == 0) {
+    for (int r = nr_bulk + tid; r < nr; r += THREADS) p.a[cm(rb + r, p.j0 + c, p.lda)] = s_a[c * R + r];
+  if (b == 0 && warp == 1) {
     if (lane < nb) {
       p.w.ipiv[p.j0 + lane] = s_ipiv[lane];
       p.w.zflag[p.j0 + lane] = s_zf[lane];
@@ -584,8 +746,10 @@ __global__ void __launch_bounds__(THREADS, 1) lu_panel_cluster_kernel(PanelArgs 
     if (lane < cnt) p.piv[s_prow_rows[lane]] = v0;
     if (lane + 32 < cnt) p.piv[s_prow_rows[lane + 32]] = v1;
   }
-  if (warp == 0 && lane < CS) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
-  cluster.sync();  // every peer's pushes into this CTA have landed and been read
+  if (nr_bulk > 0 && tid < nb) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+  trace(126);
+  cluster.sync();  // no CTA leaves while a peer may still push into it
+  trace(127);
 }
 
 static constexpr int LU_PANEL_SMEM_BYTES = 200 * 1024;
@@ -720,7 +884,7 @@ __global__ void count_nonzero_diag_kernel(const double* a, int64_t lda, int64_t 
 static size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
 
 struct LuLayout {
-  size_t off[13];
+  size_t off[14];
   size_t total;
 };
 
@@ -741,6 +905,7 @@ static LuLayout lu_layout(int64_t r, int G) {
   take(10, 2 * LU_NB * sizeof(int64_t));
   take(11, sizeof(int));
   take(12, sizeof(int64_t));
+  take(13, (size_t)(2 * 16 * (2 + LU_NB) + 2 * LU_NB) * sizeof(double));
   L.total = o;
   return L;
 }
@@ -767,6 +932,7 @@ static LuWork lu_work(void* ws, int64_t r, int G) {
   w.perm_src = reinterpret_cast<int64_t*>(base + L.off[10]);
   w.perm_cnt = reinterpret_cast<int*>(base + L.off[11]);
   w.count = reinterpret_cast<int64_t*>(base + L.off[12]);
+  w.recg = reinterpret_cast<double*>(base + L.off[13]);
   return w;
 }
 
@@ -783,6 +949,9 @@ int fill_iota(int64_t* p, int64_t m, cudaStream_t st) {
   RLRA_LAUNCHED();
   return 0;
 }
+
+unsigned long long* g_lu_trace = nullptr;  // set by rlra_b200_debug_lu_trace (tools only)
+static unsigned long long* lu_trace_buffer() { return g_lu_trace; }
 
 // Largest thread-block cluster (<= 16, non-portable above 8) that can hold one
 // 512-thread CTA with the full panel shared memory per SM; 1 if none.
@@ -878,12 +1047,14 @@ int getrf(double* a, int64_t lda, int64_t m, int64_t n, int64_t* piv, int64_t* n
       pa.piv = piv;
       pa.w = w;
       pa.bar_base = bar_base;
+      pa.trace = lu_trace_buffer();
       const int limit = use_cluster ? cmax : sms;
       // about one row per thread, never more rows than shared memory holds
       const int64_t target = std::min<int64_t>(rows_cap(pw), 512);
       int G = (int)std::min<int64_t>(limit, ceil_div(active, target));
       G = (int)std::max<int64_t>(G, ceil_div(active, rows_cap(pw)));
       pa.rows_per_cta = ceil_div(active, G);
+      pa.rows_per_cta += pa.rows_per_cta & 1;  // even: 16-byte aligned bulk copies of panel columns
       pa.above_per_cta = std::max<int64_t>(1, ceil_div(j0, G));
       const size_t smem = (size_t)pa.rows_per_cta * nb * sizeof(double);
       void* args[] = {&pa};
