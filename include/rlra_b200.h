@@ -111,7 +111,7 @@ RLRA_B200_API int rlra_b200_colsumsq(const double* a, int64_t lda, int64_t m, in
  * device; the caller resolves the rare tail draws (|x| > r; positions and the
  * following words are exposed by views()) with the host libm log1p and passes
  * them to finish(), which emits the n normals (flat == column-major order).
- * status (device int64[2]): {normals produced (== n on success), flags}. */
+ * status (device int64[3]): {normals produced (== n on success), flags, words consumed}. */
 RLRA_B200_API size_t rlra_b200_normal_workspace(int64_t n);
 RLRA_B200_API int64_t rlra_b200_normal_stream_words(int64_t n);
 RLRA_B200_API int64_t rlra_b200_normal_tail_cap(int64_t n);

@@ -102,3 +102,45 @@ def powerlu_flops(m, n, k, l, v):
         h = (v - 2) // 2
         fact += h * (gepp(m, l) + gepp(n, l))
     return passes, fact
+
+
+# ---------------------------------------------------------------- device builds
+def gen_device(name, device):
+    """Build config `name`'s A directly in HBM (column-major torch tensor).
+
+    Same recipe and random streams as the host generators: X and Y come from
+    the seeded NumPy stream and NumPy's QR on the host; the m x n noise is the
+    continuation of that same stream drawn by the bit-exact device generator;
+    A = (X diag(sigma)) Y^T is formed by the DMMA GEMM.  Equal to the host
+    build up to the GEMM's rounding (~1e-16 relative) -- the input generator
+    for C3-C5, whose host builds take minutes (C5: 68.7 GB)."""
+    import torch
+
+    from . import core, ops
+
+    spec = {
+        "C2": (20000, 10000, 400, 1.0 / np.arange(1, 401) ** 2, 1e-8, 2),
+        "C3": (16384, 16384, 1024, np.exp(-np.arange(1, 1025) / 60.0), 0.0, 3),
+        "C4": (50000, 50000, 300, np.arange(1, 301) ** -1.5, 1e-6, 4),
+        "C5": (262144, 32768, 640, 10.0 ** (-8.0 * np.arange(640) / 639), 1e-10, 5),
+    }[name]
+    m, n, r, sigma, noise, seed = spec
+    rng = np.random.default_rng(seed)
+    x, _ = np.linalg.qr(_gaussian_from(rng, m, r))
+    y, _ = np.linalg.qr(_gaussian_from(rng, n, r))
+    xs = ops.from_numpy(np.asfortranarray(x * sigma), device)
+    del x
+    yd = ops.from_numpy(y, device)
+    del y
+    a = ops.fmat(m, n, device)
+    ops.gemm(xs, yd, a, tb=True)
+    del xs, yd
+    if noise:
+        st = rng.bit_generator.state["state"]
+        flat = core.device_gaussian_flat(None, m * n, device, pcg_state=(int(st["state"]), int(st["inc"])))
+        if flat is None:
+            raise RuntimeError("device generator unavailable for the noise term")
+        a.add_(flat.view(n, m).t(), alpha=noise)
+        del flat
+    torch.cuda.synchronize(device)
+    return a

@@ -95,14 +95,44 @@ def _resolve_tails(words, nbits=16):
     return lens, vals
 
 
-def device_gaussian_flat(seed, count, device):
+_CHUNK = 1 << 28  # normals per device pass (workspace ~20 B per stream word)
+
+
+def device_gaussian_flat(seed, count, device, pcg_state=None, out=None):
     """gaussian(seed, count, 1).ravel() generated on the device (None if the
-    device generator is unavailable or reports a failure)."""
+    device generator is unavailable or reports a failure).  ``pcg_state`` =
+    (state, inc) continues an existing NumPy PCG64 stream instead.  Counts
+    beyond 2^28 are produced in chunks, each continuing the PCG64 stream at the
+    word where the previous chunk stopped (NumPy PCG64.advance)."""
     if not _device_rng or not ziggurat.validated():
         return None
+    state, inc = pcg_state if pcg_state is not None else ziggurat.pcg64_state(seed)
+    if out is None:
+        out = torch.empty(max(count, 1), dtype=torch.float64, device=device)
+    done = 0
+    while done < count:
+        n = min(_CHUNK, count - done)
+        used = _device_gaussian_chunk(state, inc, n, device, out[done:done + n])
+        if used is None:
+            return None
+        done += n
+        if done < count:
+            bg = np.random.PCG64()
+            st = bg.state
+            st["state"] = {"state": state, "inc": inc}
+            st["has_uint32"], st["uinteger"] = 0, 0
+            bg.state = st
+            bg.advance(used)
+            s2 = bg.state["state"]
+            state, inc = int(s2["state"]), int(s2["inc"])
+    return out[:count]
+
+
+def _device_gaussian_chunk(state, inc, count, device, out):
+    """One device pass: `count` normals from PCG64 (state, inc) into `out`;
+    returns the number of 64-bit words consumed, or None on failure."""
     lib = _native.load()
     ki, wi, fi = _device_tables(device)
-    state, inc = ziggurat.pcg64_state(seed)
     m64 = (1 << 64) - 1
     wsb = int(lib.rlra_b200_normal_workspace(count))
     ws = torch.empty(wsb, dtype=torch.uint8, device=device)
@@ -136,14 +166,13 @@ def device_gaussian_flat(seed, count, device):
         tl = torch.zeros(1, dtype=torch.int32, device=device)
         tv = torch.zeros(1, dtype=torch.float64, device=device)
         tp = torch.zeros(1, dtype=torch.int64, device=device)
-    out = torch.empty(max(count, 1), dtype=torch.float64, device=device)
-    status = torch.zeros(2, dtype=torch.int64, device=device)
+    status = torch.zeros(3, dtype=torch.int64, device=device)
     _native.call("rlra_b200_normal_finish", count, tp.data_ptr(), tl.data_ptr(), tv.data_ptr(), ntail,
                  out.data_ptr(), status.data_ptr(), ws.data_ptr(), wsb, st)
-    produced, flags = status.cpu().tolist()
+    produced, flags, used = status.cpu().tolist()
     if produced < count or flags:
         return None
-    return out[:count]
+    return used
 
 
 def omega(seed, m, n, device):

@@ -13,6 +13,12 @@
 //   T factor: Gram V^T V via the DMMA GEMM, then dlarft on one CTA;
 //   trailing: C -= V T^T (V^T C) as three DMMA GEMMs;
 //   orgqr:    Q = B_0 ... B_{P-1} [I; 0] accumulated backwards, GEMMs again.
+#include <cooperative_groups.h>
+
+#include <mutex>
+#include <set>
+#include <utility>
+
 #include "common.cuh"
 
 namespace rlra {
@@ -35,6 +41,7 @@ struct QrPanelArgs {
   double* tau;       // [n]
   unsigned* bar;
   unsigned bar_base;  // monotonic grid-barrier counter at kernel entry
+  double* recg;       // cluster panel: global staging of the multicast records
 };
 
 // Householder panel with the CTA's panel rows resident in SHARED MEMORY
@@ -140,6 +147,181 @@ __global__ void __launch_bounds__(THREADS, 1) qr_panel_smem_kernel(QrPanelArgs p
 
 static constexpr int QR_PANEL_SMEM_BYTES = 200 * 1024;
 
+// Cluster-resident Householder panel (<= 16 CTAs on one GPC, rows in shared
+// memory).  Per column each CTA computes its partial ||x||^2 and x . a_c
+// (c > jj) in a fixed order, stages them (plus row j when it owns it) in a
+// global slot and multicasts them with ONE bulk copy into every peer's shared
+// memory (completing on the peers' mbarriers); every CTA then sums the CS
+// partials in rank order -- identical, deterministic sums everywhere -- and
+// applies dlarfg and the rank-1 update to its rows.
+template <int PW, int THREADS>
+__global__ void __launch_bounds__(THREADS, 1) qr_panel_cluster_kernel(QrPanelArgs p) {
+  namespace cg = cooperative_groups;
+  constexpr int MAXCS = 16;
+  constexpr int RECQ = 2 + PW;  // {sum x^2, 0, sum x a_c (c < PW)}
+  constexpr int NW = THREADS / 32;
+  cg::cluster_group cluster = cg::this_cluster();
+  extern __shared__ __align__(16) double s_a[];
+  __shared__ __align__(16) double recv[2][MAXCS][RECQ];
+  __shared__ __align__(16) double recv_row[2][PW];
+  __shared__ __align__(8) uint64_t mbar[2];
+  __shared__ __align__(8) uint64_t ldbar;
+  __shared__ double s_part[RECQ];
+  __shared__ double s_w[PW + 1];
+  __shared__ double s_scal, s_tau, s_beta;
+
+  const int CS = (int)cluster.num_blocks(), b = (int)cluster.block_rank(), tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  const int nb = p.nb;
+  const int64_t R = p.rows_per_cta;
+  const int Ri = (int)R;
+  const int64_t rb = min(p.m, p.j0 + (int64_t)b * R);
+  const int64_t re = min(p.m, rb + R);
+  const int nr = (int)(re - rb);
+  const unsigned tx_bytes = CS * RECQ * 8u + PW * 8u;
+
+  if (tid == 0) {
+    mbar_init(&mbar[0], 1);
+    mbar_init(&mbar[1], 1);
+    mbar_init(&ldbar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  const bool bulk_ok = ((R & 1) == 0) && ((p.lda & 1) == 0) && ((rb & 1) == 0);
+  const int nr_bulk = bulk_ok ? (nr & ~1) : 0;
+  if (nr_bulk > 0 && tid == 0) {
+    mbar_arrive_expect_tx(&ldbar, (unsigned)(nb * nr_bulk * 8));
+    for (int c = 0; c < nb; c++)
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+              smem_u32(s_a + c * Ri)),
+          "l"(p.a + cm(rb, p.j0 + c, p.lda)), "r"((unsigned)(nr_bulk * 8)), "r"(smem_u32(&ldbar))
+          : "memory");
+  }
+  for (int c = 0; c < nb; c++)
+    for (int r = nr_bulk + tid; r < nr; r += THREADS) s_a[c * Ri + r] = p.a[cm(rb + r, p.j0 + c, p.lda)];
+  if (nr_bulk > 0) mbar_wait_parity(&ldbar, 0);
+  if (tid == 0) {
+    mbar_arrive_expect_tx(&mbar[0], tx_bytes);
+    mbar_arrive_expect_tx(&mbar[1], tx_bytes);
+  }
+  cluster.sync();  // mbarrier inits visible cluster-wide
+  unsigned phase_bits = 0u;
+
+  for (int jj = 0; jj < nb; jj++) {
+    const int64_t j = p.j0 + jj;
+    const int par = jj & 1;
+    const int r0 = (int)max((int64_t)0, j + 1 - rb);  // local rows strictly below row j
+    const double* x = s_a + jj * Ri;
+    // ---- partial sums, one warp per value (fixed order: lane-strided rows, xor tree)
+    const int cnt = nb - jj;  // value q: 0 -> ||x||^2, q >= 1 -> x . a_{jj+q}
+    for (int q = warp; q < cnt; q += NW) {
+      const double* y = s_a + (q == 0 ? jj : jj + q) * Ri;
+      double acc = 0.0;
+      for (int r = r0 + lane; r < nr; r += 32) acc += x[r] * y[r];
+#pragma unroll
+      for (int off = 16; off; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+      if (lane == 0) s_part[q == 0 ? 0 : 2 + jj + q] = acc;
+    }
+    __syncthreads();
+    if (warp == 0) {
+      // stage {sum x^2, 0, dots} (+ row j when this CTA owns it), multicast to all
+      double* slot = p.recg + ((int64_t)par * MAXCS + b) * RECQ;
+      double* rslot = p.recg + 2 * MAXCS * RECQ + par * PW;
+      for (int e = lane; e < RECQ; e += 32) {
+        double v = 0.0;
+        if (e == 0) v = s_part[0];
+        else if (e >= 2 + jj + 1 && e < 2 + nb) v = s_part[e];
+        slot[e] = v;
+      }
+      const bool own_j = (j >= rb && j < re);
+      if (own_j && lane < PW) rslot[lane] = lane < nb ? s_a[lane * Ri + (int)(j - rb)] : 0.0;
+      asm volatile("fence.proxy.async.global;\n" ::: "memory");
+      __syncwarp();
+      if (lane == 0) {
+        const unsigned short mask = (unsigned short)((1u << CS) - 1u);
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1], %2, [%3], %4;\n" ::"r"(
+                smem_u32(&recv[par][b][0])),
+            "l"(slot), "r"((unsigned)(RECQ * 8)), "r"(smem_u32(&mbar[par])), "h"(mask)
+            : "memory");
+        if (own_j)
+          asm volatile(
+              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1], %2, [%3], %4;\n" ::"r"(
+                  smem_u32(&recv_row[par][0])),
+              "l"(rslot), "r"((unsigned)(PW * 8)), "r"(smem_u32(&mbar[par])), "h"(mask)
+              : "memory");
+      }
+      mbar_wait_parity(&mbar[par], (phase_bits >> par) & 1u);
+      // fixed-order sums over the CS partials -> identical in every CTA
+      if (lane < RECQ && (lane == 0 || (lane >= 2 + jj + 1 && lane < 2 + nb))) {
+        double v = 0.0;
+        for (int q = 0; q < CS; q++) v += recv[par][q][lane];
+        if (lane == 0) s_w[0] = v;
+        else s_w[lane - 1] = v;  // s_w[1 + c] = x . a_c
+      }
+      if (lane + 32 < RECQ && lane + 32 < 2 + nb) {
+        double v = 0.0;
+        for (int q = 0; q < CS; q++) v += recv[par][q][lane + 32];
+        s_w[lane + 31] = v;
+      }
+      __syncwarp();
+      if (lane == 0) {
+        // dlarfg: alpha = a(j,j), xnorm = ||a(j+1:m, j)||
+        const double alpha = recv_row[par][jj];
+        const double xnorm = sqrt(s_w[0]);
+        if (xnorm == 0.0) {
+          s_tau = 0.0;
+          s_beta = alpha;
+          s_scal = 0.0;
+        } else {
+          const double beta = -copysign(hypot(alpha, xnorm), alpha);
+          s_tau = (beta - alpha) / beta;
+          s_scal = 1.0 / (alpha - beta);
+          s_beta = beta;
+        }
+        if (b == 0) p.tau[j] = s_tau;
+      }
+      __syncwarp();
+      if (lane < nb && lane > jj && s_tau != 0.0)
+        s_w[lane + 1] = s_tau * (recv_row[par][lane] + s_scal * s_w[lane + 1]);
+      __syncwarp();
+      if (lane == 0) mbar_arrive_expect_tx(&mbar[par], tx_bytes);  // re-arm for step jj + 2
+      phase_bits ^= 1u << par;
+    }
+    __syncthreads();
+    const double tau = s_tau, scal = s_scal;
+    if (tau != 0.0) {
+      double* xc = s_a + jj * Ri;
+      for (int r = r0 + tid; r < nr; r += THREADS) {
+        const double vi = xc[r] * scal;
+        xc[r] = vi;
+        for (int c = jj + 1; c < nb; c++) s_a[c * Ri + r] -= s_w[c + 1] * vi;
+      }
+      if (j >= rb && j < re && tid < nb) {
+        if (tid > jj) s_a[tid * Ri + (int)(j - rb)] = recv_row[par][tid] - s_w[tid + 1];
+        if (tid == jj) s_a[tid * Ri + (int)(j - rb)] = s_beta;
+      }
+    }
+    __syncthreads();
+  }
+  if (nr_bulk > 0) {
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    __syncthreads();
+    if (tid < nb) {
+      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(
+                       p.a + cm(rb, p.j0 + tid, p.lda)),
+                   "r"(smem_u32(s_a + tid * Ri)), "r"((unsigned)(nr_bulk * 8))
+                   : "memory");
+      asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+    }
+  }
+  for (int c = 0; c < nb; c++)
+    for (int r = nr_bulk + tid; r < nr; r += THREADS) p.a[cm(rb + r, p.j0 + c, p.lda)] = s_a[c * Ri + r];
+  if (nr_bulk > 0 && tid < nb) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+  cluster.sync();
+}
+
 // Explicit V (rows j0..m-1 of the panel, unit diagonal, zeros above) for the GEMMs.
 __global__ void qr_make_v_kernel(const double* __restrict__ a, int64_t lda, int64_t j0, int64_t rows,
                                  int nb, double* __restrict__ v, int64_t ldv) {
@@ -199,7 +381,7 @@ static int qr_pw(int64_t m, int sms) {
 }
 
 struct QrLayout {
-  size_t part, diag, bar, vbuf, gram, tblocks, wbuf, w2buf, gemm_ws, total;
+  size_t part, diag, bar, recg, vbuf, gram, tblocks, wbuf, w2buf, gemm_ws, total;
 };
 
 static QrLayout qr_layout(int64_t m, int64_t n, int G) {
@@ -210,6 +392,7 @@ static QrLayout qr_layout(int64_t m, int64_t n, int G) {
   take(L.part, 2 * (size_t)G * (QR_NB + 1) * sizeof(double));
   take(L.diag, 2 * QR_NB * sizeof(double));
   take(L.bar, 2 * sizeof(unsigned));
+  take(L.recg, (size_t)(2 * 16 * (2 + QR_NB) + 2 * QR_NB) * sizeof(double));
   take(L.vbuf, (size_t)m * QR_NB * sizeof(double));
   take(L.gram, QR_NB * QR_NB * sizeof(double));
   take(L.tblocks, (size_t)npan * QR_NB * QR_NB * sizeof(double));
@@ -225,6 +408,56 @@ static QrLayout qr_layout(int64_t m, int64_t n, int G) {
 
 size_t geqrf_workspace_bytes(int64_t m, int64_t n) {
   return qr_layout(m, n, device_info().sm_count).total;
+}
+
+// Largest cluster (<= 16) that co-schedules one 512-thread CTA with the full
+// panel shared memory per SM; 1 when clusters are unavailable.
+static int qr_max_cluster() {
+  static int cached[64];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 1;
+  if (cached[dev & 63]) return cached[dev & 63];
+  int best = 1;
+  const void* kern = (const void*)qr_panel_cluster_kernel<16, 512>;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, QR_PANEL_SMEM_BYTES) ==
+          cudaSuccess &&
+      cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess) {
+    for (int cs = 16; cs >= 2; cs /= 2) {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(cs);
+      cfg.blockDim = dim3(512);
+      cfg.dynamicSmemBytes = QR_PANEL_SMEM_BYTES;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = cs;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      int ncl = 0;
+      if (cudaOccupancyMaxActiveClusters(&ncl, kern, &cfg) == cudaSuccess && ncl > 0) {
+        best = cs;
+        break;
+      }
+    }
+  }
+  cudaGetLastError();
+  cached[dev & 63] = best;
+  return best;
+}
+
+static int qr_prepare_kernel(const void* kern) {
+  static std::mutex mu;
+  static std::set<std::pair<int, const void*>> done;
+  int dev = 0;
+  RLRA_CHECK_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(mu);
+  if (done.count({dev, kern})) return 0;
+  RLRA_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, QR_PANEL_SMEM_BYTES));
+  cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  cudaGetLastError();
+  done.insert({dev, kern});
+  return 0;
 }
 
 static int grid_for_q(int64_t total) {
@@ -251,33 +484,49 @@ int geqrf(double* a, int64_t lda, int64_t m, int64_t n, double* tau, void* ws, s
   void* gws = base + L.gemm_ws;
   const size_t gws_bytes = L.total - L.gemm_ws;
   RLRA_CHECK_CUDA(cudaMemsetAsync(bar, 0, 2 * sizeof(unsigned), st));
-  const int pw = qr_pw(m, sms);
+  // Panel: one thread-block cluster (DSMEM multicast exchange) while the rows
+  // fit 16 CTAs' shared memory, else one CTA per SM with a grid barrier.
+  const int cmax = qr_max_cluster();
+  const bool use_cluster = cmax > 1 && m <= cmax * qr_rows_cap(16);
+  const int pw = use_cluster ? (m <= cmax * qr_rows_cap(32) ? 32 : 16) : qr_pw(m, sms);
   RLRA_REQUIRE(m <= sms * qr_rows_cap(8), "geqrf: m = %lld exceeds the panel capacity", (long long)m);
-  const void* kern = (const void*)qr_panel_smem_kernel<256>;
-  {
-    static unsigned attr_mask = 0;
-    int dev = 0;
-    RLRA_CHECK_CUDA(cudaGetDevice(&dev));
-    if (!(attr_mask & (1u << (dev & 31)))) {
-      RLRA_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           QR_PANEL_SMEM_BYTES));
-      attr_mask |= 1u << (dev & 31);
-    }
-  }
+  const void* kern = use_cluster ? (pw == 32 ? (const void*)qr_panel_cluster_kernel<32, 512>
+                                             : (const void*)qr_panel_cluster_kernel<16, 512>)
+                                 : (const void*)qr_panel_smem_kernel<256>;
+  if (qr_prepare_kernel(kern)) return -1;
   unsigned bar_base = 0;
   for (int64_t j0 = 0, pidx = 0; j0 < n; j0 += pw, pidx++) {
     const int nb = (int)std::min<int64_t>(pw, n - j0);
     const int64_t rows = m - j0;
-    const int64_t target = std::min<int64_t>(qr_rows_cap(pw), 256);
-    int G = (int)std::min<int64_t>(sms, ceil_div(rows, target));
+    const int limit = use_cluster ? cmax : sms;
+    const int64_t target = std::min<int64_t>(qr_rows_cap(pw), use_cluster ? 512 : 256);
+    int G = (int)std::min<int64_t>(limit, ceil_div(rows, target));
     G = (int)std::max<int64_t>(G, ceil_div(rows, qr_rows_cap(pw)));
-    QrPanelArgs pa{a, lda, m, j0, nb, ceil_div(rows, G),
+    int64_t R = ceil_div(rows, G);
+    R += R & 1;  // even: 16-byte aligned bulk copies of the panel columns
+    QrPanelArgs pa{a, lda, m, j0, nb, R,
                    reinterpret_cast<double*>(base + L.part), reinterpret_cast<double*>(base + L.diag),
-                   tau, bar, bar_base};
-    bar_base += (unsigned)G * nb;
+                   tau, bar, bar_base, reinterpret_cast<double*>(base + L.recg)};
     const size_t smem = (size_t)pa.rows_per_cta * nb * sizeof(double);
     void* args[] = {&pa};
-    RLRA_CHECK_CUDA(cudaLaunchCooperativeKernel(kern, dim3(G), dim3(256), args, smem, st));
+    if (use_cluster) {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(G);
+      cfg.blockDim = dim3(512);
+      cfg.dynamicSmemBytes = smem;
+      cfg.stream = st;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = G;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      RLRA_CHECK_CUDA(cudaLaunchKernelExC(&cfg, kern, args));
+    } else {
+      RLRA_CHECK_CUDA(cudaLaunchCooperativeKernel(kern, dim3(G), dim3(256), args, smem, st));
+      bar_base += (unsigned)G * nb;
+    }
     note_launch();
     // explicit V and the T factor of this panel
     qr_make_v_kernel<<<grid_for_q(rows * nb), 256, 0, st>>>(a, lda, j0, rows, nb, vbuf, rows);
@@ -315,7 +564,9 @@ int orgqr(const double* a, int64_t lda, int64_t m, int64_t n, double* q, int64_t
   const size_t gws_bytes = L.total - L.gemm_ws;
   set_identity_kernel<<<grid_for_q(m * n), 256, 0, st>>>(q, ldq, m, n);
   RLRA_LAUNCHED();
-  const int pw = qr_pw(m, sms);
+  const int cmax = qr_max_cluster();
+  const bool use_cluster = cmax > 1 && m <= cmax * qr_rows_cap(16);
+  const int pw = use_cluster ? (m <= cmax * qr_rows_cap(32) ? 32 : 16) : qr_pw(m, sms);
   const int64_t npan = ceil_div(n, pw);
   for (int64_t pidx = npan - 1; pidx >= 0; pidx--) {
     const int64_t j0 = pidx * pw;

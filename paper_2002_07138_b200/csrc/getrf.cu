@@ -371,43 +371,6 @@ struct LuRec {
   double row[PW];
 };
 
-__device__ __forceinline__ unsigned smem_u32(const void* p) {
-  return static_cast<unsigned>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ unsigned mapa_u32(unsigned addr, int rank) {
-  unsigned r;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(addr), "r"(rank));
-  return r;
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait_parity(uint64_t* bar, unsigned parity) {
-  const unsigned a = smem_u32(bar);
-  asm volatile(
-      "{\n"
-      ".reg .pred P1;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
-      "@!P1 bra WAIT_%=;\n"
-      "}\n" ::"r"(a), "r"(parity)
-      : "memory");
-}
-// local smem [src, src+bytes) -> peer smem dst (shared::cluster), completing
-// `bytes` of transactions on the peer's mbarrier
-__device__ __forceinline__ void bulk_push(unsigned dst_cluster, const void* src, unsigned bytes,
-                                          unsigned mbar_cluster) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
-          dst_cluster),
-      "r"(smem_u32(src)), "r"(bytes), "r"(mbar_cluster)
-      : "memory");
-}
-
 template <int PW, int THREADS>
 __global__ void __launch_bounds__(THREADS, 1) lu_panel_cluster_kernel(PanelArgs p) {
   namespace cg = cooperative_groups;
@@ -776,8 +739,10 @@ __global__ void lu_laswp_kernel(double* a, int64_t lda, int64_t n, int64_t j0, i
   }
 }
 
-// U12 = L11^{-1} A12 by forward substitution in ascending step order, one thread
-// per column; zero-pivot steps are skipped (the reference never applies them).
+// U12 = L11^{-1} A12 by forward substitution in ascending step order, one WARP
+// per column (lane s holds row j0+s; step t broadcasts x[t]); zero-pivot steps
+// are skipped (the reference never applies them).  Same operation order per
+// element as the reference: bit-exact.
 __global__ void lu_trsm_kernel(double* a, int64_t lda, int64_t j0, int nb, int64_t c0, int64_t n,
                                const int* zflag) {
   __shared__ double L[LU_NB][LU_NB + 1];
@@ -788,22 +753,16 @@ __global__ void lu_trsm_kernel(double* a, int64_t lda, int64_t j0, int nb, int64
   }
   if (threadIdx.x < nb) z[threadIdx.x] = zflag[j0 + threadIdx.x];
   __syncthreads();
-  for (int64_t c = c0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < n;
-       c += (int64_t)gridDim.x * blockDim.x) {
-    double x[LU_NB];
+  const int lane = threadIdx.x & 31;
+  const int64_t wpb = blockDim.x >> 5;
+  for (int64_t c = c0 + blockIdx.x * wpb + (threadIdx.x >> 5); c < n; c += (int64_t)gridDim.x * wpb) {
     double* col = a + cm(j0, c, lda);
-#pragma unroll
-    for (int s = 0; s < LU_NB; s++) x[s] = s < nb ? col[s] : 0.0;
-#pragma unroll
-    for (int t = 0; t < LU_NB; t++) {
-      if (t >= nb || z[t]) continue;
-#pragma unroll
-      for (int s = t + 1; s < LU_NB; s++)
-        if (s < nb) x[s] = sub_mul_nofma(x[s], L[s][t], x[t]);
+    double x = lane < nb ? col[lane] : 0.0;
+    for (int t = 0; t < nb - 1; t++) {
+      const double xt = __shfl_sync(0xffffffffu, x, t);
+      if (!z[t] && lane > t && lane < nb) x = sub_mul_nofma(x, L[lane][t], xt);
     }
-#pragma unroll
-    for (int s = 1; s < LU_NB; s++)
-      if (s < nb) col[s] = x[s];
+    if (lane > 0 && lane < nb) col[lane] = x;
   }
 }
 
@@ -1085,7 +1044,7 @@ int getrf(double* a, int64_t lda, int64_t m, int64_t n, int64_t* piv, int64_t* n
       }
       const int64_t c0 = j0 + nb;
       if (c0 < ce) {  // inner update, restricted to the outer block's columns
-        lu_trsm_kernel<<<1, 128, 0, st>>>(a, lda, j0, nb, c0, ce, w.zflag);
+        lu_trsm_kernel<<<(unsigned)ceil_div(ce - c0, 4), 128, 0, st>>>(a, lda, j0, nb, c0, ce, w.zflag);
         RLRA_LAUNCHED();
         if (c0 < m) {
           dim3 grid((unsigned)ceil_div(m - c0, UPD_TM), (unsigned)ceil_div(ce - c0, UPD_TN));
@@ -1095,7 +1054,7 @@ int getrf(double* a, int64_t lda, int64_t m, int64_t n, int64_t* piv, int64_t* n
       }
     }
     if (ce < n) {  // outer trailing update with the whole 32-column block
-      int blocks = (int)std::min<int64_t>(ceil_div(n - ce, 128), 1024);
+      int blocks = (int)std::min<int64_t>(ceil_div(n - ce, 4), 4096);
       lu_trsm_kernel<<<blocks, 128, 0, st>>>(a, lda, jo, nbo, ce, n, w.zflag);
       RLRA_LAUNCHED();
       if (ce < m) {

@@ -273,7 +273,7 @@ __global__ void zig_propagate_kernel(const int8_t* __restrict__ fe, const CNT* _
 __global__ void zig_emit_kernel(const int* __restrict__ len, const double* __restrict__ val, int64_t T,
                                 int64_t nchunks, const int8_t* __restrict__ entry,
                                 const int64_t* __restrict__ prefix, int64_t N, double* __restrict__ out,
-                                unsigned long long* __restrict__ produced) {
+                                unsigned long long* __restrict__ produced, int64_t* __restrict__ consumed) {
   const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (c >= nchunks) return;
   if (entry[c] < 0) return;
@@ -286,6 +286,7 @@ __global__ void zig_emit_kernel(const int* __restrict__ len, const double* __res
     out[k] = val[pos];
     k++;
     pos += L;
+    if (k == N) *consumed = pos;  // words used by the N normals (stream continuation)
   }
   if (k >= N || pos >= end) {
     if (k > prefix[c]) atomicMax(produced, (unsigned long long)k);
@@ -370,7 +371,8 @@ int normal_views(int64_t N, void* ws, uint64_t** u, int64_t** tail_pos, unsigned
 
 // Phase 2: install the host-resolved tails, resolve rejection chains, run the
 // transducer scan and emit N normals to out.  *status_dev (device int64):
-// [0] normals produced (== N on success), [1] failure flags (0 on success).
+// [0] normals produced (== N on success), [1] failure flags (0 on success),
+// [2] 64-bit words consumed (to continue the stream in the next chunk).
 int normal_phase2(int64_t N, const int64_t* tpos, const int* tlen, const double* tval, int64_t ntail,
                   double* out, int64_t* status_dev, void* ws, size_t ws_bytes, cudaStream_t st) {
   const int64_t T = normal_stream_words(N), cap = normal_tail_cap(N);
@@ -435,9 +437,10 @@ int normal_phase2(int64_t N, const int64_t* tpos, const int* tlen, const double*
         fe0, fc0, nch, lvls[0].en, lvls[0].pf, en0, pf0);
     RLRA_LAUNCHED();
   }
-  zig_emit_kernel<<<(unsigned)ceil_div(nch, 128), 128, 0, st>>>(len, val, T, nch, en0, pf0, N, out, produced);
+  zig_emit_kernel<<<(unsigned)ceil_div(nch, 128), 128, 0, st>>>(len, val, T, nch, en0, pf0, N, out, produced,
+                                                                 status_dev + 2);
   RLRA_LAUNCHED();
-  // status_dev[0] = normals produced (== N on success), status_dev[1] = failure flags
+  // status_dev[0] = normals produced (== N on success), [1] failure flags, [2] set by emit
   RLRA_CHECK_CUDA(cudaMemcpyAsync(status_dev, produced, 8, cudaMemcpyDeviceToDevice, st));
   RLRA_CHECK_CUDA(cudaMemsetAsync(status_dev + 1, 0, 8, st));
   RLRA_CHECK_CUDA(cudaMemcpyAsync(status_dev + 1, flag, 4, cudaMemcpyDeviceToDevice, st));

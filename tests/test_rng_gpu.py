@@ -29,3 +29,19 @@ def test_omega_prefix_property_and_layout(cuda_dev):
     b = ops.to_numpy(core.omega(9, 300, 3, cuda_dev))
     assert np.array_equal(a, core.gaussian(9, 300, 7))
     assert np.array_equal(a[:, :3], b)
+
+
+def test_device_gaussian_chunked_stream_continuation(cuda_dev, monkeypatch):
+    """Counts beyond one device pass continue the PCG64 stream exactly."""
+    from paper_2002_07138_b200 import core
+
+    monkeypatch.setattr(core, "_CHUNK", 100_000)
+    got = core.device_gaussian_flat(77, 350_001, cuda_dev)
+    ref = np.random.default_rng(77).standard_normal(350_001)
+    assert np.array_equal(got.cpu().numpy().view(np.int64), ref.view(np.int64))
+    # continuing a stream mid-way (the C2-C5 noise term recipe)
+    rng = np.random.default_rng(3)
+    rng.standard_normal(12345)
+    st = rng.bit_generator.state["state"]
+    got = core.device_gaussian_flat(None, 200_000, cuda_dev, pcg_state=(int(st["state"]), int(st["inc"])))
+    assert np.array_equal(got.cpu().numpy(), rng.standard_normal(200_000))
