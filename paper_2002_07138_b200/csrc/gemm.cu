@@ -307,7 +307,7 @@ static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 
 bool tma_gemm_eligible(bool ta, bool tb, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda,
                        const double* B, int64_t ldb);
 size_t tma_gemm_workspace_bytes(int64_t M, int64_t N, int64_t K);
-int tma_gemm(bool ta, int64_t M, int64_t N, int64_t K, double alpha, const double* A, int64_t lda,
+int tma_gemm(bool ta, bool tb, int64_t M, int64_t N, int64_t K, double alpha, const double* A, int64_t lda,
              const double* B, int64_t ldb, double beta, double* C, int64_t ldc, void* ws, size_t ws_bytes,
              cudaStream_t st);
 
@@ -339,7 +339,7 @@ int gemm(bool ta, bool tb, int64_t M, int64_t N, int64_t K, double alpha, const 
   if (M == 0 || N == 0) return 0;
   RLRA_REQUIRE(ldc >= M, "gemm: ldc < M");
   if (tma_gemm_eligible(ta, tb, M, N, K, A, lda, B, ldb))
-    return tma_gemm(ta, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, ws, ws_bytes, st);
+    return tma_gemm(ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, ws, ws_bytes, st);
   // K == 0 runs one split with no k-tiles: the epilogue writes alpha*0 + beta*C.
   TileChoice tc = choose_tile(N);
   int64_t tiles = ceil_div(M, tc.bm) * ceil_div(N, tc.bn);

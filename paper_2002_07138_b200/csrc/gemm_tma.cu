@@ -73,7 +73,7 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
                : "d"(a), "d"(b));
 }
 
-template <int WARPS_M, int WARPS_N, int WM, int WN, int STAGES, bool TA>
+template <int WARPS_M, int WARPS_N, int WM, int WN, int STAGES, bool TA, bool TB>
 struct TmaCfg {
   static constexpr int BM = WARPS_M * WM * 8;
   static constexpr int BN = WARPS_N * WN * 8;
@@ -87,11 +87,11 @@ struct TmaCfg {
   static constexpr int SMEM_BYTES = STAGES * (A_BYTES + B_BYTES) + 2 * STAGES * 8 + 1024;
 };
 
-template <int WARPS_M, int WARPS_N, int WM, int WN, int STAGES, bool TA>
+template <int WARPS_M, int WARPS_N, int WM, int WN, int STAGES, bool TA, bool TB>
 __global__ void __launch_bounds__(WARPS_M * WARPS_N * 32, 1)
 dgemm_tma_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
                  TmaGemmArgs p) {
-  using Cfg = TmaCfg<WARPS_M, WARPS_N, WM, WN, STAGES, TA>;
+  using Cfg = TmaCfg<WARPS_M, WARPS_N, WM, WN, STAGES, TA, TB>;
   constexpr int BM = Cfg::BM, BN = Cfg::BN, BK = Cfg::BK;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   // 1024-byte aligned stage buffers
@@ -130,7 +130,8 @@ dgemm_tma_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant
     const int kg = (int)((kt_begin + it) * (BK / 4));  // k group index (units of 4)
     if (TA) tma_load_3d(As + s * Cfg::A_STAGE, &mapA, &full[s], 0, (int)m0, kg);
     else tma_load_3d(As + s * Cfg::A_STAGE, &mapA, &full[s], 0, kg * 4, (int)(m0 / 4));
-    tma_load_3d(Bs + s * Cfg::B_STAGE, &mapB, &full[s], 0, (int)n0, kg);
+    if (TB) tma_load_3d(Bs + s * Cfg::B_STAGE, &mapB, &full[s], 0, kg * 4, (int)(n0 / 4));
+    else tma_load_3d(Bs + s * Cfg::B_STAGE, &mapB, &full[s], 0, (int)n0, kg);
   };
   if (tid == 0) {
     asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&mapA)) : "memory");
@@ -162,7 +163,10 @@ dgemm_tma_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant
         af[i] = TA ? as[(kb * BM + m) * 4 + t] : as[((m >> 2) * BK + kb * 4 + t) * 4 + (m & 3)];
       }
 #pragma unroll
-      for (int j = 0; j < WN; j++) bf[j] = bs[(kb * BN + wn0 + j * 8 + g) * 4 + t];
+      for (int j = 0; j < WN; j++) {
+        const int n = wn0 + j * 8 + g;
+        bf[j] = TB ? bs[((n >> 2) * BK + kb * 4 + t) * 4 + (n & 3)] : bs[(kb * BN + n) * 4 + t];
+      }
 #pragma unroll
       for (int i = 0; i < WM; i++)
 #pragma unroll
@@ -246,11 +250,11 @@ static TmaTile tma_choose_tile(int64_t N) {
   return best;
 }
 
-template <int WN, bool TA>
+template <int WN, bool TA, bool TB>
 static int tma_launch(const CUtensorMap& ma, const CUtensorMap& mb, TmaGemmArgs& a, cudaStream_t st) {
   constexpr int STAGES = 6;
-  using Cfg = TmaCfg<4, 2, 4, WN, STAGES, TA>;
-  auto kern = dgemm_tma_kernel<4, 2, 4, WN, STAGES, TA>;
+  using Cfg = TmaCfg<4, 2, 4, WN, STAGES, TA, TB>;
+  auto kern = dgemm_tma_kernel<4, 2, 4, WN, STAGES, TA, TB>;
   static unsigned mask = 0;
   int dev = 0;
   RLRA_CHECK_CUDA(cudaGetDevice(&dev));
@@ -291,7 +295,8 @@ static SplitPlanT tma_plan(int64_t M, int64_t N, int bm, int bn, int64_t tiles, 
 
 bool tma_gemm_eligible(bool ta, bool tb, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda,
                        const double* B, int64_t ldb) {
-  if (tb || K <= 0 || M <= 0 || N <= 0) return false;
+  if (K <= 0 || M <= 0 || N <= 0) return false;
+  if (tb && (N & 3)) return false;
   if ((reinterpret_cast<uintptr_t>(A) & 15) || (reinterpret_cast<uintptr_t>(B) & 15)) return false;
   if ((lda & 1) || (ldb & 1) || (K & 3)) return false;
   if (!ta && (M & 3)) return false;
@@ -310,7 +315,7 @@ size_t tma_gemm_workspace_bytes(int64_t M, int64_t N, int64_t K) {
 int splitk_reduce(const double* partial, int splits, int64_t M, int64_t N, double alpha, double beta,
                   double* C, int64_t ldc, cudaStream_t st);
 
-int tma_gemm(bool ta, int64_t M, int64_t N, int64_t K, double alpha, const double* A, int64_t lda,
+int tma_gemm(bool ta, bool tb, int64_t M, int64_t N, int64_t K, double alpha, const double* A, int64_t lda,
              const double* B, int64_t ldb, double beta, double* C, int64_t ldc, void* ws, size_t ws_bytes,
              cudaStream_t st) {
   TmaTile tt = tma_choose_tile(N);
@@ -321,7 +326,10 @@ int tma_gemm(bool ta, int64_t M, int64_t N, int64_t K, double alpha, const doubl
     ok = encode3d(&ma, A, 4, (uint64_t)M, (uint64_t)(K / 4), (uint64_t)lda * 8, 32, 4, BM, 4);
   else  // A: dims {4 m, K, M/4}, strides {lda*8, 32}
     ok = encode3d(&ma, A, 4, (uint64_t)K, (uint64_t)(M / 4), (uint64_t)lda * 8, 32, 4, 16, BM / 4);
-  ok = ok && encode3d(&mb, B, 4, (uint64_t)N, (uint64_t)(K / 4), (uint64_t)ldb * 8, 32, 4, tt.bn, 4);
+  if (tb)  // B^T with B N x K (n contiguous): dims {4 n, K, N/4}
+    ok = ok && encode3d(&mb, B, 4, (uint64_t)K, (uint64_t)(N / 4), (uint64_t)ldb * 8, 32, 4, 16, tt.bn / 4);
+  else  // B (K x N, k contiguous): dims {4 k, N, K/4}
+    ok = ok && encode3d(&mb, B, 4, (uint64_t)N, (uint64_t)(K / 4), (uint64_t)ldb * 8, 32, 4, tt.bn, 4);
   RLRA_REQUIRE(ok, "tma_gemm: cuTensorMapEncodeTiled failed");
   int64_t tiles = ceil_div(M, BM) * ceil_div(N, tt.bn);
   int64_t ktiles = ceil_div(K, 16);
@@ -333,12 +341,16 @@ int tma_gemm(bool ta, int64_t M, int64_t N, int64_t K, double alpha, const doubl
     a.partial = static_cast<double*>(ws);
   }
   int rc;
+#define RLRA_TMA_CASE(WN)                                                             \
+  rc = ta ? (tb ? tma_launch<WN, true, true>(ma, mb, a, st) : tma_launch<WN, true, false>(ma, mb, a, st)) \
+          : (tb ? tma_launch<WN, false, true>(ma, mb, a, st) : tma_launch<WN, false, false>(ma, mb, a, st))
   switch (tt.which) {
-    case 0: rc = ta ? tma_launch<8, true>(ma, mb, a, st) : tma_launch<8, false>(ma, mb, a, st); break;
-    case 1: rc = ta ? tma_launch<7, true>(ma, mb, a, st) : tma_launch<7, false>(ma, mb, a, st); break;
-    case 2: rc = ta ? tma_launch<6, true>(ma, mb, a, st) : tma_launch<6, false>(ma, mb, a, st); break;
-    default: rc = ta ? tma_launch<5, true>(ma, mb, a, st) : tma_launch<5, false>(ma, mb, a, st); break;
+    case 0: RLRA_TMA_CASE(8); break;
+    case 1: RLRA_TMA_CASE(7); break;
+    case 2: RLRA_TMA_CASE(6); break;
+    default: RLRA_TMA_CASE(5); break;
   }
+#undef RLRA_TMA_CASE
   if (rc) return rc;
   if (sp.splits > 1) return splitk_reduce(a.partial, sp.splits, M, N, alpha, beta, C, ldc, st);
   return 0;
