@@ -42,8 +42,6 @@ struct QrPanelArgs {
   unsigned* bar;
   unsigned bar_base;  // monotonic grid-barrier counter at kernel entry
   double* recg;       // cluster panel: global staging of the multicast records
-  double* gram;       // cluster panel: [16][QR_NB][QR_NB] partial Gram matrices of V
-  double* T_out;      // cluster panel: the panel's QR_NB x QR_NB T factor (dlarft), ld nb
 };
 
 // Householder panel with the CTA's panel rows resident in SHARED MEMORY
@@ -320,61 +318,8 @@ __global__ void __launch_bounds__(THREADS, 1) qr_panel_cluster_kernel(QrPanelArg
   }
   for (int c = 0; c < nb; c++)
     for (int r = nr_bulk + tid; r < nr; r += THREADS) p.a[cm(rb + r, p.j0 + c, p.lda)] = s_a[c * Ri + r];
-  // ---- partial Gram V_b^T V_b of this CTA's rows (v_c(i) = 1 at i = j0 + c,
-  // a(i, c) below, 0 above), one warp per (c1 < c2) pair, fixed order
-  {
-    double* gp = p.gram + (int64_t)b * QR_NB * QR_NB;
-    for (int e = warp; e < nb * nb; e += NW) {
-      const int c1 = e % nb, c2 = e / nb;
-      if (c1 >= c2) continue;
-      double acc = 0.0;
-      for (int r = lane; r < nr; r += 32) {
-        const int64_t i = rb + r;
-        const int64_t d1 = i - (p.j0 + c1), d2 = i - (p.j0 + c2);
-        const double v1 = d1 > 0 ? s_a[c1 * Ri + r] : (d1 == 0 ? 1.0 : 0.0);
-        const double v2 = d2 > 0 ? s_a[c2 * Ri + r] : (d2 == 0 ? 1.0 : 0.0);
-        acc += v1 * v2;
-      }
-#pragma unroll
-      for (int off = 16; off; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
-      if (lane == 0) gp[c1 + c2 * QR_NB] = acc;
-    }
-  }
   if (nr_bulk > 0 && tid < nb) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
-  __threadfence();
   cluster.sync();
-  // ---- CTA 0: Gram = sum of the partials in rank order (all threads, into
-  // shared memory), then dlarft (forward, columnwise) on warp 0:
-  // T(i,i) = tau_i, T(0:i, i) = -tau_i T(0:i, 0:i) Gram(0:i, i)
-  if (b == 0) {
-    __shared__ double Gs[QR_NB][QR_NB + 1];
-    __shared__ double Ts[QR_NB][QR_NB + 1];
-    __shared__ double gy[QR_NB];
-    for (int e = tid; e < QR_NB * QR_NB; e += THREADS) {
-      const int c1 = e % QR_NB, c2 = e / QR_NB;
-      double g = 0.0;
-      if (c1 < c2 && c2 < nb)
-        for (int q = 0; q < CS; q++) g += __ldcg(p.gram + (int64_t)q * QR_NB * QR_NB + c1 + c2 * QR_NB);
-      Gs[c1][c2] = g;
-      Ts[c1][c2] = 0.0;
-    }
-    __syncthreads();
-    if (warp == 0) {
-      for (int i = 0; i < nb; i++) {
-        const double ti = p.tau[p.j0 + i];
-        if (lane < i) gy[lane] = -ti * Gs[lane][i];
-        __syncwarp();
-        if (lane < i) {
-          double acc = 0.0;
-          for (int k = lane; k < i; k++) acc += Ts[lane][k] * gy[k];
-          Ts[lane][i] = acc;
-        }
-        if (lane == 0) Ts[i][i] = ti;
-        __syncwarp();
-      }
-      for (int e = lane; e < nb * nb; e += 32) p.T_out[e] = Ts[e % nb][e / nb];
-    }
-  }
 }
 
 // Explicit V (rows j0..m-1 of the panel, unit diagonal, zeros above) for the GEMMs.
@@ -392,26 +337,36 @@ __global__ void qr_make_v_kernel(const double* __restrict__ a, int64_t lda, int6
 
 // dlarft (forward, columnwise) from the Gram matrix S = V^T V:
 // T(i,i) = tau_i ; T(0:i, i) = -tau_i * T(0:i,0:i) * S(0:i, i)
+// The block stages S and tau in shared memory; warp 0 runs the recurrence.
 __global__ void qr_larft_kernel(const double* __restrict__ gram, int nb, const double* __restrict__ tau,
                                 double* __restrict__ T) {
+  __shared__ double Ss[QR_NB][QR_NB + 1];
   __shared__ double Ts[QR_NB][QR_NB + 1];
-  __shared__ double y[QR_NB];
-  const int t = threadIdx.x;
-  for (int e = t; e < QR_NB * QR_NB; e += blockDim.x) Ts[e % QR_NB][e / QR_NB] = 0.0;
-  __syncthreads();
-  for (int i = 0; i < nb; i++) {
-    const double ti = tau[i];
-    if (t < i) y[t] = -ti * gram[t + i * nb];
-    __syncthreads();
-    if (t < i) {
-      double s = 0.0;
-      for (int k = t; k < i; k++) s += Ts[t][k] * y[k];
-      Ts[t][i] = s;
-    }
-    if (t == 0) Ts[i][i] = ti;
-    __syncthreads();
+  __shared__ double ts[QR_NB], y[QR_NB];
+  for (int e = threadIdx.x; e < QR_NB * QR_NB; e += blockDim.x) {
+    const int r = e % QR_NB, c = e / QR_NB;
+    Ss[r][c] = (r < nb && c < nb) ? gram[r + c * nb] : 0.0;
+    Ts[r][c] = 0.0;
   }
-  for (int e = t; e < nb * nb; e += blockDim.x) T[e] = Ts[e % nb][e / nb];
+  if (threadIdx.x < nb) ts[threadIdx.x] = tau[threadIdx.x];
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    const int t = threadIdx.x;
+    for (int i = 0; i < nb; i++) {
+      const double ti = ts[i];
+      if (t < i) y[t] = -ti * Ss[t][i];
+      __syncwarp();
+      if (t < i) {
+        double acc = 0.0;
+        for (int k = t; k < i; k++) acc += Ts[t][k] * y[k];
+        Ts[t][i] = acc;
+      }
+      if (t == 0) Ts[i][i] = ti;
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < nb * nb; e += blockDim.x) T[e] = Ts[e % nb][e / nb];
 }
 
 __global__ void set_identity_kernel(double* q, int64_t ldq, int64_t m, int64_t n) {
@@ -563,8 +518,7 @@ int geqrf(double* a, int64_t lda, int64_t m, int64_t n, double* tau, void* ws, s
     double* T = tbl + pidx * QR_NB * QR_NB;
     QrPanelArgs pa{a, lda, m, j0, nb, R,
                    reinterpret_cast<double*>(base + L.part), reinterpret_cast<double*>(base + L.diag),
-                   tau, bar, bar_base, reinterpret_cast<double*>(base + L.recg),
-                   reinterpret_cast<double*>(base + L.gramp), T};
+                   tau, bar, bar_base, reinterpret_cast<double*>(base + L.recg)};
     const size_t smem = (size_t)pa.rows_per_cta * nb * sizeof(double);
     void* args[] = {&pa};
     if (use_cluster) {
@@ -586,17 +540,12 @@ int geqrf(double* a, int64_t lda, int64_t m, int64_t n, double* tau, void* ws, s
       bar_base += (unsigned)G * nb;
     }
     note_launch();
-    // explicit V; the T factor came out of the cluster panel, else Gram GEMM + dlarft
-    const int64_t nc_left = n - j0 - nb;
-    if (nc_left > 0 || !use_cluster) {
-      qr_make_v_kernel<<<grid_for_q(rows * nb), 256, 0, st>>>(a, lda, j0, rows, nb, vbuf, rows);
-      RLRA_LAUNCHED();
-    }
-    if (!use_cluster) {
-      if (gemm(true, false, nb, nb, rows, 1.0, vbuf, rows, vbuf, rows, 0.0, gram, nb, gws, gws_bytes, st)) return -1;
-      qr_larft_kernel<<<1, 32, 0, st>>>(gram, nb, tau + j0, T);
-      RLRA_LAUNCHED();
-    }
+    // explicit V and the T factor of this panel (Gram on the DMMA GEMM + dlarft)
+    qr_make_v_kernel<<<grid_for_q(rows * nb), 256, 0, st>>>(a, lda, j0, rows, nb, vbuf, rows);
+    RLRA_LAUNCHED();
+    if (gemm(true, false, nb, nb, rows, 1.0, vbuf, rows, vbuf, rows, 0.0, gram, nb, gws, gws_bytes, st)) return -1;
+    qr_larft_kernel<<<1, 256, 0, st>>>(gram, nb, tau + j0, T);
+    RLRA_LAUNCHED();
     // trailing update C = (I - V T^T V^T) C on columns [j0+nb, n)
     const int64_t nc = n - j0 - nb;
     if (nc > 0) {

@@ -25,16 +25,56 @@ class DeviceMatrix:
 
     is_device_accessor = True
 
+    # Host arrays in pinned memory above this size are uploaded in column
+    # chunks on a copy stream; the first product consumes chunks as they land
+    # (H2D overlapped with Omega and the first pass -- the e2e path).
+    PIPELINE_MIN_BYTES = 256 << 20
+    PIPELINE_CHUNKS = 8
+
     def __init__(self, a, device=None):
         dev = ops.check_device(device)
+        self._pending = []  # [(c0, c1, event)] column chunks still in flight
+        self._host_keep = None
         if isinstance(a, torch.Tensor):
             if a.dim() != 2:
                 raise ValueError(f"expected a 2-d array, got ndim={a.dim()}")
             t = a.to(device=dev, dtype=torch.float64)
             self._a = ops.as_fmat(t)
         else:
-            self._a = ops.from_numpy(a, dev)
+            arr = np.asfortranarray(np.asarray(a, dtype=np.float64))
+            if arr.ndim != 2:
+                raise ValueError(f"expected a 2-d array, got ndim={arr.ndim}")
+            host = torch.from_numpy(arr) if arr.size else None
+            if host is not None and arr.nbytes >= self.PIPELINE_MIN_BYTES and host.is_pinned():
+                self._upload_pipelined(arr, host, dev)
+            else:
+                self._a = ops.from_numpy(arr, dev)
         self._fro = None
+
+    def _upload_pipelined(self, arr, host, dev):
+        m, n = arr.shape
+        self._a = ops.fmat(m, n, dev)
+        self._host_keep = arr  # the copies read it asynchronously
+        copy_stream = torch.cuda.Stream(dev)
+        # the destination allocation must be ready before the copy stream writes it
+        copy_stream.wait_stream(torch.cuda.current_stream(dev))
+        step = max(1, -(-n // self.PIPELINE_CHUNKS))
+        with torch.cuda.stream(copy_stream):
+            for c0 in range(0, n, step):
+                c1 = min(n, c0 + step)
+                self._a[:, c0:c1].copy_(host[:, c0:c1], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(copy_stream)
+                self._pending.append((c0, c1, ev))
+        self._a.record_stream(copy_stream)  # allocator: the copy stream writes this block
+        self._copy_stream = copy_stream
+
+    def _finish_upload(self):
+        if self._pending:
+            st = torch.cuda.current_stream(self.device)
+            for _, _, ev in self._pending:
+                st.wait_event(ev)
+            self._pending = []
 
     @property
     def shape(self):
@@ -42,6 +82,7 @@ class DeviceMatrix:
 
     @property
     def tensor(self):
+        self._finish_upload()
         return self._a
 
     @property
@@ -52,16 +93,33 @@ class DeviceMatrix:
         """A @ X, one pass over A (rlra/accessors.py:27-28)."""
         x = _dev(x, self.device)
         with ops.label("pass_nn"):
+            if self._pending:  # first pass behind the upload: Y = sum_c A_c X_c
+                st = torch.cuda.current_stream(self.device)
+                y = ops.fmat(self._a.shape[0], x.shape[1], self.device)
+                for i, (c0, c1, ev) in enumerate(self._pending):
+                    st.wait_event(ev)
+                    ops.gemm(self._a[:, c0:c1], x[c0:c1, :], y, beta=0.0 if i == 0 else 1.0)
+                self._finish_upload()
+                return y
             return ops.matmul(self._a, x)
 
     def rmatmul(self, x):
         """A^T @ X, one pass over A (rlra/accessors.py:30-31)."""
         x = _dev(x, self.device)
         with ops.label("pass_tn"):
+            if self._pending:  # first pass behind the upload: Z[c] = A_c^T X per chunk
+                st = torch.cuda.current_stream(self.device)
+                z = ops.fmat(self._a.shape[1], x.shape[1], self.device)
+                for c0, c1, ev in self._pending:
+                    st.wait_event(ev)
+                    ops.gemm(self._a[:, c0:c1], x, z[c0:c1, :], ta=True)
+                self._finish_upload()
+                return z
             return ops.matmul(self._a, x, ta=True)
 
     def fro_norm_sq_device(self):
         """Compensated ||A||_F^2 as a device scalar (no host sync)."""
+        self._finish_upload()
         return ops.sumsq(self._a)
 
     def fro_norm(self):
@@ -69,6 +127,7 @@ class DeviceMatrix:
         return math.sqrt(float(self.fro_norm_sq_device().item()))
 
     def to_dense(self):
+        self._finish_upload()
         return ops.to_numpy(self._a)
 
 

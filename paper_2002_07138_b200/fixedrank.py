@@ -36,6 +36,7 @@ class LowRankLU:
 
     def to_numpy(self):
         conv = lambda t: ops.to_numpy(t) if isinstance(t, torch.Tensor) else t
+        torch.cuda.synchronize() if self.on_device else None
         return LowRankLU(conv(self.p), conv(self.q), conv(self.L), conv(self.U), self.rank)
 
     @property

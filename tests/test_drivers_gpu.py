@@ -255,3 +255,28 @@ def test_distributed_path_single_rank_nccl(cuda_dev):
         assert np.array_equal(fp.p.cpu().numpy(), DRV["fpfac/p"])
     finally:
         dist.destroy_process_group()
+
+
+def test_pipelined_upload_matches_resident(cuda_dev, monkeypatch):
+    """Pinned host input: column chunks are uploaded on a copy stream and the
+    first pass consumes them as they land; results equal the resident run."""
+    import torch
+
+    import paper_2002_07138_b200 as P
+    from paper_2002_07138_b200 import device
+
+    monkeypatch.setattr(device.DeviceMatrix, "PIPELINE_MIN_BYTES", 1)
+    a = DRV["pl_a"]
+    pinned = torch.empty((a.shape[1], a.shape[0]), dtype=torch.float64, pin_memory=True)
+    ah = pinned.numpy().T
+    ah[...] = a
+    for v in (3, 4):
+        f = P.powerlu(ah, 30, q_os=10, v=v, seed=1)
+        assert np.array_equal(f.p, DRV[f"pl_v{v}/p"]) and np.array_equal(f.q, DRV[f"pl_v{v}/q"])
+        assert abs(O.rel_fro_error_factor(a, f) - META["drivers"][f"pl_v{v}"]["rel_err"]) <= REL_ERR_TOL
+    dm = P.DeviceMatrix(ah)
+    assert len(dm._pending) > 1
+    z = dm.rmatmul(np.eye(200)[:, :5])
+    from paper_2002_07138_b200 import ops
+
+    np.testing.assert_allclose(ops.to_numpy(z), a.T @ np.eye(200)[:, :5], rtol=0, atol=1e-14)
