@@ -11,8 +11,9 @@ Our arm prints ONE JSON line with:
   value      algorithmic GFLOP/s (SURVEY.md Appendix B flop count) with A and
              Omega resident in HBM, outputs left in HBM; CUDA events, K steps
   e2e        the same metric through the public API with HOST inputs (pinned
-             NumPy A), Omega drawn on the host each step, factors returned to
-             the host: H2D/D2H inside the timed region
+             NumPy A, uploaded in column chunks behind the first pass), Omega
+             regenerated every step (device replay of NumPy's stream), factors
+             returned to the host as NumPy: H2D/D2H inside the timed region
   roofline   the pass GEMM (DMMA) against the measured FP64 DMMA peak
   cpu_baseline  the unmodified reference (oracle/_ref, rlra 0.1.0) on the box's
              host cores, same call, best of a bounded sample
@@ -29,6 +30,8 @@ import subprocess
 import sys
 import tempfile
 import time
+
+import numpy as np
 
 REPO = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, REPO)
@@ -58,7 +61,7 @@ def workload(args):
     v = args.v if args.v is not None else w.v
     if w.kind != "powerlu":
         raise SystemExit(f"bench supports the fixed-rank powerlu configs (C1, C2, C5); got {args.config}")
-    gen = {"C1": configs.gen_c1, "C2": configs.gen_c2, "C5": configs.gen_c5}[w.name]
+    gen = {"C1": configs.gen_c1, "C2": configs.gen_c2, "C5": None}[w.name]  # C5: built in HBM
     passes, fact = configs.powerlu_flops(w.m, w.n, w.k, w.k + w.q_os, v)
     desc = (f"{w.name}: powerlu(A {w.m}x{w.n} float64, k={w.k}, q_os={w.q_os}, v={v}, seed={w.seed})")
     return w, v, gen, passes, fact, desc
@@ -134,7 +137,15 @@ def reference_arm(args):
         return 0
     w, v, gen, passes, fact, desc = workload(args)
     mod, kind = ref_module()
-    a = gen()
+    sample = f"{args.steps} full {w.name} factorizations (mean)"
+    if gen is None:  # C5 (68.7 GB): the survey's C5 analogue is the bounded host sample
+        from paper_2002_07138_b200 import configs
+
+        a = configs.gen_lowrank_plus_noise(32768, 8192, 640, 10.0 ** (-8.0 * np.arange(640) / 639), 1e-10, 5)
+        passes, fact = configs.powerlu_flops(32768, 8192, w.k, w.k + w.q_os, v)
+        sample = f"{args.steps} factorizations of the C5 analogue 32768x8192 (SURVEY Appendix A), mean"
+    else:
+        a = gen()
     flops = passes + fact
     for _ in range(args.warmup):
         mod.powerlu(a, w.k, w.q_os, v, w.seed)
@@ -153,7 +164,7 @@ def reference_arm(args):
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": desc, "m": w.m, "n": w.n, "k": w.k, "l": w.k + w.q_os, "v": v},
         "cpu_baseline": {"value": val, "unit": "GFLOP/s", "cores": cores, "kind": kind,
-                         "sample": f"{args.steps} full factorizations (mean), rlra {getattr(mod, '__version__', 'port')} "
+                         "sample": f"{sample}, rlra {getattr(mod, '__version__', 'port')} "
                                    f"backend={getattr(mod, 'BACKEND', 'c-oracle')}, OpenBLAS threads=all"},
         "e2e": {"value": val, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -177,8 +188,24 @@ def cpu_baseline(a, w, v, flops, budget_s=30.0):
                       f"s/factorization {best:.3f}"}, f
 
 
+def cpu_baseline_analogue(w, v):
+    """Bounded CPU sample for the 68.7 GB C5: the reference on the survey's
+    C5 analogue (32768 x 8192, same k, q_os, v and spectrum recipe; SURVEY.md
+    Appendix A) -- GFLOP/s of the same algorithm at a host-feasible size."""
+    from paper_2002_07138_b200 import configs
+
+    m, n = 32768, 8192
+    a = configs.gen_lowrank_plus_noise(m, n, 640, 10.0 ** (-8.0 * np.arange(640) / 639), 1e-10, 5)
+    mod, kind = ref_module()
+    p_, f_ = configs.powerlu_flops(m, n, w.k, w.k + w.q_os, v)
+    t0 = time.perf_counter()
+    mod.powerlu(a, w.k, w.q_os, v, w.seed)
+    sec = time.perf_counter() - t0
+    return {"value": (p_ + f_) / sec / 1e9, "unit": "GFLOP/s", "cores": os.cpu_count(), "kind": kind,
+            "sample": f"1 factorization of the C5 analogue {m}x{n} (SURVEY Appendix A), {sec:.1f} s"}
+
+
 def our_arm(args):
-    import numpy as np
     import torch
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -194,14 +221,22 @@ def our_arm(args):
 
     w, v, gen, passes, fact, desc = workload(args)
     flops = passes + fact
-    t0 = time.perf_counter()
-    a = gen()
-    gen_s = time.perf_counter() - t0
     dev = torch.device("cuda", local)
     t0 = time.perf_counter()
-    dm = P.DeviceMatrix(a, local)
-    torch.cuda.synchronize()
-    upload_s = time.perf_counter() - t0
+    if gen is not None:
+        a = gen()
+        gen_s = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        dm = P.DeviceMatrix(a, local)
+        torch.cuda.synchronize()
+        upload_s = time.perf_counter() - t0
+    else:  # C5 (68.7 GB): same recipe, built directly in HBM (configs.gen_device)
+        from paper_2002_07138_b200 import configs as _cfg
+
+        a = None
+        dm = P.DeviceMatrix(_cfg.gen_device(w.name, dev), local)
+        gen_s, upload_s = time.perf_counter() - t0, 0.0
+        args.no_e2e = True
     P.set_omega_cache(True)
     st = torch.cuda.current_stream(dev)
     for _ in range(args.warmup):
@@ -287,7 +322,7 @@ def our_arm(args):
     # ---- CPU baseline (reference on the host) + parity of this very call
     cpu = None
     parity = None
-    if not args.no_cpu_baseline:
+    if not args.no_cpu_baseline and a is not None:
         cpu, fref = cpu_baseline(a, w, v, flops)
         from oracle import rlra_oracle as O
 
@@ -298,6 +333,8 @@ def our_arm(args):
             e_gpu = O.rel_fro_error_factor(a, fd)
             e_ref = O.rel_fro_error_factor(a, fref)
             parity.update({"rel_err_gpu": e_gpu, "rel_err_ref": e_ref, "abs_diff": abs(e_gpu - e_ref)})
+    elif not args.no_cpu_baseline:
+        cpu = cpu_baseline_analogue(w, v)
 
     line = {
         "metric": f"PowerLU FP64 GFLOP/s ({w.name}, v={v})", "value": value, "unit": "GFLOP/s",

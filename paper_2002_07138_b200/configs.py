@@ -45,14 +45,21 @@ def gen_c1():
     return np.asfortranarray((u * sigma) @ v.T)
 
 
-def gen_lowrank_plus_noise(m, n, r, sigma, noise, seed):
-    """A = X diag(sigma) Y^T + noise * N(0,1); X, Y, noise from one stream."""
+def gen_lowrank_plus_noise(m, n, r, sigma, noise, seed, col_chunk=4096):
+    """A = X diag(sigma) Y^T + noise * N(0,1); X, Y, noise from one stream.
+
+    The noise is drawn in column blocks: gaussian_from fills column-major, so
+    consecutive blocks are exactly the columns of the single full draw (same
+    bits), without a second m x n temporary (C5 would need 206 GB)."""
     rng = np.random.default_rng(seed)
     x, _ = np.linalg.qr(_gaussian_from(rng, m, r))
     y, _ = np.linalg.qr(_gaussian_from(rng, n, r))
     a = np.asfortranarray((x * sigma) @ y.T)
+    del x, y
     if noise:
-        a += noise * _gaussian_from(rng, m, n)
+        for c0 in range(0, n, col_chunk):
+            c1 = min(n, c0 + col_chunk)
+            a[:, c0:c1] += noise * _gaussian_from(rng, m, c1 - c0)
     return a
 
 

@@ -58,9 +58,10 @@ def run(name):
     meta["wall_s"] = time.perf_counter() - t0
     meta["rel_err"] = rel_fro_error_factor(a, fac)
     meta["rank"] = int(fac.rank)
-    np.savez_compressed(os.path.join(HERE, f"{name.lower()}_pq.npz"), p=fac.p.astype(np.int32),
+    out_dir = os.environ.get("GOLDEN_OUT", HERE)
+    np.savez_compressed(os.path.join(out_dir, f"{name.lower()}_pq.npz"), p=fac.p.astype(np.int32),
                         q=fac.q.astype(np.int32))
-    path = os.path.join(HERE, "golden_configs.json")
+    path = os.path.join(out_dir, "golden_configs.json")
     allm = json.load(open(path)) if os.path.exists(path) else {}
     allm[name] = meta
     with open(path, "w") as fh:
