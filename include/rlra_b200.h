@@ -20,6 +20,8 @@
  *   rlra_b200_lu_extract       L/U extraction of kernels.plu  kernels.py:50-53
  *   rlra_b200_dgemm            DenseAccessor.matmul/rmatmul   accessors.py:27-31
  *                              and the assembly products      fixedrank.py:145-146, kernels.py:96
+ *   rlra_b200_oz_prep/_gemm    the same two pass products     accessors.py:27-31
+ *                              emulated on int8 tensor cores (Ozaki-II)
  *   rlra_b200_geqrf/_orgqr     kernels.eqr (np.linalg.qr)     kernels.py:57-61, :73
  *   rlra_b200_trsm_rt          solve_triangular(trans='T')    kernels.py:95
  *   rlra_b200_diag_absmin      pinv_factor rank test          kernels.py:75-79
@@ -82,6 +84,26 @@ RLRA_B200_API size_t rlra_b200_gemm_workspace(int64_t m, int64_t n, int64_t k);
 RLRA_B200_API int rlra_b200_dgemm(int transa, int transb, int64_t m, int64_t n, int64_t k, double alpha,
                     const double* a, int64_t lda, const double* b, int64_t ldb, double beta,
                     double* c, int64_t ldc, void* ws, size_t ws_bytes, void* stream);
+
+/* ---- K1/K2 emulated: the pass products on the int8 tensor cores --------
+ * FP64 GEMM by the Ozaki-II scheme: A and B are scaled by powers of two and
+ * rounded to integers (A'' = rint(2^eA A), B'' = rint(2^eB[j] B[:, j])), the
+ * integer product is computed exactly modulo nmod pairwise-coprime moduli with
+ * tcgen05 kind::i8 MMAs and reassembled by Chinese remaindering, then rounded
+ * once to double.  Accuracy: |error| <~ 2^-53 ||A_i|| ||B_j|| for nmod = 14
+ * (the DGEMM-level bound); results are exact functions of the inputs.
+ * prep: residues of A, built once per A by rlra_b200_oz_prep (both
+ * orientations); then any number of
+ *   trans = 0: C (m x ncols) = A   B,  B n x ncols
+ *   trans = 1: C (n x ncols) = A^T B,  B m x ncols
+ * nmod in [12, 16] (14 = DGEMM accuracy); K (= n or m) <= 133144. */
+RLRA_B200_API size_t rlra_b200_oz_prep_workspace(int64_t m, int64_t n, int nmod);
+RLRA_B200_API int rlra_b200_oz_prep(const double* a, int64_t lda, int64_t m, int64_t n, int nmod, void* prep,
+                                    size_t prep_bytes, void* stream);
+RLRA_B200_API size_t rlra_b200_oz_gemm_workspace(int trans, int64_t m, int64_t n, int64_t ncols, int nmod);
+RLRA_B200_API int rlra_b200_oz_gemm(int trans, const void* prep, int64_t m, int64_t n, int nmod, const double* b,
+                                    int64_t ldb, int64_t ncols, double* c, int64_t ldc, void* ws,
+                                    size_t ws_bytes, void* stream);
 
 /* ---- K4: Householder QR (m >= n) + explicit thin Q --------------------- */
 RLRA_B200_API size_t rlra_b200_geqrf_workspace(int64_t m, int64_t n);

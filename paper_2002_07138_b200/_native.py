@@ -38,6 +38,11 @@ SIGNATURES = {
     "rlra_b200_gemm_workspace": (_c_sz, [_c_i64, _c_i64, _c_i64]),
     "rlra_b200_dgemm": (_c_i, [_c_i, _c_i, _c_i64, _c_i64, _c_i64, _c_d, _c_p, _c_i64, _c_p, _c_i64,
                                _c_d, _c_p, _c_i64, _c_p, _c_sz, _c_p]),
+    "rlra_b200_oz_prep_workspace": (_c_sz, [_c_i64, _c_i64, _c_i]),
+    "rlra_b200_oz_prep": (_c_i, [_c_p, _c_i64, _c_i64, _c_i64, _c_i, _c_p, _c_sz, _c_p]),
+    "rlra_b200_oz_gemm_workspace": (_c_sz, [_c_i, _c_i64, _c_i64, _c_i64, _c_i]),
+    "rlra_b200_oz_gemm": (_c_i, [_c_i, _c_p, _c_i64, _c_i64, _c_i, _c_p, _c_i64, _c_i64, _c_p, _c_i64,
+                                 _c_p, _c_sz, _c_p]),
     "rlra_b200_geqrf_workspace": (_c_sz, [_c_i64, _c_i64]),
     "rlra_b200_geqrf": (_c_i, [_c_p, _c_i64, _c_i64, _c_i64, _c_p, _c_p, _c_sz, _c_p]),
     "rlra_b200_orgqr": (_c_i, [_c_p, _c_i64, _c_i64, _c_i64, _c_p, _c_i64, _c_p, _c_sz, _c_p]),

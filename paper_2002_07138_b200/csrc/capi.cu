@@ -68,6 +68,12 @@ int sumsq(const double* a, int64_t lda, int64_t m, int64_t n, double* out_dev, v
 int colsumsq(const double* a, int64_t lda, int64_t m, int64_t n, double* out_dev, cudaStream_t st);
 int transpose(const double* in, int64_t ldi, int64_t m, int64_t n, double* out, int64_t ldo,
               cudaStream_t st);
+size_t oz_prep_workspace(int64_t m, int64_t n, int nmod);
+int oz_prep(const double* a, int64_t lda, int64_t m, int64_t n, int nmod, void* prep, size_t prep_bytes,
+            cudaStream_t st);
+size_t oz_gemm_workspace(int trans, int64_t m, int64_t n, int64_t ncols, int nmod);
+int oz_gemm(int trans, const void* prep, int64_t m, int64_t n, int nmod, const double* b, int64_t ldb,
+            int64_t ncols, double* c, int64_t ldc, void* ws, size_t ws_bytes, cudaStream_t st);
 size_t normal_workspace_bytes(int64_t N);
 int64_t normal_stream_words(int64_t N);
 int64_t normal_tail_cap(int64_t N);
@@ -160,6 +166,23 @@ int rlra_b200_lu_extract(const double* lu, int64_t ldlu, int64_t m, int64_t n, d
   if (l && extract_l(lu, ldlu, m, r, l, ldl, S(stream))) return -1;
   if (u && extract_u(lu, ldlu, r, n, u, ldu, S(stream))) return -1;
   return 0;
+}
+
+size_t rlra_b200_oz_prep_workspace(int64_t m, int64_t n, int nmod) { return oz_prep_workspace(m, n, nmod); }
+
+int rlra_b200_oz_prep(const double* a, int64_t lda, int64_t m, int64_t n, int nmod, void* prep,
+                      size_t prep_bytes, void* stream) {
+  return oz_prep(a, lda, m, n, nmod, prep, prep_bytes, static_cast<cudaStream_t>(stream));
+}
+
+size_t rlra_b200_oz_gemm_workspace(int trans, int64_t m, int64_t n, int64_t ncols, int nmod) {
+  return oz_gemm_workspace(trans, m, n, ncols, nmod);
+}
+
+int rlra_b200_oz_gemm(int trans, const void* prep, int64_t m, int64_t n, int nmod, const double* b,
+                      int64_t ldb, int64_t ncols, double* c, int64_t ldc, void* ws, size_t ws_bytes,
+                      void* stream) {
+  return oz_gemm(trans, prep, m, n, nmod, b, ldb, ncols, c, ldc, ws, ws_bytes, static_cast<cudaStream_t>(stream));
 }
 
 size_t rlra_b200_gemm_workspace(int64_t m, int64_t n, int64_t k) { return gemm_workspace_bytes(m, n, k); }

@@ -1,0 +1,749 @@
+// K1/K2 pass GEMMs as FP64 emulation on the int8 tensor cores (Ozaki scheme
+// II: integer scaling + Chinese remaindering), the B200-first replacement of
+// the DMMA pass for the two big products of every PowerLU pass
+//   NN  C (m x l) = A   B      (rlra/accessors.py:27-28, A.matmul)
+//   TN  C (n x l) = A^T B      (rlra/accessors.py:30-31, A.rmatmul)
+// B200 runs FP64 at ~37 TFLOP/s (DMMA) but int8 MMA at ~4.5 POPS, so the
+// product is computed exactly in integers:
+//   1. A'' = rint(2^eA A) with one power-of-two scale such that every row and
+//      column 2-norm of A'' is < 2^PA; B'' = rint(2^eB[j] B[:, j]) per column,
+//      ||B''_j|| < 2^PB.  By Cauchy-Schwarz |(A''B'')_ij| < 2^(PA+PB) < M/2.
+//   2. For NMOD pairwise-coprime moduli m_l <= 249 (M = prod m_l ~ 2^109.5 for
+//      14) the residues A''_l = A'' mod m_l, B''_l in [-127, 127] are int8 and
+//      C_l = A''_l B''_l is EXACT in the int32 accumulators (K <= 133144).
+//   3. t_l = C_l mod m_l (uint8), and A''B'' = CRT(t_1..t_NMOD) in (-M/2, M/2)
+//      is reconstructed exactly in 128-bit integers, rounded once to double
+//      and unscaled by 2^-(eA+eB[j]).
+// The only rounding is the scaling step (|error| <= 2^-PA relative to the row /
+// column norm of A, 2^-PB for B), which for NMOD = 14 (PA = 54, PB = 53) is
+// below DGEMM's own accumulation error; results are exact functions of the
+// inputs (tiling- and order-independent, so bitwise deterministic).
+//
+// Data layout.  The residues of A are written once per PowerLU call into
+// 128 x 128-byte tiles (16 KB), tile (jb, ib) holding A''[ib*128 .. +128,
+// jb*128 .. +128] with the ROW index i contiguous: row r = column j, byte c =
+// row i, in the 128-byte-swizzled image the tensor core reads (16-byte chunk
+// c/16 stored at chunk (c/16) ^ (r % 8)).  The TN product reads a tile as a
+// K-major operand (K = i), the NN product reads the SAME bytes as an MN-major
+// operand (M = i, K = j), so one residue set serves both orientations.  Tiles
+// are plain contiguous 16 KB blocks moved with 1-D bulk copies (no tensor map).
+//
+// GEMM kernel: persistent, 1 CTA / SM, warp-specialized: warp 0 = bulk-copy
+// producer, warp 1 = tcgen05.mma issuer (one thread) + TMEM owner, warps 2-5 =
+// epilogue (tcgen05.ld -> mod m_l -> uint8).  A unit of work is (modulus l,
+// 256-row block, column group); two M=128 MMAs share each B tile; int32
+// accumulators live in TMEM (2 x N_g <= 512 columns).
+#include <algorithm>
+#include <cmath>
+#include <mutex>
+
+#include "common.cuh"
+
+namespace rlra {
+namespace oz {
+
+constexpr int kMaxMod = 16;
+constexpr int kModuli[kMaxMod] = {249, 247, 245, 244, 241, 239, 233, 229,
+                                  227, 223, 211, 199, 197, 193, 191, 181};
+constexpr int kTile = 128;                 // rows / bytes per residue tile
+constexpr int kTileBytes = kTile * kTile;  // 16 KB
+constexpr int kMaxK = 133144;              // 127^2 * K < 2^31
+constexpr int kStages = 3;
+constexpr int kGemmThreads = 192;
+
+__host__ __device__ constexpr int pow2mod(int e, int m) {
+  int r = 1 % m;
+  for (int i = 0; i < e; ++i) r = (r * 2) % m;
+  return r;
+}
+
+typedef unsigned __int128 u128;
+
+struct Crt {
+  uint64_t M_lo, M_hi;        // M = prod m_l
+  uint64_t H_lo, H_hi;        // floor(M / 2)
+  uint64_t md_lo[kMaxMod];    // M / m_l
+  uint64_t md_hi[kMaxMod];
+  int y[kMaxMod];             // (M / m_l)^{-1} mod m_l
+  int m[kMaxMod];
+  float inv_m[kMaxMod];
+  int nmod;
+};
+
+// Precision split of the 128-bit budget: PA + PB = floor(log2 M) - 2, each <= 55.
+struct Budget {
+  int pa, pb;
+};
+static Budget budget(int nmod) {
+  long double lg = 0;
+  for (int l = 0; l < nmod; ++l) lg += std::log2((long double)kModuli[l]);
+  int tot = (int)std::floor(lg) - 2;
+  Budget b;
+  b.pa = tot - tot / 2;
+  b.pb = tot / 2;
+  if (b.pa > 55) b.pa = 55;
+  if (b.pb > 55) b.pb = 55;
+  return b;
+}
+
+static Crt make_crt(int nmod) {
+  Crt c{};
+  u128 M = 1;
+  for (int l = 0; l < nmod; ++l) M *= (u128)kModuli[l];
+  c.M_lo = (uint64_t)M;
+  c.M_hi = (uint64_t)(M >> 64);
+  u128 H = M >> 1;
+  c.H_lo = (uint64_t)H;
+  c.H_hi = (uint64_t)(H >> 64);
+  for (int l = 0; l < nmod; ++l) {
+    const int m = kModuli[l];
+    u128 md = M / (u128)m;
+    c.md_lo[l] = (uint64_t)md;
+    c.md_hi[l] = (uint64_t)(md >> 64);
+    int r = (int)(md % (u128)m);
+    int inv = 0;
+    for (int y = 1; y < m; ++y)
+      if ((r * y) % m == 1) {
+        inv = y;
+        break;
+      }
+    c.y[l] = inv;
+    c.m[l] = m;
+    c.inv_m[l] = 1.0f / (float)m;
+  }
+  c.nmod = nmod;
+  return c;
+}
+
+// ----------------------------------------------------------------- residues
+// x = rint(v * 2^e) as four signed 14-bit float parts (|x| < 2^56).
+struct Parts {
+  float p0, p1, p2, p3;
+};
+__device__ __forceinline__ Parts split_parts(double v, double scale) {
+  const long long xi = __double2ll_rn(v * scale);
+  const unsigned long long u = (unsigned long long)(xi < 0 ? -xi : xi);
+  const float s = xi < 0 ? -1.0f : 1.0f;
+  Parts p;
+  p.p0 = s * (__int_as_float(0x4B000000 | (unsigned)(u & 0x3FFF)) - 8388608.0f);
+  p.p1 = s * (__int_as_float(0x4B000000 | (unsigned)((u >> 14) & 0x3FFF)) - 8388608.0f);
+  p.p2 = s * (__int_as_float(0x4B000000 | (unsigned)((u >> 28) & 0x3FFF)) - 8388608.0f);
+  p.p3 = s * (__int_as_float(0x4B000000 | (unsigned)((u >> 42) & 0x3FFF)) - 8388608.0f);
+  return p;
+}
+
+// Residue of the part-encoded integer modulo kModuli[L], in [-m/2-1, m/2+1]
+// (|r| <= 125), returned as the low byte of a float-encoded integer.
+template <int L>
+__device__ __forceinline__ unsigned residue_byte(const Parts& x) {
+  constexpr int m = kModuli[L];
+  constexpr float c1 = (float)pow2mod(14, m);
+  constexpr float c2 = (float)pow2mod(28, m);
+  constexpr float c3 = (float)pow2mod(42, m);
+  constexpr float inv = 1.0f / (float)m;
+  const float v = fmaf(x.p3, c3, fmaf(x.p2, c2, fmaf(x.p1, c1, x.p0)));  // exact, |v| < 2^24
+  const float q = __fadd_rn(fmaf(v, inv, 12582912.0f), -12582912.0f);  // ~rint(v / m)
+  const float r = fmaf(-q, (float)m, v);                                // exact
+  return (unsigned)__float_as_int(__fadd_rn(r, 12582912.0f));           // low byte = r (two's compl.)
+}
+
+__device__ __forceinline__ unsigned pack4(unsigned b0, unsigned b1, unsigned b2, unsigned b3) {
+  return __byte_perm(__byte_perm(b0, b1, 0x0040), __byte_perm(b2, b3, 0x0040), 0x5410);
+}
+
+// 16 consecutive values -> 16 residue bytes for modulus L (one swizzle chunk).
+template <int L>
+__device__ __forceinline__ uint4 residue_chunk(const Parts (&x)[16]) {
+  uint4 o;
+  o.x = pack4(residue_byte<L>(x[0]), residue_byte<L>(x[1]), residue_byte<L>(x[2]), residue_byte<L>(x[3]));
+  o.y = pack4(residue_byte<L>(x[4]), residue_byte<L>(x[5]), residue_byte<L>(x[6]), residue_byte<L>(x[7]));
+  o.z = pack4(residue_byte<L>(x[8]), residue_byte<L>(x[9]), residue_byte<L>(x[10]), residue_byte<L>(x[11]));
+  o.w = pack4(residue_byte<L>(x[12]), residue_byte<L>(x[13]), residue_byte<L>(x[14]), residue_byte<L>(x[15]));
+  return o;
+}
+
+template <int L, int NMOD>
+struct ChunkWriter {
+  __device__ __forceinline__ static void run(const Parts (&x)[16], int8_t* base, size_t mod_stride) {
+    *reinterpret_cast<uint4*>(base + (size_t)L * mod_stride) = residue_chunk<L>(x);
+    ChunkWriter<L + 1, NMOD>::run(x, base, mod_stride);
+  }
+};
+template <int NMOD>
+struct ChunkWriter<NMOD, NMOD> {
+  __device__ __forceinline__ static void run(const Parts (&)[16], int8_t*, size_t) {}
+};
+
+__device__ __forceinline__ int swz(int r, int c) {  // byte offset of 16-byte chunk c of row r
+  return r * kTile + (((c ^ (r & 7)) & 7) << 4);
+}
+
+// Residues of A: one CTA per 128 x 128 block of A (tile (jb, ib)).
+template <int NMOD>
+__global__ void __launch_bounds__(256) residue_a_kernel(const double* __restrict__ a, int64_t lda, int64_t m,
+                                                        int64_t n, const int* __restrict__ e_a,
+                                                        int8_t* __restrict__ tiles, int64_t nib, int64_t njb) {
+  const int64_t ib = blockIdx.x, jb = blockIdx.y;
+  const double scale = scalbn(1.0, e_a[0]);
+  const size_t mod_stride = (size_t)njb * nib * kTileBytes;
+  int8_t* tile = tiles + ((size_t)jb * nib + ib) * kTileBytes;
+#pragma unroll 1
+  for (int s = 0; s < 4; ++s) {
+    const int ch = threadIdx.x + 256 * s;
+    const int r = ch >> 3, c = ch & 7;
+    const int64_t j = jb * kTile + r;
+    const int64_t i0 = ib * kTile + c * 16;
+    Parts x[16];
+#pragma unroll
+    for (int t = 0; t < 16; ++t) {
+      const int64_t i = i0 + t;
+      const double v = (j < n && i < m) ? __ldg(a + i + j * lda) : 0.0;
+      x[t] = split_parts(v, scale);
+    }
+    ChunkWriter<0, NMOD>::run(x, tile + swz(r, c), mod_stride);
+  }
+}
+
+// Residues of the skinny operand B (K x ncols): one CTA per (padded) column,
+// per-column scale, K-major tiles of n_g rows x 128 bytes per (l, group, kb).
+template <int NMOD>
+__global__ void __launch_bounds__(256) residue_b_kernel(const double* __restrict__ b, int64_t ldb, int64_t k,
+                                                        int64_t ncols, int n_g, int64_t nkb, int pb,
+                                                        int* __restrict__ e_b, int8_t* __restrict__ tiles,
+                                                        int ng) {
+  const int64_t jj = blockIdx.x;
+  const int g = (int)(jj / n_g), r = (int)(jj % n_g);
+  __shared__ double red[8];
+  __shared__ int e_sh;
+  double ss = 0.0;
+  if (jj < ncols)
+    for (int64_t i = threadIdx.x; i < k; i += 256) {
+      const double v = b[i + jj * ldb];
+      ss = fma(v, v, ss);
+    }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < 8; ++w) t += red[w];
+    int e = 0;
+    if (t > 0.0) {
+      int ex;
+      frexp(sqrt(t) * (1.0 + 0x1p-40), &ex);  // ||b_j|| < 2^ex
+      e = pb - ex;
+    }
+    e_sh = e;
+    e_b[jj] = e;
+  }
+  __syncthreads();
+  const double scale = scalbn(1.0, e_sh);
+  const size_t mod_stride = (size_t)ng * nkb * n_g * kTile;
+  int8_t* tile0 = tiles + (size_t)g * nkb * n_g * kTile;
+  for (int64_t ch = threadIdx.x; ch < nkb * 8; ch += 256) {
+    const int64_t kb = ch >> 3;
+    const int c = (int)(ch & 7);
+    const int64_t i0 = kb * kTile + c * 16;
+    Parts x[16];
+#pragma unroll
+    for (int t = 0; t < 16; ++t) {
+      const int64_t i = i0 + t;
+      const double v = (jj < ncols && i < k) ? b[i + jj * ldb] : 0.0;
+      x[t] = split_parts(v, scale);
+    }
+    ChunkWriter<0, NMOD>::run(x, tile0 + (size_t)kb * n_g * kTile + swz(r, c), mod_stride);
+  }
+}
+
+// ----------------------------------------------------------------- A scale
+// Row / column 2-norms of A -> max -> eA = PA - ceil(log2(max norm)).
+__global__ void rownorm_partial_kernel(const double* __restrict__ a, int64_t lda, int64_t m, int64_t n,
+                                       int64_t cols_per, double* __restrict__ part) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t cb = blockIdx.y;
+  if (i >= m) return;
+  const int64_t j0 = cb * cols_per, j1 = min(n, j0 + cols_per);
+  double s0 = 0.0, s1 = 0.0;
+  int64_t j = j0;
+  for (; j + 1 < j1; j += 2) {
+    const double v0 = __ldg(a + i + j * lda), v1 = __ldg(a + i + (j + 1) * lda);
+    s0 = fma(v0, v0, s0);
+    s1 = fma(v1, v1, s1);
+  }
+  if (j < j1) {
+    const double v0 = __ldg(a + i + j * lda);
+    s0 = fma(v0, v0, s0);
+  }
+  part[cb * m + i] = s0 + s1;
+}
+
+__device__ __forceinline__ void atomic_max_pos(unsigned long long* p, double v) {
+  atomicMax(p, (unsigned long long)__double_as_longlong(v));  // v >= 0: bit order = value order
+}
+
+__global__ void rownorm_final_kernel(const double* __restrict__ part, int64_t m, int64_t ncb,
+                                     unsigned long long* __restrict__ maxbits) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  double v = 0.0;
+  if (i < m)
+    for (int64_t cb = 0; cb < ncb; ++cb) v += part[cb * m + i];
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  if ((threadIdx.x & 31) == 0) atomic_max_pos(maxbits, v);
+}
+
+__global__ void colnorm_kernel(const double* __restrict__ a, int64_t lda, int64_t m, int64_t n,
+                               unsigned long long* __restrict__ maxbits) {
+  const int64_t j = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (j >= n) return;
+  const double* col = a + j * lda;
+  double s0 = 0.0, s1 = 0.0;
+  int64_t i = lane;
+  for (; i + 32 < m; i += 64) {
+    const double v0 = __ldg(col + i), v1 = __ldg(col + i + 32);
+    s0 = fma(v0, v0, s0);
+    s1 = fma(v1, v1, s1);
+  }
+  if (i < m) {
+    const double v0 = __ldg(col + i);
+    s0 = fma(v0, v0, s0);
+  }
+  double v = s0 + s1;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if (lane == 0) atomic_max_pos(maxbits, v);
+}
+
+__global__ void scale_a_kernel(const unsigned long long* __restrict__ maxbits, int pa, int* __restrict__ e_a) {
+  const double t = __longlong_as_double((long long)maxbits[0]);
+  int e = 0;
+  if (t > 0.0) {
+    int ex;
+    frexp(sqrt(t) * (1.0 + 0x1p-40), &ex);
+    e = pa - ex;
+  }
+  e_a[0] = e;
+}
+
+// ----------------------------------------------------------------- tcgen05 GEMM
+struct GemmArgs {
+  const int8_t* a_tiles;
+  int64_t nib, njb;  // residue tile grid of A (both padded to even)
+  int trans;         // 1: C = A^T B (M tiles = jb, K tiles = ib); 0: C = A B (M = ib, K = jb)
+  const int8_t* b_tiles;
+  int ng, n_g;  // column groups, columns per group (multiple of 32, <= 256)
+  int64_t nkb;  // K tiles
+  int64_t nmb;  // 256-row blocks
+  uint8_t* out;  // t[l][col][row], rows padded to nmb*256, cols to ng*n_g
+  int nmod;
+  int mods[kMaxMod];
+};
+
+__device__ __forceinline__ uint64_t sw128_desc(unsigned saddr, unsigned lbo, unsigned sbo) {
+  uint64_t d = (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;  // descriptor version (sm_100)
+  d |= (uint64_t)2 << 61;  // 128-byte swizzle
+  return d;
+}
+
+__device__ __forceinline__ void bulk_g2s(unsigned dst, const void* src, unsigned bytes, unsigned mbar,
+                                         uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], "
+      "%4;\n" ::"r"(dst),
+      "l"(src), "r"(bytes), "r"(mbar), "l"(policy)
+      : "memory");
+}
+
+__device__ __forceinline__ void mma_i8(unsigned tmem_d, uint64_t adesc, uint64_t bdesc, unsigned idesc,
+                                       unsigned acc) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc)
+      : "memory");
+}
+
+__device__ __forceinline__ void mma_commit(unsigned mbar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(mbar)
+               : "memory");
+}
+
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+}
+
+#define OZ_LD32(taddr, v)                                                                                      \
+  asm volatile(                                                                                                \
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17," \
+      "%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"                                     \
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),       \
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),             \
+        "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]),           \
+        "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]),           \
+        "=r"(v[29]), "=r"(v[30]), "=r"(v[31])                                                                 \
+      : "r"(taddr))
+
+__global__ void __launch_bounds__(kGemmThreads, 1) gemm_i8_kernel(const GemmArgs g) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  // 1024-byte alignment of the stage buffers (swizzle atoms)
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const unsigned b_bytes = (unsigned)g.n_g * kTile;
+  const unsigned stage_bytes = 2 * kTileBytes + b_bytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * stage_bytes);
+  uint64_t* empty = full + kStages;
+  uint64_t* tmem_full = empty + kStages;
+  uint64_t* tmem_empty = tmem_full + 1;
+  unsigned* tmem_slot = reinterpret_cast<unsigned*>(tmem_empty + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(full + s, 1);
+      mbar_init(empty + s, 1);
+    }
+    mbar_init(tmem_full, 1);
+    mbar_init(tmem_empty, 128);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(smem_u32(tmem_slot))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const unsigned tmem_base = *tmem_slot;
+
+  const int64_t mtiles = g.trans ? g.njb : g.nib;
+  (void)mtiles;
+  const int64_t units = (int64_t)g.nmod * g.nmb * g.ng;
+  const size_t mod_stride_a = (size_t)g.njb * g.nib * kTileBytes;
+  const size_t mod_stride_b = (size_t)g.ng * g.nkb * b_bytes;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      uint64_t pol_a, pol_b;
+      asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(pol_a));
+      asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(pol_b));
+      int stage = 0;
+      unsigned phase = 0;
+      for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
+        const int gi = (int)(u % g.ng);
+        const int64_t mb = (u / g.ng) % g.nmb;
+        const int l = (int)(u / ((int64_t)g.ng * g.nmb));
+        const int8_t* abase = g.a_tiles + (size_t)l * mod_stride_a;
+        const int8_t* bbase = g.b_tiles + (size_t)l * mod_stride_b + (size_t)gi * g.nkb * b_bytes;
+        for (int64_t kb = 0; kb < g.nkb; ++kb) {
+          mbar_wait_parity(empty + stage, phase ^ 1);
+          uint8_t* st = smem + (size_t)stage * stage_bytes;
+          const unsigned fb = smem_u32(full + stage);
+          mbar_arrive_expect_tx(full + stage, stage_bytes);
+          for (int t = 0; t < 2; ++t) {
+            const int64_t mt = 2 * mb + t;
+            const size_t tix = g.trans ? ((size_t)mt * g.nib + kb) : ((size_t)kb * g.nib + mt);
+            bulk_g2s(smem_u32(st + t * kTileBytes), abase + tix * kTileBytes, kTileBytes, fb, pol_a);
+          }
+          bulk_g2s(smem_u32(st + 2 * kTileBytes), bbase + (size_t)kb * b_bytes, b_bytes, fb, pol_b);
+          if (++stage == kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // instruction descriptor: s32 accum, s8 x s8, A K-major (TN) or MN-major (NN), B K-major
+      const unsigned idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((g.trans ? 0u : 1u) << 15) |
+                             ((unsigned)(g.n_g >> 3) << 17) | ((unsigned)(128 >> 4) << 24);
+      int stage = 0;
+      unsigned phase = 0, acc_phase = 0;
+      for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
+        mbar_wait_parity(tmem_empty, acc_phase ^ 1);
+        tc_fence_after();
+        for (int64_t kb = 0; kb < g.nkb; ++kb) {
+          mbar_wait_parity(full + stage, phase);
+          tc_fence_after();
+          const unsigned sa = smem_u32(smem + (size_t)stage * stage_bytes);
+          const unsigned sb = sa + 2 * kTileBytes;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const uint64_t bdesc = sw128_desc(sb + 32 * k, 16, 1024);
+#pragma unroll
+            for (int t = 0; t < 2; ++t) {
+              const unsigned at = sa + t * kTileBytes;
+              const uint64_t adesc =
+                  g.trans ? sw128_desc(at + 32 * k, 16, 1024) : sw128_desc(at + 4096 * k, kTileBytes, 1024);
+              mma_i8(tmem_base + (unsigned)(t * g.n_g), adesc, bdesc, idesc, (kb | k) ? 1u : 0u);
+            }
+          }
+          mma_commit(smem_u32(empty + stage));
+          if (++stage == kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        mma_commit(smem_u32(tmem_full));
+        acc_phase ^= 1;
+      }
+    }
+  } else {
+    // epilogue: warps 2..5 -> TMEM lane quadrant (warp % 4)
+    const int q = warp & 3;
+    const int64_t rows_pad = g.nmb * 256;
+    const int64_t cols_pad = (int64_t)g.ng * g.n_g;
+    unsigned acc_phase = 0;
+    for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
+      const int gi = (int)(u % g.ng);
+      const int64_t mb = (u / g.ng) % g.nmb;
+      const int l = (int)(u / ((int64_t)g.ng * g.nmb));
+      mbar_wait_parity(tmem_full, acc_phase);
+      tc_fence_after();
+      const int ml = g.mods[l];
+      const double md = (double)ml, inv = 1.0 / md;
+      for (int t = 0; t < 2; ++t) {
+        const int64_t row = mb * 256 + t * 128 + q * 32 + lane;
+        uint8_t* orow = g.out + ((size_t)l * cols_pad + (size_t)gi * g.n_g) * rows_pad + row;
+        for (int cc = 0; cc < g.n_g; cc += 32) {
+          unsigned v[32];
+          const unsigned taddr = tmem_base + ((unsigned)(q * 32) << 16) + (unsigned)(t * g.n_g + cc);
+          OZ_LD32(taddr, v);
+          asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+          for (int e = 0; e < 32; ++e) {
+            const double cv = (double)(int)v[e];
+            double r = fma(-floor(cv * inv), md, cv);
+            if (r < 0.0) r += md;
+            if (r >= md) r -= md;
+            orow[(size_t)(cc + e) * rows_pad] = (uint8_t)(int)r;
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(tmem_empty);
+      acc_phase ^= 1;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem_base) : "memory");
+  }
+}
+
+// ----------------------------------------------------------------- CRT
+__device__ __forceinline__ double u128_to_double(u128 x) {
+  if (x == 0) return 0.0;
+  const uint64_t hi = (uint64_t)(x >> 64), lo = (uint64_t)x;
+  const int lz = hi ? __clzll((long long)hi) : 64 + __clzll((long long)lo);
+  const u128 y = x << lz;  // top bit at 127
+  uint64_t top = (uint64_t)(y >> 64);
+  top |= ((uint64_t)y != 0) ? 1ull : 0ull;  // sticky (below the rounding bit)
+  return scalbn(__ull2double_rn(top), 64 - lz);
+}
+
+__global__ void crt_kernel(const uint8_t* __restrict__ t, int64_t rows_pad, int64_t cols_pad, int64_t mrows,
+                           int64_t ncols, const int* __restrict__ e_a, const int* __restrict__ e_b, const Crt crt,
+                           double* __restrict__ c, int64_t ldc) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t j = blockIdx.y;
+  if (i >= mrows) return;
+  const u128 M = ((u128)crt.M_hi << 64) | crt.M_lo;
+  const u128 H = ((u128)crt.H_hi << 64) | crt.H_lo;
+  u128 s = 0;
+  for (int l = 0; l < crt.nmod; ++l) {
+    const int tv = t[((size_t)l * cols_pad + j) * rows_pad + i];
+    const int p = tv * crt.y[l];  // < 2^16, exact in float
+    int qv = (int)floorf((float)p * crt.inv_m[l]);
+    int u = p - qv * crt.m[l];
+    if (u < 0) u += crt.m[l];
+    if (u >= crt.m[l]) u -= crt.m[l];
+    s += (u128)(unsigned)u * (((u128)crt.md_hi[l] << 64) | crt.md_lo[l]);
+    if (s >= M) s -= M;
+  }
+  double v;
+  if (s > H)
+    v = -u128_to_double(M - s);
+  else
+    v = u128_to_double(s);
+  c[i + j * ldc] = scalbn(v, -(e_a[0] + e_b[j]));
+}
+
+// ----------------------------------------------------------------- host side
+struct PrepLayout {
+  int64_t nib, njb, ncb, cols_per;
+  size_t off_hdr, off_part, off_tiles, total;
+};
+static PrepLayout prep_layout(int64_t m, int64_t n, int nmod) {
+  PrepLayout p;
+  p.nib = ceil_div(m, kTile);
+  p.nib += p.nib & 1;
+  p.njb = ceil_div(n, kTile);
+  p.njb += p.njb & 1;
+  p.cols_per = 512;
+  p.ncb = ceil_div(n, p.cols_per);
+  p.off_hdr = 0;
+  p.off_part = 256;
+  p.off_tiles = (p.off_part + (size_t)p.ncb * m * sizeof(double) + 1023) & ~size_t(1023);
+  p.total = p.off_tiles + (size_t)nmod * p.njb * p.nib * kTileBytes;
+  return p;
+}
+
+struct GemmLayout {
+  int ng, n_g;
+  int64_t nkb, nmb, rows_pad, cols_pad;
+  size_t off_eb, off_b, off_t, total;
+};
+static GemmLayout gemm_layout(const PrepLayout& p, int trans, int64_t ncols, int nmod) {
+  GemmLayout g;
+  g.ng = (int)ceil_div(ncols, 256);
+  if (g.ng < 1) g.ng = 1;
+  g.n_g = (int)ceil_div(ceil_div(ncols, g.ng), 32) * 32;
+  if (g.n_g < 32) g.n_g = 32;
+  g.nkb = trans ? p.nib : p.njb;
+  g.nmb = (trans ? p.njb : p.nib) / 2;
+  g.rows_pad = g.nmb * 256;
+  g.cols_pad = (int64_t)g.ng * g.n_g;
+  g.off_eb = 0;
+  g.off_b = (((size_t)g.cols_pad * sizeof(int)) + 1023) & ~size_t(1023);
+  g.off_t = g.off_b + (size_t)nmod * g.cols_pad * g.nkb * kTile;
+  g.total = g.off_t + (size_t)nmod * g.cols_pad * g.rows_pad;
+  return g;
+}
+
+static size_t gemm_smem_bytes(int n_g) {
+  return 1024 + (size_t)kStages * (2 * kTileBytes + (size_t)n_g * kTile) + 256;
+}
+
+template <int NMOD>
+static void launch_residue_a(const double* a, int64_t lda, int64_t m, int64_t n, const int* e_a, int8_t* tiles,
+                             const PrepLayout& p, cudaStream_t st) {
+  residue_a_kernel<NMOD><<<dim3((unsigned)p.nib, (unsigned)p.njb), 256, 0, st>>>(a, lda, m, n, e_a, tiles, p.nib,
+                                                                                  p.njb);
+}
+template <int NMOD>
+static void launch_residue_b(const double* b, int64_t ldb, int64_t k, int64_t ncols, const GemmLayout& g, int pb,
+                             int* e_b, int8_t* tiles, cudaStream_t st) {
+  residue_b_kernel<NMOD><<<(unsigned)g.cols_pad, 256, 0, st>>>(b, ldb, k, ncols, g.n_g, g.nkb, pb, e_b, tiles, g.ng);
+}
+
+#define OZ_DISPATCH(NM, FN, ...)      \
+  switch (NM) {                       \
+    case 12: FN<12>(__VA_ARGS__); break; \
+    case 13: FN<13>(__VA_ARGS__); break; \
+    case 14: FN<14>(__VA_ARGS__); break; \
+    case 15: FN<15>(__VA_ARGS__); break; \
+    default: FN<16>(__VA_ARGS__); break; \
+  }
+
+}  // namespace oz
+
+size_t oz_prep_workspace(int64_t m, int64_t n, int nmod) {
+  if (nmod < 12 || nmod > oz::kMaxMod || m < 1 || n < 1) return 0;
+  return oz::prep_layout(m, n, nmod).total;
+}
+
+int oz_prep(const double* a, int64_t lda, int64_t m, int64_t n, int nmod, void* prep, size_t prep_bytes,
+            cudaStream_t st) {
+  RLRA_REQUIRE(nmod >= 12 && nmod <= oz::kMaxMod, "oz_prep: nmod must be in [12, 16], got %d", nmod);
+  RLRA_REQUIRE(m >= 1 && n >= 1 && lda >= m, "oz_prep: bad shape m=%lld n=%lld lda=%lld", (long long)m,
+               (long long)n, (long long)lda);
+  const oz::PrepLayout p = oz::prep_layout(m, n, nmod);
+  RLRA_REQUIRE(prep && prep_bytes >= p.total, "oz_prep: workspace too small (%zu < %zu)", prep_bytes, p.total);
+  RLRA_REQUIRE(p.njb <= 65535, "oz_prep: n too large (%lld)", (long long)n);
+  uint8_t* base = static_cast<uint8_t*>(prep);
+  int* e_a = reinterpret_cast<int*>(base + p.off_hdr);
+  unsigned long long* maxbits = reinterpret_cast<unsigned long long*>(base + p.off_hdr + 8);
+  double* part = reinterpret_cast<double*>(base + p.off_part);
+  int8_t* tiles = reinterpret_cast<int8_t*>(base + p.off_tiles);
+  RLRA_CHECK_CUDA(cudaMemsetAsync(maxbits, 0, sizeof(unsigned long long), st));
+  oz::colnorm_kernel<<<(unsigned)ceil_div(n, 8), 256, 0, st>>>(a, lda, m, n, maxbits);
+  RLRA_LAUNCHED();
+  oz::rownorm_partial_kernel<<<dim3((unsigned)ceil_div(m, 256), (unsigned)p.ncb), 256, 0, st>>>(a, lda, m, n,
+                                                                                                 p.cols_per, part);
+  RLRA_LAUNCHED();
+  oz::rownorm_final_kernel<<<(unsigned)ceil_div(m, 256), 256, 0, st>>>(part, m, p.ncb, maxbits);
+  RLRA_LAUNCHED();
+  oz::scale_a_kernel<<<1, 1, 0, st>>>(maxbits, oz::budget(nmod).pa, e_a);
+  RLRA_LAUNCHED();
+  OZ_DISPATCH(nmod, oz::launch_residue_a, a, lda, m, n, e_a, tiles, p, st);
+  RLRA_LAUNCHED();
+  return 0;
+}
+
+size_t oz_gemm_workspace(int trans, int64_t m, int64_t n, int64_t ncols, int nmod) {
+  if (nmod < 12 || nmod > oz::kMaxMod || m < 1 || n < 1 || ncols < 1) return 0;
+  const oz::PrepLayout p = oz::prep_layout(m, n, nmod);
+  return oz::gemm_layout(p, trans, ncols, nmod).total;
+}
+
+int oz_gemm(int trans, const void* prep, int64_t m, int64_t n, int nmod, const double* b, int64_t ldb,
+            int64_t ncols, double* c, int64_t ldc, void* ws, size_t ws_bytes, cudaStream_t st) {
+  RLRA_REQUIRE(nmod >= 12 && nmod <= oz::kMaxMod, "oz_gemm: nmod must be in [12, 16], got %d", nmod);
+  const int64_t K = trans ? m : n, mrows = trans ? n : m;
+  RLRA_REQUIRE(ncols >= 0 && ldb >= K && ldc >= mrows, "oz_gemm: bad leading dimensions");
+  if (ncols == 0) return 0;
+  const oz::PrepLayout p = oz::prep_layout(m, n, nmod);
+  const oz::GemmLayout g = oz::gemm_layout(p, trans, ncols, nmod);
+  RLRA_REQUIRE(ws && ws_bytes >= g.total, "oz_gemm: workspace too small (%zu < %zu)", ws_bytes, g.total);
+  RLRA_REQUIRE(g.nkb * oz::kTile <= oz::kMaxK, "oz_gemm: K=%lld exceeds the exact int32 range",
+               (long long)(g.nkb * oz::kTile));
+  RLRA_REQUIRE(g.cols_pad <= 65535, "oz_gemm: too many columns (%lld)", (long long)ncols);
+  const uint8_t* pb = static_cast<const uint8_t*>(prep);
+  const int* e_a = reinterpret_cast<const int*>(pb + p.off_hdr);
+  const int8_t* a_tiles = reinterpret_cast<const int8_t*>(pb + p.off_tiles);
+  uint8_t* w = static_cast<uint8_t*>(ws);
+  int* e_b = reinterpret_cast<int*>(w + g.off_eb);
+  int8_t* b_tiles = reinterpret_cast<int8_t*>(w + g.off_b);
+  uint8_t* tout = w + g.off_t;
+  const oz::Budget bud = oz::budget(nmod);
+  OZ_DISPATCH(nmod, oz::launch_residue_b, b, ldb, K, ncols, g, bud.pb, e_b, b_tiles, st);
+  RLRA_LAUNCHED();
+
+  oz::GemmArgs ga;
+  ga.a_tiles = a_tiles;
+  ga.nib = p.nib;
+  ga.njb = p.njb;
+  ga.trans = trans;
+  ga.b_tiles = b_tiles;
+  ga.ng = g.ng;
+  ga.n_g = g.n_g;
+  ga.nkb = g.nkb;
+  ga.nmb = g.nmb;
+  ga.out = tout;
+  ga.nmod = nmod;
+  for (int l = 0; l < oz::kMaxMod; ++l) ga.mods[l] = oz::kModuli[l];
+  const size_t smem = oz::gemm_smem_bytes(g.n_g);
+  static std::once_flag once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(once, [] {
+    attr_err = cudaFuncSetAttribute(oz::gemm_i8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)oz::gemm_smem_bytes(256));
+  });
+  RLRA_CHECK_CUDA(attr_err);
+  const int64_t units = (int64_t)nmod * g.nmb * g.ng;
+  const int grid = (int)std::min<int64_t>(units, device_info().sm_count);
+  oz::gemm_i8_kernel<<<grid, oz::kGemmThreads, smem, st>>>(ga);
+  RLRA_LAUNCHED();
+
+  const oz::Crt crt = oz::make_crt(nmod);
+  oz::crt_kernel<<<dim3((unsigned)ceil_div(mrows, 256), (unsigned)ncols), 256, 0, st>>>(
+      tout, g.rows_pad, g.cols_pad, mrows, ncols, e_a, e_b, crt, c, ldc);
+  RLRA_LAUNCHED();
+  return 0;
+}
+
+}  // namespace rlra

@@ -2,7 +2,8 @@
 and column-stream protocol (rlra/singlepass.py:27-57) over HBM-resident data.
 
 A ``DeviceMatrix`` holds A column-major in HBM (one upload); ``matmul`` and
-``rmatmul`` are one pass over A each on the DMMA GEMM (K1/K2), ``fro_norm`` is
+``rmatmul`` are one pass over A each (K1/K2: the int8 tensor-core emulation of
+csrc/ozaki.cu, or the DMMA GEMM with RLRA_B200_PASS_GEMM=dmma), ``fro_norm`` is
 the compensated K2b reduction.  Host ndarrays handed to the drivers are wrapped
 in a DeviceMatrix; duck-typed host accessors are adapted so their products feed
 the device pipeline (their own products run wherever they run).
@@ -10,7 +11,9 @@ the device pipeline (their own products run wherever they run).
 
 from __future__ import annotations
 
+import contextlib
 import math
+import os
 
 import numpy as np
 import torch
@@ -18,6 +21,22 @@ import torch
 from . import ops
 
 DEFAULT_PANEL = 256  # rlra/singlepass.py:19
+
+# Pass-product engine: "oz" = FP64 emulated on the int8 tensor cores
+# (csrc/ozaki.cu, DGEMM-level accuracy, ~5x the DMMA pass), "dmma" = native
+# FP64 DMMA GEMM (csrc/gemm_tma.cu).
+PASS_GEMM = os.environ.get("RLRA_B200_PASS_GEMM", "oz")
+OZ_MAX_K = 133144
+# residues take nmod bytes per element of A (14 B vs 8 B of float64); larger
+# operands stay on the DMMA pass (C5: 68.7 GB A would need 120 GB of residues)
+OZ_MAX_RESIDUE_BYTES = int(os.environ.get("RLRA_B200_OZ_MAX_BYTES", str(48 << 30)))
+
+
+def product_session(a):
+    """Context in which the pass products of one driver call share the int8
+    residues of A (built at the first product, dropped at exit)."""
+    fn = getattr(a, "products", None)
+    return fn() if fn is not None else contextlib.nullcontext()
 
 
 class DeviceMatrix:
@@ -50,6 +69,33 @@ class DeviceMatrix:
             else:
                 self._a = ops.from_numpy(arr, dev)
         self._fro = None
+        self._sessions = 0
+        self._oz_prep = None
+
+    @contextlib.contextmanager
+    def products(self):
+        self._sessions += 1
+        try:
+            yield self
+        finally:
+            self._sessions -= 1
+            if self._sessions == 0:
+                self._oz_prep = None
+
+    def _oz_ok(self, k, ncols):
+        m, n = self._a.shape
+        return (PASS_GEMM == "oz" and 0 < k <= OZ_MAX_K and 0 < ncols <= 4096 and min(m, n) > 0
+                and max(m, n) <= OZ_MAX_K and ops.OZ_NMOD * m * n <= OZ_MAX_RESIDUE_BYTES)
+
+    def _oz(self):
+        """Residues of A for this product session (or a transient one)."""
+        if self._oz_prep is not None:
+            return self._oz_prep
+        with ops.label("oz_prep"):
+            prep = ops.OzPrep(self.tensor)
+        if self._sessions > 0:
+            self._oz_prep = prep
+        return prep
 
     def _upload_pipelined(self, arr, host, dev):
         m, n = arr.shape
@@ -101,6 +147,8 @@ class DeviceMatrix:
                     ops.gemm(self._a[:, c0:c1], x[c0:c1, :], y, beta=0.0 if i == 0 else 1.0)
                 self._finish_upload()
                 return y
+            if self._oz_ok(self._a.shape[1], x.shape[1]):
+                return self._oz().gemm(x, trans=False)
             return ops.matmul(self._a, x)
 
     def rmatmul(self, x):
@@ -115,6 +163,8 @@ class DeviceMatrix:
                     ops.gemm(self._a[:, c0:c1], x, z[c0:c1, :], ta=True)
                 self._finish_upload()
                 return z
+            if self._oz_ok(self._a.shape[0], x.shape[1]):
+                return self._oz().gemm(x, trans=True)
             return ops.matmul(self._a, x, ta=True)
 
     def fro_norm_sq_device(self):
@@ -179,6 +229,9 @@ class InstrumentedAccessor:
     @property
     def device(self):
         return self.inner.device
+
+    def products(self):
+        return product_session(self.inner)
 
     def matmul(self, x):
         self.product_count += 1

@@ -21,6 +21,7 @@ suite only -- on CPU tensors with gloo and an oracle-backed ops object
 
 from __future__ import annotations
 
+import contextlib
 import os
 from dataclasses import dataclass
 
@@ -55,6 +56,21 @@ class CudaOps:
 
     def matmul(self, a, b, ta=False, tb=False):
         return self.o.matmul(a, b, ta=ta, tb=tb)
+
+    def pass_prep(self, a):
+        """Int8 residues of the local shard for the emulated pass products."""
+        from .device import OZ_MAX_K, OZ_MAX_RESIDUE_BYTES, PASS_GEMM
+
+        if PASS_GEMM != "oz" or min(a.shape) == 0 or max(a.shape) > OZ_MAX_K:
+            return None
+        if self.o.OZ_NMOD * a.shape[0] * a.shape[1] > OZ_MAX_RESIDUE_BYTES:
+            return None
+        return self.o.OzPrep(a)
+
+    def pass_matmul(self, a, prep, x, ta=False):
+        if prep is not None and 0 < x.shape[1] <= 4096:
+            return prep.gemm(x, trans=ta)
+        return self.o.matmul(a, x, ta=ta)
 
     def getrf_(self, a):
         return self.o.getrf_(a)
@@ -100,6 +116,30 @@ class ShardedMatrix:
         self.world = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
         self.product_count = 0
+        self._sessions = 0
+        self._prep = None
+        self._prep_built = False
+
+    @contextlib.contextmanager
+    def products(self):
+        """Pass products of one driver call share the residues of A_i."""
+        self._sessions += 1
+        try:
+            yield self
+        finally:
+            self._sessions -= 1
+            if self._sessions == 0:
+                self._prep, self._prep_built = None, False
+
+    def _pass(self, x, ta):
+        if not hasattr(self.ops, "pass_matmul"):
+            return self.ops.matmul(self.local, x, ta=ta)
+        prep = self._prep
+        if not self._prep_built:
+            prep = self.ops.pass_prep(self.local)
+            if self._sessions > 0:
+                self._prep, self._prep_built = prep, True
+        return self.ops.pass_matmul(self.local, prep, x, ta=ta)
 
     @property
     def shape(self):
@@ -109,12 +149,12 @@ class ShardedMatrix:
     def matmul(self, w):
         """Y_i = A_i W (W replicated n x w) -> local rows of Y."""
         self.product_count += 1
-        return self.ops.matmul(self.local, w)
+        return self._pass(w, False)
 
     def rmatmul(self, y_local):
         """Z = sum_i A_i^T Y_i -> replicated n x w (NCCL all-reduce)."""
         self.product_count += 1
-        z = self.ops.matmul(self.local, y_local, ta=True)
+        z = self._pass(y_local, True)
         # column-major (n, w) == contiguous (w, n) storage: reduce that view in place
         dist.all_reduce(z.t(), op=dist.ReduceOp.SUM, group=self.group)
         return z
@@ -228,9 +268,11 @@ def powerlu(A: ShardedMatrix, k, q_os=10, v=3, seed=0, omega_fn=None):
         raise ValueError("oversampling must be >= 0")
     if k + q_os > min(m, n):
         raise ValueError(f"sketch width {k + q_os} exceeds min{(m, n)}")
-    V, _ = general_power_basis_v(A, k + q_os, v, seed, omega_fn)
-    vk = V[:, :k]
-    return lu_from_projection(A, A.matmul(vk), vk)
+    with A.products():
+        V, _ = general_power_basis_v(A, k + q_os, v, seed, omega_fn)
+        vk = V[:, :k]
+        g_local = A.matmul(vk)
+    return lu_from_projection(A, g_local, vk)
 
 
 def adaptive_rank(A: ShardedMatrix, eps, b, l, v, seed, omega_fn):
@@ -241,8 +283,9 @@ def adaptive_rank(A: ShardedMatrix, eps, b, l, v, seed, omega_fn):
     m, n = A.shape
     if l > min(m, n):
         raise ValueError(f"sketch width {l} exceeds min{(m, n)}")
-    V, _ = general_power_basis_v(A, l, v, seed, omega_fn)
-    g_local = A.matmul(V)
+    with A.products():
+        V, _ = general_power_basis_v(A, l, v, seed, omega_fn)
+        g_local = A.matmul(V)
     e = A.ops.colsumsq(g_local).clone()
     dist.all_reduce(e, op=dist.ReduceOp.SUM, group=A.group)
     total = math.sqrt(float(A.fro_norm_sq().item())) ** 2

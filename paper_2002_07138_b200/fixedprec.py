@@ -18,7 +18,7 @@ import numpy as np
 import torch
 
 from . import ops
-from .device import as_accessor
+from .device import as_accessor, product_session
 from .errors import NotConverged, Unsatisfiable
 from .fixedrank import _host_input, lu_from_projection_
 from .kernels import _copy
@@ -110,8 +110,9 @@ def _adaptive(a, params, seed):
     if params.l > min(m, n):
         raise ValueError(f"sketch width {params.l} exceeds min{(m, n)}")
     checks = RankChecks()
-    basis = general_power_basis_v(a, params.l, params.v, seed, _checks=checks)
-    g = a.matmul(basis.V)
+    with product_session(a):
+        basis = general_power_basis_v(a, params.l, params.v, seed, _checks=checks)
+        g = a.matmul(basis.V)
     fro2 = a.fro_norm_sq_device()
     energies = ops.colsumsq(g)
     checks.raise_if_collapsed()

@@ -16,7 +16,7 @@ import numpy as np
 import torch
 
 from . import ops
-from .device import DeviceMatrix, as_accessor
+from .device import DeviceMatrix, as_accessor, product_session
 from .kernels import plu_, _copy
 from .rangefinder import RankChecks, general_power_basis_v
 
@@ -91,9 +91,10 @@ def powerlu(a, k, q_os=10, v=3, seed=0):
     if v < 2:
         raise ValueError("pass budget v must be >= 2")
     checks = RankChecks()
-    basis = general_power_basis_v(a, k + q_os, v, seed, _checks=checks)
-    vk = basis.V[:, :k]
-    g = a.matmul(vk)
+    with product_session(a):
+        basis = general_power_basis_v(a, k + q_os, v, seed, _checks=checks)
+        vk = basis.V[:, :k]
+        g = a.matmul(vk)
     f = lu_from_projection_(g, vk)
     checks.raise_if_collapsed()
     return f.to_numpy() if host else f

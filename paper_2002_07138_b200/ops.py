@@ -8,6 +8,8 @@ used only for device memory, streams and views (plumbing), never for math.
 
 from __future__ import annotations
 
+import os
+
 import numpy as np
 import torch
 
@@ -154,6 +156,40 @@ def gemm(a, b, c, *, ta=False, tb=False, alpha=1.0, beta=0.0):
                  ptr(b), ld_of(b), float(beta), ptr(c), ld_of(c), ptr(ws), wsb,
                  _stream(c.device))
     return c
+
+
+OZ_NMOD = int(os.environ.get("RLRA_B200_OZ_NMOD", "14"))
+
+
+class OzPrep:
+    """Int8 residues of A for the emulated pass products (csrc/ozaki.cu): built
+    once per A, they serve both C = A B (trans=False) and C = A^T B."""
+
+    def __init__(self, a, nmod=None):
+        m, n = a.shape
+        self.m, self.n = int(m), int(n)
+        self.nmod = OZ_NMOD if nmod is None else int(nmod)
+        self.device = a.device
+        wsb = _native.query("rlra_b200_oz_prep_workspace", self.m, self.n, self.nmod)
+        self.ws = torch.empty(max(wsb, 8), dtype=torch.uint8, device=a.device)
+        _call("rlra_b200_oz_prep", a.device, ptr(a), ld_of(a), self.m, self.n, self.nmod, ptr(self.ws), wsb,
+              _stream(a.device))
+
+    def gemm(self, b, trans=False, keep_ws=False):
+        """C = A B (trans=False, b n x l) or A^T B (trans=True, b m x l)."""
+        k, rows = (self.m, self.n) if trans else (self.n, self.m)
+        if b.shape[0] != k:
+            raise ValueError(f"oz gemm shape mismatch: A {(self.m, self.n)} trans={trans}, B {tuple(b.shape)}")
+        ncols = int(b.shape[1])
+        c = fmat(rows, ncols, self.device)
+        if ncols == 0:
+            return (c, None) if keep_ws else c
+        b = as_fmat(b)
+        wsb = _native.query("rlra_b200_oz_gemm_workspace", int(trans), self.m, self.n, ncols, self.nmod)
+        ws = torch.empty(max(wsb, 8), dtype=torch.uint8, device=self.device)
+        _call("rlra_b200_oz_gemm", self.device, int(trans), ptr(self.ws), self.m, self.n, self.nmod, ptr(b),
+              ld_of(b), ncols, ptr(c), ld_of(c), ptr(ws), wsb, _stream(self.device))
+        return (c, ws) if keep_ws else c
 
 
 def matmul(a, b, *, ta=False, tb=False):

@@ -53,3 +53,23 @@ def test_c4_single_pass_pivots_and_error(cuda_dev):
     assert np.array_equal(f.p.cpu().numpy(), p) and np.array_equal(f.q.cpu().numpy(), q)
     err = validate.rel_err_device(a, f)
     assert abs(err - CFG["C4"]["rel_err"]) <= REL_ERR_TOL, (err, CFG["C4"]["rel_err"])
+
+
+@pytest.mark.skipif("C5" not in CFG, reason="C5 golden not generated")
+def test_c5_powerlu_pivots_and_error(cuda_dev):
+    """262144 x 32768 (68.7 GB in HBM): the reference ran on the GPU box's host
+    (tests/golden/make_golden_configs.py C5, 126 s on 16 cores)."""
+    import torch
+
+    import paper_2002_07138_b200 as P
+    from paper_2002_07138_b200 import configs, validate
+
+    a = configs.gen_device("C5", cuda_dev)
+    f = P.powerlu(P.DeviceMatrix(a), 512, 32, 4, 0)
+    assert f.rank == CFG["C5"]["rank"]
+    p, q = _pq("C5")
+    assert np.array_equal(f.p.cpu().numpy(), p) and np.array_equal(f.q.cpu().numpy(), q)
+    err = validate.rel_err_device(a, f)
+    assert abs(err - CFG["C5"]["rel_err"]) <= REL_ERR_TOL, (err, CFG["C5"]["rel_err"])
+    del a, f
+    torch.cuda.empty_cache()

@@ -1,0 +1,89 @@
+"""K1/K2 emulated on the int8 tensor cores (csrc/ozaki.cu, Ozaki scheme II).
+
+Accuracy contract (include/rlra_b200.h): for nmod = 14 the error of every
+element is bounded by the scaling step alone,
+    |C_ij - (A B)_ij| <= (2^-PA sqrt(K) ||A||_max-norm ||B_j|| + 2^-PB ...)
+which we check in its normwise form against an extended-precision reference
+(np.longdouble products), with tolerance
+    |C - C_ref|_ij <= 2^-50 * N_A * ||B_j||_2,   N_A = max row / column norm of A,
+and we also check that the emulation is at least as accurate as NumPy's
+float64 DGEMM on the same inputs (max error within 4x of DGEMM's).  Results
+are exact functions of the inputs, so repeated calls are bitwise identical.
+"""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _ref(opa, b):
+    return opa.astype(np.longdouble) @ b.astype(np.longdouble)
+
+
+def run(m, n, l, trans, seed=0, scale_rows=False, nmod=14):
+    from paper_2002_07138_b200 import ops
+
+    dev = ops.check_device()
+    rng = np.random.default_rng(seed)
+    a = rng.standard_normal((m, n))
+    if scale_rows:
+        a *= np.exp(rng.uniform(-3, 3, size=(m, 1)))
+        a *= np.exp(rng.uniform(-3, 3, size=(1, n)))
+    k = m if trans else n
+    b = rng.standard_normal((k, l)) * np.exp(rng.uniform(-5, 5, size=(1, l)))
+    prep = ops.OzPrep(ops.from_numpy(a, dev), nmod)
+    c = ops.to_numpy(prep.gemm(ops.from_numpy(b, dev), trans=trans))
+    opa = a.T if trans else a
+    ref = _ref(opa, b)
+    na = max(np.sqrt((a * a).sum(0)).max(), np.sqrt((a * a).sum(1)).max())
+    nb = np.sqrt((b * b).sum(0))
+    err = np.abs(c - ref).astype(np.float64)
+    tol = 2.0 ** -50 * na * nb[None, :]
+    assert np.all(err <= tol), float((err / tol).max())
+    err_np = np.abs(opa @ b - ref).astype(np.float64)
+    return c, float((err / nb).max()), float((err_np / nb).max())
+
+
+@pytest.mark.parametrize("trans", [False, True])
+@pytest.mark.parametrize("m,n,l", [(700, 500, 100), (1000, 1000, 220), (257, 129, 33), (130, 300, 1),
+                                   (384, 256, 300), (2000, 1500, 544), (129, 127, 32)])
+def test_oz_gemm_accuracy(cuda_dev, m, n, l, trans):
+    _, e_oz, e_np = run(m, n, l, trans)
+    assert e_oz <= 4 * e_np + 1e-300, (e_oz, e_np)
+
+
+@pytest.mark.parametrize("trans", [False, True])
+def test_oz_gemm_badly_scaled_rows_and_columns(cuda_dev, trans):
+    run(600, 400, 64, trans, seed=3, scale_rows=True)
+
+
+def test_oz_gemm_deterministic_and_zero_columns(cuda_dev):
+    from paper_2002_07138_b200 import ops
+
+    rng = np.random.default_rng(5)
+    a = rng.standard_normal((500, 300))
+    b = rng.standard_normal((300, 40))
+    b[:, 7] = 0.0
+    ad = ops.from_numpy(a, cuda_dev)
+    prep = ops.OzPrep(ad)
+    c1 = ops.to_numpy(prep.gemm(ops.from_numpy(b, cuda_dev)))
+    c2 = ops.to_numpy(ops.OzPrep(ad).gemm(ops.from_numpy(b, cuda_dev)))
+    assert np.array_equal(c1, c2)
+    assert np.all(c1[:, 7] == 0.0)
+    z = ops.OzPrep(ops.from_numpy(np.zeros((200, 100)), cuda_dev))
+    assert np.all(ops.to_numpy(z.gemm(ops.from_numpy(b[:100], cuda_dev))) == 0.0)
+
+
+@pytest.mark.parametrize("nmod", [12, 13, 15, 16])
+def test_oz_gemm_other_moduli_counts(cuda_dev, nmod):
+    from paper_2002_07138_b200 import ops
+
+    rng = np.random.default_rng(nmod)
+    a = rng.standard_normal((400, 300))
+    b = rng.standard_normal((300, 50))
+    c = ops.to_numpy(ops.OzPrep(ops.from_numpy(a, cuda_dev), nmod).gemm(ops.from_numpy(b, cuda_dev)))
+    ref = _ref(a, b)
+    rel = float(np.abs(c - ref).max() / np.abs(ref).max())
+    # each modulus is ~7.8 bits of product budget, split between A and B
+    assert rel < max(2.0 ** (-(3.9 * nmod - 8)), 2.0 ** -50), rel
