@@ -116,24 +116,25 @@ static Crt make_crt(int nmod) {
 }
 
 // ----------------------------------------------------------------- residues
-// x = rint(v * 2^e) as four signed 14-bit float parts (|x| < 2^56).
+// x = rint(v * 2^e), |x| < 2^55, as four float parts x = p3 2^42 + p2 2^28 +
+// p1 2^14 + p0 with p0..p2 in [0, 2^14) and p3 signed (two's complement split).
 struct Parts {
   float p0, p1, p2, p3;
 };
 __device__ __forceinline__ Parts split_parts(double v, double scale) {
   const long long xi = __double2ll_rn(v * scale);
-  const unsigned long long u = (unsigned long long)(xi < 0 ? -xi : xi);
-  const float s = xi < 0 ? -1.0f : 1.0f;
+  const unsigned lo = (unsigned)xi;
+  const unsigned hi = (unsigned)(xi >> 28);  // bits 28..59 (sign-extended)
   Parts p;
-  p.p0 = s * (__int_as_float(0x4B000000 | (unsigned)(u & 0x3FFF)) - 8388608.0f);
-  p.p1 = s * (__int_as_float(0x4B000000 | (unsigned)((u >> 14) & 0x3FFF)) - 8388608.0f);
-  p.p2 = s * (__int_as_float(0x4B000000 | (unsigned)((u >> 28) & 0x3FFF)) - 8388608.0f);
-  p.p3 = s * (__int_as_float(0x4B000000 | (unsigned)((u >> 42) & 0x3FFF)) - 8388608.0f);
+  p.p0 = __int_as_float(0x4B000000 | (lo & 0x3FFF)) - 8388608.0f;
+  p.p1 = __int_as_float(0x4B000000 | ((lo >> 14) & 0x3FFF)) - 8388608.0f;
+  p.p2 = __int_as_float(0x4B000000 | (hi & 0x3FFF)) - 8388608.0f;
+  p.p3 = __int_as_float(0x4B400000 + ((int)hi >> 14)) - 12582912.0f;  // signed, |p3| < 2^13
   return p;
 }
 
 // Residue of the part-encoded integer modulo kModuli[L], in [-m/2-1, m/2+1]
-// (|r| <= 125), returned as the low byte of a float-encoded integer.
+// (|r| <= 126), returned as the low byte of a float-encoded integer.
 template <int L>
 __device__ __forceinline__ unsigned residue_byte(const Parts& x) {
   constexpr int m = kModuli[L];
@@ -151,169 +152,206 @@ __device__ __forceinline__ unsigned pack4(unsigned b0, unsigned b1, unsigned b2,
   return __byte_perm(__byte_perm(b0, b1, 0x0040), __byte_perm(b2, b3, 0x0040), 0x5410);
 }
 
-// 16 consecutive values -> 16 residue bytes for modulus L (one swizzle chunk).
-template <int L>
-__device__ __forceinline__ uint4 residue_chunk(const Parts (&x)[16]) {
-  uint4 o;
-  o.x = pack4(residue_byte<L>(x[0]), residue_byte<L>(x[1]), residue_byte<L>(x[2]), residue_byte<L>(x[3]));
-  o.y = pack4(residue_byte<L>(x[4]), residue_byte<L>(x[5]), residue_byte<L>(x[6]), residue_byte<L>(x[7]));
-  o.z = pack4(residue_byte<L>(x[8]), residue_byte<L>(x[9]), residue_byte<L>(x[10]), residue_byte<L>(x[11]));
-  o.w = pack4(residue_byte<L>(x[12]), residue_byte<L>(x[13]), residue_byte<L>(x[14]), residue_byte<L>(x[15]));
+template <int N>
+struct Bytes;
+template <>
+struct Bytes<16> {
+  typedef uint4 T;
+};
+template <>
+struct Bytes<8> {
+  typedef uint2 T;
+};
+
+// N (8 or 16) consecutive values -> N residue bytes for modulus L.
+template <int L, int N>
+__device__ __forceinline__ typename Bytes<N>::T residue_chunk(const Parts (&x)[N]) {
+  unsigned w[N / 4];
+#pragma unroll
+  for (int q = 0; q < N / 4; ++q)
+    w[q] = pack4(residue_byte<L>(x[4 * q]), residue_byte<L>(x[4 * q + 1]), residue_byte<L>(x[4 * q + 2]),
+                 residue_byte<L>(x[4 * q + 3]));
+  typename Bytes<N>::T o;
+  if constexpr (N == 16) {
+    o.x = w[0]; o.y = w[1]; o.z = w[2]; o.w = w[3];
+  } else {
+    o.x = w[0]; o.y = w[1];
+  }
   return o;
 }
 
-template <int L, int NMOD>
+template <int L, int NMOD, int N>
 struct ChunkWriter {
-  __device__ __forceinline__ static void run(const Parts (&x)[16], int8_t* base, size_t mod_stride) {
-    *reinterpret_cast<uint4*>(base + (size_t)L * mod_stride) = residue_chunk<L>(x);
-    ChunkWriter<L + 1, NMOD>::run(x, base, mod_stride);
+  __device__ __forceinline__ static void run(const Parts (&x)[N], int8_t* base, size_t mod_stride) {
+    *reinterpret_cast<typename Bytes<N>::T*>(base + (size_t)L * mod_stride) = residue_chunk<L, N>(x);
+    ChunkWriter<L + 1, NMOD, N>::run(x, base, mod_stride);
   }
 };
-template <int NMOD>
-struct ChunkWriter<NMOD, NMOD> {
-  __device__ __forceinline__ static void run(const Parts (&)[16], int8_t*, size_t) {}
+template <int NMOD, int N>
+struct ChunkWriter<NMOD, NMOD, N> {
+  __device__ __forceinline__ static void run(const Parts (&)[N], int8_t*, size_t) {}
 };
 
 __device__ __forceinline__ int swz(int r, int c) {  // byte offset of 16-byte chunk c of row r
   return r * kTile + (((c ^ (r & 7)) & 7) << 4);
 }
 
-// Residues of A: one CTA per 128 x 128 block of A (tile (jb, ib)).
+// Residues of A: one CTA per 128 x 128 block of A (tile (jb, ib)); each thread
+// converts 8 x 8 consecutive rows of one column (half swizzle chunks), with the
+// next group's loads in flight while the current one is converted.
 template <int NMOD>
-__global__ void __launch_bounds__(256) residue_a_kernel(const double* __restrict__ a, int64_t lda, int64_t m,
-                                                        int64_t n, const int* __restrict__ e_a,
-                                                        int8_t* __restrict__ tiles, int64_t nib, int64_t njb) {
+__global__ void __launch_bounds__(256, 2) residue_a_kernel(const double* __restrict__ a, int64_t lda, int64_t m,
+                                                           int64_t n, const int* __restrict__ e_a,
+                                                           int8_t* __restrict__ tiles, int64_t nib, int64_t njb) {
   const int64_t ib = blockIdx.x, jb = blockIdx.y;
   const double scale = scalbn(1.0, e_a[0]);
   const size_t mod_stride = (size_t)njb * nib * kTileBytes;
   int8_t* tile = tiles + ((size_t)jb * nib + ib) * kTileBytes;
-#pragma unroll 1
-  for (int s = 0; s < 4; ++s) {
-    const int ch = threadIdx.x + 256 * s;
-    const int r = ch >> 3, c = ch & 7;
+  const bool full = (ib + 1) * kTile <= m && (jb + 1) * kTile <= n;
+  double cur[8], nxt[8];
+  auto load = [&](int s, double (&d)[8]) {
+    const int ch = threadIdx.x + 256 * s;  // 2048 half chunks per tile
+    const int r = ch >> 4, h = ch & 15;
     const int64_t j = jb * kTile + r;
-    const int64_t i0 = ib * kTile + c * 16;
-    Parts x[16];
+    const int64_t i0 = ib * kTile + h * 8;
+    const double* src = a + i0 + j * lda;
+    if (full) {
 #pragma unroll
-    for (int t = 0; t < 16; ++t) {
-      const int64_t i = i0 + t;
-      const double v = (j < n && i < m) ? __ldg(a + i + j * lda) : 0.0;
-      x[t] = split_parts(v, scale);
+      for (int t = 0; t < 8; ++t) d[t] = __ldcs(src + t);
+    } else {
+#pragma unroll
+      for (int t = 0; t < 8; ++t) d[t] = (j < n && i0 + t < m) ? __ldcs(src + t) : 0.0;
     }
-    ChunkWriter<0, NMOD>::run(x, tile + swz(r, c), mod_stride);
+  };
+  load(0, cur);
+#pragma unroll 1
+  for (int s = 0; s < 8; ++s) {
+    if (s + 1 < 8) load(s + 1, nxt);
+    const int ch = threadIdx.x + 256 * s;
+    const int r = ch >> 4, h = ch & 15;
+    Parts x[8];
+#pragma unroll
+    for (int t = 0; t < 8; ++t) x[t] = split_parts(cur[t], scale);
+    ChunkWriter<0, NMOD, 8>::run(x, tile + swz(r, h >> 1) + (h & 1) * 8, mod_stride);
+#pragma unroll
+    for (int t = 0; t < 8; ++t) cur[t] = nxt[t];
   }
 }
 
-// Residues of the skinny operand B (K x ncols): one CTA per (padded) column,
-// per-column scale, K-major tiles of n_g rows x 128 bytes per (l, group, kb).
-template <int NMOD>
-__global__ void __launch_bounds__(256) residue_b_kernel(const double* __restrict__ b, int64_t ldb, int64_t k,
-                                                        int64_t ncols, int n_g, int64_t nkb, int pb,
-                                                        int* __restrict__ e_b, int8_t* __restrict__ tiles,
-                                                        int ng) {
-  const int64_t jj = blockIdx.x;
-  const int g = (int)(jj / n_g), r = (int)(jj % n_g);
-  __shared__ double red[8];
-  __shared__ int e_sh;
+// Per-column scale of the skinny operand B (K x ncols): warp per (padded) column.
+__global__ void bscale_kernel(const double* __restrict__ b, int64_t ldb, int64_t k, int64_t ncols, int64_t cols_pad,
+                              int pb, int* __restrict__ e_b) {
+  const int64_t jj = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (jj >= cols_pad) return;
   double ss = 0.0;
   if (jj < ncols)
-    for (int64_t i = threadIdx.x; i < k; i += 256) {
+    for (int64_t i = lane; i < k; i += 32) {
       const double v = b[i + jj * ldb];
       ss = fma(v, v, ss);
     }
 #pragma unroll
   for (int o = 16; o; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double t = 0.0;
-    for (int w = 0; w < 8; ++w) t += red[w];
+  if (lane == 0) {
     int e = 0;
-    if (t > 0.0) {
+    if (ss > 0.0) {
       int ex;
-      frexp(sqrt(t) * (1.0 + 0x1p-40), &ex);  // ||b_j|| < 2^ex
+      frexp(sqrt(ss) * (1.0 + 0x1p-40), &ex);  // ||b_j|| < 2^ex
       e = pb - ex;
     }
-    e_sh = e;
     e_b[jj] = e;
-  }
-  __syncthreads();
-  const double scale = scalbn(1.0, e_sh);
-  const size_t mod_stride = (size_t)ng * nkb * n_g * kTile;
-  int8_t* tile0 = tiles + (size_t)g * nkb * n_g * kTile;
-  for (int64_t ch = threadIdx.x; ch < nkb * 8; ch += 256) {
-    const int64_t kb = ch >> 3;
-    const int c = (int)(ch & 7);
-    const int64_t i0 = kb * kTile + c * 16;
-    Parts x[16];
-#pragma unroll
-    for (int t = 0; t < 16; ++t) {
-      const int64_t i = i0 + t;
-      const double v = (jj < ncols && i < k) ? b[i + jj * ldb] : 0.0;
-      x[t] = split_parts(v, scale);
-    }
-    ChunkWriter<0, NMOD>::run(x, tile0 + (size_t)kb * n_g * kTile + swz(r, c), mod_stride);
   }
 }
 
+// Residues of B: K-major tiles of n_g rows x 128 bytes per (l, group, kb);
+// grid (padded column, chunk block), 16 consecutive k per thread.
+template <int NMOD>
+__global__ void __launch_bounds__(256) residue_b_kernel(const double* __restrict__ b, int64_t ldb, int64_t k,
+                                                        int64_t ncols, int n_g, int64_t nkb,
+                                                        const int* __restrict__ e_b, int8_t* __restrict__ tiles,
+                                                        int ng) {
+  const int64_t jj = blockIdx.x;
+  const int g = (int)(jj / n_g), r = (int)(jj % n_g);
+  const double scale = scalbn(1.0, e_b[jj]);
+  const size_t mod_stride = (size_t)ng * nkb * n_g * kTile;
+  int8_t* tile0 = tiles + (size_t)g * nkb * n_g * kTile;
+  const int64_t ch = (int64_t)blockIdx.y * 256 + threadIdx.x;
+  if (ch >= nkb * 8) return;
+  const int64_t kb = ch >> 3;
+  const int c = (int)(ch & 7);
+  const int64_t i0 = kb * kTile + c * 16;
+  Parts x[16];
+#pragma unroll
+  for (int t = 0; t < 16; ++t) {
+    const int64_t i = i0 + t;
+    const double v = (jj < ncols && i < k) ? b[i + jj * ldb] : 0.0;
+    x[t] = split_parts(v, scale);
+  }
+  ChunkWriter<0, NMOD, 16>::run(x, tile0 + (size_t)kb * n_g * kTile + swz(r, c), mod_stride);
+}
+
 // ----------------------------------------------------------------- A scale
-// Row / column 2-norms of A -> max -> eA = PA - ceil(log2(max norm)).
-__global__ void rownorm_partial_kernel(const double* __restrict__ a, int64_t lda, int64_t m, int64_t n,
-                                       int64_t cols_per, double* __restrict__ part) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t cb = blockIdx.y;
-  if (i >= m) return;
-  const int64_t j0 = cb * cols_per, j1 = min(n, j0 + cols_per);
-  double s0 = 0.0, s1 = 0.0;
-  int64_t j = j0;
-  for (; j + 1 < j1; j += 2) {
-    const double v0 = __ldg(a + i + j * lda), v1 = __ldg(a + i + (j + 1) * lda);
-    s0 = fma(v0, v0, s0);
-    s1 = fma(v1, v1, s1);
+// Row and column 2-norms of A in ONE read: CTA = 2048 rows x 256 columns;
+// partial sums in fixed order (deterministic), then max -> eA.
+constexpr int kNormRows = 2048, kNormCols = 256;
+
+__global__ void __launch_bounds__(256) norms_partial_kernel(const double* __restrict__ a, int64_t lda, int64_t m,
+                                                            int64_t n, double* __restrict__ part_row,
+                                                            double* __restrict__ part_col) {
+  const int64_t rb = blockIdx.x, cb = blockIdx.y;
+  const int64_t r0 = rb * kNormRows, c0 = cb * kNormCols;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __shared__ double colw[8][kNormCols];
+  double rs[8];
+#pragma unroll
+  for (int s = 0; s < 8; ++s) rs[s] = 0.0;
+  const int ncols = (int)(n - c0 < kNormCols ? n - c0 : kNormCols);
+  const bool full = r0 + kNormRows <= m;
+#pragma unroll 2
+  for (int jj = 0; jj < ncols; ++jj) {
+    const double* col = a + (c0 + jj) * lda + r0 + threadIdx.x;
+    double cs = 0.0;
+#pragma unroll
+    for (int s = 0; s < 8; ++s) {
+      const double v = (full || r0 + threadIdx.x + 256 * s < m) ? __ldcs(col + 256 * s) : 0.0;
+      rs[s] = fma(v, v, rs[s]);
+      cs = fma(v, v, cs);
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) cs += __shfl_xor_sync(0xffffffffu, cs, o);
+    if (lane == 0) colw[warp][jj] = cs;
   }
-  if (j < j1) {
-    const double v0 = __ldg(a + i + j * lda);
-    s0 = fma(v0, v0, s0);
+  __syncthreads();
+#pragma unroll
+  for (int s = 0; s < 8; ++s) {
+    const int64_t i = r0 + threadIdx.x + 256 * s;
+    if (i < m) part_row[cb * m + i] = rs[s];
   }
-  part[cb * m + i] = s0 + s1;
+  if (threadIdx.x < ncols) {
+    double t = 0.0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) t += colw[w][threadIdx.x];
+    part_col[rb * n + c0 + threadIdx.x] = t;
+  }
 }
 
 __device__ __forceinline__ void atomic_max_pos(unsigned long long* p, double v) {
   atomicMax(p, (unsigned long long)__double_as_longlong(v));  // v >= 0: bit order = value order
 }
 
-__global__ void rownorm_final_kernel(const double* __restrict__ part, int64_t m, int64_t ncb,
-                                     unsigned long long* __restrict__ maxbits) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+__global__ void norms_final_kernel(const double* __restrict__ part_row, int64_t ncb, int64_t m,
+                                   const double* __restrict__ part_col, int64_t nrb, int64_t n,
+                                   unsigned long long* __restrict__ maxbits) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   double v = 0.0;
-  if (i < m)
-    for (int64_t cb = 0; cb < ncb; ++cb) v += part[cb * m + i];
+  if (t < m) {
+    for (int64_t cb = 0; cb < ncb; ++cb) v += part_row[cb * m + t];
+  } else if (t < m + n) {
+    for (int64_t rb = 0; rb < nrb; ++rb) v += part_col[rb * n + (t - m)];
+  }
 #pragma unroll
   for (int o = 16; o; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
   if ((threadIdx.x & 31) == 0) atomic_max_pos(maxbits, v);
-}
-
-__global__ void colnorm_kernel(const double* __restrict__ a, int64_t lda, int64_t m, int64_t n,
-                               unsigned long long* __restrict__ maxbits) {
-  const int64_t j = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
-  if (j >= n) return;
-  const double* col = a + j * lda;
-  double s0 = 0.0, s1 = 0.0;
-  int64_t i = lane;
-  for (; i + 32 < m; i += 64) {
-    const double v0 = __ldg(col + i), v1 = __ldg(col + i + 32);
-    s0 = fma(v0, v0, s0);
-    s1 = fma(v1, v1, s1);
-  }
-  if (i < m) {
-    const double v0 = __ldg(col + i);
-    s0 = fma(v0, v0, s0);
-  }
-  double v = s0 + s1;
-#pragma unroll
-  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  if (lane == 0) atomic_max_pos(maxbits, v);
 }
 
 __global__ void scale_a_kernel(const unsigned long long* __restrict__ maxbits, int pa, int* __restrict__ e_a) {
@@ -339,6 +377,7 @@ struct GemmArgs {
   uint8_t* out;  // t[l][col][row], rows padded to nmb*256, cols to ng*n_g
   int nmod;
   int mods[kMaxMod];
+  int ys[kMaxMod];  // CRT weights (M/m_l)^-1 mod m_l, folded into the epilogue
 };
 
 __device__ __forceinline__ uint64_t sw128_desc(unsigned saddr, unsigned lbo, unsigned sbo) {
@@ -512,7 +551,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_i8_kernel(const GemmArgs
       mbar_wait_parity(tmem_full, acc_phase);
       tc_fence_after();
       const int ml = g.mods[l];
-      const double md = (double)ml, inv = 1.0 / md;
+      const double md = (double)ml, inv = 1.0 / md, yl = (double)g.ys[l];
       for (int t = 0; t < 2; ++t) {
         const int64_t row = mb * 256 + t * 128 + q * 32 + lane;
         uint8_t* orow = g.out + ((size_t)l * cols_pad + (size_t)gi * g.n_g) * rows_pad + row;
@@ -523,7 +562,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_i8_kernel(const GemmArgs
           asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
 #pragma unroll
           for (int e = 0; e < 32; ++e) {
-            const double cv = (double)(int)v[e];
+            const double cv = (double)(int)v[e] * yl;  // exact: |c y| < 2^39
             double r = fma(-floor(cv * inv), md, cv);
             if (r < 0.0) r += md;
             if (r >= md) r -= md;
@@ -563,16 +602,24 @@ __global__ void crt_kernel(const uint8_t* __restrict__ t, int64_t rows_pad, int6
   if (i >= mrows) return;
   const u128 M = ((u128)crt.M_hi << 64) | crt.M_lo;
   const u128 H = ((u128)crt.H_hi << 64) | crt.H_lo;
+  // t'_l = (C_l (M/m_l)^-1) mod m_l (epilogue)  ->  s = sum_l t'_l M/m_l  (< nmod M)
   u128 s = 0;
-  for (int l = 0; l < crt.nmod; ++l) {
-    const int tv = t[((size_t)l * cols_pad + j) * rows_pad + i];
-    const int p = tv * crt.y[l];  // < 2^16, exact in float
-    int qv = (int)floorf((float)p * crt.inv_m[l]);
-    int u = p - qv * crt.m[l];
-    if (u < 0) u += crt.m[l];
-    if (u >= crt.m[l]) u -= crt.m[l];
-    s += (u128)(unsigned)u * (((u128)crt.md_hi[l] << 64) | crt.md_lo[l]);
+  const uint8_t* tp = t + (size_t)j * rows_pad + i;
+  const size_t lstride = (size_t)cols_pad * rows_pad;
+  if (crt.nmod <= 15) {
+    for (int l = 0; l < crt.nmod; ++l)
+      s += (u128)tp[l * lstride] * (((u128)crt.md_hi[l] << 64) | crt.md_lo[l]);
+    // s mod M with s < 15 M: quotient from a double estimate, then fix by one
+    uint64_t q = (uint64_t)floor(u128_to_double(s) / u128_to_double(M));
+    u128 qm = (u128)q * M;
+    if (qm > s) qm -= M;
+    s -= qm;
     if (s >= M) s -= M;
+  } else {
+    for (int l = 0; l < crt.nmod; ++l) {
+      s += (u128)tp[l * lstride] * (((u128)crt.md_hi[l] << 64) | crt.md_lo[l]);
+      if (s >= M) s -= M;
+    }
   }
   double v;
   if (s > H)
@@ -584,8 +631,8 @@ __global__ void crt_kernel(const uint8_t* __restrict__ t, int64_t rows_pad, int6
 
 // ----------------------------------------------------------------- host side
 struct PrepLayout {
-  int64_t nib, njb, ncb, cols_per;
-  size_t off_hdr, off_part, off_tiles, total;
+  int64_t nib, njb, ncb, nrb;
+  size_t off_hdr, off_prow, off_pcol, off_tiles, total;
 };
 static PrepLayout prep_layout(int64_t m, int64_t n, int nmod) {
   PrepLayout p;
@@ -593,11 +640,12 @@ static PrepLayout prep_layout(int64_t m, int64_t n, int nmod) {
   p.nib += p.nib & 1;
   p.njb = ceil_div(n, kTile);
   p.njb += p.njb & 1;
-  p.cols_per = 512;
-  p.ncb = ceil_div(n, p.cols_per);
+  p.ncb = ceil_div(n, kNormCols);
+  p.nrb = ceil_div(m, kNormRows);
   p.off_hdr = 0;
-  p.off_part = 256;
-  p.off_tiles = (p.off_part + (size_t)p.ncb * m * sizeof(double) + 1023) & ~size_t(1023);
+  p.off_prow = 256;
+  p.off_pcol = p.off_prow + (size_t)p.ncb * m * sizeof(double);
+  p.off_tiles = (p.off_pcol + (size_t)p.nrb * n * sizeof(double) + 1023) & ~size_t(1023);
   p.total = p.off_tiles + (size_t)nmod * p.njb * p.nib * kTileBytes;
   return p;
 }
@@ -637,7 +685,9 @@ static void launch_residue_a(const double* a, int64_t lda, int64_t m, int64_t n,
 template <int NMOD>
 static void launch_residue_b(const double* b, int64_t ldb, int64_t k, int64_t ncols, const GemmLayout& g, int pb,
                              int* e_b, int8_t* tiles, cudaStream_t st) {
-  residue_b_kernel<NMOD><<<(unsigned)g.cols_pad, 256, 0, st>>>(b, ldb, k, ncols, g.n_g, g.nkb, pb, e_b, tiles, g.ng);
+  bscale_kernel<<<(unsigned)ceil_div(g.cols_pad, 8), 256, 0, st>>>(b, ldb, k, ncols, g.cols_pad, pb, e_b);
+  residue_b_kernel<NMOD><<<dim3((unsigned)g.cols_pad, (unsigned)ceil_div(g.nkb * 8, 256)), 256, 0, st>>>(
+      b, ldb, k, ncols, g.n_g, g.nkb, e_b, tiles, g.ng);
 }
 
 #define OZ_DISPATCH(NM, FN, ...)      \
@@ -667,15 +717,14 @@ int oz_prep(const double* a, int64_t lda, int64_t m, int64_t n, int nmod, void* 
   uint8_t* base = static_cast<uint8_t*>(prep);
   int* e_a = reinterpret_cast<int*>(base + p.off_hdr);
   unsigned long long* maxbits = reinterpret_cast<unsigned long long*>(base + p.off_hdr + 8);
-  double* part = reinterpret_cast<double*>(base + p.off_part);
+  double* prow = reinterpret_cast<double*>(base + p.off_prow);
+  double* pcol = reinterpret_cast<double*>(base + p.off_pcol);
   int8_t* tiles = reinterpret_cast<int8_t*>(base + p.off_tiles);
+  RLRA_REQUIRE(p.nrb <= 2147483647 && p.ncb <= 65535, "oz_prep: A too large for the norm grid");
   RLRA_CHECK_CUDA(cudaMemsetAsync(maxbits, 0, sizeof(unsigned long long), st));
-  oz::colnorm_kernel<<<(unsigned)ceil_div(n, 8), 256, 0, st>>>(a, lda, m, n, maxbits);
+  oz::norms_partial_kernel<<<dim3((unsigned)p.nrb, (unsigned)p.ncb), 256, 0, st>>>(a, lda, m, n, prow, pcol);
   RLRA_LAUNCHED();
-  oz::rownorm_partial_kernel<<<dim3((unsigned)ceil_div(m, 256), (unsigned)p.ncb), 256, 0, st>>>(a, lda, m, n,
-                                                                                                 p.cols_per, part);
-  RLRA_LAUNCHED();
-  oz::rownorm_final_kernel<<<(unsigned)ceil_div(m, 256), 256, 0, st>>>(part, m, p.ncb, maxbits);
+  oz::norms_final_kernel<<<(unsigned)ceil_div(m + n, 256), 256, 0, st>>>(prow, p.ncb, m, pcol, p.nrb, n, maxbits);
   RLRA_LAUNCHED();
   oz::scale_a_kernel<<<1, 1, 0, st>>>(maxbits, oz::budget(nmod).pa, e_a);
   RLRA_LAUNCHED();
@@ -712,6 +761,7 @@ int oz_gemm(int trans, const void* prep, int64_t m, int64_t n, int nmod, const d
   const oz::Budget bud = oz::budget(nmod);
   OZ_DISPATCH(nmod, oz::launch_residue_b, b, ldb, K, ncols, g, bud.pb, e_b, b_tiles, st);
   RLRA_LAUNCHED();
+  note_launch();  // bscale + residue_b
 
   oz::GemmArgs ga;
   ga.a_tiles = a_tiles;
@@ -725,7 +775,11 @@ int oz_gemm(int trans, const void* prep, int64_t m, int64_t n, int nmod, const d
   ga.nmb = g.nmb;
   ga.out = tout;
   ga.nmod = nmod;
-  for (int l = 0; l < oz::kMaxMod; ++l) ga.mods[l] = oz::kModuli[l];
+  const oz::Crt crt = oz::make_crt(nmod);
+  for (int l = 0; l < oz::kMaxMod; ++l) {
+    ga.mods[l] = oz::kModuli[l];
+    ga.ys[l] = l < nmod ? crt.y[l] : 1;
+  }
   const size_t smem = oz::gemm_smem_bytes(g.n_g);
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
@@ -739,7 +793,6 @@ int oz_gemm(int trans, const void* prep, int64_t m, int64_t n, int nmod, const d
   oz::gemm_i8_kernel<<<grid, oz::kGemmThreads, smem, st>>>(ga);
   RLRA_LAUNCHED();
 
-  const oz::Crt crt = oz::make_crt(nmod);
   oz::crt_kernel<<<dim3((unsigned)ceil_div(mrows, 256), (unsigned)ncols), 256, 0, st>>>(
       tout, g.rows_pad, g.cols_pad, mrows, ncols, e_a, e_b, crt, c, ldc);
   RLRA_LAUNCHED();

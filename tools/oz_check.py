@@ -50,8 +50,9 @@ def main():
     pa, pb = budget(nmod)
     nib = -(-m // T); nib += nib & 1
     njb = -(-n // T); njb += njb & 1
-    ncb = -(-n // 512)
-    off_tiles = (256 + ncb * m * 8 + 1023) & ~1023
+    ncb = -(-n // 256)
+    nrb = -(-m // 2048)
+    off_tiles = (256 + ncb * m * 8 + nrb * n * 8 + 1023) & ~1023
     print(f"e_a={e_a} pa={pa} pb={pb} nib={nib} njb={njb}")
     x = np.rint(a * 2.0 ** e_a).astype(np.int64)
     maxnorm = max(np.sqrt((a * a).sum(0)).max(), np.sqrt((a * a).sum(1)).max())
@@ -105,11 +106,13 @@ def main():
         # integer products mod m from the t array
         xx = (xpad[:m, :n].T if trans else xpad[:m, :n])  # rows x k
         tbad = 0
+        big_m = math.prod(MODS[:nmod])
         for li in range(nmod):
             mod = MODS[li]
+            ycrt = pow((big_m // mod) % mod, -1, mod)
             xm = (xx % mod).astype(np.int64)
             ym = (y % mod).astype(np.int64)
-            ref = (xm @ ym) % mod  # rows x l, exact in int64 (k * 249^2 < 2^63)
+            ref = ((xm @ ym) % mod * ycrt) % mod  # rows x l, exact in int64
             tt = g[off_t + li * cols_pad * rows_pad: off_t + (li + 1) * cols_pad * rows_pad].reshape(cols_pad, rows_pad)
             got = tt[:l, :rows].T.astype(np.int64)
             nb = int((got != ref).sum())
