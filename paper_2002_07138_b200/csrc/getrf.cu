@@ -582,15 +582,20 @@ __global__ void __launch_bounds__(THREADS, 1) lu_panel_cluster_kernel(PanelArgs 
       mbar_wait_parity(&mbar[par], (phase_bits >> par) & 1u);
       if (jj < 12) trace(8 + 8 * jj + 1);
       // decide from the local copies of every peer's record
-      double v = -1.0, dummy = -1.0;
-      int64_t idx = INT64_MAX;
+      // first max over the CTA records: ranks hold ascending row ranges and each
+      // record is its CTA's first max, so the smallest lane among equal maxima wins
+      double rv = -1.0;
+      long long ri = INT64_MAX;
       if (lane < CS) {
-        const double rv = recv[par][lane][0];
-        if (rv >= 0.0) { v = rv; idx = (int64_t)__double_as_longlong(recv[par][lane][1]); }
+        rv = recv[par][lane][0];
+        ri = __double_as_longlong(recv[par][lane][1]);
       }
-      warp_argmax(v, idx, dummy);
-      v = __shfl_sync(0xffffffffu, v, 0);
-      idx = __shfl_sync(0xffffffffu, (long long)idx, 0);
+      double vm = rv;
+#pragma unroll
+      for (int o = 16; o; o >>= 1) vm = fmax(vm, __shfl_xor_sync(0xffffffffu, vm, o));
+      const unsigned win = __reduce_min_sync(0xffffffffu, (rv == vm && rv >= 0.0) ? (unsigned)lane : 32u);
+      const double v = (win < 32u) ? vm : -1.0;
+      const int64_t idx = (int64_t)__shfl_sync(0xffffffffu, ri, (int)(win & 31u));
       // rlra/_lu_cython.pyx:23-39: first max, whole-column colmax, zero pivot
       double colmax = v;
       const double cm_j = __shfl_sync(0xffffffffu, colmax_mine, jj);
@@ -599,7 +604,7 @@ __global__ void __launch_bounds__(THREADS, 1) lu_panel_cluster_kernel(PanelArgs 
       const int64_t prow = zero ? j : idx;
       // pivot row (post-swap row j): the winner's record, or row j itself
       double u = 0.0;
-      if (lane < nb) u = zero ? recv_diag[par][lane] : recv[par][(int)((prow - p.j0) / R)][2 + lane];
+      if (lane < nb) u = zero ? recv_diag[par][lane] : recv[par][win & 31u][2 + lane];
       if (lane < PW) s_u[par][lane] = u;
       if (lane > jj && lane < nb && fabs(u) > colmax_mine) colmax_mine = fabs(u);
       if (lane == 0) {
