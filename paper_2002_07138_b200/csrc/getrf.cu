@@ -16,6 +16,7 @@
 // outside the panel are permuted after the panel by a gather/scatter kernel.
 #include <cooperative_groups.h>
 
+#include <cstdlib>
 #include <mutex>
 #include <set>
 #include <utility>
@@ -953,6 +954,32 @@ static int lu_max_cluster() {
   return best;
 }
 
+// Per-device auxiliary stream for the look-ahead trailing updates (NULL when
+// disabled with RLRA_B200_LU_LOOKAHEAD=0).
+static cudaStream_t lu_aux_stream() {
+  static std::mutex mu;
+  static cudaStream_t streams[64];
+  static bool init[64];
+  static int enabled = -1;
+  if (enabled < 0) {
+    const char* e = getenv("RLRA_B200_LU_LOOKAHEAD");
+    enabled = (e && e[0] == '0') ? 0 : 1;
+  }
+  if (!enabled) return nullptr;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+  std::lock_guard<std::mutex> lock(mu);
+  if (!init[dev & 63]) {
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    if (cudaStreamCreateWithPriority(&streams[dev & 63], cudaStreamNonBlocking, lo) != cudaSuccess)
+      streams[dev & 63] = nullptr;
+    cudaGetLastError();
+    init[dev & 63] = true;
+  }
+  return streams[dev & 63];
+}
+
 static int lu_prepare_kernel(const void* kern) {
   static std::mutex mu;
   static std::set<std::pair<int, const void*>> done;
@@ -1000,6 +1027,48 @@ int getrf(double* a, int64_t lda, int64_t m, int64_t n, int64_t* piv, int64_t* n
                   : pw == 16 ? (const void*)lu_panel_smem_kernel<16, 512> : (const void*)lu_panel_smem_kernel<8, 512>);
   if (lu_prepare_kernel(kern)) return -1;
   unsigned bar_base = 0;
+  // Look-ahead: after block b's panels, only the NEXT block's columns get the
+  // trailing update on `st` (narrow); the rest (wide) runs on an auxiliary
+  // stream while block b+1's panel factorization -- a 16-SM cluster -- runs on
+  // `st`, joined before b+1's first row interchange touches those columns.
+  // Every element still receives its rank-1 terms in ascending step order.
+  cudaStream_t aux = lu_aux_stream();
+  cudaEvent_t ev_narrow = nullptr, ev_wide = nullptr;
+  if (aux) {
+    RLRA_CHECK_CUDA(cudaEventCreateWithFlags(&ev_narrow, cudaEventDisableTiming));
+    RLRA_CHECK_CUDA(cudaEventCreateWithFlags(&ev_wide, cudaEventDisableTiming));
+  }
+  struct Wide {
+    bool pending = false, submitted = false;
+    int64_t jo = 0, c0 = 0, ce = 0;
+    int nbo = 0;
+  } wide;
+  auto trailing = [&](int64_t jo_, int nbo_, int64_t ce_, int64_t c0_, int64_t c1_, cudaStream_t s_) -> int {
+    int blocks = (int)std::min<int64_t>(ceil_div(c1_ - c0_, 4), 4096);
+    lu_trsm_kernel<<<blocks, 128, 0, s_>>>(a, lda, jo_, nbo_, c0_, c1_, w.zflag);
+    RLRA_LAUNCHED();
+    if (ce_ < m) {
+      dim3 grid((unsigned)ceil_div(m - ce_, UPD_TM), (unsigned)ceil_div(c1_ - c0_, UPD_TN));
+      lu_update_kernel<<<grid, 256, 0, s_>>>(a, lda, jo_, nbo_, ce_, m, c0_, c1_, w.zflag);
+      RLRA_LAUNCHED();
+    }
+    return 0;
+  };
+  auto submit_wide = [&]() -> int {
+    if (!wide.pending || wide.submitted) return 0;
+    RLRA_CHECK_CUDA(cudaStreamWaitEvent(aux, ev_narrow, 0));
+    if (trailing(wide.jo, wide.nbo, wide.ce, wide.c0, n, aux)) return -1;
+    RLRA_CHECK_CUDA(cudaEventRecord(ev_wide, aux));
+    wide.submitted = true;
+    return 0;
+  };
+  auto join_wide = [&]() -> int {
+    if (!wide.pending) return 0;
+    if (submit_wide()) return -1;
+    RLRA_CHECK_CUDA(cudaStreamWaitEvent(st, ev_wide, 0));
+    wide.pending = wide.submitted = false;
+    return 0;
+  };
   for (int64_t jo = 0; jo < r; jo += LU_NB) {
     const int nbo = (int)std::min<int64_t>(LU_NB, r - jo);
     const int64_t ce = jo + nbo;
@@ -1041,6 +1110,9 @@ int getrf(double* a, int64_t lda, int64_t m, int64_t n, int64_t* piv, int64_t* n
         bar_base += (unsigned)G * nb;
       }
       note_launch();
+      // the previous block's wide update overlaps this panel; join before the
+      // interchanges reach its columns
+      if (join_wide()) return -1;
       if (n > nb) {
         int64_t ncols = n - nb;
         int blocks = (int)std::min<int64_t>(ceil_div(ncols * 32, 256), 2048);
@@ -1059,16 +1131,22 @@ int getrf(double* a, int64_t lda, int64_t m, int64_t n, int64_t* piv, int64_t* n
       }
     }
     if (ce < n) {  // outer trailing update with the whole 32-column block
-      int blocks = (int)std::min<int64_t>(ceil_div(n - ce, 4), 4096);
-      lu_trsm_kernel<<<blocks, 128, 0, st>>>(a, lda, jo, nbo, ce, n, w.zflag);
-      RLRA_LAUNCHED();
-      if (ce < m) {
-        dim3 grid((unsigned)ceil_div(m - ce, UPD_TM), (unsigned)ceil_div(n - ce, UPD_TN));
-        lu_update_kernel<<<grid, 256, 0, st>>>(a, lda, jo, nbo, ce, m, ce, n, w.zflag);
-        RLRA_LAUNCHED();
+      const int64_t ce2 = aux ? std::min<int64_t>(n, ce + LU_NB) : n;
+      if (trailing(jo, nbo, ce, ce, ce2, st)) return -1;  // narrow: the next block's columns
+      if (ce2 < n) {                                      // wide: deferred past the next panel launch
+        RLRA_CHECK_CUDA(cudaEventRecord(ev_narrow, st));
+        wide.pending = true;
+        wide.submitted = false;
+        wide.jo = jo;
+        wide.nbo = nbo;
+        wide.ce = ce;
+        wide.c0 = ce2;
       }
     }
   }
+  if (join_wide()) return -1;
+  if (ev_narrow) cudaEventDestroy(ev_narrow);
+  if (ev_wide) cudaEventDestroy(ev_wide);
   if (nonzero_diag_dev) {
     count_nonzero_diag_kernel<<<1, 256, 0, st>>>(a, lda, r, nonzero_diag_dev);
     RLRA_LAUNCHED();

@@ -11,6 +11,16 @@ __device__ __forceinline__ unsigned long long clk() {
 }
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 
+__device__ __forceinline__ double ieee_div_by(double x, double d, double rcp) {
+  const double ax = fabs(x), ad = fabs(d);
+  if (ax > 0x1p-960 && ax < 0x1p+960 && ad > 0x1p-960 && ad < 0x1p+960) {
+    const double q0 = __dmul_rn(x, rcp);
+    const double rem = fma(-d, q0, x);
+    return fma(rem, rcp, q0);
+  }
+  return x / d;
+}
+
 __global__ void __cluster_dims__(16, 1, 1) __launch_bounds__(256, 1) probe(unsigned long long* out, double seed) {
   cg::cluster_group cluster = cg::this_cluster();
   __shared__ double buf[64];
@@ -143,6 +153,24 @@ __global__ void __cluster_dims__(16, 1, 1) __launch_bounds__(256, 1) probe(unsig
     }
     if (tid == 0) { out[b * 16 + 11] = tot / 16; out[b * 16 + 12] = tw / 16; }
   }
+  // (13) 3 independent ieee divisions + look-ahead per thread, all 256 threads
+  {
+    double xs[3] = {seed + tid, seed * 2 + tid, seed * 3 + tid}, ys[3] = {1.0 + tid, 2.0, 3.0};
+    const double d = 1.2345 + b, rcp = __drcp_rn(d);
+    __syncthreads();
+    unsigned long long ta = clk();
+    for (int rep = 0; rep < 16; rep++) {
+#pragma unroll
+      for (int k = 0; k < 3; k++) {
+        const double l = ieee_div_by(xs[k], d, rcp);
+        xs[k] = l;
+        ys[k] = __dsub_rn(ys[k], __dmul_rn(l, 0.5));
+      }
+    }
+    unsigned long long tb = clk();
+    if (tid == 0) out[b * 16 + 13] = (tb - ta) / 16;
+    acc += xs[0] + xs[1] + xs[2] + ys[0] + ys[1] + ys[2];
+  }
   if (acc == 12345.678) out[4000] = 1;
   cluster.sync();
 }
@@ -159,6 +187,7 @@ int main() {
   const char* names[] = {"cluster barrier release/acquire", "cluster barrier relaxed", "DSMEM ld dependent",
                          "DFMA dependent", "__drcp_rn dependent", "fmax shfl64 round", "__syncthreads",
                          "LDS dependent", "STG+fence.proxy.async.global", "redux.min", "DMUL+DSUB dependent"};
+  printf("3x ieee_div + lookahead per thread (256 thr): %llu cycles\n", h[13]);
   printf("decision seq (warp0, 2 DSMEM rounds) %llu / %llu cycles; barrier wait %llu\n", h[11], h[15*16+11], h[12]);
   for (int i = 0; i < 11; i++) printf("%-36s %llu cycles (CTA0) %llu (CTA15)\n", names[i], h[i], h[15 * 16 + i]);
   printf("err: %s\n", cudaGetErrorString(cudaGetLastError()));
