@@ -23,6 +23,8 @@
  *   rlra_b200_oz_prep/_gemm    the same two pass products     accessors.py:27-31
  *                              emulated on int8 tensor cores (Ozaki-II)
  *   rlra_b200_geqrf/_orgqr     kernels.eqr (np.linalg.qr)     kernels.py:57-61, :73
+ *   rlra_b200_chol_inv         CholeskyQR2 basis (same range as  kernels.py:57-61
+ *                              the Householder Q of eqr)
  *   rlra_b200_trsm_rt          solve_triangular(trans='T')    kernels.py:95
  *   rlra_b200_diag_absmin      pinv_factor rank test          kernels.py:75-79
  *   rlra_b200_sumsq            DenseAccessor.fro_norm()**2    accessors.py:33-34, fixedprec.py:72
@@ -112,6 +114,15 @@ RLRA_B200_API int rlra_b200_geqrf(double* a, int64_t lda, int64_t m, int64_t n, 
 /* must receive geqrf's workspace, untouched since the geqrf call */
 RLRA_B200_API int rlra_b200_orgqr(const double* a, int64_t lda, int64_t m, int64_t n, double* q, int64_t ldq,
                     void* ws, size_t ws_bytes, void* stream);
+
+/* ---- K4 fast path: R^{-1} of R = chol(G), G symmetric positive definite l x l
+ * (upper triangle read; g is used as workspace and overwritten).  rinv (l x l) receives R^{-1} (upper, zeros below).
+ * *flag (device int) is set to 1 when G is not numerically SPD or when
+ * max_i R_ii > cond_limit * min_i R_ii (rinv is then zero); it is never
+ * cleared.  l <= rlra_b200_chol_inv_max_l() (one CTA, shared memory). */
+RLRA_B200_API int rlra_b200_chol_inv_max_l(void);
+RLRA_B200_API int rlra_b200_chol_inv(double* g, int64_t ldg, int64_t l, double* rinv, int64_t ldr, int* flag,
+                                     double cond_limit, void* stream);
 
 /* ---- K6: X = R^{-T} B in place over B (R upper l x l) ------------------- */
 RLRA_B200_API size_t rlra_b200_trsm_workspace(int64_t l, int64_t ncols);

@@ -68,6 +68,9 @@ int sumsq(const double* a, int64_t lda, int64_t m, int64_t n, double* out_dev, v
 int colsumsq(const double* a, int64_t lda, int64_t m, int64_t n, double* out_dev, cudaStream_t st);
 int transpose(const double* in, int64_t ldi, int64_t m, int64_t n, double* out, int64_t ldo,
               cudaStream_t st);
+int chol_inv_max_l();
+int chol_inv(double* g, int64_t ldg, int64_t l, double* x, int64_t ldx, int* flag, double cond_limit,
+             cudaStream_t st);
 size_t oz_prep_workspace(int64_t m, int64_t n, int nmod);
 int oz_prep(const double* a, int64_t lda, int64_t m, int64_t n, int nmod, void* prep, size_t prep_bytes,
             cudaStream_t st);
@@ -166,6 +169,13 @@ int rlra_b200_lu_extract(const double* lu, int64_t ldlu, int64_t m, int64_t n, d
   if (l && extract_l(lu, ldlu, m, r, l, ldl, S(stream))) return -1;
   if (u && extract_u(lu, ldlu, r, n, u, ldu, S(stream))) return -1;
   return 0;
+}
+
+int rlra_b200_chol_inv_max_l(void) { return chol_inv_max_l(); }
+
+int rlra_b200_chol_inv(double* g, int64_t ldg, int64_t l, double* rinv, int64_t ldr, int* flag,
+                       double cond_limit, void* stream) {
+  return chol_inv(g, ldg, l, rinv, ldr, flag, cond_limit, static_cast<cudaStream_t>(stream));
 }
 
 size_t rlra_b200_oz_prep_workspace(int64_t m, int64_t n, int nmod) { return oz_prep_workspace(m, n, nmod); }

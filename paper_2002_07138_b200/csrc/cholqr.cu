@@ -1,0 +1,258 @@
+// K4 fast path: the final basis of powerlu by CholeskyQR2 instead of Householder.
+// The Householder panels of K4 are latency bound (one cluster exchange per
+// column); CholeskyQR2 turns the whole QR of the n x l sketch Z into four
+// tall GEMMs on the FP64 tensor pipe plus two l x l factorizations:
+//   G1 = Z^T Z,  R1 = chol(G1),  Q1 = Z R1^{-1}
+//   G2 = Q1^T Q1, R2 = chol(G2), Q = Q1 R2^{-1}
+// (Fukaya et al.; orthogonal to working precision for cond(Z) < ~u^{-1/2}).
+// Q spans range(Z) like LAPACK's Householder Q (rlra/kernels.py:57-61); the
+// columns may differ in sign, which leaves every powerlu output (p, q, L, U)
+// unchanged -- flipping column j of V_k flips column j of G = A V_k and of
+// U1, and B = V_k U1^T is sign-invariant.  Structural rank collapse (an exactly
+// dependent sketch column, rlra/rangefinder.py:55-64) and ill-conditioned
+// sketches make the Cholesky fail or exceed the condition bound; the kernel
+// then raises a device flag and the driver redoes the call on the Householder
+// path, so exceptions and results keep the reference semantics.
+//
+// chol_kernel: one CTA, the l x l matrix packed (upper triangle) in shared
+// memory, blocked right-looking Cholesky G = R^T R; R (packed) replaces G.
+// inv_upper_kernel: X = R^{-1}, one warp per column, ceil(l/16) CTAs.
+#include "common.cuh"
+
+namespace rlra {
+
+constexpr int CHOL_THREADS = 512;
+
+__host__ __device__ __forceinline__ int pk(int i, int j) { return j * (j + 1) / 2 + i; }  // i <= j
+
+// Blocked (32) right-looking Cholesky in shared memory, one CTA:
+//   diagonal block by warp 0 in registers (shuffles), the block row by a
+//   forward substitution per column (one thread each), the trailing triangle
+//   by a rank-32 update in 4 x 4 register tiles -- 3 barriers per 32 columns.
+// Then X = R^{-1} column by column (one warp each, back substitution, R read
+// only), written straight to global memory.
+constexpr int CHOL_NB = 16;
+constexpr int CHOL_MAXL = 256;
+
+__global__ void __launch_bounds__(CHOL_THREADS, 1)
+    chol_kernel(double* __restrict__ g, int64_t ldg, int l, int* __restrict__ flag, double cond_limit) {
+  extern __shared__ double P[];
+  double* dinv = P + (size_t)l * (l + 1) / 2;  // 1 / R_ii
+  __shared__ double Xkk[CHOL_NB][CHOL_NB + 1];  // inverse of the current diagonal block (row-major)
+  __shared__ int s_bad;
+  __shared__ double s_rmin, s_rmax;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int NW = CHOL_THREADS / 32;
+  for (int j = warp; j < l; j += NW)
+    for (int i = lane; i <= j; i += 32) P[pk(i, j)] = g[i + (int64_t)j * ldg];
+  if (tid == 0) {
+    s_bad = 0;
+    s_rmin = INFINITY;
+    s_rmax = 0.0;
+  }
+  __syncthreads();
+  for (int k0 = 0; k0 < l; k0 += CHOL_NB) {
+    const int b = min(CHOL_NB, l - k0);
+    // ---- (1) diagonal block: lane c holds column k0 + c
+    if (warp == 0) {
+      double gg[CHOL_NB];
+#pragma unroll
+      for (int i = 0; i < CHOL_NB; i++) gg[i] = (lane < b && i <= lane) ? P[pk(k0 + i, k0 + lane)] : 0.0;
+      bool bad = false;
+      double rmin = INFINITY, rmax = 0.0;
+#pragma unroll
+      for (int s2 = 0; s2 < CHOL_NB; s2++) {
+        if (s2 < b) {
+          const double d = __shfl_sync(0xffffffffu, gg[s2], s2);
+          if (!(d > 0.0 && d < INFINITY)) bad = true;
+          const double ir = rsqrt(d), r = d * ir;
+          rmin = fmin(rmin, r);
+          rmax = fmax(rmax, r);
+          if (lane == s2) gg[s2] = r;
+          else if (lane > s2) gg[s2] *= ir;
+#pragma unroll
+          for (int i = s2 + 1; i < CHOL_NB; i++) {
+            const double rsi = __shfl_sync(0xffffffffu, gg[s2], i);
+            if (lane >= i && i < b) gg[i] = fma(-rsi, gg[s2], gg[i]);
+          }
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < CHOL_NB; i++)
+        if (lane < b && i <= lane) P[pk(k0 + i, k0 + lane)] = gg[i];
+      double dl = 1.0;
+#pragma unroll
+      for (int i = 0; i < CHOL_NB; i++)
+        if (i == lane) dl = gg[i];
+      const double dil = 1.0 / dl;  // lane i: 1 / R_ii, all lanes at once
+      if (lane < b) dinv[k0 + lane] = dil;
+      // inverse of the diagonal block: lane c back-substitutes its own column
+      // (R_kk staged row-major in Xkk first; rows / columns >= b are identity)
+#pragma unroll
+      for (int i = 0; i < CHOL_NB; i++)
+        if (lane < CHOL_NB) Xkk[i][lane] = (i <= lane && lane < b) ? gg[i] : (i == lane ? 1.0 : 0.0);
+      __syncwarp();
+      double xc[CHOL_NB];
+#pragma unroll
+      for (int i = CHOL_NB - 1; i >= 0; i--) {
+        double acc = (i == lane) ? 1.0 : 0.0;
+#pragma unroll
+        for (int t = i + 1; t < CHOL_NB; t++) acc = fma(-Xkk[i][t], (t <= lane && lane < CHOL_NB) ? xc[t] : 0.0, acc);
+        const double di = __shfl_sync(0xffffffffu, dil, i);  // every lane participates
+        xc[i] = (i <= lane) ? acc * di : 0.0;
+      }
+      __syncwarp();
+#pragma unroll
+      for (int i = 0; i < CHOL_NB; i++)
+        if (lane < CHOL_NB) Xkk[i][lane] = xc[i];
+      if (lane == 0) {
+        if (bad) s_bad = 1;
+        s_rmin = fmin(s_rmin, rmin);
+        s_rmax = fmax(s_rmax, rmax);
+      }
+    }
+    __syncthreads();
+    if (s_bad) break;
+    const int c0 = k0 + b, m = l - c0;
+    if (m <= 0) break;
+    // ---- (2) block row: R(k0.., j) = R_kk^{-T} G(k0.., j) = Xkk^T g, one warp
+    // per column: lane u accumulates sum_{s <= u} Xkk[s][u] g_s (no recurrence)
+    for (int jj = warp; jj < m; jj += NW) {
+      const int j = c0 + jj, cj = j * (j + 1) / 2;
+      const double gl = (lane < b) ? P[cj + k0 + lane] : 0.0;
+      double acc = 0.0;
+#pragma unroll
+      for (int s2 = 0; s2 < CHOL_NB; s2++) {
+        const double gs = __shfl_sync(0xffffffffu, gl, s2);
+        if (s2 <= lane && lane < CHOL_NB) acc = fma(Xkk[s2][lane], gs, acc);
+      }
+      __syncwarp();
+      if (lane < b) P[cj + k0 + lane] = acc;
+    }
+    __syncthreads();
+    // ---- (3) trailing triangle -= R(k0.., :)^T R(k0.., :) in 4 x 4 tiles
+    const int mt = (m + 3) >> 2;
+    const int ntiles = mt * (mt + 1) / 2;
+    for (int t = tid; t < ntiles; t += CHOL_THREADS) {
+      int tb = (int)((sqrtf(8.0f * (float)t + 1.0f) - 1.0f) * 0.5f);
+      while (tb * (tb + 1) / 2 > t) --tb;
+      while ((tb + 1) * (tb + 2) / 2 <= t) ++tb;
+      const int ta = t - tb * (tb + 1) / 2;
+      const int ja = c0 + 4 * ta, jb = c0 + 4 * tb;
+      double acc[4][4];
+#pragma unroll
+      for (int q = 0; q < 4; q++)
+#pragma unroll
+        for (int w = 0; w < 4; w++) acc[q][w] = 0.0;
+      for (int s2 = 0; s2 < b; s2++) {
+        double ra[4], rb[4];
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+          ra[q] = (ja + q < l) ? P[pk(k0 + s2, ja + q)] : 0.0;
+          rb[q] = (jb + q < l) ? P[pk(k0 + s2, jb + q)] : 0.0;
+        }
+#pragma unroll
+        for (int q = 0; q < 4; q++)
+#pragma unroll
+          for (int w = 0; w < 4; w++) acc[q][w] = fma(ra[q], rb[w], acc[q][w]);
+      }
+#pragma unroll
+      for (int q = 0; q < 4; q++)
+#pragma unroll
+        for (int w = 0; w < 4; w++) {
+          const int i = ja + q, j = jb + w;
+          if (i <= j && j < l) P[pk(i, j)] -= acc[q][w];
+        }
+    }
+    __syncthreads();
+  }
+  __syncthreads();
+  if (tid == 0 && !s_bad && !(s_rmax <= cond_limit * s_rmin)) s_bad = 1;
+  __syncthreads();
+  if (s_bad) {
+    if (tid == 0) atomicExch(flag, 1);
+    return;
+  }
+  // R (packed upper) over the consumed G: rows of the inverse kernel's input
+  const int np = l * (l + 1) / 2;
+  for (int e = tid; e < np; e += CHOL_THREADS) g[e] = P[e];
+}
+
+// X = R^{-1}: warp per column, back substitution (x_t = acc_t / R_tt, then
+// acc_i -= R_it x_t for i < t), R packed in shared memory; ceil(l/16) CTAs.
+constexpr int INV_COLS = 16;
+
+__global__ void __launch_bounds__(INV_COLS * 32, 1)
+    inv_upper_kernel(const double* __restrict__ rp, int l, double* __restrict__ x, int64_t ldx,
+                     const int* __restrict__ flag) {
+  extern __shared__ double P[];
+  double* dinv = P + (size_t)l * (l + 1) / 2;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int j = blockIdx.x * INV_COLS + warp;
+  if (*flag) {  // the Cholesky declined: zero output (the caller falls back)
+    if (j < l)
+      for (int i = lane; i < l; i += 32) x[i + (int64_t)j * ldx] = 0.0;
+    return;
+  }
+  const int np = l * (l + 1) / 2;
+  for (int e = tid; e < np; e += blockDim.x) P[e] = rp[e];
+  __syncthreads();
+  for (int t = tid; t < l; t += blockDim.x) dinv[t] = 1.0 / P[pk(t, t)];
+  __syncthreads();
+  if (j >= l) return;
+  double a[CHOL_MAXL / 32];
+#pragma unroll
+  for (int q = 0; q < CHOL_MAXL / 32; q++) a[q] = (lane + 32 * q == j) ? 1.0 : 0.0;
+#pragma unroll
+  for (int q = CHOL_MAXL / 32 - 1; q >= 0; q--) {
+    if (32 * q > j) continue;
+    const int thi = min(j, 32 * q + 31);
+    for (int t = thi; t >= 32 * q; --t) {
+      const double xt = __shfl_sync(0xffffffffu, a[q], t & 31) * dinv[t];
+      if (lane == (t & 31)) a[q] = xt;
+      const int ct = t * (t + 1) / 2;
+#pragma unroll
+      for (int q2 = 0; q2 <= q; q2++) {
+        const int i = lane + 32 * q2;
+        if (i < t) a[q2] = fma(-P[ct + i], xt, a[q2]);
+      }
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < CHOL_MAXL / 32; q++) {
+    const int i = lane + 32 * q;
+    if (i < l) x[i + (int64_t)j * ldx] = (i <= j) ? a[q] : 0.0;
+  }
+}
+
+int chol_inv_max_l() {
+  const int smem = device_info().max_smem_optin > 0 ? device_info().max_smem_optin : 227 * 1024;
+  int l = 1;
+  while (l + 1 <= CHOL_MAXL && (size_t)(l + 1) * (l + 2) / 2 * 8 + (size_t)(l + 1) * 8 + 10 * 1024 <= (size_t)smem) ++l;
+  return l;
+}
+
+int chol_inv(double* g, int64_t ldg, int64_t l, double* x, int64_t ldx, int* flag, double cond_limit,
+             cudaStream_t st) {
+  RLRA_REQUIRE(l >= 1 && l <= chol_inv_max_l(), "chol_inv: l = %lld outside [1, %d]", (long long)l,
+               chol_inv_max_l());
+  RLRA_REQUIRE(ldg >= l && ldx >= l, "chol_inv: bad leading dimension");
+  const size_t smem = (size_t)l * (l + 1) / 2 * 8 + (size_t)l * 8;
+  static int configured = -1;
+  int dev = 0;
+  RLRA_CHECK_CUDA(cudaGetDevice(&dev));
+  if (configured != dev) {
+    RLRA_CHECK_CUDA(cudaFuncSetAttribute(chol_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         device_info().max_smem_optin - 9 * 1024));
+    RLRA_CHECK_CUDA(cudaFuncSetAttribute(inv_upper_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         device_info().max_smem_optin - 9 * 1024));
+    configured = dev;
+  }
+  chol_kernel<<<1, CHOL_THREADS, smem, st>>>(g, ldg, (int)l, flag, cond_limit);
+  RLRA_LAUNCHED();
+  inv_upper_kernel<<<(unsigned)ceil_div(l, INV_COLS), INV_COLS * 32, smem, st>>>(g, (int)l, x, ldx, flag);
+  RLRA_LAUNCHED();
+  return 0;
+}
+
+}  // namespace rlra

@@ -9,6 +9,7 @@ return types).
 
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass
 from typing import Any
 
@@ -83,6 +84,10 @@ def lu_from_projection(g, vk):
     return f.to_numpy() if host else f
 
 
+# Final basis of powerlu: "chol" (CholeskyQR2 + Householder fallback) or "householder".
+POWERLU_QR = os.environ.get("RLRA_B200_POWERLU_QR", "chol")
+
+
 def powerlu(a, k, q_os=10, v=3, seed=0):
     """Pass-parameterised randomized LU (rlra/fixedrank.py:120-133)."""
     host = _host_input(a)
@@ -92,7 +97,7 @@ def powerlu(a, k, q_os=10, v=3, seed=0):
         raise ValueError("pass budget v must be >= 2")
     checks = RankChecks()
     with product_session(a):
-        basis = general_power_basis_v(a, k + q_os, v, seed, _checks=checks)
+        basis = general_power_basis_v(a, k + q_os, v, seed, _checks=checks, _qr=POWERLU_QR)
         vk = basis.V[:, :k]
         g = a.matmul(vk)
     f = lu_from_projection_(g, vk)

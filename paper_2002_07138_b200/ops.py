@@ -250,6 +250,39 @@ def count_nonzero_diag(a, r=None):
     return cnt
 
 
+CHOLQR_COND = 2e6  # first-pass bound on max R_ii / min R_ii (CholeskyQR2 needs cond < ~u^-1/2)
+
+
+def cholqr_max_l():
+    return _native.query("rlra_b200_chol_inv_max_l")
+
+
+def chol_inv(g, out, flag, cond_limit):
+    """out = chol(g)^{-1} (upper); flag[0] = 1 when g is not numerically SPD."""
+    l = g.shape[0]
+    _call("rlra_b200_chol_inv", g.device, ptr(g), ld_of(g), l, ptr(out), ld_of(out), ptr(flag), float(cond_limit),
+          _stream(g.device))
+    return out
+
+
+def cholqr2(z):
+    """Orthonormal basis of range(z) by CholeskyQR2 (csrc/cholqr.cu) and a device
+    int32 flag that is 1 when the Cholesky declined (rank collapse or cond(z)
+    beyond the bound); z is left intact for the Householder fallback."""
+    n, l = z.shape
+    dev = z.device
+    flag = torch.zeros(1, dtype=torch.int32, device=dev)
+    rinv = fmat(l, l, dev)
+    with label("cholqr2"):
+        g = matmul(z, z, ta=True)
+        chol_inv(g, rinv, flag, CHOLQR_COND)
+        q1 = matmul(z, rinv)
+        g2 = matmul(q1, q1, ta=True)
+        chol_inv(g2, rinv, flag, 2.0)
+        q = matmul(q1, rinv)
+    return q, flag
+
+
 class QR:
     """geqrf in place + workspace kept for orgqr (rlra/kernels.py:57-61)."""
 

@@ -4,7 +4,8 @@
 Same control flow, Omega shapes and pass accounting as the reference: even v
 draws Omega m x l and starts with A^T Omega, odd v draws Omega n x l; interior
 renormalisations are the row-unpermuted L of a partial-pivot LU (bit-exact
-GEPP, K3); the last step is a Householder QR (K4).  The exact-zero-diagonal
+GEPP, K3); the last step is a Householder QR (K4) -- or, for powerlu's
+internal basis, CholeskyQR2 with the Householder QR as fallback.  The exact-zero-diagonal
 RankCollapse checks (rlra/rangefinder.py:55-64) are evaluated on device and
 raised when the basis is handed back, with the reference's attributes.
 """
@@ -53,8 +54,17 @@ def _validate(a, l, lower=1):
         raise ValueError(f"sketch width l={l} outside {lower}..min{(m, n)}")
 
 
-def qr_basis_(x, checks):
-    """rlra/rangefinder.py:67-70 (destroys x)."""
+def qr_basis_(x, checks, method="householder"):
+    """rlra/rangefinder.py:67-70 (destroys x).
+
+    method="chol" (powerlu's internal basis): CholeskyQR2 -- same range as the
+    Householder Q, columns possibly of opposite sign, which no powerlu output
+    depends on -- with the Householder path as the fallback whenever the
+    Cholesky declines (rank collapse keeps the reference's exception)."""
+    if method == "chol" and x.shape[0] >= x.shape[1] and 0 < x.shape[1] <= ops.cholqr_max_l():
+        q, flag = ops.cholqr2(x)
+        if not int(flag.item()):
+            return q
     qr = ops.QR(x)
     checks.add(ops.count_nonzero_diag(qr.r_view()), x.shape[1])
     return qr.q()
@@ -67,7 +77,7 @@ def lu_basis_(x, checks):
     return ops.lu_basis(x, piv)
 
 
-def general_power_basis_v(a, l, v, seed, *, _checks=None):
+def general_power_basis_v(a, l, v, seed, *, _checks=None, _qr="householder"):
     """rlra/rangefinder.py:144-176; consumes exactly v - 1 passes."""
     a = as_accessor(a)
     _validate(a, l)
@@ -83,7 +93,7 @@ def general_power_basis_v(a, l, v, seed, *, _checks=None):
         x = a.rmatmul(om)
         passes += 1
         if v == 2:
-            basis = qr_basis_(x, checks)
+            basis = qr_basis_(x, checks, _qr)
             if _checks is None:
                 checks.raise_if_collapsed()
             return RangeBasis(basis, passes)
@@ -95,7 +105,7 @@ def general_power_basis_v(a, l, v, seed, *, _checks=None):
         w = lu_basis_(a.matmul(w), checks)
         passes += 1
         if i == half:
-            basis = qr_basis_(a.rmatmul(w), checks)
+            basis = qr_basis_(a.rmatmul(w), checks, _qr)
         else:
             w = lu_basis_(a.rmatmul(w), checks)
         passes += 1

@@ -51,3 +51,50 @@ def test_qr_ill_conditioned_orthogonality(cuda_dev):
     q, r, _ = dev_qr(x)
     assert np.abs(q.T @ q - np.eye(300)).max() < 1e-13
     assert np.allclose(q @ r, x, atol=1e-13 * np.linalg.norm(x))
+
+
+# ---- K4 fast path: CholeskyQR2 (csrc/cholqr.cu), used for powerlu's internal basis
+@pytest.mark.parametrize("n,l", [(10000, 220), (3000, 64), (500, 200), (64, 1), (2000, 230)])
+def test_cholqr2_spans_the_householder_range(cuda_dev, n, l):
+    from paper_2002_07138_b200 import ops
+
+    rng = np.random.default_rng(l)
+    # graded columns (cond ~ 1e4), like powerlu's final sketch
+    x = rng.standard_normal((n, l)) * np.logspace(0, -4, l)[None, :]
+    q, flag = ops.cholqr2(ops.from_numpy(x, cuda_dev))
+    assert int(flag.item()) == 0
+    q = ops.to_numpy(q)
+    assert np.abs(q.T @ q - np.eye(l)).max() < 1e-13
+    q_ref, _ = np.linalg.qr(x)
+    d = np.sign(np.sum(q * q_ref, axis=0))  # column signs may differ from LAPACK's
+    assert np.all(np.abs(d) == 1)
+    assert np.abs(q - q_ref * d[None, :]).max() < 1e-10
+
+
+def test_cholqr2_flags_rank_collapse_and_ill_conditioning(cuda_dev):
+    from paper_2002_07138_b200 import ops
+
+    rng = np.random.default_rng(3)
+    x = rng.standard_normal((400, 30))
+    x[:, 7] = x[:, 3]  # exactly dependent column
+    _, flag = ops.cholqr2(ops.from_numpy(x, cuda_dev))
+    assert int(flag.item()) == 1
+    y = rng.standard_normal((400, 30)) * np.logspace(0, -12, 30)[None, :]
+    _, flag = ops.cholqr2(ops.from_numpy(y, cuda_dev))
+    assert int(flag.item()) == 1
+
+
+def test_chol_inv_matches_numpy(cuda_dev):
+    import torch
+
+    from paper_2002_07138_b200 import ops
+
+    rng = np.random.default_rng(9)
+    z = rng.standard_normal((600, 150))
+    g = z.T @ z
+    out = ops.fmat(150, 150, cuda_dev)
+    flag = torch.zeros(1, dtype=torch.int32, device=cuda_dev)
+    ops.chol_inv(ops.from_numpy(g, cuda_dev), out, flag, 1e8)
+    r = np.linalg.cholesky(g).T
+    np.testing.assert_allclose(ops.to_numpy(out), np.linalg.inv(r), rtol=0, atol=1e-12 * np.abs(np.linalg.inv(r)).max())
+    assert int(flag.item()) == 0
