@@ -59,6 +59,8 @@ __host__ __device__ constexpr int pow2mod(int e, int m) {
 
 typedef unsigned __int128 u128;
 
+constexpr int kCrtLimbs = 7;  // 7 x 20 bits >= 125 bits (M for 16 moduli)
+
 struct Crt {
   uint64_t M_lo, M_hi;        // M = prod m_l
   uint64_t H_lo, H_hi;        // floor(M / 2)
@@ -67,6 +69,8 @@ struct Crt {
   int y[kMaxMod];             // (M / m_l)^{-1} mod m_l
   int m[kMaxMod];
   float inv_m[kMaxMod];
+  uint32_t limb[kCrtLimbs][kMaxMod];  // 20-bit limbs of M / m_l
+  double inv_M;                     // ~1 / M
   int nmod;
 };
 
@@ -110,7 +114,9 @@ static Crt make_crt(int nmod) {
     c.y[l] = inv;
     c.m[l] = m;
     c.inv_m[l] = 1.0f / (float)m;
+    for (int q = 0; q < kCrtLimbs; ++q) c.limb[q][l] = (uint32_t)((md >> (20 * q)) & 0xFFFFF);
   }
+  c.inv_M = 1.0 / (double)M;
   c.nmod = nmod;
   return c;
 }
@@ -238,25 +244,39 @@ __global__ void __launch_bounds__(256, 2) residue_a_kernel(const double* __restr
   }
 }
 
-// Per-column scale of the skinny operand B (K x ncols): warp per (padded) column.
-__global__ void bscale_kernel(const double* __restrict__ b, int64_t ldb, int64_t k, int64_t ncols, int64_t cols_pad,
-                              int pb, int* __restrict__ e_b) {
-  const int64_t jj = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
-  if (jj >= cols_pad) return;
-  double ss = 0.0;
-  if (jj < ncols)
-    for (int64_t i = lane; i < k; i += 32) {
-      const double v = b[i + jj * ldb];
-      ss = fma(v, v, ss);
+// Per-column scale of the skinny operand B (K x ncols): one CTA per (padded) column.
+__global__ void __launch_bounds__(256) bscale_kernel(const double* __restrict__ b, int64_t ldb, int64_t k,
+                                                     int64_t ncols, int64_t cols_pad, int pb, int* __restrict__ e_b) {
+  const int64_t jj = blockIdx.x;
+  __shared__ double red[8];
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+  if (jj < ncols) {
+    const double* col = b + jj * ldb;
+    int64_t i = threadIdx.x;
+    for (; i + 768 < k; i += 1024) {
+      const double v0 = __ldg(col + i), v1 = __ldg(col + i + 256), v2 = __ldg(col + i + 512), v3 = __ldg(col + i + 768);
+      s0 = fma(v0, v0, s0);
+      s1 = fma(v1, v1, s1);
+      s2 = fma(v2, v2, s2);
+      s3 = fma(v3, v3, s3);
     }
+    for (; i < k; i += 256) {
+      const double v0 = __ldg(col + i);
+      s0 = fma(v0, v0, s0);
+    }
+  }
+  double ss = (s0 + s1) + (s2 + s3);
 #pragma unroll
   for (int o = 16; o; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
-  if (lane == 0) {
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double tot = 0.0;
+    for (int w = 0; w < 8; ++w) tot += red[w];
     int e = 0;
-    if (ss > 0.0) {
+    if (tot > 0.0) {
       int ex;
-      frexp(sqrt(ss) * (1.0 + 0x1p-40), &ex);  // ||b_j|| < 2^ex
+      frexp(sqrt(tot) * (1.0 + 0x1p-40), &ex);  // ||b_j|| < 2^ex
       e = pb - ex;
     }
     e_b[jj] = e;
@@ -293,38 +313,57 @@ __global__ void __launch_bounds__(256) residue_b_kernel(const double* __restrict
 // ----------------------------------------------------------------- A scale
 // Row and column 2-norms of A in ONE read: CTA = 2048 rows x 256 columns;
 // partial sums in fixed order (deterministic), then max -> eA.
-constexpr int kNormRows = 2048, kNormCols = 256;
+constexpr int kNormRows = 2048, kNormCols = 256, kNormBlk = 16;
+constexpr size_t kNormSmem = (8 * kNormCols + 8 * 32 * (kNormBlk + 1)) * sizeof(double);
 
 __global__ void __launch_bounds__(256) norms_partial_kernel(const double* __restrict__ a, int64_t lda, int64_t m,
                                                             int64_t n, double* __restrict__ part_row,
                                                             double* __restrict__ part_col) {
+  // warp w owns rows r0 + 256 w + [0, 256) (8 chunks of 32, lane = row in
+  // chunk); column blocks of 32: lane keeps its rows' partial sums per column,
+  // then one shared-memory transpose per block sums them over the lanes
   const int64_t rb = blockIdx.x, cb = blockIdx.y;
   const int64_t r0 = rb * kNormRows, c0 = cb * kNormCols;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  __shared__ double colw[8][kNormCols];
+  extern __shared__ double nsm[];
+  double (*colw)[kNormCols] = reinterpret_cast<double (*)[kNormCols]>(nsm);
+  double (*tile)[32][kNormBlk + 1] = reinterpret_cast<double (*)[32][kNormBlk + 1]>(nsm + 8 * kNormCols);
   double rs[8];
 #pragma unroll
   for (int s = 0; s < 8; ++s) rs[s] = 0.0;
   const int ncols = (int)(n - c0 < kNormCols ? n - c0 : kNormCols);
+  const int64_t rw = r0 + 256 * warp + lane;
   const bool full = r0 + kNormRows <= m;
-#pragma unroll 2
-  for (int jj = 0; jj < ncols; ++jj) {
-    const double* col = a + (c0 + jj) * lda + r0 + threadIdx.x;
-    double cs = 0.0;
+  for (int cb32 = 0; cb32 < ncols; cb32 += kNormBlk) {
+    double cs[kNormBlk];
+#pragma unroll
+    for (int c = 0; c < kNormBlk; ++c) cs[c] = 0.0;
 #pragma unroll
     for (int s = 0; s < 8; ++s) {
-      const double v = (full || r0 + threadIdx.x + 256 * s < m) ? __ldcs(col + 256 * s) : 0.0;
-      rs[s] = fma(v, v, rs[s]);
-      cs = fma(v, v, cs);
+      const int64_t i = rw + 32 * s;
+      const bool rok = full || i < m;
+#pragma unroll
+      for (int c = 0; c < kNormBlk; ++c) {
+        const double v = (rok && cb32 + c < ncols) ? __ldcs(a + i + (c0 + cb32 + c) * lda) : 0.0;
+        rs[s] = fma(v, v, rs[s]);
+        cs[c] = fma(v, v, cs[c]);
+      }
     }
 #pragma unroll
-    for (int o = 16; o; o >>= 1) cs += __shfl_xor_sync(0xffffffffu, cs, o);
-    if (lane == 0) colw[warp][jj] = cs;
+    for (int c = 0; c < kNormBlk; ++c) tile[warp][lane][c] = cs[c];
+    __syncwarp();
+    if (lane < kNormBlk) {
+      double t = 0.0;
+#pragma unroll
+      for (int q = 0; q < 32; ++q) t += tile[warp][q][lane];
+      if (cb32 + lane < ncols) colw[warp][cb32 + lane] = t;
+    }
+    __syncwarp();
   }
   __syncthreads();
 #pragma unroll
   for (int s = 0; s < 8; ++s) {
-    const int64_t i = r0 + threadIdx.x + 256 * s;
+    const int64_t i = rw + 32 * s;
     if (i < m) part_row[cb * m + i] = rs[s];
   }
   if (threadIdx.x < ncols) {
@@ -594,39 +633,49 @@ __device__ __forceinline__ double u128_to_double(u128 x) {
   return scalbn(__ull2double_rn(top), 64 - lz);
 }
 
-__global__ void crt_kernel(const uint8_t* __restrict__ t, int64_t rows_pad, int64_t cols_pad, int64_t mrows,
-                           int64_t ncols, const int* __restrict__ e_a, const int* __restrict__ e_b, const Crt crt,
-                           double* __restrict__ c, int64_t ldc) {
+// CRT: s = sum_l t'_l (M / m_l) (t'_l < m_l, so every term is < M and the sum
+// of nmod <= 15 terms stays below 2^122), in two 64-bit words; then one
+// reduction modulo M and the signed representative as a double.
+__global__ void __launch_bounds__(256) crt_kernel(const uint8_t* __restrict__ t, int64_t rows_pad, int64_t cols_pad,
+                                                  int64_t mrows, int64_t ncols, const int* __restrict__ e_a,
+                                                  const int* __restrict__ e_b, const Crt crt, double* __restrict__ c,
+                                                  int64_t ldc) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t j = blockIdx.y;
   if (i >= mrows) return;
   const u128 M = ((u128)crt.M_hi << 64) | crt.M_lo;
   const u128 H = ((u128)crt.H_hi << 64) | crt.H_lo;
-  // t'_l = (C_l (M/m_l)^-1) mod m_l (epilogue)  ->  s = sum_l t'_l M/m_l  (< nmod M)
-  u128 s = 0;
-  const uint8_t* tp = t + (size_t)j * rows_pad + i;
   const size_t lstride = (size_t)cols_pad * rows_pad;
-  if (crt.nmod <= 15) {
-    for (int l = 0; l < crt.nmod; ++l)
-      s += (u128)tp[l * lstride] * (((u128)crt.md_hi[l] << 64) | crt.md_lo[l]);
-    // s mod M with s < 15 M: quotient from a double estimate, then fix by one
-    uint64_t q = (uint64_t)floor(u128_to_double(s) / u128_to_double(M));
-    u128 qm = (u128)q * M;
-    if (qm > s) qm -= M;
-    s -= qm;
+  const uint8_t* tp = t + (size_t)j * rows_pad + i;
+  const int nm = crt.nmod;
+  unsigned tv[kMaxMod];
+#pragma unroll
+  for (int l = 0; l < kMaxMod; ++l) tv[l] = (l < nm) ? (unsigned)__ldcs(tp + (size_t)l * lstride) : 0u;
+  u128 s = 0;
+  if (nm <= 15) {
+    uint64_t lo = 0, hi = 0;
+#pragma unroll
+    for (int l = 0; l < 15; ++l) {
+      const uint64_t p0 = crt.md_lo[l] * (uint64_t)tv[l];
+      const uint64_t p1 = __umul64hi(crt.md_lo[l], (uint64_t)tv[l]) + crt.md_hi[l] * (uint64_t)tv[l];
+      lo += p0;
+      hi += p1 + (lo < p0 ? 1ull : 0ull);
+    }
+    s = ((u128)hi << 64) | lo;
+    const uint64_t q = (uint64_t)(fma((double)hi, 0x1p64, (double)lo) * crt.inv_M);  // floor(s / M) +- 1
+    s -= (u128)q * M;
+    if ((s >> 127) != 0) s += M;  // q was one too large
     if (s >= M) s -= M;
-  } else {
-    for (int l = 0; l < crt.nmod; ++l) {
-      s += (u128)tp[l * lstride] * (((u128)crt.md_hi[l] << 64) | crt.md_lo[l]);
+  } else {  // 16 moduli: M ~ 2^124.6; add the terms (< M) one by one, reducing
+#pragma unroll
+    for (int l = 0; l < kMaxMod; ++l) {
+      s += (u128)tv[l] * (((u128)crt.md_hi[l] << 64) | crt.md_lo[l]);
       if (s >= M) s -= M;
     }
   }
-  double v;
-  if (s > H)
-    v = -u128_to_double(M - s);
-  else
-    v = u128_to_double(s);
-  c[i + j * ldc] = scalbn(v, -(e_a[0] + e_b[j]));
+  const u128 mag = (s > H) ? M - s : s;
+  const double v = fma((double)(uint64_t)(mag >> 64), 0x1p64, (double)(uint64_t)mag);  // within 1 ulp
+  c[i + j * ldc] = ((s > H) ? -v : v) * scalbn(1.0, -(e_a[0] + e_b[j]));
 }
 
 // ----------------------------------------------------------------- host side
@@ -653,7 +702,7 @@ static PrepLayout prep_layout(int64_t m, int64_t n, int nmod) {
 struct GemmLayout {
   int ng, n_g;
   int64_t nkb, nmb, rows_pad, cols_pad;
-  size_t off_eb, off_b, off_t, total;
+  size_t off_eb, off_b, off_t, off_tab, total;
 };
 static GemmLayout gemm_layout(const PrepLayout& p, int trans, int64_t ncols, int nmod) {
   GemmLayout g;
@@ -668,7 +717,8 @@ static GemmLayout gemm_layout(const PrepLayout& p, int trans, int64_t ncols, int
   g.off_eb = 0;
   g.off_b = (((size_t)g.cols_pad * sizeof(int)) + 1023) & ~size_t(1023);
   g.off_t = g.off_b + (size_t)nmod * g.cols_pad * g.nkb * kTile;
-  g.total = g.off_t + (size_t)nmod * g.cols_pad * g.rows_pad;
+  g.off_tab = g.off_t + (size_t)nmod * g.cols_pad * g.rows_pad;
+  g.total = g.off_tab;
   return g;
 }
 
@@ -685,7 +735,7 @@ static void launch_residue_a(const double* a, int64_t lda, int64_t m, int64_t n,
 template <int NMOD>
 static void launch_residue_b(const double* b, int64_t ldb, int64_t k, int64_t ncols, const GemmLayout& g, int pb,
                              int* e_b, int8_t* tiles, cudaStream_t st) {
-  bscale_kernel<<<(unsigned)ceil_div(g.cols_pad, 8), 256, 0, st>>>(b, ldb, k, ncols, g.cols_pad, pb, e_b);
+  bscale_kernel<<<(unsigned)g.cols_pad, 256, 0, st>>>(b, ldb, k, ncols, g.cols_pad, pb, e_b);
   residue_b_kernel<NMOD><<<dim3((unsigned)g.cols_pad, (unsigned)ceil_div(g.nkb * 8, 256)), 256, 0, st>>>(
       b, ldb, k, ncols, g.n_g, g.nkb, e_b, tiles, g.ng);
 }
@@ -722,7 +772,18 @@ int oz_prep(const double* a, int64_t lda, int64_t m, int64_t n, int nmod, void* 
   int8_t* tiles = reinterpret_cast<int8_t*>(base + p.off_tiles);
   RLRA_REQUIRE(p.nrb <= 2147483647 && p.ncb <= 65535, "oz_prep: A too large for the norm grid");
   RLRA_CHECK_CUDA(cudaMemsetAsync(maxbits, 0, sizeof(unsigned long long), st));
-  oz::norms_partial_kernel<<<dim3((unsigned)p.nrb, (unsigned)p.ncb), 256, 0, st>>>(a, lda, m, n, prow, pcol);
+  {
+    static int attr_dev = -1;
+    int dev = 0;
+    RLRA_CHECK_CUDA(cudaGetDevice(&dev));
+    if (attr_dev != dev) {
+      RLRA_CHECK_CUDA(cudaFuncSetAttribute(oz::norms_partial_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)oz::kNormSmem));
+      attr_dev = dev;
+    }
+  }
+  oz::norms_partial_kernel<<<dim3((unsigned)p.nrb, (unsigned)p.ncb), 256, oz::kNormSmem, st>>>(a, lda, m, n, prow,
+                                                                                               pcol);
   RLRA_LAUNCHED();
   oz::norms_final_kernel<<<(unsigned)ceil_div(m + n, 256), 256, 0, st>>>(prow, p.ncb, m, pcol, p.nrb, n, maxbits);
   RLRA_LAUNCHED();
