@@ -313,10 +313,10 @@ __global__ void __launch_bounds__(256) residue_b_kernel(const double* __restrict
 // ----------------------------------------------------------------- A scale
 // Row and column 2-norms of A in ONE read: CTA = 2048 rows x 256 columns;
 // partial sums in fixed order (deterministic), then max -> eA.
-constexpr int kNormRows = 2048, kNormCols = 256, kNormBlk = 16;
+constexpr int kNormRows = 2048, kNormCols = 256, kNormBlk = 8;
 constexpr size_t kNormSmem = (8 * kNormCols + 8 * 32 * (kNormBlk + 1)) * sizeof(double);
 
-__global__ void __launch_bounds__(256) norms_partial_kernel(const double* __restrict__ a, int64_t lda, int64_t m,
+__global__ void __launch_bounds__(256, 4) norms_partial_kernel(const double* __restrict__ a, int64_t lda, int64_t m,
                                                             int64_t n, double* __restrict__ part_row,
                                                             double* __restrict__ part_col) {
   // warp w owns rows r0 + 256 w + [0, 256) (8 chunks of 32, lane = row in
