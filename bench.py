@@ -14,7 +14,10 @@ Our arm prints ONE JSON line with:
              NumPy A, uploaded in column chunks behind the first pass), Omega
              regenerated every step (device replay of NumPy's stream), factors
              returned to the host as NumPy: H2D/D2H inside the timed region
-  roofline   the pass GEMM (DMMA) against the measured FP64 DMMA peak
+  roofline   the dominant kernel -- the int8 tensor-core pass GEMM of the
+             Ozaki-II emulation (HBM bound) -- achieved GB/s from CUDA events
+             on its launch stream vs MEASURED_PEAKS.json, plus its int8-tensor
+             fraction and the passes' FP64-equivalent rate vs the DMMA peak
   cpu_baseline  the unmodified reference (oracle/_ref, rlra 0.1.0) on the box's
              host cores, same call, best of a bounded sample
 `--impl reference` times the reference's own CPU implementation (oracle/_ref).
@@ -37,6 +40,10 @@ REPO = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, REPO)
 
 FP64_PEAK_TFLOPS = 37.1  # measured DMMA m8n8k4 sustained, profiles/fp64_peak_r01.log
+try:
+    MEASURED = json.load(open(os.path.join(REPO, "MEASURED_PEAKS.json")))
+except (OSError, ValueError):
+    MEASURED = {"hbm_gbs": 7700.0, "bf16_tflops": 2250.0}  # B200_PROFILING.md fallback
 FP64_PEAK_SRC = "measured: tools/fp64_peak.cu on this pool's B200 (profiles/fp64_peak_r01.log); MEASURED_PEAKS.json has no FP64 entry"
 
 
@@ -129,6 +136,80 @@ class Clocks:
         loaded = [s for s in sm if s > 0.5 * max(sm)] or sm
         return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": max(smax), "reasons": sorted(reasons),
                 "samples": len(sm)}
+
+
+KTIMERS = ("oz_gemm_i8", "oz_residue_a", "oz_norms", "oz_crt", "oz_residue_b")
+
+
+def _ktimer_read(lib, name):
+    import ctypes
+
+    ms, cnt = ctypes.c_double(0.0), ctypes.c_longlong(0)
+    rc = lib.rlra_b200_ktimer_read(name.encode(), ctypes.byref(ms), ctypes.byref(cnt))
+    if rc != 0:
+        raise RuntimeError(lib.rlra_b200_last_error().decode())
+    return ms.value, cnt.value
+
+
+def _ktimer_reset(lib):
+    for nm in KTIMERS:
+        _ktimer_read(lib, nm)
+
+
+def roofline_line(w, v, passes, reps, kt, pass_ms, step_ms):
+    """Roofline of the dominant kernel, the int8 tensor-core pass GEMM
+    (csrc/ozaki.cu gemm_i8_kernel), from CUDA events recorded on its launch
+    stream around every launch of `reps` profiled factorizations.
+
+    Algorithmic bytes per pass of width w: the residues of
+    A (nmod bytes per element, read once), the residues of the skinny operand
+    (nmod * K * w) and the residue output (nmod * rows * w); K + rows = m + n
+    for both orientations.  The kernel is HBM bound: its int8 work
+    (nmod * 2mnw ops) at the int8 tensor peak takes less time than its bytes
+    at the HBM peak."""
+    from paper_2002_07138_b200 import ops
+
+    nmod = ops.OZ_NMOD
+    l_ = w.k + w.q_os
+    widths = [l_] * (v - 1) + [w.k]
+    bytes_step = sum(nmod * (w.m * w.n + (w.m + w.n) * x) for x in widths)
+    i8ops_step = sum(nmod * 2.0 * w.m * w.n * x for x in widths)
+    g_ms, g_cnt = kt["oz_gemm_i8"]
+    hbm_peak = MEASURED.get("hbm_gbs")
+    if g_cnt == 0:  # DMMA pass (RLRA_B200_PASS_GEMM=dmma or operands too large for the residues)
+        achieved = passes * reps / (pass_ms / 1e3) / 1e12 if pass_ms else None
+        return {"bound": "tensor", "kernel": "dgemm_tma_kernel (FP64 DMMA pass products)", "achieved": achieved,
+                "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                "frac": achieved / FP64_PEAK_TFLOPS if achieved else None, "traffic": None,
+                "peak_source": FP64_PEAK_SRC, "pass_ms_per_step": pass_ms / reps}
+    per_launch_bytes = bytes_step * reps / g_cnt
+    per_launch_ms = g_ms / g_cnt
+    achieved = per_launch_bytes / (per_launch_ms / 1e3) / 1e9
+    traffic = None
+    tpath = os.path.join(REPO, "profiles", "ncu_pass_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get(f"oz_gemm_i8_{w.name}_v{v}")
+        except Exception:
+            traffic = None
+    i8_peak = 2.0 * MEASURED.get("bf16_tflops", 1690.0)  # dense int8 = 2x dense bf16 on B200
+    fp64_eq = passes * reps / (pass_ms / 1e3) / 1e12 if pass_ms else None
+    other = {nm: {"ms_per_step": t / reps, "launches_per_step": c / reps} for nm, (t, c) in kt.items()}
+    return {"bound": "hbm", "kernel": "gemm_i8_kernel (tcgen05 kind::i8 Ozaki-II pass products, csrc/ozaki.cu)",
+            "achieved": achieved, "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
+            "traffic": traffic, "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)",
+            "algorithmic_bytes_per_launch": per_launch_bytes, "ms_per_launch": per_launch_ms,
+            "launches_per_step": g_cnt / reps,
+            "bytes_per_unit": f"nmod*(m*n + (m+n)*w) per pass of width w, nmod={nmod}",
+            "int8_tensor": {"achieved_tops": i8ops_step * reps / (g_ms / 1e3) / 1e12, "peak_tops": i8_peak,
+                            "frac": i8ops_step * reps / (g_ms / 1e3) / 1e12 / i8_peak,
+                            "peak_source": "2 x MEASURED_PEAKS.json bf16_tflops (B200 dense int8 rate)"},
+            "kernel_share_of_step": g_ms / reps / step_ms,
+            "fp64_equivalent": {"pass_tflops": fp64_eq, "dmma_peak_tflops": FP64_PEAK_TFLOPS,
+                                "frac_of_dmma_peak": fp64_eq / FP64_PEAK_TFLOPS if fp64_eq else None,
+                                "pass_ms_per_step": pass_ms / reps,
+                                "note": "pass products (incl. B residues + CRT) as FP64 flops 2*m*n*w"},
+            "other_kernels": other}
 
 
 def reference_arm(args):
@@ -261,33 +342,22 @@ def our_arm(args):
     clk = clocks.stop()
     value = flops / (ms / 1e3) / 1e9
 
-    # ---- roofline of the dominant kernel (pass GEMMs), CUDA events per launch
+    # ---- roofline of the dominant kernel, CUDA events per launch on its stream
+    reps = max(1, min(args.steps, 3))
     ops.PROF.records.clear()
     ops.PROF.on = True
-    for _ in range(max(1, min(args.steps, 3))):
+    _ktimer_reset(lib)
+    lib.rlra_b200_ktimer_enable(1)
+    for _ in range(reps):
         P.powerlu(dm, w.k, w.q_os, v, w.seed)
+    torch.cuda.synchronize()
+    lib.rlra_b200_ktimer_enable(0)
+    kt = {nm: _ktimer_read(lib, nm) for nm in KTIMERS}
     summ = ops.PROF.summary()
     ops.PROF.on = False
     ops.PROF.records.clear()
     pass_ms = sum(summ.get(k, (0.0, 0))[0] for k in ("pass_nn", "pass_tn"))
-    pass_cnt = sum(summ.get(k, (0.0, 0))[1] for k in ("pass_nn", "pass_tn"))
-    reps = max(1, min(args.steps, 3))
-    achieved = passes * reps / (pass_ms / 1e3) / 1e12 if pass_ms else None
-    total_prof_ms = sum(t for t, _ in summ.values())
-    traffic = None
-    tpath = os.path.join(REPO, "profiles", "ncu_pass_traffic.json")
-    if os.path.exists(tpath):
-        try:
-            traffic = json.load(open(tpath)).get(f"{w.name}_v{v}")
-        except Exception:
-            traffic = None
-    roofline = {"bound": "tensor", "kernel": "dgemm_dmma_kernel (pass products A W / A^T W)",
-                "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
-                "frac": (achieved / FP64_PEAK_TFLOPS) if achieved else None, "traffic": traffic,
-                "peak_source": FP64_PEAK_SRC,
-                "pass_ms_per_step": pass_ms / reps, "pass_launches_per_step": pass_cnt / reps,
-                "pass_share_of_step": (pass_ms / total_prof_ms) if total_prof_ms else None,
-                "flops_per_unit": "2*m*n*w per pass of width w (SURVEY.md Appendix B)"}
+    roofline = roofline_line(w, v, passes, reps, kt, pass_ms, ms)
     if args.breakdown:
         for k2, (t, c) in sorted(summ.items(), key=lambda kv: -kv[1][0]):
             print(f"  {k2:32s} {t / reps:9.3f} ms/step  {c / reps:6.1f} calls/step", file=sys.stderr)

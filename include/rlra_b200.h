@@ -56,6 +56,13 @@ RLRA_B200_API const char* rlra_b200_last_error(void);
 RLRA_B200_API int rlra_b200_device_count(int* out);
 /* number of kernels this library has launched in this process (instrumentation) */
 RLRA_B200_API long long rlra_b200_launch_count(void);
+/* per-kernel CUDA-event timing (instrumentation for bench.py's roofline):
+ * while enabled, events are recorded on the launch stream around the named
+ * kernels ("oz_gemm_i8", "oz_residue_a", "oz_norms", "oz_crt", "oz_residue_b");
+ * read() waits for them, returns the summed milliseconds and launch count
+ * since the last read, and clears the record. */
+RLRA_B200_API int rlra_b200_ktimer_enable(int on);
+RLRA_B200_API int rlra_b200_ktimer_read(const char* name, double* ms_total, long long* launches);
 
 /* ---- host seam: drop-in for backend.plu_inplace(lu, piv) ---------------
  * lu: HOST F-contiguous float64 m x n (ld = m), overwritten with packed L\U;

@@ -28,6 +28,8 @@ SIGNATURES = {
     "rlra_b200_last_error": (ctypes.c_char_p, []),
     "rlra_b200_device_count": (_c_i, [_c_p]),
     "rlra_b200_launch_count": (ctypes.c_longlong, []),
+    "rlra_b200_ktimer_enable": (_c_i, [_c_i]),
+    "rlra_b200_ktimer_read": (_c_i, [ctypes.c_char_p, _c_p, _c_p]),
     "rlra_b200_plu_inplace": (_c_i, [_c_p, _c_i64, _c_i64, _c_p]),
     "rlra_b200_getrf_workspace": (_c_sz, [_c_i64, _c_i64]),
     "rlra_b200_getrf": (_c_i, [_c_p, _c_i64, _c_i64, _c_i64, _c_p, _c_p, _c_p, _c_sz, _c_p]),

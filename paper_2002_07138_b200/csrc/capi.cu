@@ -22,6 +22,32 @@ const char* last_error() { return g_err; }
 static std::atomic<long long> g_launches{0};
 void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
+static std::atomic<bool> g_ktimer{false};
+static std::mutex g_ktimer_mu;
+static std::vector<std::pair<cudaEvent_t, cudaEvent_t>> g_ktimer_ev[KT_COUNT];
+static const char* const kKTimerNames[KT_COUNT] = {"oz_gemm_i8", "oz_residue_a", "oz_norms", "oz_crt",
+                                                   "oz_residue_b"};
+
+bool ktimer_on() { return g_ktimer.load(std::memory_order_relaxed); }
+
+void ktimer_mark(int id, cudaStream_t st, bool end) {
+  if (!ktimer_on() || id < 0 || id >= KT_COUNT) return;
+  std::lock_guard<std::mutex> lock(g_ktimer_mu);
+  auto& v = g_ktimer_ev[id];
+  if (!end) {
+    cudaEvent_t a, b;
+    if (cudaEventCreate(&a) != cudaSuccess) return;
+    if (cudaEventCreate(&b) != cudaSuccess) {
+      cudaEventDestroy(a);
+      return;
+    }
+    cudaEventRecord(a, st);
+    v.emplace_back(a, b);
+  } else if (!v.empty()) {
+    cudaEventRecord(v.back().second, st);
+  }
+}
+
 const DeviceInfo& device_info() {
   static std::mutex mu;
   static std::vector<DeviceInfo> cache;
@@ -99,6 +125,37 @@ int rlra_b200_abi_version(void) { return RLRA_B200_ABI_VERSION; }
 const char* rlra_b200_last_error(void) { return last_error(); }
 
 long long rlra_b200_launch_count(void) { return g_launches.load(); }
+
+int rlra_b200_ktimer_enable(int on) {
+  g_ktimer.store(on != 0);
+  return 0;
+}
+
+int rlra_b200_ktimer_read(const char* name, double* ms_total, long long* launches) {
+  RLRA_REQUIRE(name && ms_total && launches, "ktimer_read: null argument");
+  int id = -1;
+  for (int i = 0; i < KT_COUNT; ++i)
+    if (std::strcmp(name, kKTimerNames[i]) == 0) id = i;
+  RLRA_REQUIRE(id >= 0, "ktimer_read: unknown kernel timer '%s'", name);
+  std::lock_guard<std::mutex> lock(g_ktimer_mu);
+  double tot = 0.0;
+  long long cnt = 0;
+  cudaError_t err = cudaSuccess;
+  for (auto& pr : g_ktimer_ev[id]) {
+    float ms = 0.0f;
+    if (err == cudaSuccess) err = cudaEventSynchronize(pr.second);
+    if (err == cudaSuccess) err = cudaEventElapsedTime(&ms, pr.first, pr.second);
+    tot += ms;
+    ++cnt;
+    cudaEventDestroy(pr.first);
+    cudaEventDestroy(pr.second);
+  }
+  g_ktimer_ev[id].clear();
+  RLRA_CHECK_CUDA(err);
+  *ms_total = tot;
+  *launches = cnt;
+  return 0;
+}
 
 int rlra_b200_device_count(int* out) {
   RLRA_CHECK_CUDA(cudaGetDeviceCount(out));

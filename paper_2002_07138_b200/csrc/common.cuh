@@ -40,6 +40,13 @@ void note_launch();
     RLRA_CHECK_CUDA(cudaGetLastError());                                        \
   } while (0)
 
+// Optional per-kernel CUDA-event timing (bench.py's roofline): while enabled
+// (rlra_b200_ktimer_enable), ktimer_mark() records an event on the launch
+// stream before (end=false) and after (end=true) a named kernel launch.
+enum KTimerId { KT_OZ_GEMM = 0, KT_OZ_RESIDUE_A, KT_OZ_NORMS, KT_OZ_CRT, KT_OZ_RESIDUE_B, KT_COUNT };
+bool ktimer_on();
+void ktimer_mark(int id, cudaStream_t st, bool end);
+
 struct DeviceInfo {
   int sm_count = 0;
   int max_smem_optin = 0;

@@ -915,6 +915,10 @@ int fill_iota(int64_t* p, int64_t m, cudaStream_t st) {
   return 0;
 }
 
+bool getrf_full_eligible(int64_t m, int64_t n, int cluster_max);
+int getrf_full(double* a, int64_t lda, int64_t m, int64_t n, int64_t* piv, int64_t* ipiv, int* zflag, double* recg,
+               cudaStream_t st);
+
 unsigned long long* g_lu_trace = nullptr;  // set by rlra_b200_debug_lu_trace (tools only)
 static unsigned long long* lu_trace_buffer() { return g_lu_trace; }
 
@@ -1016,6 +1020,17 @@ int getrf(double* a, int64_t lda, int64_t m, int64_t n, int64_t* piv, int64_t* n
   // (same rounding sequence per element: still bit-exact).
   auto rows_cap = [](int pw) { return (int64_t)(LU_PANEL_SMEM_BYTES / (pw * 8)); };
   const int cmax = lu_max_cluster();
+  if (getrf_full_eligible(m, n, cmax)) {
+    // narrow sketch: the whole factorization in one cluster launch (getrf_full.cu)
+    if (getrf_full(a, lda, m, n, piv, w.ipiv, w.zflag, w.recg, st)) return -1;
+    if (nonzero_diag_dev) {
+      count_nonzero_diag_kernel<<<1, 256, 0, st>>>(a, lda, r, nonzero_diag_dev);
+      RLRA_LAUNCHED();
+    }
+    if (zflag_out && r > 0)
+      RLRA_CHECK_CUDA(cudaMemcpyAsync(zflag_out, w.zflag, r * sizeof(int), cudaMemcpyDeviceToDevice, st));
+    return 0;
+  }
   const bool use_cluster = cmax > 1 && m <= cmax * rows_cap(16);
   int pw;
   if (use_cluster) pw = (m <= cmax * rows_cap(32)) ? 32 : 16;

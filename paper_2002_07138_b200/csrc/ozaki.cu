@@ -782,14 +782,18 @@ int oz_prep(const double* a, int64_t lda, int64_t m, int64_t n, int nmod, void* 
       attr_dev = dev;
     }
   }
+  ktimer_mark(KT_OZ_NORMS, st, false);
   oz::norms_partial_kernel<<<dim3((unsigned)p.nrb, (unsigned)p.ncb), 256, oz::kNormSmem, st>>>(a, lda, m, n, prow,
                                                                                                pcol);
+  ktimer_mark(KT_OZ_NORMS, st, true);
   RLRA_LAUNCHED();
   oz::norms_final_kernel<<<(unsigned)ceil_div(m + n, 256), 256, 0, st>>>(prow, p.ncb, m, pcol, p.nrb, n, maxbits);
   RLRA_LAUNCHED();
   oz::scale_a_kernel<<<1, 1, 0, st>>>(maxbits, oz::budget(nmod).pa, e_a);
   RLRA_LAUNCHED();
+  ktimer_mark(KT_OZ_RESIDUE_A, st, false);
   OZ_DISPATCH(nmod, oz::launch_residue_a, a, lda, m, n, e_a, tiles, p, st);
+  ktimer_mark(KT_OZ_RESIDUE_A, st, true);
   RLRA_LAUNCHED();
   return 0;
 }
@@ -820,7 +824,9 @@ int oz_gemm(int trans, const void* prep, int64_t m, int64_t n, int nmod, const d
   int8_t* b_tiles = reinterpret_cast<int8_t*>(w + g.off_b);
   uint8_t* tout = w + g.off_t;
   const oz::Budget bud = oz::budget(nmod);
+  ktimer_mark(KT_OZ_RESIDUE_B, st, false);
   OZ_DISPATCH(nmod, oz::launch_residue_b, b, ldb, K, ncols, g, bud.pb, e_b, b_tiles, st);
+  ktimer_mark(KT_OZ_RESIDUE_B, st, true);
   RLRA_LAUNCHED();
   note_launch();  // bscale + residue_b
 
@@ -851,11 +857,15 @@ int oz_gemm(int trans, const void* prep, int64_t m, int64_t n, int nmod, const d
   RLRA_CHECK_CUDA(attr_err);
   const int64_t units = (int64_t)nmod * g.nmb * g.ng;
   const int grid = (int)std::min<int64_t>(units, device_info().sm_count);
+  ktimer_mark(KT_OZ_GEMM, st, false);
   oz::gemm_i8_kernel<<<grid, oz::kGemmThreads, smem, st>>>(ga);
+  ktimer_mark(KT_OZ_GEMM, st, true);
   RLRA_LAUNCHED();
 
+  ktimer_mark(KT_OZ_CRT, st, false);
   oz::crt_kernel<<<dim3((unsigned)ceil_div(mrows, 256), (unsigned)ncols), 256, 0, st>>>(
       tout, g.rows_pad, g.cols_pad, mrows, ncols, e_a, e_b, crt, c, ldc);
+  ktimer_mark(KT_OZ_CRT, st, true);
   RLRA_LAUNCHED();
   return 0;
 }

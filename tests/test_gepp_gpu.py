@@ -64,7 +64,10 @@ def test_host_seam_plu_inplace_bit_exact(cuda_dev, name):
 
 @pytest.mark.parametrize("m,n,seed", [(20000, 220, 0), (10000, 220, 1), (3001, 97, 2),
                                       (16384, 256, 3), (65, 64, 4), (64, 200, 5),
-                                      (100000, 70, 6), (200000, 45, 7)])
+                                      (100000, 70, 6), (200000, 45, 7),
+                                      # one-launch cluster GEPP (csrc/getrf_full.cu): edges of its range
+                                      (24576, 256, 10), (8193, 33, 11), (2000, 60, 12), (520, 256, 13),
+                                      (16385, 200, 14)])
 def test_device_gepp_bit_exact_vs_oracle_sketch_shapes(cuda_dev, m, n, seed):
     a = np.random.default_rng(seed).standard_normal((m, n))
     if n > 40:

@@ -1,4 +1,5 @@
-// Timeline of one cluster GEPP panel (globaltimer stamps per CTA and step).
+// Timeline of the one-launch cluster GEPP (csrc/getrf_full.cu): globaltimer
+// stamps per panel on CTA 0 (build with -DRLRA_LU_TRACE; see tools/build_traces.sh).
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
@@ -11,7 +12,7 @@ size_t getrf_workspace_bytes(int64_t m, int64_t n);
 int fill_iota(int64_t* p, int64_t m, cudaStream_t st);
 }
 int main(int argc, char** argv) {
-  int64_t m = argc > 1 ? atoll(argv[1]) : 10000, n = argc > 2 ? atoll(argv[2]) : 32;
+  int64_t m = argc > 1 ? atoll(argv[1]) : 20000, n = argc > 2 ? atoll(argv[2]) : 220;
   std::vector<double> h(m * n);
   srand(1);
   for (auto& x : h) x = rand() / (double)RAND_MAX - 0.5;
@@ -33,15 +34,18 @@ int main(int argc, char** argv) {
   }
   std::vector<unsigned long long> t(16 * 128);
   cudaMemcpy(t.data(), tr, t.size() * 8, cudaMemcpyDeviceToHost);
-  unsigned long long t0 = ~0ull;
-  for (int b = 0; b < 16; b++) if (t[b * 128] && t[b * 128] < t0) t0 = t[b * 128];
-  auto T = [&](int b, int s) { return t[b * 128 + s] ? (t[b * 128 + s] - t0) / 1e3 : -1.0; };
-  for (int b : {0, 15}) {
-    printf("CTA %d: start %.2f before-sync %.2f after-sync %.2f end %.2f exit %.2f\n", b, T(b, 0), T(b, 1), T(b, 2),
-           T(b, 126), T(b, 127));
-    for (int jj = 0; jj < 12; jj++)
-      printf("  step %d: pre %.2f got %.2f synced %.2f lookahead %.2f argmax %.2f pushed %.2f\n", jj, T(b, 8 + 8 * jj),
-             T(b, 8 + 8 * jj + 1), T(b, 8 + 8 * jj + 2), T(b, 8 + 8 * jj + 3), T(b, 8 + 8 * jj + 4), T(b, 8 + 8 * jj + 5));
-  }
+  unsigned long long t0 = t[0];
+  auto T = [&](int s) { return t[s] ? (t[s] - t0) / 1e3 : -1.0; };
+  printf("panel: start | steps done | sync1 | sync2 | U12 | trailing   (us from panel 0 start, CTA 0)\n");
+  for (int p = 0; p * 6 + 5 < 64 && t[p * 6]; p++)
+    printf("  %2d: %8.2f %8.2f %8.2f %8.2f %8.2f %8.2f   steps %.2f  inter %.2f\n", p, T(6 * p), T(6 * p + 1),
+           T(6 * p + 2), T(6 * p + 3), T(6 * p + 4), T(6 * p + 5), T(6 * p + 1) - T(6 * p),
+           (t[6 * p + 5] ? T(6 * p + 5) : T(6 * p + 2)) - T(6 * p + 1));
+  printf("steps of panel 0 (CTA 0 / 15, tid 0): pre-wait | got | decided | swapped | mult done\n");
+  for (int b : {0, 15})
+    for (int jj = 0; jj < 12; jj++) {
+      auto S = [&](int i) { unsigned long long v = t[b * 128 + 64 + 5 * jj + i]; return v ? (v - t0) / 1e3 : -1.0; };
+      printf("  cta %2d step %2d: %7.2f %7.2f %7.2f %7.2f %7.2f\n", b, jj, S(0), S(1), S(2), S(3), S(4));
+    }
   return 0;
 }
