@@ -846,6 +846,7 @@ __global__ void count_nonzero_diag_kernel(const double* a, int64_t lda, int64_t 
 }
 
 // ------------------------------------------------------------------ host side
+size_t getrf_full_state_bytes();  // getrf_full.cu
 static size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
 
 struct LuLayout {
@@ -870,7 +871,7 @@ static LuLayout lu_layout(int64_t r, int G) {
   take(10, 2 * LU_NB * sizeof(int64_t));
   take(11, sizeof(int));
   take(12, sizeof(int64_t));
-  take(13, (size_t)(2 * 16 * (2 + LU_NB) + 2 * LU_NB) * sizeof(double));
+  take(13, std::max((size_t)(2 * 16 * (2 + LU_NB) + 2 * LU_NB) * sizeof(double), getrf_full_state_bytes()));
   L.total = o;
   return L;
 }
@@ -1021,15 +1022,19 @@ int getrf(double* a, int64_t lda, int64_t m, int64_t n, int64_t* piv, int64_t* n
   auto rows_cap = [](int pw) { return (int64_t)(LU_PANEL_SMEM_BYTES / (pw * 8)); };
   const int cmax = lu_max_cluster();
   if (getrf_full_eligible(m, n, cmax)) {
-    // narrow sketch: the whole factorization in one cluster launch (getrf_full.cu)
-    if (getrf_full(a, lda, m, n, piv, w.ipiv, w.zflag, w.recg, st)) return -1;
-    if (nonzero_diag_dev) {
-      count_nonzero_diag_kernel<<<1, 256, 0, st>>>(a, lda, r, nonzero_diag_dev);
-      RLRA_LAUNCHED();
+    // narrow sketch: the whole factorization in one cooperative launch (getrf_full.cu)
+    const int rc = getrf_full(a, lda, m, n, piv, w.ipiv, w.zflag, w.recg, st);
+    if (rc < 0) return -1;
+    if (rc == 0) {
+      if (nonzero_diag_dev) {
+        count_nonzero_diag_kernel<<<1, 256, 0, st>>>(a, lda, r, nonzero_diag_dev);
+        RLRA_LAUNCHED();
+      }
+      if (zflag_out && r > 0)
+        RLRA_CHECK_CUDA(cudaMemcpyAsync(zflag_out, w.zflag, r * sizeof(int), cudaMemcpyDeviceToDevice, st));
+      return 0;
     }
-    if (zflag_out && r > 0)
-      RLRA_CHECK_CUDA(cudaMemcpyAsync(zflag_out, w.zflag, r * sizeof(int), cudaMemcpyDeviceToDevice, st));
-    return 0;
+    // rc == 1: no room for helper clusters next to the panel cluster -> blocked path
   }
   const bool use_cluster = cmax > 1 && m <= cmax * rows_cap(16);
   int pw;

@@ -49,18 +49,19 @@ struct Args {
   int64_t* piv;        // int64[m], permuted like the reference's piv
   int64_t* ipiv;       // [n] pivot row of each step (== step when none / zero)
   int* zflag;          // [n] 1 for zero-pivot steps
-  double* recg;        // [2][CS][RECD] records + [2][W] diagonal rows (multicast staging)
+  double* recg;        // Handoff state (workspace, zeroed per launch)
   int64_t R;           // rows per CTA
+  unsigned nhelpers;   // helper CTAs (grid = CS + nhelpers)
   unsigned long long* trace;  // RLRA_LU_TRACE builds: [CTA][128] globaltimer stamps
 };
 
 #ifdef RLRA_LU_TRACE
 #define STEP_TRACE(jj, i)                                                                          \
   do {                                                                                              \
-    if (threadIdx.x == 0 && x.p->trace && j0 == 0 && (jj) < 12) {                                   \
+    if (threadIdx.x == 0 && x.p->trace && j0 == 0 && (jj) < 8) {                                    \
       unsigned long long t_;                                                                        \
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                                        \
-      x.p->trace[(int64_t)x.b * 128 + 64 + 5 * (jj) + (i)] = t_;                                    \
+      x.p->trace[(int64_t)x.b * 128 + 64 + 8 * (jj) + (i)] = t_;                                    \
     }                                                                                               \
   } while (0)
 #define FULL_TRACE(slot)                                                                            \
@@ -195,17 +196,54 @@ __device__ int panel_perm(int64_t j0, int nb, const int64_t* ipiv, int64_t* rows
   return cnt;
 }
 
-// Shared-memory plan of one configuration (dynamic part).
+// Dynamic shared memory of the cooperative GEPP (same size for every CTA):
+// panel CTAs: sL [W][T*RPT] + s_cmab [n] + s_u12 [W][W];
+// helper CTAs: U12 of the far columns [W][n].
 template <int RPT, int W>
 struct Plan {
-  static constexpr int RS = T * RPT;                       // row slots per CTA (slot = k * T + tid)
-  static constexpr int CB = RPT == 1 ? 8 : (RPT == 2 ? 4 : (RPT == 3 ? 3 : 2));  // trailing columns per chunk
-  static constexpr int NCH = (RPT <= 2 || RPT >= 5) ? 3 : 2;                    // chunks in flight
+  static constexpr int RS = T * RPT;  // row slots per CTA (slot = k * T + tid)
   static size_t bytes(int64_t n) {
-    return ((size_t)W * RS + (size_t)n * (1 + W) + (size_t)NCH * CB * RS) * sizeof(double);
+    const size_t panel = (size_t)W * RS + (size_t)n + (size_t)W * W;
+    const size_t helper = (size_t)W * n;
+    return (panel > helper ? panel : helper) * sizeof(double);
   }
   static size_t max_bytes() { return bytes(MAXN); }
 };
+
+// Handoff state between the panel cluster and the helper clusters (global
+// memory, zeroed per launch): counters, per-column max |U| over the rows
+// above the current panel (as ordered bit patterns), each panel's net row
+// permutation.
+constexpr int MAXP = MAXN / 16;
+struct Handoff {
+  unsigned ready;            // panels whose L, U12 rows and permutation are published
+  unsigned fardone[MAXP];    // helper CTAs done with panel b (interchanges + far update)
+  unsigned u12done[MAXP];    // helper CTAs done with panel b's far U12 rows
+  unsigned pad[64 - 1 - 2 * MAXP];
+  unsigned long long cmax[MAXN];
+  int64_t prow[MAXP][2 * 16], psrc[MAXP][2 * 16];
+  int pcnt[MAXP];
+  __align__(16) double stage[2 * CS * (2 + 16) + 2 * 16];  // multicast staging (records, diagonal rows)
+};
+
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void red_release_add(unsigned* p, unsigned v) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
+}
+// one thread waits until *p >= target (acquire); bounded: a protocol error traps
+__device__ __forceinline__ void wait_geq(const unsigned* p, unsigned target) {
+  for (long long spin = 0; ld_acquire(p) < target; ++spin) {
+    __nanosleep(64);
+    if (spin > (1ll << 26)) __trap();
+  }
+}
 
 // Per-thread context of the cluster kernel.
 struct Ctx {
@@ -213,8 +251,8 @@ struct Ctx {
   Shared* S;
   double* sL;      // [W][RS] retired panel columns of my row slots (L below, U on pivot rows)
   double* s_cmab;  // [n] max |a| over the rows above the current panel, per column
-  double* s_u12;   // [W][n] U12 of the finished panel (column index relative)
-  double* ring;    // [NCH][CB][RS] trailing-column staging
+  double* s_u12;   // [W][W] U12 of the next panel's columns
+  double* gstage;  // global staging of this CTA's outgoing records (multicast source)
   int b, tid, lane, warp, nk;
   int64_t rb, re, g0;
 };
@@ -236,6 +274,7 @@ struct Panel {
 template <int RPT, int W, int SC>
 __device__ __forceinline__ unsigned publish(const Ctx& x, Panel<RPT, W>& P, int jj, int nb, int jn, bool fin,
                                             const double* urow, unsigned par) {
+  const int j0 = SC == 0 ? 1 : jn - 1 - jj;  // for STEP_TRACE (panel 0 steps only)
   constexpr int RECD = 2 + W;
   constexpr int RS = Plan<RPT, W>::RS;
   Shared& S = *x.S;
@@ -260,23 +299,12 @@ __device__ __forceinline__ unsigned publish(const Ctx& x, Panel<RPT, W>& P, int 
     S.wkey[x.warp] = wk;
     S.widx[x.warp] = wi;
   }
-  unsigned done = 0u;
-  if (fin) {
-#pragma unroll
-    for (int k = 0; k < RPT; k++) {
-      if ((k == kb && wi != NONE && bi == wi) || P.lr[k] == jn) {
-        done |= 1u << k;
-        const double l = P.a[k][0];
-#pragma unroll
-        for (int i = 2; i < W; i++)
-          if (jj + i < nb) P.a[k][i] = sub_mul_nofma(P.a[k][i], l, urow[jj + i]);
-      }
-    }
-  }
+  if (SC) STEP_TRACE(jj, 3);
   __syncthreads();
   unsigned long long ck = x.lane < NW ? S.wkey[x.lane] : 0ull;
   unsigned ci = x.lane < NW ? S.widx[x.lane] : NONE;
   warp_keymax(ck, ci);
+  if (SC) STEP_TRACE(jj, 4);
   const bool has = (ci != NONE);
   int kw = -1, kd = -1;  // my slot holding the CTA winner / row jn
 #pragma unroll
@@ -286,6 +314,21 @@ __device__ __forceinline__ unsigned publish(const Ctx& x, Panel<RPT, W>& P, int 
   }
   const unsigned bw = __ballot_sync(0xffffffffu, kw >= 0), bd = __ballot_sync(0xffffffffu, kd >= 0);
   const unsigned bar_l = smem_u32(&S.mbar[par]);
+  // look-ahead of the two published rows only (CTA winner, row jn): step jj's
+  // terms on their columns jj+2.. (warp-uniform branch: two warps at most)
+  unsigned done = 0u;
+  if (fin && (bw | bd) != 0u) {
+#pragma unroll
+    for (int k = 0; k < RPT; k++) {
+      if (k == kw || k == kd) {
+        done |= 1u << k;
+        const double l = P.a[k][0];
+#pragma unroll
+        for (int i = 2; i < W; i++)
+          if (jj + i < nb) P.a[k][i] = sub_mul_nofma(P.a[k][i], l, urow[jj + i]);
+      }
+    }
+  }
   // stage a row (registers -> its sL slot, columns >= jj) for the pushing lanes
   auto stage = [&](int kk) {
 #pragma unroll
@@ -295,9 +338,11 @@ __device__ __forceinline__ unsigned publish(const Ctx& x, Panel<RPT, W>& P, int 
         for (int i = 0; i < W; i++)
           if (jj + i < W) x.sL[(size_t)(jj + i) * RS + k * T + x.tid] = P.a[k][i];
   };
+#ifdef LUF_PUSH_DSMEM
   if (bw != 0u || (!has && x.warp == 0)) {  // this warp publishes the CTA record
     if (kw >= 0) stage(kw);
     __syncwarp();
+    if (SC) STEP_TRACE(jj, 5);
     const int ol = bw ? __ffs(bw) - 1 : 0;
     const int ko = __shfl_sync(0xffffffffu, kw, ol);
     if (x.lane < CS) {
@@ -329,6 +374,48 @@ __device__ __forceinline__ unsigned publish(const Ctx& x, Panel<RPT, W>& P, int 
         st_async2(rdst + 8u * c, x.sL[(size_t)c * RS + sl], x.sL[(size_t)(c + 1) * RS + sl], rbar);
     }
   }
+#else
+  // the holder thread writes the row from registers (columns >= jj) and sL
+  // (retired columns < jj) to a global staging slot and multicasts it into
+  // every CTA with one bulk copy completing on each peer's mbarrier
+  auto emit = [&](int kk, double* slot) {
+    for (int c = 0; c < jj; c++) slot[c] = x.sL[(size_t)c * RS + kk * T + x.tid];
+#pragma unroll
+    for (int k = 0; k < RPT; k++)
+      if (k == kk)
+#pragma unroll
+        for (int i = 0; i < W; i++)
+          if (jj + i < W) slot[jj + i] = P.a[k][i];
+  };
+  const unsigned short mask = (unsigned short)0xffffu;
+  if (kw >= 0 || (!has && x.tid == 0)) {
+    double* slot = x.gstage + ((size_t)par * CS + x.b) * RECD;
+    const double v = has ? __longlong_as_double((long long)ck) : -1.0;
+    const long long gi = has ? (long long)ci : (long long)INT64_MAX;
+    slot[0] = v;
+    slot[1] = __longlong_as_double(gi);
+    if (has) emit(kw, slot + 2);
+    else
+      for (int c = 0; c < W; c++) slot[2 + c] = 0.0;
+    asm volatile("fence.proxy.async.global;\n" ::: "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1], %2, [%3], "
+        "%4;\n" ::"r"(smem_u32(S.recv + ((size_t)par * CS + x.b) * RECD)),
+        "l"(slot), "r"((unsigned)(RECD * 8)), "r"(bar_l), "h"(mask)
+        : "memory");
+  }
+  if (kd >= 0) {
+    double* dslot = x.gstage + (size_t)2 * CS * RECD + (size_t)par * W;
+    emit(kd, dslot);
+    asm volatile("fence.proxy.async.global;\n" ::: "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1], %2, [%3], "
+        "%4;\n" ::"r"(smem_u32(S.recv_diag + (size_t)par * W)),
+        "l"(dslot), "r"((unsigned)(W * 8)), "r"(bar_l), "h"(mask)
+        : "memory");
+  }
+#endif
+  if (SC) STEP_TRACE(jj, 6);
   return done;
 }
 
@@ -376,7 +463,6 @@ __device__ __forceinline__ void step(const Ctx& x, Panel<RPT, W>& P, double& cm,
     S.s_ipiv[jj] = prow;
     S.s_zf[jj] = zero ? 1 : 0;
   }
-  STEP_TRACE(jj, 2);
   // full-row interchange (:40-48): the rows' data stay where they are, their
   // logical labels swap (the write-back stores each slot at its logical row)
   unsigned below = 0u;
@@ -388,7 +474,6 @@ __device__ __forceinline__ void step(const Ctx& x, Panel<RPT, W>& P, double& cm,
     }
     if (P.lr[k] > j) below |= 1u << k;  // rows strictly below the diagonal
   }
-  STEP_TRACE(jj, 3);
   // multipliers (IEEE division, :49-51) and the next column (:52-55)
   const double ujj = urow[jj];
   const double rcp = zero ? 0.0 : __drcp_rn(ujj);
@@ -405,7 +490,7 @@ __device__ __forceinline__ void step(const Ctx& x, Panel<RPT, W>& P, double& cm,
       }
     }
   }
-  STEP_TRACE(jj, 4);
+  STEP_TRACE(jj, 2);
   if (jj + 1 < nb) {
     const unsigned done = publish<RPT, W, 1>(x, P, jj, nb, j + 1, !zero, urow, par ^ 1u);
 #ifndef LUF_EXP_NOBULK
@@ -426,6 +511,7 @@ __device__ __forceinline__ void step(const Ctx& x, Panel<RPT, W>& P, double& cm,
       }
     }
   }
+  STEP_TRACE(jj, 7);
   // retire column jj, rotate
 #pragma unroll
   for (int k = 0; k < RPT; k++) {
@@ -436,27 +522,33 @@ __device__ __forceinline__ void step(const Ctx& x, Panel<RPT, W>& P, double& cm,
   }
 }
 
+// Cooperative launch: cluster 0 factors the panels (register-resident rows,
+// see step / publish) and updates the NEXT panel's columns itself; clusters
+// 1..NH (the helpers) apply each panel's interchanges to the other columns,
+// form the far columns' U12 rows and update the far columns' rows below --
+// in parallel with the panel cluster's next panel.  Ordering is by release /
+// acquire counters in global memory; co-residency is guaranteed by the
+// cooperative launch (a grid that does not fit fails to launch).
 template <int RPT, int W>
-__global__ void __launch_bounds__(T, 1) lu_full_kernel(const Args p) {
+__device__ void panel_role(const Args& p, Handoff* hs, double* dyn) {
   namespace cg = cooperative_groups;
   constexpr int RECD = 2 + W;
-  using PL = Plan<RPT, W>;
-  constexpr int RS = PL::RS, CB = PL::CB, NCH = PL::NCH;
+  constexpr int RS = Plan<RPT, W>::RS;
   cg::cluster_group cluster = cg::this_cluster();
   __shared__ Shared S;
-  extern __shared__ __align__(16) double dyn[];
   Ctx x;
   x.p = &p;
   x.S = &S;
   x.sL = dyn;
   x.s_cmab = x.sL + (size_t)W * RS;
   x.s_u12 = x.s_cmab + p.n;
-  x.ring = x.s_u12 + (size_t)W * p.n;
+  x.gstage = hs->stage;
   x.b = (int)cluster.block_rank();
   x.tid = threadIdx.x;
   x.lane = x.tid & 31;
   x.warp = x.tid >> 5;
   const int64_t m = p.m, n = p.n, lda = p.lda;
+  const unsigned nhc = p.nhelpers;
   x.rb = min(m, (int64_t)x.b * p.R);
   x.re = min(m, x.rb + p.R);
   x.g0 = x.rb + x.tid;
@@ -478,28 +570,31 @@ __global__ void __launch_bounds__(T, 1) lu_full_kernel(const Args p) {
   for (int64_t c = tid; c < n; c += T) x.s_cmab[c] = -1.0;
   unsigned phase = 0u;  // bit q: parity of mbar[q]'s current phase
   Panel<RPT, W> P;
+  // panel 0: plain loads
+  {
+    const int nb0 = (int)min((int64_t)W, n);
+#pragma unroll
+    for (int k = 0; k < RPT; k++) {
+      const int64_t g = x.g0 + (int64_t)k * T;
+      const bool act = k < x.nk;
+      P.lr[k] = act ? (int)g : -1;
+#pragma unroll
+      for (int c = 0; c < W; c++) P.a[k][c] = (act && c < nb0) ? p.a[g + c * lda] : 0.0;
+    }
+  }
   cluster.sync();  // mbarriers initialised everywhere before the first DSMEM store
 
   for (int j0 = 0; j0 < (int)n; j0 += W) {
     const int nb = (int)min((int64_t)W, n - j0);
-    // ---- panel prologue: my rows >= j0 of columns j0 .. j0+W-1 into registers
-#pragma unroll
-    for (int k = 0; k < RPT; k++) {
-      const int64_t g = x.g0 + (int64_t)k * T;
-      const bool act = k < x.nk && g >= j0;
-      P.lr[k] = act ? (int)g : -1;
-#pragma unroll
-      for (int c = 0; c < W; c++) P.a[k][c] = (act && c < nb) ? p.a[g + (j0 + c) * lda] : 0.0;
-    }
-    double cm = (lane < nb) ? x.s_cmab[j0 + lane] : -1.0;  // lane c: colmax of panel column c so far
     const int pidx = j0 / W;
+    double cm = (lane < nb) ? x.s_cmab[j0 + lane] : -1.0;  // lane c: colmax of panel column c so far
     FULL_TRACE(6 * pidx + 0);
     publish<RPT, W, 0>(x, P, 0, nb, j0, false, nullptr, (unsigned)(j0 & 1));
 #pragma unroll 1
     for (int jj = 0; jj < nb; jj++) step<RPT, W>(x, P, cm, phase, j0, jj, nb);
     FULL_TRACE(6 * pidx + 1);
 
-    // ---- panel epilogue: every slot's row to its LOGICAL row, interchanges elsewhere
+    // ---- epilogue: every slot's row to its LOGICAL row; pivots; permutation
 #pragma unroll
     for (int k = 0; k < RPT; k++)
       if (P.lr[k] >= 0)
@@ -513,126 +608,222 @@ __global__ void __launch_bounds__(T, 1) lu_full_kernel(const Args p) {
           p.ipiv[j0 + lane] = S.s_ipiv[lane];
           p.zflag[j0 + lane] = S.s_zf[lane];
         }
+        if (lane < cnt) {
+          hs->prow[pidx][lane] = S.prow_rows[lane];
+          hs->psrc[pidx][lane] = S.prow_src[lane];
+        }
+        if (lane == 0) hs->pcnt[pidx] = cnt;
         int64_t v0 = 0;  // the same net permutation on piv (:46-48)
         if (lane < cnt) v0 = p.piv[S.prow_src[lane]];
         __syncwarp();
         if (lane < cnt) p.piv[S.prow_rows[lane]] = v0;
       }
     }
-    cluster.sync();  // (1) every panel row at its logical place; perm ready
-    FULL_TRACE(6 * pidx + 2);
-    const int cnt = S.pcnt;
-    const int ce = j0 + nb;
-    if (cnt > 0) {  // columns outside the panel: one warp per column, gather then scatter
-      const int64_t nother = n - nb;
-      for (int64_t q = b + (int64_t)CS * warp; q < nother; q += (int64_t)CS * NW) {
-        const int64_t c = q < j0 ? q : q + nb;
-        double* col = p.a + c * lda;
-        const double v0 = lane < cnt ? col[S.prow_src[lane]] : 0.0;
-        __syncwarp();
-        if (lane < cnt) col[S.prow_rows[lane]] = v0;
-      }
+    cluster.sync();  // (1) the whole panel at its logical rows, in global memory
+    if (b == 0 && tid == 0) {
+      __threadfence();
+      st_release(&hs->ready, (unsigned)pidx + 1);  // helpers may start on panel pidx
     }
+    FULL_TRACE(6 * pidx + 2);
+    const int ce = j0 + nb;
     if (ce >= n) break;
-    cluster.sync();  // (2) interchanges visible
+    const int nbn = (int)min((int64_t)W, n - ce);
+    // ---- the next panel's columns: interchanges, U12, rank-nb update -> registers
+    if (pidx >= 1) {  // helpers done with panel pidx-1 (whose far columns include these)
+      if (tid == 0) wait_geq(&hs->fardone[pidx - 1], nhc);
+      __syncthreads();
+    }
+    const int cnt = S.pcnt;
+    if (b < nbn && warp == 0 && cnt > 0) {
+      double* col = p.a + (int64_t)(ce + b) * lda;
+      const double v0 = lane < cnt ? col[S.prow_src[lane]] : 0.0;
+      __syncwarp();
+      if (lane < cnt) col[S.prow_rows[lane]] = v0;
+    }
+    cluster.sync();  // (2) next columns interchanged
     FULL_TRACE(6 * pidx + 3);
-    // ---- U12 = L11^-1 A12 (every CTA, redundantly), forward substitution in
-    // ascending step order, zero-pivot steps skipped; owners store their rows
     for (int e = tid; e < nb * nb; e += T) {
       const int r = e % nb, c = e / nb;
-      S.l11[r][c] = p.a[(j0 + r) + (j0 + c) * lda];
+      S.l11[r][c] = p.a[(j0 + r) + (int64_t)(j0 + c) * lda];
     }
     unsigned zmask = 0u;
     for (int s2 = 0; s2 < nb; s2++)
       if (S.s_zf[s2]) zmask |= 1u << s2;
     __syncthreads();
-    const int64_t ntr = n - ce;
-    for (int64_t cr = tid; cr < ntr; cr += T) {  // one thread per column, U12 built in shared memory
-      const double* col = p.a + (ce + cr) * lda + j0;
-      double* uc = x.s_u12 + cr;
-      double mx = x.s_cmab[ce + cr];
+    if (tid < nbn) {  // U12 of next column ce + tid (forward substitution, ascending steps)
+      const double* col = p.a + (int64_t)(ce + tid) * lda + j0;
+      double* uc = x.s_u12 + tid;
+      double mx = __longlong_as_double((long long)hs->cmax[ce + tid]);  // far U12 of earlier panels
+      if (mx == 0.0 && hs->cmax[ce + tid] == 0ull) mx = -1.0;
 #pragma unroll 1
       for (int s2 = 0; s2 < nb; s2++) {
         double acc = col[s2];
 #pragma unroll 4
         for (int t = 0; t < s2; t++)
-          if (!((zmask >> t) & 1u)) acc = sub_mul_nofma(acc, S.l11[s2][t], uc[t * n]);
-        uc[s2 * n] = acc;
+          if (!((zmask >> t) & 1u)) acc = sub_mul_nofma(acc, S.l11[s2][t], uc[t * W]);
+        uc[s2 * W] = acc;
         mx = fmax(mx, fabs(acc));
       }
-      x.s_cmab[ce + cr] = mx;
+      x.s_cmab[ce + tid] = mx;
     }
     __syncthreads();
-    // CTAs owning rows j0 .. j0+nb-1 (all above the trailing rows) store U12
-    for (int64_t e = tid; e < (int64_t)nb * ntr; e += T) {
-      const int s2 = (int)(e % nb);
-      const int64_t cr = e / nb, g = j0 + s2;
-      if (g >= x.rb && g < x.re) p.a[g + (ce + cr) * lda] = x.s_u12[s2 * n + cr];
+    for (int e = tid; e < nb * nbn; e += T) {  // owners store the U12 rows
+      const int s2 = e % nb, c = e / nb;
+      const int64_t g = j0 + s2;
+      if (g >= x.rb && g < x.re) p.a[g + (int64_t)(ce + c) * lda] = x.s_u12[s2 * W + c];
     }
-    FULL_TRACE(6 * pidx + 4);
-    // ---- trailing update of my logical rows >= ce: multipliers back into
-    // registers, the rows of the trailing columns streamed through a private
-    // cp.async ring (NCH chunks of CB columns), CB x RPT independent chains
-    bool act[RPT];
+    // my physical rows >= ce: next columns (registers) minus L21 (global -> sL) * U12
 #pragma unroll
     for (int k = 0; k < RPT; k++) {
-      act[k] = P.lr[k] >= ce;
+      const int64_t g = x.g0 + (int64_t)k * T;
+      const bool act = k < x.nk && g >= ce;
+      P.lr[k] = act ? (int)g : -1;
+      double* lk = x.sL + k * T + tid;
+      if (act) {
 #pragma unroll
-      for (int s2 = 0; s2 < W; s2++) P.a[k][s2] = (s2 < nb) ? x.sL[(size_t)s2 * RS + k * T + tid] : 0.0;
-    }
-    auto issue = [&](int64_t c0) {
-      if (c0 < ntr) {
-        double* slot = x.ring + (size_t)((c0 / CB) % NCH) * CB * RS + tid;
-#pragma unroll
-        for (int q = 0; q < CB; q++)
-          if (c0 + q < ntr) {
-            const double* src = p.a + (ce + c0 + q) * lda;
-#pragma unroll
-            for (int k = 0; k < RPT; k++)
-              if (act[k]) cp_async8(slot + q * RS + k * T, src + P.lr[k]);
-          }
-      }
-      cp_async_commit();
-    };
-#pragma unroll 1
-    for (int q = 0; q < NCH - 1; q++) issue((int64_t)q * CB);
-#pragma unroll 1
-    for (int64_t c0 = 0; c0 < ntr; c0 += CB) {
-      issue(c0 + (int64_t)(NCH - 1) * CB);
-      cp_async_wait<NCH - 1>();
-      const double* slot = x.ring + (size_t)((c0 / CB) % NCH) * CB * RS + tid;
-      double y[CB][RPT];
-#pragma unroll
-      for (int q = 0; q < CB; q++)
-#pragma unroll
-        for (int k = 0; k < RPT; k++) y[q][k] = (act[k] && c0 + q < ntr) ? slot[q * RS + k * T] : 0.0;
-#pragma unroll
-      for (int s2 = 0; s2 < W; s2++) {
-        if (s2 < nb && !((zmask >> s2) & 1u)) {
-#pragma unroll
-          for (int q = 0; q < CB; q++) {
-            const double u = x.s_u12[s2 * n + min(c0 + q, ntr - 1)];
-#pragma unroll
-            for (int k = 0; k < RPT; k++) y[q][k] = sub_mul_nofma(y[q][k], P.a[k][s2], u);
-          }
-        }
+        for (int s2 = 0; s2 < W; s2++)
+          if (s2 < nb) lk[(size_t)s2 * RS] = p.a[g + (int64_t)(j0 + s2) * lda];
       }
 #pragma unroll
-      for (int q = 0; q < CB; q++)
-        if (c0 + q < ntr) {
-          double* dst = p.a + (ce + c0 + q) * lda;
+      for (int c = 0; c < W; c++) P.a[k][c] = (act && c < nbn) ? p.a[g + (int64_t)(ce + c) * lda] : 0.0;
+      if (act) {
+        for (int s2 = 0; s2 < nb; s2++) {
+          if ((zmask >> s2) & 1u) continue;
+          const double l = lk[(size_t)s2 * RS];
+          const double* us = x.s_u12 + s2 * W;
 #pragma unroll
-          for (int k = 0; k < RPT; k++)
-            if (act[k]) dst[P.lr[k]] = y[q][k];
+          for (int c = 0; c < W; c++) P.a[k][c] = sub_mul_nofma(P.a[k][c], l, c < nbn ? us[c] : 0.0);
         }
+      }
     }
-    cp_async_wait<0>();
-    // relabelled rows were updated by their holder CTA, not their owner: the
-    // next panel's loads need every CTA's stores (also orders s_u12 reuse)
-    cluster.sync();
+    __syncthreads();
     FULL_TRACE(6 * pidx + 5);
   }
   cluster.sync();  // nobody leaves while a peer may still address its shared memory
+}
+
+template <int W>
+__device__ void helper_role(const Args& p, Handoff* hs, double* dyn) {
+  __shared__ double l11[W][W + 1];
+  __shared__ int64_t prw[2 * W], psr[2 * W];
+  __shared__ int s_cnt;
+  __shared__ unsigned s_zm;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const unsigned h = blockIdx.x - CS, nhc = p.nhelpers;
+  const int64_t m = p.m, n = p.n, lda = p.lda;
+  double* u12 = dyn;  // [W][n - fs]
+  const int np = (int)((n + W - 1) / W);
+  for (int pidx = 0; pidx < np; pidx++) {
+    const int j0 = pidx * W;
+    const int nb = (int)min((int64_t)W, n - j0);
+    const int ce = j0 + nb;
+    const int nbn = ce < n ? (int)min((int64_t)W, n - ce) : 0;
+    const int fs = ce + nbn;  // far columns [fs, n)
+    const int nfar = (int)n - fs;
+    if (tid == 0) {
+      wait_geq(&hs->ready, (unsigned)pidx + 1);
+      if (pidx >= 1) wait_geq(&hs->fardone[pidx - 1], nhc);
+    }
+    __syncthreads();
+    const int cnt = hs->pcnt[pidx];
+    if (tid < cnt) {
+      prw[tid] = hs->prow[pidx][tid];
+      psr[tid] = hs->psrc[pidx][tid];
+    }
+    if (tid == 0) {
+      unsigned z = 0u;
+      for (int s2 = 0; s2 < nb; s2++)
+        if (p.zflag[j0 + s2]) z |= 1u << s2;
+      s_zm = z;
+      s_cnt = cnt;
+    }
+    if (nfar > 0)
+      for (int e = tid; e < nb * nb; e += T) {
+        const int r = e % nb, c = e / nb;
+        l11[r][c] = p.a[(j0 + r) + (int64_t)(j0 + c) * lda];
+      }
+    __syncthreads();
+    const unsigned zm = s_zm;
+    // ---- phase A: interchanges on columns [0, j0) and [fs, n); far U12 rows
+    const int64_t na = (int64_t)j0 + nfar;
+    for (int64_t q = (int64_t)h * (T / 32) + warp; q < na; q += (int64_t)nhc * (T / 32)) {
+      const int64_t c = q < j0 ? q : fs + (q - j0);
+      double* col = p.a + c * lda;
+      if (cnt > 0) {
+        const double v0 = lane < cnt ? col[psr[lane]] : 0.0;
+        __syncwarp();
+        if (lane < cnt) col[prw[lane]] = v0;
+        __syncwarp();
+      }
+      if (c >= fs) {
+        double xv = lane < nb ? col[j0 + lane] : 0.0;
+        for (int t = 0; t + 1 < nb; t++) {
+          const double xt = __shfl_sync(0xffffffffu, xv, t);
+          if (lane > t && lane < nb && !((zm >> t) & 1u)) xv = sub_mul_nofma(xv, l11[lane < W ? lane : 0][t], xt);
+        }
+        if (lane < nb) col[j0 + lane] = xv;
+        unsigned long long key = lane < nb ? vkey(fabs(xv)) : 0ull;
+        unsigned dummy = 0u;
+        warp_keymax(key, dummy);
+        if (lane == 0 && key) atomicMax(&hs->cmax[c], key);
+      }
+    }
+    __syncthreads();
+    if (nfar <= 0) {
+      if (tid == 0) red_release_add(&hs->fardone[pidx], 1u);
+      continue;
+    }
+    if (tid == 0) {
+      __threadfence();
+      red_release_add(&hs->u12done[pidx], 1u);
+      wait_geq(&hs->u12done[pidx], nhc);
+    }
+    __syncthreads();
+    for (int e = tid; e < nb * nfar; e += T) {  // far U12 rows -> shared memory
+      const int s2 = e % nb, c = e / nb;
+      u12[(size_t)s2 * nfar + c] = p.a[(j0 + s2) + (int64_t)(fs + c) * lda];
+    }
+    __syncthreads();
+    // ---- phase B: my block of rows >= ce, all far columns (16-column batches)
+    const int64_t nrow = m - ce;
+    const int64_t rbk = (nrow + nhc - 1) / nhc;
+    const int64_t iend = min(m, ce + (int64_t)(h + 1) * rbk);
+    for (int64_t i = ce + (int64_t)h * rbk + tid; i < iend; i += T) {
+      double lv[W];
+#pragma unroll
+      for (int s2 = 0; s2 < W; s2++) lv[s2] = s2 < nb ? p.a[i + (int64_t)(j0 + s2) * lda] : 0.0;
+      constexpr int CBH = 16;
+      for (int c0 = 0; c0 < nfar; c0 += CBH) {
+        double y[CBH];
+#pragma unroll
+        for (int q = 0; q < CBH; q++) y[q] = (c0 + q < nfar) ? p.a[i + (int64_t)(fs + c0 + q) * lda] : 0.0;
+#pragma unroll
+        for (int s2 = 0; s2 < W; s2++) {
+          if (s2 < nb && !((zm >> s2) & 1u)) {
+            const double* us = u12 + (size_t)s2 * nfar + c0;
+#pragma unroll
+            for (int q = 0; q < CBH; q++) y[q] = sub_mul_nofma(y[q], lv[s2], (c0 + q < nfar) ? us[q] : 0.0);
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < CBH; q++)
+          if (c0 + q < nfar) p.a[i + (int64_t)(fs + c0 + q) * lda] = y[q];
+      }
+    }
+    __syncthreads();
+    if (tid == 0) {
+      __threadfence();
+      red_release_add(&hs->fardone[pidx], 1u);
+    }
+  }
+}
+
+template <int RPT, int W>
+__global__ void __launch_bounds__(T, 1) lu_coop_kernel(const Args p) {
+  extern __shared__ __align__(16) double dyn[];
+  Handoff* hs = reinterpret_cast<Handoff*>(p.recg);
+  if (blockIdx.x < (unsigned)CS) panel_role<RPT, W>(p, hs, dyn);
+  else helper_role<W>(p, hs, dyn);
 }
 
 }  // namespace lufull
@@ -642,43 +833,60 @@ bool getrf_full_eligible(int64_t m, int64_t n, int cluster_max) {
   static int enabled = -1;
   if (enabled < 0) {
     const char* e = getenv("RLRA_B200_LU_FULL");
-    enabled = (e && e[0] == '1') ? 1 : 0;  // opt-in until it beats the blocked path
+    enabled = (e && e[0] == '0') ? 0 : 1;  // RLRA_B200_LU_FULL=0 selects the blocked path
   }
   return enabled && cluster_max >= lufull::CS && n >= 1 && m >= n && n <= lufull::MAXN &&
          m >= (int64_t)lufull::CS * 32 && m <= (int64_t)lufull::CS * lufull::T * lufull::MAXRPT;
 }
 
+size_t getrf_full_state_bytes() { return sizeof(lufull::Handoff); }
+
+// Cooperative launch of the panel cluster + NH helper clusters (returns 1 when
+// the device cannot hold a helper cluster next to the panel cluster: the
+// caller then uses the blocked path).
 template <int RPT, int W>
-static int launch_full(const lufull::Args& a, cudaStream_t st) {
-  const void* kern = (const void*)lufull::lu_full_kernel<RPT, W>;
+static int launch_full(lufull::Args a, cudaStream_t st) {
+  const void* kern = (const void*)lufull::lu_coop_kernel<RPT, W>;
   using PL = lufull::Plan<RPT, W>;
   const size_t dyn = PL::bytes(a.n);
   static std::mutex mu;
-  static bool done[64][lufull::MAXRPT + 1];
+  static int nclusters[64][lufull::MAXRPT + 1];
   int dev = 0;
   RLRA_CHECK_CUDA(cudaGetDevice(&dev));
-  {
-    std::lock_guard<std::mutex> lock(mu);
-    if (!done[dev & 63][RPT]) {
-      RLRA_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-      RLRA_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PL::max_bytes()));
-      done[dev & 63][RPT] = true;
-    }
-  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(lufull::CS);
   cfg.blockDim = dim3(lufull::T);
-  cfg.dynamicSmemBytes = dyn;
+  cfg.dynamicSmemBytes = PL::max_bytes();
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = lufull::CS;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeCooperative;
+  attr[1].val.cooperative = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  lufull::Args args = a;
-  void* kargs[] = {&args};
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    if (!nclusters[dev & 63][RPT]) {
+      RLRA_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+      RLRA_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PL::max_bytes()));
+      int ncl = 0;
+      if (cudaOccupancyMaxActiveClusters(&ncl, kern, &cfg) != cudaSuccess) ncl = 0;
+      cudaGetLastError();
+      nclusters[dev & 63][RPT] = ncl > 0 ? ncl : -1;
+    }
+  }
+  const int ncl = nclusters[dev & 63][RPT];
+  if (ncl < 2) return 1;
+  const int nh = ncl - 1 < 6 ? ncl - 1 : 6;  // helper clusters
+  a.nhelpers = (unsigned)(nh * lufull::CS);
+  RLRA_CHECK_CUDA(cudaMemsetAsync(a.recg, 0, sizeof(lufull::Handoff), st));
+  cfg.gridDim = dim3(lufull::CS * (1 + nh));
+  cfg.dynamicSmemBytes = dyn;
+  cfg.numAttrs = 2;
+  void* kargs[] = {&a};
   RLRA_CHECK_CUDA(cudaLaunchKernelExC(&cfg, kern, kargs));
   note_launch();
   return 0;
@@ -707,8 +915,8 @@ int getrf_full(double* a, int64_t lda, int64_t m, int64_t n, int64_t* piv, int64
     case 2: return launch_full<2, 16>(args, st);
     case 3: return launch_full<3, 16>(args, st);
     case 4: return launch_full<4, 16>(args, st);
-    case 5: return launch_full<5, 8>(args, st);
-    default: return launch_full<6, 8>(args, st);
+    case 5: return launch_full<5, 16>(args, st);
+    default: return launch_full<6, 16>(args, st);
   }
 }
 

@@ -37,15 +37,16 @@ int main(int argc, char** argv) {
   unsigned long long t0 = t[0];
   auto T = [&](int s) { return t[s] ? (t[s] - t0) / 1e3 : -1.0; };
   printf("panel: start | steps done | sync1 | sync2 | U12 | trailing   (us from panel 0 start, CTA 0)\n");
-  for (int p = 0; p * 6 + 5 < 64 && t[p * 6]; p++)
+  for (int p = 0; p * 6 + 5 < 64 && p < 10 && t[p * 6]; p++)
     printf("  %2d: %8.2f %8.2f %8.2f %8.2f %8.2f %8.2f   steps %.2f  inter %.2f\n", p, T(6 * p), T(6 * p + 1),
            T(6 * p + 2), T(6 * p + 3), T(6 * p + 4), T(6 * p + 5), T(6 * p + 1) - T(6 * p),
            (t[6 * p + 5] ? T(6 * p + 5) : T(6 * p + 2)) - T(6 * p + 1));
-  printf("steps of panel 0 (CTA 0 / 15, tid 0): pre-wait | got | decided | swapped | mult done\n");
+  printf("steps of panel 0 (CTA 0 / 15, tid 0): pre-wait got mult pre-bar post-red staged(w0) pushed bulk\n");
   for (int b : {0, 15})
-    for (int jj = 0; jj < 12; jj++) {
-      auto S = [&](int i) { unsigned long long v = t[b * 128 + 64 + 5 * jj + i]; return v ? (v - t0) / 1e3 : -1.0; };
-      printf("  cta %2d step %2d: %7.2f %7.2f %7.2f %7.2f %7.2f\n", b, jj, S(0), S(1), S(2), S(3), S(4));
+    for (int jj = 0; jj < 8; jj++) {
+      auto S = [&](int i) { unsigned long long v = t[b * 128 + 64 + 8 * jj + i]; return v ? (v - t0) / 1e3 : -1.0; };
+      printf("  cta %2d step %2d: %7.2f %7.2f %7.2f %7.2f %7.2f %7.2f %7.2f %7.2f\n", b, jj, S(0), S(1), S(2), S(3),
+             S(4), S(5), S(6), S(7));
     }
   return 0;
 }
