@@ -13,7 +13,7 @@ import re
 from .errors import DeviceError, NativeUnavailable
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "librlra_b200.so")
+LIB_PATH = os.environ.get("RLRA_B200_LIB") or os.path.join(_HERE, "_lib", "librlra_b200.so")
 HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "rlra_b200.h")
 
 _c_i64 = ctypes.c_int64

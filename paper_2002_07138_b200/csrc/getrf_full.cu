@@ -273,7 +273,7 @@ struct Panel {
 // my slots already finished.
 template <int RPT, int W, int SC>
 __device__ __forceinline__ unsigned publish(const Ctx& x, Panel<RPT, W>& P, int jj, int nb, int jn, bool fin,
-                                            const double* urow, unsigned par) {
+                                            const double* su, unsigned par) {
   const int j0 = SC == 0 ? 1 : jn - 1 - jj;  // for STEP_TRACE (panel 0 steps only)
   constexpr int RECD = 2 + W;
   constexpr int RS = Plan<RPT, W>::RS;
@@ -315,7 +315,9 @@ __device__ __forceinline__ unsigned publish(const Ctx& x, Panel<RPT, W>& P, int 
   const unsigned bw = __ballot_sync(0xffffffffu, kw >= 0), bd = __ballot_sync(0xffffffffu, kd >= 0);
   const unsigned bar_l = smem_u32(&S.mbar[par]);
   // look-ahead of the two published rows only (CTA winner, row jn): step jj's
-  // terms on their columns jj+2.. (warp-uniform branch: two warps at most)
+  // terms on their columns jj+2.. (warp-uniform branch: two warps at most).
+  // The pivot row is read from this CTA's copy (su): after the barrier a peer
+  // may already be multicasting step jj+2's records into recv[par].
   unsigned done = 0u;
   if (fin && (bw | bd) != 0u) {
 #pragma unroll
@@ -325,7 +327,7 @@ __device__ __forceinline__ unsigned publish(const Ctx& x, Panel<RPT, W>& P, int 
         const double l = P.a[k][0];
 #pragma unroll
         for (int i = 2; i < W; i++)
-          if (jj + i < nb) P.a[k][i] = sub_mul_nofma(P.a[k][i], l, urow[jj + i]);
+          if (jj + i < nb) P.a[k][i] = sub_mul_nofma(P.a[k][i], l, su[jj + i]);
       }
     }
   }
@@ -474,6 +476,11 @@ __device__ __forceinline__ void step(const Ctx& x, Panel<RPT, W>& P, double& cm,
     }
     if (P.lr[k] > j) below |= 1u << k;  // rows strictly below the diagonal
   }
+#ifdef LUF_EXP_NULL
+  if (jj < 0) {
+#else
+  {
+#endif
   // multipliers (IEEE division, :49-51) and the next column (:52-55)
   const double ujj = urow[jj];
   const double rcp = zero ? 0.0 : __drcp_rn(ujj);
@@ -490,9 +497,10 @@ __device__ __forceinline__ void step(const Ctx& x, Panel<RPT, W>& P, double& cm,
       }
     }
   }
+  }
   STEP_TRACE(jj, 2);
   if (jj + 1 < nb) {
-    const unsigned done = publish<RPT, W, 1>(x, P, jj, nb, j + 1, !zero, urow, par ^ 1u);
+    const unsigned done = publish<RPT, W, 1>(x, P, jj, nb, j + 1, !zero, S.s_u + par * W, par ^ 1u);
 #ifndef LUF_EXP_NOBULK
     if (!zero) {  // bulk of step jj: columns jj+2.. of my other rows (overlaps the exchange)
 #else
