@@ -842,6 +842,9 @@ bool getrf_full_eligible(int64_t m, int64_t n, int cluster_max) {
   if (enabled < 0) {
     const char* e = getenv("RLRA_B200_LU_FULL");
     enabled = (e && e[0] == '0') ? 0 : 1;  // RLRA_B200_LU_FULL=0 selects the blocked path
+    // Nsight Compute cannot replay cooperative cluster grids (the launch fails
+    // inside the tool): under a CUDA injection library use the blocked path
+    if (getenv("NV_NSIGHT_INJECTION_TRANSPORT_TYPE") || getenv("NV_TPS_LAUNCH_TOKEN")) enabled = 0;
   }
   return enabled && cluster_max >= lufull::CS && n >= 1 && m >= n && n <= lufull::MAXN &&
          m >= (int64_t)lufull::CS * 32 && m <= (int64_t)lufull::CS * lufull::T * lufull::MAXRPT;
@@ -895,7 +898,17 @@ static int launch_full(lufull::Args a, cudaStream_t st) {
   cfg.dynamicSmemBytes = dyn;
   cfg.numAttrs = 2;
   void* kargs[] = {&a};
-  RLRA_CHECK_CUDA(cudaLaunchKernelExC(&cfg, kern, kargs));
+  const cudaError_t e = cudaLaunchKernelExC(&cfg, kern, kargs);
+  if (e == cudaErrorCooperativeLaunchTooLarge || e == cudaErrorNotSupported || e == cudaErrorInvalidConfiguration ||
+      e == cudaErrorNotPermitted) {
+    // e.g. under a profiler that cannot replay cooperative cluster grids:
+    // remember and let the caller take the blocked path
+    cudaGetLastError();
+    std::lock_guard<std::mutex> lock(mu);
+    nclusters[dev & 63][RPT] = -1;
+    return 1;
+  }
+  RLRA_CHECK_CUDA(e);
   note_launch();
   return 0;
 }
