@@ -204,7 +204,7 @@ struct Plan {
   static constexpr int RS = T * RPT;  // row slots per CTA (slot = k * T + tid)
   static size_t bytes(int64_t n) {
     const size_t panel = (size_t)W * RS + (size_t)n + (size_t)W * W;
-    const size_t helper = (size_t)W * n;
+    const size_t helper = (size_t)W * W + (size_t)W * n;
     return (panel > helper ? panel : helper) * sizeof(double);
   }
   static size_t max_bytes() { return bytes(MAXN); }
@@ -219,7 +219,8 @@ struct Handoff {
   unsigned ready;            // panels whose L, U12 rows and permutation are published
   unsigned fardone[MAXP];    // helper CTAs done with panel b (interchanges + far update)
   unsigned u12done[MAXP];    // helper CTAs done with panel b's far U12 rows
-  unsigned pad[64 - 1 - 2 * MAXP];
+  unsigned nextdone[MAXP];   // helper CTAs done with the next panel's columns (update by panel b)
+  unsigned pad[64 - 1 - 3 * MAXP];
   unsigned long long cmax[MAXN];
   int64_t prow[MAXP][2 * 16], psrc[MAXP][2 * 16];
   int pcnt[MAXP];
@@ -628,81 +629,46 @@ __device__ void panel_role(const Args& p, Handoff* hs, double* dyn) {
       }
     }
     cluster.sync();  // (1) the whole panel at its logical rows, in global memory
-    if (b == 0 && tid == 0) {
-      __threadfence();
-      st_release(&hs->ready, (unsigned)pidx + 1);  // helpers may start on panel pidx
-    }
     FULL_TRACE(6 * pidx + 2);
     const int ce = j0 + nb;
-    if (ce >= n) break;
-    const int nbn = (int)min((int64_t)W, n - ce);
-    // ---- the next panel's columns: interchanges, U12, rank-nb update -> registers
-    if (pidx >= 1) {  // helpers done with panel pidx-1 (whose far columns include these)
-      if (tid == 0) wait_geq(&hs->fardone[pidx - 1], nhc);
-      __syncthreads();
-    }
-    const int cnt = S.pcnt;
-    if (b < nbn && warp == 0 && cnt > 0) {
-      double* col = p.a + (int64_t)(ce + b) * lda;
-      const double v0 = lane < cnt ? col[S.prow_src[lane]] : 0.0;
-      __syncwarp();
-      if (lane < cnt) col[S.prow_rows[lane]] = v0;
-    }
-    cluster.sync();  // (2) next columns interchanged
-    FULL_TRACE(6 * pidx + 3);
-    for (int e = tid; e < nb * nb; e += T) {
-      const int r = e % nb, c = e / nb;
-      S.l11[r][c] = p.a[(j0 + r) + (int64_t)(j0 + c) * lda];
-    }
-    unsigned zmask = 0u;
-    for (int s2 = 0; s2 < nb; s2++)
-      if (S.s_zf[s2]) zmask |= 1u << s2;
-    __syncthreads();
-    if (tid < nbn) {  // U12 of next column ce + tid (forward substitution, ascending steps)
-      const double* col = p.a + (int64_t)(ce + tid) * lda + j0;
-      double* uc = x.s_u12 + tid;
-      double mx = __longlong_as_double((long long)hs->cmax[ce + tid]);  // far U12 of earlier panels
-      if (mx == 0.0 && hs->cmax[ce + tid] == 0ull) mx = -1.0;
-#pragma unroll 1
-      for (int s2 = 0; s2 < nb; s2++) {
-        double acc = col[s2];
-#pragma unroll 4
-        for (int t = 0; t < s2; t++)
-          if (!((zmask >> t) & 1u)) acc = sub_mul_nofma(acc, S.l11[s2][t], uc[t * W]);
-        uc[s2 * W] = acc;
-        mx = fmax(mx, fabs(acc));
+    const int nbn = ce < n ? (int)min((int64_t)W, n - ce) : 0;
+    if (nbn > 0) {
+      // the next panel's columns: helpers finished panel pidx-1's far update
+      // of them; apply this panel's interchanges (one column per CTA)
+      if (pidx >= 1) {
+        if (tid == 0) wait_geq(&hs->fardone[pidx - 1], nhc);
+        __syncthreads();
       }
-      x.s_cmab[ce + tid] = mx;
+      const int cnt = S.pcnt;
+      if (b < nbn && warp == 0 && cnt > 0) {
+        double* col = p.a + (int64_t)(ce + b) * lda;
+        const double v0 = lane < cnt ? col[S.prow_src[lane]] : 0.0;
+        __syncwarp();
+        if (lane < cnt) col[S.prow_rows[lane]] = v0;
+      }
+      cluster.sync();  // (2) next columns interchanged
     }
+    if (b == 0 && tid == 0) {
+      __threadfence();
+      st_release(&hs->ready, (unsigned)pidx + 1);  // helpers: next columns, far columns, L columns
+    }
+    FULL_TRACE(6 * pidx + 3);
+    if (nbn == 0) break;
+    // ---- next panel: the helpers form its U12 rows and update its rows below
+    // (rank-nb with this panel's multipliers); load my physical rows >= ce
+    if (tid == 0) wait_geq(&hs->nextdone[pidx], nhc);
     __syncthreads();
-    for (int e = tid; e < nb * nbn; e += T) {  // owners store the U12 rows
-      const int s2 = e % nb, c = e / nb;
-      const int64_t g = j0 + s2;
-      if (g >= x.rb && g < x.re) p.a[g + (int64_t)(ce + c) * lda] = x.s_u12[s2 * W + c];
-    }
-    // my physical rows >= ce: next columns (registers) minus L21 (global -> sL) * U12
 #pragma unroll
     for (int k = 0; k < RPT; k++) {
       const int64_t g = x.g0 + (int64_t)k * T;
       const bool act = k < x.nk && g >= ce;
       P.lr[k] = act ? (int)g : -1;
-      double* lk = x.sL + k * T + tid;
-      if (act) {
-#pragma unroll
-        for (int s2 = 0; s2 < W; s2++)
-          if (s2 < nb) lk[(size_t)s2 * RS] = p.a[g + (int64_t)(j0 + s2) * lda];
-      }
 #pragma unroll
       for (int c = 0; c < W; c++) P.a[k][c] = (act && c < nbn) ? p.a[g + (int64_t)(ce + c) * lda] : 0.0;
-      if (act) {
-        for (int s2 = 0; s2 < nb; s2++) {
-          if ((zmask >> s2) & 1u) continue;
-          const double l = lk[(size_t)s2 * RS];
-          const double* us = x.s_u12 + s2 * W;
-#pragma unroll
-          for (int c = 0; c < W; c++) P.a[k][c] = sub_mul_nofma(P.a[k][c], l, c < nbn ? us[c] : 0.0);
-        }
-      }
+    }
+    if (tid < nbn) {  // colmax of the next columns over the rows above: every U12 row so far
+      const unsigned long long cb = hs->cmax[ce + tid];
+      x.s_cmab[ce + tid] = cb ? __longlong_as_double((long long)cb) : -1.0;
     }
     __syncthreads();
     FULL_TRACE(6 * pidx + 5);
@@ -719,7 +685,8 @@ __device__ void helper_role(const Args& p, Handoff* hs, double* dyn) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const unsigned h = blockIdx.x - CS, nhc = p.nhelpers;
   const int64_t m = p.m, n = p.n, lda = p.lda;
-  double* u12 = dyn;  // [W][n - fs]
+  double* u12 = dyn;              // [W][W] U12 of the next panel's columns
+  double* u12f = dyn + W * W;     // [W][n - fs] U12 of the far columns
   const int np = (int)((n + W - 1) / W);
   for (int pidx = 0; pidx < np; pidx++) {
     const int j0 = pidx * W;
@@ -738,12 +705,12 @@ __device__ void helper_role(const Args& p, Handoff* hs, double* dyn) {
       prw[tid] = hs->prow[pidx][tid];
       psr[tid] = hs->psrc[pidx][tid];
     }
-    if (tid == 0) {
-      unsigned z = 0u;
-      for (int s2 = 0; s2 < nb; s2++)
-        if (p.zflag[j0 + s2]) z |= 1u << s2;
-      s_zm = z;
-      s_cnt = cnt;
+    if (warp == 0) {  // zero-pivot mask: one load per lane
+      const unsigned z = __ballot_sync(0xffffffffu, lane < nb && p.zflag[j0 + lane] != 0);
+      if (lane == 0) {
+        s_zm = z;
+        s_cnt = cnt;
+      }
     }
     if (nfar > 0)
       for (int e = tid; e < nb * nb; e += T) {
@@ -752,6 +719,68 @@ __device__ void helper_role(const Args& p, Handoff* hs, double* dyn) {
       }
     __syncthreads();
     const unsigned zm = s_zm;
+    // ---- phase N: the next panel's columns [ce, fs) (already interchanged by
+    // the panel cluster): U12 rows (every helper, half-warp per column), the
+    // rank-nb update of my block of rows >= ce; helper 0 publishes U12 + colmax
+    if (nbn > 0) {
+      if (nfar <= 0)  // L11 not loaded above
+        for (int e = tid; e < nb * nb; e += T) {
+          const int r = e % nb, c = e / nb;
+          l11[r][c] = p.a[(j0 + r) + (int64_t)(j0 + c) * lda];
+        }
+      __syncthreads();
+      {
+        const int cw = warp * 2 + (lane >> 4), l = lane & 15;
+        double xv = 0.0;
+        if (cw < nbn && l < nb) xv = p.a[(int64_t)(ce + cw) * lda + j0 + l];
+        for (int t = 0; t + 1 < nb; t++) {
+          const double xt = __shfl_sync(0xffffffffu, xv, t, 16);
+          if (l > t && l < nb && !((zm >> t) & 1u)) xv = sub_mul_nofma(xv, l11[l][t], xt);
+        }
+        if (cw < nbn && l < nb) u12[(size_t)l * W + cw] = xv;
+      }
+      __syncthreads();
+      if (h == 0) {
+        for (int e = tid; e < nb * nbn; e += T) {
+          const int s2 = e % nb, c = e / nb;
+          p.a[(j0 + s2) + (int64_t)(ce + c) * lda] = u12[(size_t)s2 * W + c];
+        }
+        if (tid < nbn) {
+          unsigned long long key = 0ull;
+          for (int s2 = 0; s2 < nb; s2++) {
+            const unsigned long long kk = vkey(fabs(u12[(size_t)s2 * W + tid]));
+            key = kk > key ? kk : key;
+          }
+          if (key) atomicMax(&hs->cmax[ce + tid], key);
+        }
+      }
+      const int64_t nrow = m - ce;
+      const int64_t rbk = (nrow + nhc - 1) / nhc;
+      const int64_t iend = min(m, ce + (int64_t)(h + 1) * rbk);
+      for (int64_t i = ce + (int64_t)h * rbk + tid; i < iend; i += T) {
+        double y[W];
+#pragma unroll
+        for (int c = 0; c < W; c++) y[c] = c < nbn ? p.a[i + (int64_t)(ce + c) * lda] : 0.0;
+        double lv[W];  // all loads in flight before the update
+#pragma unroll
+        for (int s2 = 0; s2 < W; s2++) lv[s2] = s2 < nb ? p.a[i + (int64_t)(j0 + s2) * lda] : 0.0;
+#pragma unroll
+        for (int s2 = 0; s2 < W; s2++) {
+          if (s2 >= nb || ((zm >> s2) & 1u)) continue;
+          const double* us = u12 + (size_t)s2 * W;
+#pragma unroll
+          for (int c = 0; c < W; c++) y[c] = sub_mul_nofma(y[c], lv[s2], c < nbn ? us[c] : 0.0);
+        }
+#pragma unroll
+        for (int c = 0; c < W; c++)
+          if (c < nbn) p.a[i + (int64_t)(ce + c) * lda] = y[c];
+      }
+      __syncthreads();
+      if (tid == 0) {
+        __threadfence();
+        red_release_add(&hs->nextdone[pidx], 1u);
+      }
+    }
     // ---- phase A: interchanges on columns [0, j0) and [fs, n); far U12 rows
     const int64_t na = (int64_t)j0 + nfar;
     for (int64_t q = (int64_t)h * (T / 32) + warp; q < na; q += (int64_t)nhc * (T / 32)) {
@@ -789,7 +818,7 @@ __device__ void helper_role(const Args& p, Handoff* hs, double* dyn) {
     __syncthreads();
     for (int e = tid; e < nb * nfar; e += T) {  // far U12 rows -> shared memory
       const int s2 = e % nb, c = e / nb;
-      u12[(size_t)s2 * nfar + c] = p.a[(j0 + s2) + (int64_t)(fs + c) * lda];
+      u12f[(size_t)s2 * nfar + c] = p.a[(j0 + s2) + (int64_t)(fs + c) * lda];
     }
     __syncthreads();
     // ---- phase B: my block of rows >= ce, all far columns (16-column batches)
@@ -808,7 +837,7 @@ __device__ void helper_role(const Args& p, Handoff* hs, double* dyn) {
 #pragma unroll
         for (int s2 = 0; s2 < W; s2++) {
           if (s2 < nb && !((zm >> s2) & 1u)) {
-            const double* us = u12 + (size_t)s2 * nfar + c0;
+            const double* us = u12f + (size_t)s2 * nfar + c0;
 #pragma unroll
             for (int q = 0; q < CBH; q++) y[q] = sub_mul_nofma(y[q], lv[s2], (c0 + q < nfar) ? us[q] : 0.0);
           }
