@@ -51,10 +51,8 @@ __global__ void __launch_bounds__(CHOL_THREADS, 1)
     s_rmax = 0.0;
   }
   __syncthreads();
-  for (int k0 = 0; k0 < l; k0 += CHOL_NB) {
-    const int b = min(CHOL_NB, l - k0);
-    // ---- (1) diagonal block: lane c holds column k0 + c
-    if (warp == 0) {
+  // (1) factor + invert the diagonal block at k0 (warp 0): lane c holds column k0 + c
+  auto diag = [&](const int k0, const int b) {
       double gg[CHOL_NB];
 #pragma unroll
       for (int i = 0; i < CHOL_NB; i++) gg[i] = (lane < b && i <= lane) ? P[pk(k0 + i, k0 + lane)] : 0.0;
@@ -110,8 +108,11 @@ __global__ void __launch_bounds__(CHOL_THREADS, 1)
         s_rmin = fmin(s_rmin, rmin);
         s_rmax = fmax(s_rmax, rmax);
       }
-    }
-    __syncthreads();
+  };
+  if (warp == 0) diag(0, min(CHOL_NB, l));
+  __syncthreads();
+  for (int k0 = 0; k0 < l; k0 += CHOL_NB) {
+    const int b = min(CHOL_NB, l - k0);
     if (s_bad) break;
     const int c0 = k0 + b, m = l - c0;
     if (m <= 0) break;
@@ -130,39 +131,63 @@ __global__ void __launch_bounds__(CHOL_THREADS, 1)
       if (lane < b) P[cj + k0 + lane] = acc;
     }
     __syncthreads();
-    // ---- (3) trailing triangle -= R(k0.., :)^T R(k0.., :) in 4 x 4 tiles
-    const int mt = (m + 3) >> 2;
-    const int ntiles = mt * (mt + 1) / 2;
-    for (int t = tid; t < ntiles; t += CHOL_THREADS) {
-      int tb = (int)((sqrtf(8.0f * (float)t + 1.0f) - 1.0f) * 0.5f);
-      while (tb * (tb + 1) / 2 > t) --tb;
-      while ((tb + 1) * (tb + 2) / 2 <= t) ++tb;
-      const int ta = t - tb * (tb + 1) / 2;
-      const int ja = c0 + 4 * ta, jb = c0 + 4 * tb;
-      double acc[4][4];
+    // ---- (3) trailing triangle -= R(k0.., :)^T R(k0.., :).  Look-ahead: warp 0
+    // updates the NEXT diagonal block and factors it while warps 1.. update
+    // the rest of the triangle in 4 x 4 tiles.
+    const int bn = min(CHOL_NB, m);
+    if (warp == 0) {
+      const int ne = bn * (bn + 1) / 2;
+      for (int e = lane; e < ne; e += 32) {
+        int jj = (int)((sqrtf(8.0f * (float)e + 1.0f) - 1.0f) * 0.5f);
+        while (jj * (jj + 1) / 2 > e) --jj;
+        while ((jj + 1) * (jj + 2) / 2 <= e) ++jj;
+        const int i = c0 + (e - jj * (jj + 1) / 2), j = c0 + jj;
+        double acc = 0.0;
+        for (int s2 = 0; s2 < b; s2++) acc = fma(P[pk(k0 + s2, i)], P[pk(k0 + s2, j)], acc);
+        P[pk(i, j)] -= acc;
+      }
+      __syncwarp();
+      diag(c0, bn);
+    } else {
+#ifdef CHOL_EXP_NOTRAIL
+      const int mt = 0;
+#else
+      const int mt = (m + 3) >> 2;
+#endif
+      const int ntiles = mt * (mt + 1) / 2;
+      const int lim = c0 + bn;  // entries with i, j < lim belong to warp 0
+      for (int t = tid - 32; t < ntiles; t += CHOL_THREADS - 32) {
+        int tb = (int)((sqrtf(8.0f * (float)t + 1.0f) - 1.0f) * 0.5f);
+        while (tb * (tb + 1) / 2 > t) --tb;
+        while ((tb + 1) * (tb + 2) / 2 <= t) ++tb;
+        const int ta = t - tb * (tb + 1) / 2;
+        const int ja = c0 + 4 * ta, jb = c0 + 4 * tb;
+        if (jb + 3 < lim) continue;  // whole tile inside the next diagonal block
+        double acc[4][4];
 #pragma unroll
-      for (int q = 0; q < 4; q++)
+        for (int q = 0; q < 4; q++)
 #pragma unroll
-        for (int w = 0; w < 4; w++) acc[q][w] = 0.0;
-      for (int s2 = 0; s2 < b; s2++) {
-        double ra[4], rb[4];
+          for (int w = 0; w < 4; w++) acc[q][w] = 0.0;
+        for (int s2 = 0; s2 < b; s2++) {
+          double ra[4], rb[4];
 #pragma unroll
-        for (int q = 0; q < 4; q++) {
-          ra[q] = (ja + q < l) ? P[pk(k0 + s2, ja + q)] : 0.0;
-          rb[q] = (jb + q < l) ? P[pk(k0 + s2, jb + q)] : 0.0;
+          for (int q = 0; q < 4; q++) {
+            ra[q] = (ja + q < l) ? P[pk(k0 + s2, ja + q)] : 0.0;
+            rb[q] = (jb + q < l) ? P[pk(k0 + s2, jb + q)] : 0.0;
+          }
+#pragma unroll
+          for (int q = 0; q < 4; q++)
+#pragma unroll
+            for (int w = 0; w < 4; w++) acc[q][w] = fma(ra[q], rb[w], acc[q][w]);
         }
 #pragma unroll
         for (int q = 0; q < 4; q++)
 #pragma unroll
-          for (int w = 0; w < 4; w++) acc[q][w] = fma(ra[q], rb[w], acc[q][w]);
+          for (int w = 0; w < 4; w++) {
+            const int i = ja + q, j = jb + w;
+            if (i <= j && j < l && !(j < lim)) P[pk(i, j)] -= acc[q][w];
+          }
       }
-#pragma unroll
-      for (int q = 0; q < 4; q++)
-#pragma unroll
-        for (int w = 0; w < 4; w++) {
-          const int i = ja + q, j = jb + w;
-          if (i <= j && j < l) P[pk(i, j)] -= acc[q][w];
-        }
     }
     __syncthreads();
   }
