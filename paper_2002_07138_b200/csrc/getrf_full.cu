@@ -155,7 +155,7 @@ __device__ __forceinline__ void static_for(F&& f) {
 struct Shared {
   __align__(16) double recv[2 * CS * RECD];  // every CTA's record, multicast in (by step parity)
   __align__(16) double recv_diag[2 * W];     // current diagonal row (pre-swap), multicast in
-  double s_u[2 * W];                         // local copy of the step's pivot row (post-barrier readers)
+  double s_u[2 * 2 * W];                     // local copy of the step's pivot row, zero beyond nb (post-barrier readers)
   double l11[W][W + 1];
   unsigned long long wkey[NW];
   unsigned widx[NW];
@@ -328,7 +328,7 @@ __device__ __forceinline__ unsigned publish(const Ctx& x, Panel<RPT, W>& P, int 
         const double l = P.a[k][0];
 #pragma unroll
         for (int i = 2; i < W; i++)
-          if (jj + i < nb) P.a[k][i] = sub_mul_nofma(P.a[k][i], l, su[jj + i]);
+          P.a[k][i] = sub_mul_nofma(P.a[k][i], l, su[jj + i]);  // columns >= nb: padding, u = 0
       }
     }
   }
@@ -461,7 +461,7 @@ __device__ __forceinline__ void step(const Ctx& x, Panel<RPT, W>& P, double& cm,
   const int prow = zero ? j : idx;
   const double* urow = zero ? S.recv_diag + (size_t)par * W : rec + (rl & 31u) * RECD + 2;
   if (x.lane > jj && x.lane < W) cm = fmax(cm, fabs(urow[x.lane]));  // row j joins the rows above
-  if (x.tid < W) S.s_u[par * W + x.tid] = urow[x.tid];
+  if (x.tid < 2 * W) S.s_u[par * 2 * W + x.tid] = x.tid < nb ? urow[x.tid] : 0.0;
   if (x.tid == 0) {
     S.s_ipiv[jj] = prow;
     S.s_zf[jj] = zero ? 1 : 0;
@@ -501,21 +501,20 @@ __device__ __forceinline__ void step(const Ctx& x, Panel<RPT, W>& P, double& cm,
   }
   STEP_TRACE(jj, 2);
   if (jj + 1 < nb) {
-    const unsigned done = publish<RPT, W, 1>(x, P, jj, nb, j + 1, !zero, S.s_u + par * W, par ^ 1u);
+    const unsigned done = publish<RPT, W, 1>(x, P, jj, nb, j + 1, !zero, S.s_u + par * 2 * W, par ^ 1u);
 #ifndef LUF_EXP_NOBULK
     if (!zero) {  // bulk of step jj: columns jj+2.. of my other rows (overlaps the exchange)
 #else
     if (false) {
 #endif
-      const double* su = S.s_u + par * W + jj;
+      const double* su = S.s_u + par * 2 * W + jj;  // zero beyond nb: padding columns stay inert
       const unsigned bm = below & ~done;
 #pragma unroll
-      for (int i = 2; i < W; i++) {
-        if (jj + i < nb) {
-          const double uc = su[i];
+      for (int k = 0; k < RPT; k++) {
+        if ((bm >> k) & 1u) {
+          const double l = P.a[k][0];
 #pragma unroll
-          for (int k = 0; k < RPT; k++)
-            if ((bm >> k) & 1u) P.a[k][i] = sub_mul_nofma(P.a[k][i], P.a[k][0], uc);
+          for (int i = 2; i < W; i++) P.a[k][i] = sub_mul_nofma(P.a[k][i], l, su[i]);
         }
       }
     }
