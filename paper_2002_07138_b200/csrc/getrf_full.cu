@@ -220,7 +220,8 @@ struct Handoff {
   unsigned fardone[MAXP];    // helper CTAs done with panel b (interchanges + far update)
   unsigned u12done[MAXP];    // helper CTAs done with panel b's far U12 rows
   unsigned nextdone[MAXP];   // helper CTAs done with the next panel's columns (update by panel b)
-  unsigned pad[64 - 1 - 3 * MAXP];
+  unsigned u12read[MAXP];    // helper CTAs (other than 0) done reading the next columns' rows j0..ce
+  unsigned pad[128 - 1 - 4 * MAXP];
   unsigned long long cmax[MAXN];
   int64_t prow[MAXP][2 * 16], psrc[MAXP][2 * 16];
   int pcnt[MAXP];
@@ -739,20 +740,9 @@ __device__ void helper_role(const Args& p, Handoff* hs, double* dyn) {
         if (cw < nbn && l < nb) u12[(size_t)l * W + cw] = xv;
       }
       __syncthreads();
-      if (h == 0) {
-        for (int e = tid; e < nb * nbn; e += T) {
-          const int s2 = e % nb, c = e / nb;
-          p.a[(j0 + s2) + (int64_t)(ce + c) * lda] = u12[(size_t)s2 * W + c];
-        }
-        if (tid < nbn) {
-          unsigned long long key = 0ull;
-          for (int s2 = 0; s2 < nb; s2++) {
-            const unsigned long long kk = vkey(fabs(u12[(size_t)s2 * W + tid]));
-            key = kk > key ? kk : key;
-          }
-          if (key) atomicMax(&hs->cmax[ce + tid], key);
-        }
-      }
+      // helper 0 overwrites rows j0..ce of the next columns with U12 only
+      // after every other helper has read the (interchanged) originals
+      if (h != 0 && tid == 0) red_release_add(&hs->u12read[pidx], 1u);
       const int64_t nrow = m - ce;
       const int64_t rbk = (nrow + nhc - 1) / nhc;
       const int64_t iend = min(m, ce + (int64_t)(h + 1) * rbk);
@@ -773,6 +763,22 @@ __device__ void helper_role(const Args& p, Handoff* hs, double* dyn) {
 #pragma unroll
         for (int c = 0; c < W; c++)
           if (c < nbn) p.a[i + (int64_t)(ce + c) * lda] = y[c];
+      }
+      if (h == 0) {
+        if (tid == 0) wait_geq(&hs->u12read[pidx], nhc - 1);
+        __syncthreads();
+        for (int e = tid; e < nb * nbn; e += T) {
+          const int s2 = e % nb, c = e / nb;
+          p.a[(j0 + s2) + (int64_t)(ce + c) * lda] = u12[(size_t)s2 * W + c];
+        }
+        if (tid < nbn) {
+          unsigned long long key = 0ull;
+          for (int s2 = 0; s2 < nb; s2++) {
+            const unsigned long long kk = vkey(fabs(u12[(size_t)s2 * W + tid]));
+            key = kk > key ? kk : key;
+          }
+          if (key) atomicMax(&hs->cmax[ce + tid], key);
+        }
       }
       __syncthreads();
       if (tid == 0) {
