@@ -113,6 +113,28 @@ RLRA_B200_API size_t rlra_b200_oz_gemm_workspace(int trans, int64_t m, int64_t n
 RLRA_B200_API int rlra_b200_oz_gemm(int trans, const void* prep, int64_t m, int64_t n, int nmod, const double* b,
                                     int64_t ldb, int64_t ncols, double* c, int64_t ldc, void* ws,
                                     size_t ws_bytes, void* stream);
+/* Block-wise pass products for operands whose residues do not fit next to A
+ * (or whose K exceeds 133144): A is cut into rectangular blocks that share
+ * ONE scale eA (rlra_b200_oz_scale over the whole A, passed to
+ * rlra_b200_oz_prep_ex) and one per-column scale eB of the whole B
+ * (rlra_b200_oz_bscale, int[rlra_b200_oz_cols_pad(ncols)]).  A K-split
+ * product accumulates its residues exactly across calls
+ * (RLRA_B200_OZ_ACCUMULATE on every call but the first, RLRA_B200_OZ_NO_CRT on
+ * every call but the last, the same workspace throughout), so the result is
+ * bit-identical to the one-block product. */
+#define RLRA_B200_OZ_ACCUMULATE 1
+#define RLRA_B200_OZ_NO_CRT 2
+RLRA_B200_API size_t rlra_b200_oz_scale_workspace(int64_t m, int64_t n);
+RLRA_B200_API int rlra_b200_oz_scale(const double* a, int64_t lda, int64_t m, int64_t n, int nmod, int* e_a,
+                                     void* ws, size_t ws_bytes, void* stream);
+RLRA_B200_API int rlra_b200_oz_prep_ex(const double* a, int64_t lda, int64_t m, int64_t n, int nmod,
+                                       const int* e_a, void* prep, size_t prep_bytes, void* stream);
+RLRA_B200_API int64_t rlra_b200_oz_cols_pad(int64_t ncols);
+RLRA_B200_API int rlra_b200_oz_bscale(const double* b, int64_t ldb, int64_t k, int64_t ncols, int nmod, int* e_b,
+                                      void* stream);
+RLRA_B200_API int rlra_b200_oz_gemm_ex(int trans, const void* prep, int64_t m, int64_t n, int nmod,
+                                       const double* b, int64_t ldb, int64_t ncols, double* c, int64_t ldc,
+                                       void* ws, size_t ws_bytes, const int* e_b, int flags, void* stream);
 
 /* ---- K4: Householder QR (m >= n) + explicit thin Q --------------------- */
 RLRA_B200_API size_t rlra_b200_geqrf_workspace(int64_t m, int64_t n);

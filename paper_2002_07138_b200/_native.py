@@ -45,6 +45,13 @@ SIGNATURES = {
     "rlra_b200_oz_gemm_workspace": (_c_sz, [_c_i, _c_i64, _c_i64, _c_i64, _c_i]),
     "rlra_b200_oz_gemm": (_c_i, [_c_i, _c_p, _c_i64, _c_i64, _c_i, _c_p, _c_i64, _c_i64, _c_p, _c_i64,
                                  _c_p, _c_sz, _c_p]),
+    "rlra_b200_oz_scale_workspace": (_c_sz, [_c_i64, _c_i64]),
+    "rlra_b200_oz_scale": (_c_i, [_c_p, _c_i64, _c_i64, _c_i64, _c_i, _c_p, _c_p, _c_sz, _c_p]),
+    "rlra_b200_oz_prep_ex": (_c_i, [_c_p, _c_i64, _c_i64, _c_i64, _c_i, _c_p, _c_p, _c_sz, _c_p]),
+    "rlra_b200_oz_cols_pad": (_c_i64, [_c_i64]),
+    "rlra_b200_oz_bscale": (_c_i, [_c_p, _c_i64, _c_i64, _c_i64, _c_i, _c_p, _c_p]),
+    "rlra_b200_oz_gemm_ex": (_c_i, [_c_i, _c_p, _c_i64, _c_i64, _c_i, _c_p, _c_i64, _c_i64, _c_p, _c_i64,
+                                    _c_p, _c_sz, _c_p, _c_i, _c_p]),
     "rlra_b200_geqrf_workspace": (_c_sz, [_c_i64, _c_i64]),
     "rlra_b200_geqrf": (_c_i, [_c_p, _c_i64, _c_i64, _c_i64, _c_p, _c_p, _c_sz, _c_p]),
     "rlra_b200_orgqr": (_c_i, [_c_p, _c_i64, _c_i64, _c_i64, _c_p, _c_i64, _c_p, _c_sz, _c_p]),

@@ -103,6 +103,16 @@ int oz_prep(const double* a, int64_t lda, int64_t m, int64_t n, int nmod, void* 
 size_t oz_gemm_workspace(int trans, int64_t m, int64_t n, int64_t ncols, int nmod);
 int oz_gemm(int trans, const void* prep, int64_t m, int64_t n, int nmod, const double* b, int64_t ldb,
             int64_t ncols, double* c, int64_t ldc, void* ws, size_t ws_bytes, cudaStream_t st);
+size_t oz_scale_workspace(int64_t m, int64_t n);
+int oz_scale(const double* a, int64_t lda, int64_t m, int64_t n, int nmod, int* e_a, void* ws, size_t ws_bytes,
+             cudaStream_t st);
+int oz_prep_ex(const double* a, int64_t lda, int64_t m, int64_t n, int nmod, const int* e_a_ext, void* prep,
+               size_t prep_bytes, cudaStream_t st);
+int64_t oz_cols_pad(int64_t ncols);
+int oz_bscale(const double* b, int64_t ldb, int64_t k, int64_t ncols, int nmod, int* e_b, cudaStream_t st);
+int oz_gemm_ex(int trans, const void* prep, int64_t m, int64_t n, int nmod, const double* b, int64_t ldb,
+               int64_t ncols, double* c, int64_t ldc, void* ws, size_t ws_bytes, const int* e_b_ext, int flags,
+               cudaStream_t st);
 size_t normal_workspace_bytes(int64_t N);
 int64_t normal_stream_words(int64_t N);
 int64_t normal_tail_cap(int64_t N);
@@ -250,6 +260,32 @@ int rlra_b200_oz_gemm(int trans, const void* prep, int64_t m, int64_t n, int nmo
                       int64_t ldb, int64_t ncols, double* c, int64_t ldc, void* ws, size_t ws_bytes,
                       void* stream) {
   return oz_gemm(trans, prep, m, n, nmod, b, ldb, ncols, c, ldc, ws, ws_bytes, static_cast<cudaStream_t>(stream));
+}
+
+size_t rlra_b200_oz_scale_workspace(int64_t m, int64_t n) { return oz_scale_workspace(m, n); }
+
+int rlra_b200_oz_scale(const double* a, int64_t lda, int64_t m, int64_t n, int nmod, int* e_a, void* ws,
+                       size_t ws_bytes, void* stream) {
+  return oz_scale(a, lda, m, n, nmod, e_a, ws, ws_bytes, static_cast<cudaStream_t>(stream));
+}
+
+int rlra_b200_oz_prep_ex(const double* a, int64_t lda, int64_t m, int64_t n, int nmod, const int* e_a,
+                         void* prep, size_t prep_bytes, void* stream) {
+  return oz_prep_ex(a, lda, m, n, nmod, e_a, prep, prep_bytes, static_cast<cudaStream_t>(stream));
+}
+
+int64_t rlra_b200_oz_cols_pad(int64_t ncols) { return oz_cols_pad(ncols); }
+
+int rlra_b200_oz_bscale(const double* b, int64_t ldb, int64_t k, int64_t ncols, int nmod, int* e_b,
+                        void* stream) {
+  return oz_bscale(b, ldb, k, ncols, nmod, e_b, static_cast<cudaStream_t>(stream));
+}
+
+int rlra_b200_oz_gemm_ex(int trans, const void* prep, int64_t m, int64_t n, int nmod, const double* b,
+                         int64_t ldb, int64_t ncols, double* c, int64_t ldc, void* ws, size_t ws_bytes,
+                         const int* e_b, int flags, void* stream) {
+  return oz_gemm_ex(trans, prep, m, n, nmod, b, ldb, ncols, c, ldc, ws, ws_bytes, e_b, flags,
+                    static_cast<cudaStream_t>(stream));
 }
 
 size_t rlra_b200_gemm_workspace(int64_t m, int64_t n, int64_t k) { return gemm_workspace_bytes(m, n, k); }

@@ -415,6 +415,7 @@ struct GemmArgs {
   int64_t nmb;  // 256-row blocks
   uint8_t* out;  // t[l][col][row], rows padded to nmb*256, cols to ng*n_g
   int nmod;
+  int accum;  // 1: t = (t + C_l) mod m_l (K split over several calls), 0: t = C_l mod m_l
   int mods[kMaxMod];
   int ys[kMaxMod];  // CRT weights (M/m_l)^-1 mod m_l, folded into the epilogue
 };
@@ -600,12 +601,24 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_i8_kernel(const GemmArgs
           OZ_LD32(taddr, v);
           asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
 #pragma unroll
-          for (int e = 0; e < 32; ++e) {
-            const double cv = (double)(int)v[e] * yl;  // exact: |c y| < 2^39
-            double r = fma(-floor(cv * inv), md, cv);
-            if (r < 0.0) r += md;
-            if (r >= md) r -= md;
-            orow[(size_t)(cc + e) * rows_pad] = (uint8_t)(int)r;
+          for (int h = 0; h < 32; h += 16) {
+            unsigned prev[16];  // accumulate: previous K blocks' residues, 16 loads in flight at once
+            if (g.accum) {
+#pragma unroll
+              for (int e = 0; e < 16; ++e) prev[e] = orow[(size_t)(cc + h + e) * rows_pad];
+            }
+#pragma unroll
+            for (int e = 0; e < 16; ++e) {
+              const double cv = (double)(int)v[h + e] * yl;  // exact: |c y| < 2^39
+              double r = fma(-floor(cv * inv), md, cv);
+              if (r < 0.0) r += md;
+              if (r >= md) r -= md;
+              if (g.accum) {  // exact modular sum with the previous K blocks
+                r += (double)prev[e];
+                if (r >= md) r -= md;
+              }
+              orow[(size_t)(cc + h + e) * rows_pad] = (uint8_t)(int)r;
+            }
           }
         }
       }
@@ -714,10 +727,13 @@ static GemmLayout gemm_layout(const PrepLayout& p, int trans, int64_t ncols, int
   g.nmb = (trans ? p.njb : p.nib) / 2;
   g.rows_pad = g.nmb * 256;
   g.cols_pad = (int64_t)g.ng * g.n_g;
+  // t first: its offset depends only on the output block, so a K-split
+  // sequence of calls (accumulating t) may pass workspaces sized for its
+  // largest K block
   g.off_eb = 0;
-  g.off_b = (((size_t)g.cols_pad * sizeof(int)) + 1023) & ~size_t(1023);
-  g.off_t = g.off_b + (size_t)nmod * g.cols_pad * g.nkb * kTile;
-  g.off_tab = g.off_t + (size_t)nmod * g.cols_pad * g.rows_pad;
+  g.off_t = (((size_t)g.cols_pad * sizeof(int)) + 1023) & ~size_t(1023);
+  g.off_b = (g.off_t + (size_t)nmod * g.cols_pad * g.rows_pad + 1023) & ~size_t(1023);
+  g.off_tab = g.off_b + (size_t)nmod * g.cols_pad * g.nkb * kTile;
   g.total = g.off_tab;
   return g;
 }
@@ -734,8 +750,8 @@ static void launch_residue_a(const double* a, int64_t lda, int64_t m, int64_t n,
 }
 template <int NMOD>
 static void launch_residue_b(const double* b, int64_t ldb, int64_t k, int64_t ncols, const GemmLayout& g, int pb,
-                             int* e_b, int8_t* tiles, cudaStream_t st) {
-  bscale_kernel<<<(unsigned)g.cols_pad, 256, 0, st>>>(b, ldb, k, ncols, g.cols_pad, pb, e_b);
+                             int* e_b, int8_t* tiles, bool scale, cudaStream_t st) {
+  if (scale) bscale_kernel<<<(unsigned)g.cols_pad, 256, 0, st>>>(b, ldb, k, ncols, g.cols_pad, pb, e_b);
   residue_b_kernel<NMOD><<<dim3((unsigned)g.cols_pad, (unsigned)ceil_div(g.nkb * 8, 256)), 256, 0, st>>>(
       b, ldb, k, ncols, g.n_g, g.nkb, e_b, tiles, g.ng);
 }
@@ -756,21 +772,10 @@ size_t oz_prep_workspace(int64_t m, int64_t n, int nmod) {
   return oz::prep_layout(m, n, nmod).total;
 }
 
-int oz_prep(const double* a, int64_t lda, int64_t m, int64_t n, int nmod, void* prep, size_t prep_bytes,
-            cudaStream_t st) {
-  RLRA_REQUIRE(nmod >= 12 && nmod <= oz::kMaxMod, "oz_prep: nmod must be in [12, 16], got %d", nmod);
-  RLRA_REQUIRE(m >= 1 && n >= 1 && lda >= m, "oz_prep: bad shape m=%lld n=%lld lda=%lld", (long long)m,
-               (long long)n, (long long)lda);
-  const oz::PrepLayout p = oz::prep_layout(m, n, nmod);
-  RLRA_REQUIRE(prep && prep_bytes >= p.total, "oz_prep: workspace too small (%zu < %zu)", prep_bytes, p.total);
-  RLRA_REQUIRE(p.njb <= 65535, "oz_prep: n too large (%lld)", (long long)n);
-  uint8_t* base = static_cast<uint8_t*>(prep);
-  int* e_a = reinterpret_cast<int*>(base + p.off_hdr);
-  unsigned long long* maxbits = reinterpret_cast<unsigned long long*>(base + p.off_hdr + 8);
-  double* prow = reinterpret_cast<double*>(base + p.off_prow);
-  double* pcol = reinterpret_cast<double*>(base + p.off_pcol);
-  int8_t* tiles = reinterpret_cast<int8_t*>(base + p.off_tiles);
-  RLRA_REQUIRE(p.nrb <= 2147483647 && p.ncb <= 65535, "oz_prep: A too large for the norm grid");
+static int oz_norms(const double* a, int64_t lda, int64_t m, int64_t n, int nmod, int* e_a,
+                    unsigned long long* maxbits, double* prow, double* pcol, cudaStream_t st) {
+  const int64_t ncb = ceil_div(n, oz::kNormCols), nrb = ceil_div(m, oz::kNormRows);
+  RLRA_REQUIRE(nrb <= 2147483647 && ncb <= 65535, "oz: A too large for the norm grid");
   RLRA_CHECK_CUDA(cudaMemsetAsync(maxbits, 0, sizeof(unsigned long long), st));
   {
     static int attr_dev = -1;
@@ -783,17 +788,76 @@ int oz_prep(const double* a, int64_t lda, int64_t m, int64_t n, int nmod, void* 
     }
   }
   ktimer_mark(KT_OZ_NORMS, st, false);
-  oz::norms_partial_kernel<<<dim3((unsigned)p.nrb, (unsigned)p.ncb), 256, oz::kNormSmem, st>>>(a, lda, m, n, prow,
-                                                                                               pcol);
+  oz::norms_partial_kernel<<<dim3((unsigned)nrb, (unsigned)ncb), 256, oz::kNormSmem, st>>>(a, lda, m, n, prow,
+                                                                                           pcol);
   ktimer_mark(KT_OZ_NORMS, st, true);
   RLRA_LAUNCHED();
-  oz::norms_final_kernel<<<(unsigned)ceil_div(m + n, 256), 256, 0, st>>>(prow, p.ncb, m, pcol, p.nrb, n, maxbits);
+  oz::norms_final_kernel<<<(unsigned)ceil_div(m + n, 256), 256, 0, st>>>(prow, ncb, m, pcol, nrb, n, maxbits);
   RLRA_LAUNCHED();
   oz::scale_a_kernel<<<1, 1, 0, st>>>(maxbits, oz::budget(nmod).pa, e_a);
   RLRA_LAUNCHED();
+  return 0;
+}
+
+size_t oz_scale_workspace(int64_t m, int64_t n) {
+  if (m < 1 || n < 1) return 0;
+  return 256 + ((size_t)ceil_div(n, oz::kNormCols) * m + (size_t)ceil_div(m, oz::kNormRows) * n) * sizeof(double);
+}
+
+int oz_scale(const double* a, int64_t lda, int64_t m, int64_t n, int nmod, int* e_a, void* ws, size_t ws_bytes,
+             cudaStream_t st) {
+  RLRA_REQUIRE(nmod >= 12 && nmod <= oz::kMaxMod, "oz_scale: nmod must be in [12, 16], got %d", nmod);
+  RLRA_REQUIRE(m >= 1 && n >= 1 && lda >= m, "oz_scale: bad shape m=%lld n=%lld lda=%lld", (long long)m,
+               (long long)n, (long long)lda);
+  RLRA_REQUIRE(ws && e_a && ws_bytes >= oz_scale_workspace(m, n), "oz_scale: workspace too small");
+  uint8_t* base = static_cast<uint8_t*>(ws);
+  double* prow = reinterpret_cast<double*>(base + 256);
+  double* pcol = prow + (size_t)ceil_div(n, oz::kNormCols) * m;
+  return oz_norms(a, lda, m, n, nmod, e_a, reinterpret_cast<unsigned long long*>(base), prow, pcol, st);
+}
+
+int oz_prep_ex(const double* a, int64_t lda, int64_t m, int64_t n, int nmod, const int* e_a_ext, void* prep,
+               size_t prep_bytes, cudaStream_t st) {
+  RLRA_REQUIRE(nmod >= 12 && nmod <= oz::kMaxMod, "oz_prep: nmod must be in [12, 16], got %d", nmod);
+  RLRA_REQUIRE(m >= 1 && n >= 1 && lda >= m, "oz_prep: bad shape m=%lld n=%lld lda=%lld", (long long)m,
+               (long long)n, (long long)lda);
+  const oz::PrepLayout p = oz::prep_layout(m, n, nmod);
+  RLRA_REQUIRE(prep && prep_bytes >= p.total, "oz_prep: workspace too small (%zu < %zu)", prep_bytes, p.total);
+  RLRA_REQUIRE(p.njb <= 65535, "oz_prep: n too large (%lld)", (long long)n);
+  uint8_t* base = static_cast<uint8_t*>(prep);
+  int* e_a = reinterpret_cast<int*>(base + p.off_hdr);
+  unsigned long long* maxbits = reinterpret_cast<unsigned long long*>(base + p.off_hdr + 8);
+  double* prow = reinterpret_cast<double*>(base + p.off_prow);
+  double* pcol = reinterpret_cast<double*>(base + p.off_pcol);
+  int8_t* tiles = reinterpret_cast<int8_t*>(base + p.off_tiles);
+  if (e_a_ext) {  // scale of an enclosing matrix (block-wise residues)
+    RLRA_CHECK_CUDA(cudaMemcpyAsync(e_a, e_a_ext, sizeof(int), cudaMemcpyDeviceToDevice, st));
+  } else {
+    const int rc = oz_norms(a, lda, m, n, nmod, e_a, maxbits, prow, pcol, st);
+    if (rc) return rc;
+  }
   ktimer_mark(KT_OZ_RESIDUE_A, st, false);
   OZ_DISPATCH(nmod, oz::launch_residue_a, a, lda, m, n, e_a, tiles, p, st);
   ktimer_mark(KT_OZ_RESIDUE_A, st, true);
+  RLRA_LAUNCHED();
+  return 0;
+}
+
+int oz_prep(const double* a, int64_t lda, int64_t m, int64_t n, int nmod, void* prep, size_t prep_bytes,
+            cudaStream_t st) {
+  return oz_prep_ex(a, lda, m, n, nmod, nullptr, prep, prep_bytes, st);
+}
+
+int64_t oz_cols_pad(int64_t ncols) {
+  const oz::PrepLayout p = oz::prep_layout(1, 1, 14);
+  return oz::gemm_layout(p, 0, ncols < 1 ? 1 : ncols, 14).cols_pad;
+}
+
+int oz_bscale(const double* b, int64_t ldb, int64_t k, int64_t ncols, int nmod, int* e_b, cudaStream_t st) {
+  RLRA_REQUIRE(nmod >= 12 && nmod <= oz::kMaxMod, "oz_bscale: nmod must be in [12, 16], got %d", nmod);
+  RLRA_REQUIRE(k >= 1 && ncols >= 1 && ldb >= k && e_b, "oz_bscale: bad arguments");
+  const int64_t cp = oz_cols_pad(ncols);
+  oz::bscale_kernel<<<(unsigned)cp, 256, 0, st>>>(b, ldb, k, ncols, cp, oz::budget(nmod).pb, e_b);
   RLRA_LAUNCHED();
   return 0;
 }
@@ -804,8 +868,9 @@ size_t oz_gemm_workspace(int trans, int64_t m, int64_t n, int64_t ncols, int nmo
   return oz::gemm_layout(p, trans, ncols, nmod).total;
 }
 
-int oz_gemm(int trans, const void* prep, int64_t m, int64_t n, int nmod, const double* b, int64_t ldb,
-            int64_t ncols, double* c, int64_t ldc, void* ws, size_t ws_bytes, cudaStream_t st) {
+int oz_gemm_ex(int trans, const void* prep, int64_t m, int64_t n, int nmod, const double* b, int64_t ldb,
+               int64_t ncols, double* c, int64_t ldc, void* ws, size_t ws_bytes, const int* e_b_ext, int flags,
+               cudaStream_t st) {
   RLRA_REQUIRE(nmod >= 12 && nmod <= oz::kMaxMod, "oz_gemm: nmod must be in [12, 16], got %d", nmod);
   const int64_t K = trans ? m : n, mrows = trans ? n : m;
   RLRA_REQUIRE(ncols >= 0 && ldb >= K && ldc >= mrows, "oz_gemm: bad leading dimensions");
@@ -820,12 +885,12 @@ int oz_gemm(int trans, const void* prep, int64_t m, int64_t n, int nmod, const d
   const int* e_a = reinterpret_cast<const int*>(pb + p.off_hdr);
   const int8_t* a_tiles = reinterpret_cast<const int8_t*>(pb + p.off_tiles);
   uint8_t* w = static_cast<uint8_t*>(ws);
-  int* e_b = reinterpret_cast<int*>(w + g.off_eb);
+  int* e_b = e_b_ext ? const_cast<int*>(e_b_ext) : reinterpret_cast<int*>(w + g.off_eb);
   int8_t* b_tiles = reinterpret_cast<int8_t*>(w + g.off_b);
   uint8_t* tout = w + g.off_t;
   const oz::Budget bud = oz::budget(nmod);
   ktimer_mark(KT_OZ_RESIDUE_B, st, false);
-  OZ_DISPATCH(nmod, oz::launch_residue_b, b, ldb, K, ncols, g, bud.pb, e_b, b_tiles, st);
+  OZ_DISPATCH(nmod, oz::launch_residue_b, b, ldb, K, ncols, g, bud.pb, e_b, b_tiles, e_b_ext == nullptr, st);
   ktimer_mark(KT_OZ_RESIDUE_B, st, true);
   RLRA_LAUNCHED();
   note_launch();  // bscale + residue_b
@@ -842,6 +907,7 @@ int oz_gemm(int trans, const void* prep, int64_t m, int64_t n, int nmod, const d
   ga.nmb = g.nmb;
   ga.out = tout;
   ga.nmod = nmod;
+  ga.accum = (flags & 1) ? 1 : 0;
   const oz::Crt crt = oz::make_crt(nmod);
   for (int l = 0; l < oz::kMaxMod; ++l) {
     ga.mods[l] = oz::kModuli[l];
@@ -862,12 +928,18 @@ int oz_gemm(int trans, const void* prep, int64_t m, int64_t n, int nmod, const d
   ktimer_mark(KT_OZ_GEMM, st, true);
   RLRA_LAUNCHED();
 
+  if (flags & 2) return 0;  // RLRA_B200_OZ_NO_CRT: more K blocks follow
   ktimer_mark(KT_OZ_CRT, st, false);
   oz::crt_kernel<<<dim3((unsigned)ceil_div(mrows, 256), (unsigned)ncols), 256, 0, st>>>(
       tout, g.rows_pad, g.cols_pad, mrows, ncols, e_a, e_b, crt, c, ldc);
   ktimer_mark(KT_OZ_CRT, st, true);
   RLRA_LAUNCHED();
   return 0;
+}
+
+int oz_gemm(int trans, const void* prep, int64_t m, int64_t n, int nmod, const double* b, int64_t ldb,
+            int64_t ncols, double* c, int64_t ldc, void* ws, size_t ws_bytes, cudaStream_t st) {
+  return oz_gemm_ex(trans, prep, m, n, nmod, b, ldb, ncols, c, ldc, ws, ws_bytes, nullptr, 0, st);
 }
 
 }  // namespace rlra

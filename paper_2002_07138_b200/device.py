@@ -28,7 +28,8 @@ DEFAULT_PANEL = 256  # rlra/singlepass.py:19
 PASS_GEMM = os.environ.get("RLRA_B200_PASS_GEMM", "oz")
 OZ_MAX_K = 133144
 # residues take nmod bytes per element of A (14 B vs 8 B of float64); larger
-# operands stay on the DMMA pass (C5: 68.7 GB A would need 120 GB of residues)
+# operands (C5: 68.7 GB A would need 120 GB of residues) use block-wise
+# residues (ops.OzBlocked), bit-identical to the one-block product
 OZ_MAX_RESIDUE_BYTES = int(os.environ.get("RLRA_B200_OZ_MAX_BYTES", str(48 << 30)))
 
 
@@ -84,15 +85,16 @@ class DeviceMatrix:
 
     def _oz_ok(self, k, ncols):
         m, n = self._a.shape
-        return (PASS_GEMM == "oz" and 0 < k <= OZ_MAX_K and 0 < ncols <= 4096 and min(m, n) > 0
-                and max(m, n) <= OZ_MAX_K and ops.OZ_NMOD * m * n <= OZ_MAX_RESIDUE_BYTES)
+        return PASS_GEMM == "oz" and 0 < k and 0 < ncols <= 4096 and min(m, n) > 0
 
     def _oz(self):
-        """Residues of A for this product session (or a transient one)."""
+        """Residues of A for this product session (or a transient one): all
+        of A (ops.OzPrep) when they fit next to it, else block-wise
+        (ops.OzBlocked: cached blocks + per-product rebuilt blocks)."""
         if self._oz_prep is not None:
             return self._oz_prep
         with ops.label("oz_prep"):
-            prep = ops.OzPrep(self.tensor)
+            prep = ops.oz_engine(self.tensor, OZ_MAX_RESIDUE_BYTES)
         if self._sessions > 0:
             self._oz_prep = prep
         return prep

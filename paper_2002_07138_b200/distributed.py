@@ -59,13 +59,11 @@ class CudaOps:
 
     def pass_prep(self, a):
         """Int8 residues of the local shard for the emulated pass products."""
-        from .device import OZ_MAX_K, OZ_MAX_RESIDUE_BYTES, PASS_GEMM
+        from .device import OZ_MAX_RESIDUE_BYTES, PASS_GEMM
 
-        if PASS_GEMM != "oz" or min(a.shape) == 0 or max(a.shape) > OZ_MAX_K:
+        if PASS_GEMM != "oz" or min(a.shape) == 0:
             return None
-        if self.o.OZ_NMOD * a.shape[0] * a.shape[1] > OZ_MAX_RESIDUE_BYTES:
-            return None
-        return self.o.OzPrep(a)
+        return self.o.oz_engine(a, OZ_MAX_RESIDUE_BYTES)
 
     def pass_matmul(self, a, prep, x, ta=False):
         if prep is not None and 0 < x.shape[1] <= 4096:

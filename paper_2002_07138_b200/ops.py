@@ -192,6 +192,125 @@ class OzPrep:
         return (c, ws) if keep_ws else c
 
 
+OZ_BLOCK_K = 133120  # largest multiple of 256 inside the exact int32 K range (133144)
+OZ_ACCUMULATE, OZ_NO_CRT = 1, 2  # include/rlra_b200.h
+
+
+def _split(total, cap):
+    """[(s0, s1)] cutting `total` into equal pieces of at most `cap`, each a
+    multiple of 256 except the last."""
+    nb = max(1, -(-total // cap))
+    step = -(-(-(-total // nb)) // 256) * 256
+    return [(s, min(total, s + step)) for s in range(0, total, step)]
+
+
+class OzBlocked:
+    """Pass products of an A whose residues do not fit next to it, or whose K
+    exceeds the exact int32 range (C5: 262144 x 32768 needs 120 GB of
+    residues next to its 68.7 GB).  A is cut into row x column blocks that
+    share ONE scale eA (norms over the whole A) and every product one
+    per-column scale eB of the whole B, so K-split products accumulate their
+    residues exactly (RLRA_B200_OZ_ACCUMULATE) and the result is bit-identical
+    to OzPrep's.  Residues of as many blocks as the memory budget allows are
+    kept for the product session; the others are rebuilt per product in one
+    scratch workspace (8 B read + nmod B written per element)."""
+
+    def __init__(self, a, nmod=None, block_bytes=None, cache_bytes=None, row_cap=OZ_BLOCK_K,
+                 col_cap=OZ_BLOCK_K):
+        m, n = a.shape
+        self.a = a
+        self.m, self.n = int(m), int(n)
+        self.nmod = OZ_NMOD if nmod is None else int(nmod)
+        self.device = a.device
+        dev = a.device
+        wsb = _native.query("rlra_b200_oz_scale_workspace", self.m, self.n)
+        ws = torch.empty(max(wsb, 8), dtype=torch.uint8, device=dev)
+        self.e_a = torch.empty(1, dtype=torch.int32, device=dev)
+        _call("rlra_b200_oz_scale", dev, ptr(a), ld_of(a), self.m, self.n, self.nmod, ptr(self.e_a), ptr(ws), wsb,
+              _stream(dev))
+        del ws
+        if block_bytes is None:
+            block_bytes = int(os.environ.get("RLRA_B200_OZ_BLOCK_BYTES", str(16 << 30)))
+        # full-width row blocks when n allows (long K for the NN product, K
+        # split -- exact accumulation -- only in the TN product)
+        self.cols = _split(self.n, min(int(col_cap), OZ_BLOCK_K))
+        wb = self.cols[0][1] - self.cols[0][0]
+        hcap = max(256, min(int(row_cap), OZ_BLOCK_K, (block_bytes // (self.nmod * wb)) // 256 * 256))
+        self.rows = _split(self.m, hcap)
+        self.blocks = [(i, j) for i in range(len(self.rows)) for j in range(len(self.cols))]
+        size = lambda ij: _native.query("rlra_b200_oz_prep_workspace", self.rows[ij[0]][1] - self.rows[ij[0]][0],
+                                        self.cols[ij[1]][1] - self.cols[ij[1]][0], self.nmod)
+        self.block_ws = {ij: size(ij) for ij in self.blocks}
+        biggest = max(self.block_ws.values())
+        if cache_bytes is None:
+            free, _ = torch.cuda.mem_get_info(dev)
+            free += torch.cuda.memory_reserved(dev) - torch.cuda.memory_allocated(dev)  # allocator cache
+            reserve = int(os.environ.get("RLRA_B200_OZ_RESERVE_BYTES", str(12 << 30)))
+            cache_bytes = free - reserve
+        total = sum(self.block_ws.values())
+        if total > cache_bytes:
+            cache_bytes -= biggest  # room for the scratch block
+        self.cache = {}
+        used = 0
+        for ij in self.blocks:
+            if used + self.block_ws[ij] <= cache_bytes:
+                self.cache[ij] = self._build(ij, None)
+                used += self.block_ws[ij]
+        self.scratch = None
+        if len(self.cache) < len(self.blocks):
+            self.scratch = torch.empty(biggest, dtype=torch.uint8, device=dev)
+        self.rebuilt = len(self.blocks) - len(self.cache)
+
+    def _build(self, ij, into):
+        (r0, r1), (c0, c1) = self.rows[ij[0]], self.cols[ij[1]]
+        wsb = self.block_ws[ij]
+        ws = into if into is not None else torch.empty(max(wsb, 8), dtype=torch.uint8, device=self.device)
+        a = self.a
+        _call("rlra_b200_oz_prep_ex", self.device, ptr(a) + (r0 + c0 * ld_of(a)) * 8, ld_of(a), r1 - r0, c1 - c0,
+              self.nmod, ptr(self.e_a), ptr(ws), wsb, _stream(self.device))
+        return ws
+
+    def _prep(self, ij):
+        ws = self.cache.get(ij)
+        return ws if ws is not None else self._build(ij, self.scratch)
+
+    def gemm(self, b, trans=False):
+        """C = A B (trans=False, b n x l) or A^T B (trans=True, b m x l)."""
+        k, rows = (self.m, self.n) if trans else (self.n, self.m)
+        if b.shape[0] != k:
+            raise ValueError(f"oz gemm shape mismatch: A {(self.m, self.n)} trans={trans}, B {tuple(b.shape)}")
+        ncols = int(b.shape[1])
+        c = fmat(rows, ncols, self.device)
+        if ncols == 0:
+            return c
+        b = as_fmat(b)
+        dev, st = self.device, _stream(self.device)
+        cp = int(_native.load().rlra_b200_oz_cols_pad(ncols))
+        e_b = torch.empty(cp, dtype=torch.int32, device=dev)
+        _call("rlra_b200_oz_bscale", dev, ptr(b), ld_of(b), k, ncols, self.nmod, ptr(e_b), st)
+        wsb = max(_native.query("rlra_b200_oz_gemm_workspace", int(trans), r1 - r0, c1 - c0, ncols, self.nmod)
+                  for (r0, r1) in self.rows for (c0, c1) in self.cols)
+        ws = torch.empty(max(wsb, 8), dtype=torch.uint8, device=dev)
+        # output blocks (outer) x K blocks (inner, accumulated exactly)
+        outer, inner = (self.cols, self.rows) if trans else (self.rows, self.cols)
+        for o, (o0, o1) in enumerate(outer):
+            for q, (k0, k1) in enumerate(inner):
+                ij = (q, o) if trans else (o, q)
+                (r0, r1), (c0, c1) = self.rows[ij[0]], self.cols[ij[1]]
+                flags = (OZ_ACCUMULATE if q > 0 else 0) | (OZ_NO_CRT if q + 1 < len(inner) else 0)
+                _call("rlra_b200_oz_gemm_ex", dev, int(trans), ptr(self._prep(ij)), r1 - r0, c1 - c0, self.nmod,
+                      ptr(b) + k0 * 8, ld_of(b), ncols, ptr(c) + o0 * 8, ld_of(c), ptr(ws), wsb, ptr(e_b), flags, st)
+        return c
+
+
+def oz_engine(a, max_residue_bytes):
+    """OzPrep when the residues of all of A fit (and K is in range), else OzBlocked."""
+    m, n = a.shape
+    if max(m, n) <= OZ_BLOCK_K and OZ_NMOD * m * n <= max_residue_bytes:
+        return OzPrep(a)
+    return OzBlocked(a)
+
+
 def matmul(a, b, *, ta=False, tb=False):
     m = a.shape[1] if ta else a.shape[0]
     n = b.shape[0] if tb else b.shape[1]

@@ -87,3 +87,29 @@ def test_oz_gemm_other_moduli_counts(cuda_dev, nmod):
     rel = float(np.abs(c - ref).max() / np.abs(ref).max())
     # each modulus is ~7.8 bits of product budget, split between A and B
     assert rel < max(2.0 ** (-(3.9 * nmod - 8)), 2.0 ** -50), rel
+
+
+@pytest.mark.parametrize("trans", [False, True])
+@pytest.mark.parametrize("cache_frac", [0.0, 0.5, 1.0])
+def test_oz_blocked_bit_identical_to_one_block(cuda_dev, trans, cache_frac):
+    """Block-wise residues (ops.OzBlocked: one global eA, one eB of the whole
+    B, exact modular accumulation over the K blocks) reproduce the one-block
+    product bit for bit -- with every block cached, none, or half of them."""
+    import torch
+
+    from paper_2002_07138_b200 import ops
+
+    dev = ops.check_device()
+    rng = np.random.default_rng(5)
+    m, n, l = 3000, 2600, 37
+    a = rng.standard_normal((m, n)) * np.exp(rng.uniform(-4, 4, size=(m, 1)))
+    b = rng.standard_normal((m if trans else n, l)) * np.exp(rng.uniform(-3, 3, size=(1, l)))
+    ad, bd = ops.from_numpy(a, dev), ops.from_numpy(b, dev)
+    c_full = ops.OzPrep(ad).gemm(bd, trans=trans)
+    total = 14 * m * n * 2
+    blk = ops.OzBlocked(ad, block_bytes=14 * 1024 * 1024, col_cap=1000, cache_bytes=int(cache_frac * total))
+    assert len(blk.rows) == 3 and len(blk.cols) == 3
+    assert (blk.rebuilt == 0) == (cache_frac == 1.0)
+    for _ in range(2):  # rebuilt blocks reuse the scratch workspace
+        c_blk = blk.gemm(bd, trans=trans)
+        assert torch.equal(c_full.view(torch.int64), c_blk.view(torch.int64))

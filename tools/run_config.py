@@ -44,6 +44,16 @@ for _ in range(reps):
     e1.record()
     torch.cuda.synchronize()
     times.append(e0.elapsed_time(e1))
+if os.environ.get("BREAKDOWN"):
+    from paper_2002_07138_b200 import ops
+
+    ops.PROF.on = True
+    call()
+    ops.PROF.on = False
+    summ = ops.PROF.summary()
+    for lab, (tot, cnt) in sorted(summ.items(), key=lambda x: -x[1][0]):
+        print(f"  {lab:32s} {tot:9.3f} ms  {cnt:4d} calls", file=sys.stderr)
+    ops.PROF.records.clear()
 err = validate.rel_err_device(a, f)
 sha = lambda x: hashlib.sha256(np.ascontiguousarray(x.cpu().numpy(), dtype=np.int64).tobytes()).hexdigest()
 if w.kind == "powerlu":
