@@ -26,6 +26,10 @@
  *   rlra_b200_chol_inv         CholeskyQR2 basis (same range as  kernels.py:57-61
  *                              the Householder Q of eqr)
  *   rlra_b200_trsm_rt          solve_triangular(trans='T')    kernels.py:95
+ *   rlra_b200_trsm_un          solve_triangular(R, C^T)       fixedrank.py:113 (randlu assembly)
+ *   rlra_b200_apply_inv_row_perm core.apply_inv_row_perm      core.py:103-109, fixedrank.py:111
+ *   rlra_b200_svd_jacobi       np.linalg.svd of the l x l     fixedrank.py:71 (randsvd)
+ *                              triangular factor of B = Q^T A
  *   rlra_b200_diag_absmin      pinv_factor rank test          kernels.py:75-79
  *   rlra_b200_sumsq            DenseAccessor.fro_norm()**2    accessors.py:33-34, fixedprec.py:72
  *   rlra_b200_colsumsq         per-column energies of G       fixedprec.py:75-80, :105-107
@@ -158,6 +162,22 @@ RLRA_B200_API size_t rlra_b200_trsm_workspace(int64_t l, int64_t ncols);
 RLRA_B200_API int rlra_b200_trsm_rt(const double* r, int64_t ldr, int64_t l, double* x, int64_t ldx,
                       int64_t ncols, void* ws, size_t ws_bytes, void* stream);
 RLRA_B200_API int rlra_b200_diag_absmin(const double* a, int64_t lda, int64_t r, double* out, void* stream);
+/* X = R^{-1} B in place over B (R upper l x l; same workspace query). */
+RLRA_B200_API int rlra_b200_trsm_un(const double* r, int64_t ldr, int64_t l, double* x, int64_t ldx,
+                                    int64_t ncols, void* ws, size_t ws_bytes, void* stream);
+/* out[p[i], :] = x[i, :] for a permutation p of 0..m-1 (pinv_ws: int64[m]). */
+RLRA_B200_API int rlra_b200_apply_inv_row_perm(const int64_t* p, int64_t m, int64_t n, const double* x,
+                                               int64_t ldx, int64_t* pinv_ws, double* out, int64_t ldo,
+                                               void* stream);
+
+/* ---- randsvd's small SVD: one-sided Jacobi, A (m x l, m >= l, l <= max_l)
+ * = U diag(s) V^T, s nonincreasing (ties by column index); sweeps_out
+ * (device int, nullable) receives the number of sweeps. */
+RLRA_B200_API int rlra_b200_svd_jacobi_max_l(void);
+RLRA_B200_API size_t rlra_b200_svd_jacobi_workspace(int64_t m, int64_t l);
+RLRA_B200_API int rlra_b200_svd_jacobi(const double* a, int64_t lda, int64_t m, int64_t l, double* u, int64_t ldu,
+                                       double* s, double* v, int64_t ldv, int* sweeps_out, void* ws,
+                                       size_t ws_bytes, void* stream);
 
 /* ---- K8 / K2b: compensated deterministic energies ----------------------- */
 RLRA_B200_API size_t rlra_b200_sumsq_workspace(int64_t m, int64_t n);

@@ -36,8 +36,10 @@ from .fixedprec import (
     refine_rank,
     restart_policy,
 )
-from .fixedrank import LowRankLU, lu_from_projection, powerlu, reconstruct
-from .rangefinder import RangeBasis, general_power_basis_v, power_basis_v
+from .fixedrank import (LowRankLU, LowRankSVD, lu_from_projection, powerlu, randlu, randlu_noreorth, randsvd,
+                        range_agreement, reconstruct)
+from .rangefinder import (PowerParams, RangeBasis, SketchLU, general_power_basis_v, power_basis_lu_l,
+                          power_basis_q, power_basis_v)
 from .singlepass import SketchPair, single_pass_lu, stream_sketch
 
 __version__ = "0.1.0"
@@ -50,4 +52,7 @@ __all__ = [
     "default_width", "gaussian", "general_power_basis_v", "lu_from_projection", "plu_inplace",
     "power_basis_v", "powerlu", "powerlu_fp", "reconstruct", "refine_rank", "restart_policy",
     "set_omega_cache", "single_pass_lu", "stream_sketch",
+    # paper's comparison baselines
+    "LowRankSVD", "PowerParams", "SketchLU", "power_basis_lu_l", "power_basis_q", "randlu",
+    "randlu_noreorth", "randsvd", "range_agreement",
 ]

@@ -59,6 +59,12 @@ SIGNATURES = {
     "rlra_b200_chol_inv": (_c_i, [_c_p, _c_i64, _c_i64, _c_p, _c_i64, _c_p, _c_d, _c_p]),
     "rlra_b200_trsm_workspace": (_c_sz, [_c_i64, _c_i64]),
     "rlra_b200_trsm_rt": (_c_i, [_c_p, _c_i64, _c_i64, _c_p, _c_i64, _c_i64, _c_p, _c_sz, _c_p]),
+    "rlra_b200_trsm_un": (_c_i, [_c_p, _c_i64, _c_i64, _c_p, _c_i64, _c_i64, _c_p, _c_sz, _c_p]),
+    "rlra_b200_apply_inv_row_perm": (_c_i, [_c_p, _c_i64, _c_i64, _c_p, _c_i64, _c_p, _c_p, _c_i64, _c_p]),
+    "rlra_b200_svd_jacobi_max_l": (_c_i, []),
+    "rlra_b200_svd_jacobi_workspace": (_c_sz, [_c_i64, _c_i64]),
+    "rlra_b200_svd_jacobi": (_c_i, [_c_p, _c_i64, _c_i64, _c_i64, _c_p, _c_i64, _c_p, _c_p, _c_i64, _c_p, _c_p,
+                                    _c_sz, _c_p]),
     "rlra_b200_diag_absmin": (_c_i, [_c_p, _c_i64, _c_i64, _c_p, _c_p]),
     "rlra_b200_sumsq_workspace": (_c_sz, [_c_i64, _c_i64]),
     "rlra_b200_sumsq": (_c_i, [_c_p, _c_i64, _c_i64, _c_i64, _c_p, _c_p, _c_sz, _c_p]),

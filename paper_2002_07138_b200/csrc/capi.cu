@@ -85,6 +85,14 @@ int geqrf(double* a, int64_t lda, int64_t m, int64_t n, double* tau, void* ws, s
           cudaStream_t st);
 int orgqr(const double* a, int64_t lda, int64_t m, int64_t n, double* q, int64_t ldq, void* ws,
           size_t ws_bytes, cudaStream_t st);
+int trsm_un(const double* r, int64_t ldr, int64_t l, double* x, int64_t ldx, int64_t ncols, void* ws,
+            size_t ws_bytes, cudaStream_t st);
+int apply_inv_row_perm(const int64_t* p, int64_t m, int64_t n, const double* x, int64_t ldx, int64_t* pinv_ws,
+                       double* out, int64_t ldo, cudaStream_t st);
+int svd_jacobi_max_l();
+size_t svd_jacobi_workspace(int64_t m, int64_t l);
+int svd_jacobi(const double* a, int64_t lda, int64_t m, int64_t l, double* u, int64_t ldu, double* s, double* v,
+               int64_t ldv, int* sweeps_out, void* ws, size_t ws_bytes, cudaStream_t st);
 int trsm_rt(const double* r, int64_t ldr, int64_t l, double* x, int64_t ldx, int64_t ncols,
             void* ws, size_t ws_bytes, cudaStream_t st);
 int diag_absmin(const double* a, int64_t lda, int64_t r, double* out_dev, cudaStream_t st);
@@ -317,6 +325,25 @@ size_t rlra_b200_trsm_workspace(int64_t l, int64_t ncols) {
 int rlra_b200_trsm_rt(const double* r, int64_t ldr, int64_t l, double* x, int64_t ldx,
                       int64_t ncols, void* ws, size_t ws_bytes, void* stream) {
   return trsm_rt(r, ldr, l, x, ldx, ncols, ws, ws_bytes, S(stream));
+}
+
+int rlra_b200_trsm_un(const double* r, int64_t ldr, int64_t l, double* x, int64_t ldx, int64_t ncols, void* ws,
+                      size_t ws_bytes, void* stream) {
+  return trsm_un(r, ldr, l, x, ldx, ncols, ws, ws_bytes, S(stream));
+}
+
+int rlra_b200_apply_inv_row_perm(const int64_t* p, int64_t m, int64_t n, const double* x, int64_t ldx,
+                                 int64_t* pinv_ws, double* out, int64_t ldo, void* stream) {
+  return apply_inv_row_perm(p, m, n, x, ldx, pinv_ws, out, ldo, S(stream));
+}
+
+int rlra_b200_svd_jacobi_max_l(void) { return svd_jacobi_max_l(); }
+
+size_t rlra_b200_svd_jacobi_workspace(int64_t m, int64_t l) { return svd_jacobi_workspace(m, l); }
+
+int rlra_b200_svd_jacobi(const double* a, int64_t lda, int64_t m, int64_t l, double* u, int64_t ldu, double* s,
+                         double* v, int64_t ldv, int* sweeps_out, void* ws, size_t ws_bytes, void* stream) {
+  return svd_jacobi(a, lda, m, l, u, ldu, s, v, ldv, sweeps_out, ws, ws_bytes, S(stream));
 }
 
 int rlra_b200_diag_absmin(const double* a, int64_t lda, int64_t r, double* out, void* stream) {

@@ -145,6 +145,17 @@ __global__ void lu_basis_kernel(const double* __restrict__ lu, int64_t ldlu, int
   }
 }
 
+// out[r, c] = x[pinv[r], c], i.e. out[p[i], :] = x[i, :] (rlra/core.py:103-109).
+__global__ void row_gather_kernel(const double* __restrict__ x, int64_t ldx, int64_t m, int64_t n,
+                                  const int64_t* __restrict__ pinv, double* __restrict__ out, int64_t ldo) {
+  const int64_t total = m * n;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e % m, c = e / m;
+    out[cm(r, c, ldo)] = __ldg(x + cm(__ldg(pinv + r), c, ldx));
+  }
+}
+
 __global__ void extract_l_kernel(const double* __restrict__ lu, int64_t ldlu, int64_t m, int64_t k,
                                  double* __restrict__ l, int64_t ldl) {
   const int64_t total = m * k;
@@ -197,6 +208,15 @@ int lu_basis(const double* lu, int64_t ldlu, int64_t m, int64_t k, const int64_t
   if (m <= 0 || k <= 0) return 0;
   if (inv_perm(piv, m, pinv_ws, st)) return -1;
   lu_basis_kernel<<<grid_for(m * k), 256, 0, st>>>(lu, ldlu, m, k, pinv_ws, w, ldw);
+  RLRA_LAUNCHED();
+  return 0;
+}
+
+int apply_inv_row_perm(const int64_t* p, int64_t m, int64_t n, const double* x, int64_t ldx, int64_t* pinv_ws,
+                       double* out, int64_t ldo, cudaStream_t st) {
+  if (m <= 0 || n <= 0) return 0;
+  if (inv_perm(p, m, pinv_ws, st)) return -1;
+  row_gather_kernel<<<grid_for(m * n), 256, 0, st>>>(x, ldx, m, n, pinv_ws, out, ldo);
   RLRA_LAUNCHED();
   return 0;
 }

@@ -62,6 +62,61 @@ int trsm_rt(const double* r, int64_t ldr, int64_t l, double* x, int64_t ldx, int
   return 0;
 }
 
+// Solve R_bb X_b = X_b in place (backward substitution), R_bb the nb x nb
+// diagonal block at (i0, i0) of the upper-triangular R.
+__global__ void trsm_un_diag_kernel(const double* __restrict__ r, int64_t ldr, int64_t i0, int nb,
+                                    double* x, int64_t ldx, int64_t ncols) {
+  __shared__ double R[TRSM_NB][TRSM_NB + 1];
+  for (int e = threadIdx.x; e < nb * nb; e += blockDim.x) {
+    int a = e % nb, b = e / nb;
+    R[a][b] = r[cm(i0 + a, i0 + b, ldr)];
+  }
+  __syncthreads();
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < ncols;
+       c += (int64_t)gridDim.x * blockDim.x) {
+    double v[TRSM_NB];
+    double* col = x + cm(i0, c, ldx);
+#pragma unroll
+    for (int s = 0; s < TRSM_NB; s++) v[s] = s < nb ? col[s] : 0.0;
+#pragma unroll
+    for (int s = TRSM_NB - 1; s >= 0; s--) {
+      if (s >= nb) continue;
+      double acc = v[s];
+#pragma unroll
+      for (int t = 0; t < TRSM_NB; t++)
+        if (t > s && t < nb) acc -= R[s][t] * v[t];
+      v[s] = acc / R[s][s];
+    }
+#pragma unroll
+    for (int s = 0; s < TRSM_NB; s++)
+      if (s < nb) col[s] = v[s];
+  }
+}
+
+// X (l x ncols, in place over B) = R^{-1} B, R upper triangular l x l
+// (SciPy solve_triangular(R, B, lower=False), rlra/fixedrank.py:113); blocks
+// from the bottom: X_b -= R(b, below) X(below, :) on the DMMA pipe, then the
+// diagonal block.
+int trsm_un(const double* r, int64_t ldr, int64_t l, double* x, int64_t ldx, int64_t ncols,
+            void* ws, size_t ws_bytes, cudaStream_t st) {
+  if (l <= 0 || ncols <= 0) return 0;
+  const int64_t nblk = ceil_div(l, TRSM_NB);
+  for (int64_t b = nblk - 1; b >= 0; b--) {
+    const int64_t i0 = b * TRSM_NB;
+    const int nb = (int)std::min<int64_t>(TRSM_NB, l - i0);
+    const int64_t i1 = i0 + nb;
+    if (i1 < l) {
+      if (gemm(false, false, nb, ncols, l - i1, -1.0, r + cm(i0, i1, ldr), ldr, x + cm(i1, 0, ldx), ldx, 1.0,
+               x + cm(i0, 0, ldx), ldx, ws, ws_bytes, st))
+        return -1;
+    }
+    int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(ncols, 64), 1024));
+    trsm_un_diag_kernel<<<blocks, 64, 0, st>>>(r, ldr, i0, nb, x, ldx, ncols);
+    RLRA_LAUNCHED();
+  }
+  return 0;
+}
+
 __global__ void diag_absmin_kernel(const double* a, int64_t lda, int64_t r, double* out) {
   __shared__ double s[32];
   double mn = INFINITY;

@@ -33,6 +33,19 @@ OZ_MAX_K = 133144
 OZ_MAX_RESIDUE_BYTES = int(os.environ.get("RLRA_B200_OZ_MAX_BYTES", str(48 << 30)))
 
 
+_ENGINE = [None]  # per-call override of PASS_GEMM (pass_engine)
+
+
+@contextlib.contextmanager
+def pass_engine(name):
+    """Run the pass products of the enclosed calls on `name` ("oz" | "dmma")."""
+    prev, _ENGINE[0] = _ENGINE[0], name
+    try:
+        yield
+    finally:
+        _ENGINE[0] = prev
+
+
 def product_session(a):
     """Context in which the pass products of one driver call share the int8
     residues of A (built at the first product, dropped at exit)."""
@@ -85,7 +98,7 @@ class DeviceMatrix:
 
     def _oz_ok(self, k, ncols):
         m, n = self._a.shape
-        return PASS_GEMM == "oz" and 0 < k and 0 < ncols <= 4096 and min(m, n) > 0
+        return (_ENGINE[0] or PASS_GEMM) == "oz" and 0 < k and 0 < ncols <= 4096 and min(m, n) > 0
 
     def _oz(self):
         """Residues of A for this product session (or a transient one): all

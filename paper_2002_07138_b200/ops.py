@@ -439,6 +439,42 @@ def trsm_rt_(r, x):
     return x
 
 
+def trsm_un_(r, x):
+    """x <- R^{-1} x in place, R upper triangular (rlra/fixedrank.py:113)."""
+    l = r.shape[0]
+    ncols = x.shape[1]
+    wsb = _native.query("rlra_b200_trsm_workspace", l, ncols)
+    ws = torch.empty(max(wsb, 8), dtype=torch.uint8, device=x.device)
+    _call("rlra_b200_trsm_un", x.device, ptr(r), ld_of(r), l, ptr(x), ld_of(x), ncols, ptr(ws), wsb,
+          _stream(x.device))
+    return x
+
+
+def apply_inv_row_perm(p, x):
+    """out[p[i], :] = x[i, :] (rlra/core.py:103-109)."""
+    m, n = x.shape
+    out = fmat(m, n, x.device)
+    pinv = torch.empty(max(int(m), 1), dtype=I64, device=x.device)
+    _call("rlra_b200_apply_inv_row_perm", x.device, ptr(p), m, n, ptr(x), ld_of(x), ptr(pinv), ptr(out),
+          ld_of(out), _stream(x.device))
+    return out
+
+
+def svd_jacobi(a):
+    """a (m x l, m >= l) = U diag(s) V^T by one-sided Jacobi (csrc/svd.cu);
+    s nonincreasing.  Returns (U m x l, s (l,), V l x l, sweeps device int)."""
+    m, l = a.shape
+    dev = a.device
+    u, v = fmat(m, l, dev), fmat(l, l, dev)
+    s = torch.empty(max(int(l), 1), dtype=F64, device=dev)[: int(l)]
+    sweeps = torch.zeros(1, dtype=torch.int32, device=dev)
+    wsb = _native.query("rlra_b200_svd_jacobi_workspace", m, l)
+    ws = torch.empty(max(wsb, 8), dtype=torch.uint8, device=dev)
+    _call("rlra_b200_svd_jacobi", dev, ptr(a), ld_of(a), m, l, ptr(u), ld_of(u), ptr(s), ptr(v), ld_of(v),
+          ptr(sweeps), ptr(ws), wsb, _stream(dev))
+    return u, s, v, sweeps
+
+
 def diag_absmin(a):
     out = torch.empty(1, dtype=F64, device=a.device)
     _call("rlra_b200_diag_absmin", a.device, ptr(a), ld_of(a), min(a.shape), ptr(out), _stream(a.device))

@@ -12,6 +12,7 @@ raised when the basis is handed back, with the reference's attributes.
 
 from __future__ import annotations
 
+from dataclasses import dataclass
 from typing import NamedTuple
 
 import torch
@@ -24,6 +25,35 @@ from .errors import RankCollapse
 class RangeBasis(NamedTuple):
     V: torch.Tensor  # n x l, orthonormal columns (device)
     passes_used: int
+
+
+class SketchLU(NamedTuple):
+    """rlra/rangefinder.py:25-28 (device tensors)."""
+
+    L: torch.Tensor  # m x l, unit-diagonal lower trapezoidal
+    U: torch.Tensor  # l x l
+    p: torch.Tensor  # row permutation of the sketch
+
+
+@dataclass(frozen=True)
+class PowerParams:
+    """Sketch-size bookkeeping l = k + q_os, exponent p, passes v = 2p + 2
+    (rlra/rangefinder.py:31-52; host-only arithmetic)."""
+
+    l: int
+    p: int
+    v: int
+    q_oversample: int
+
+    @classmethod
+    def from_power(cls, k, q_oversample, p):
+        return cls(l=k + q_oversample, p=p, v=2 * p + 2, q_oversample=q_oversample)
+
+    @classmethod
+    def from_passes(cls, k, q_oversample, v):
+        if v < 2 or v % 2:
+            raise ValueError(f"pass budget {v} has no power-exponent equivalent")
+        return cls(l=k + q_oversample, p=(v - 2) // 2, v=v, q_oversample=q_oversample)
 
 
 class RankChecks:
@@ -119,3 +149,58 @@ def power_basis_v(a, l, p, seed):
     if p < 1:
         raise ValueError("p must be >= 1: no products means no basis")
     return general_power_basis_v(a, l, 2 * p + 1, seed)
+
+
+def final_sketch_lu_(y, checks):
+    """rlra/rangefinder.py:129-132 (destroys y): SketchLU of the last sketch."""
+    from .kernels import plu_
+
+    f = plu_(y)
+    checks.add(f.nonzero_diag, y.shape[1])
+    return SketchLU(f.L, f.U, f.p)
+
+
+def power_basis_q(a, l, p, seed):
+    """rlra/rangefinder.py:86-103: column-space basis of (A A^T)^p A Omega with
+    a Householder QR (K4) after every product; 2p + 1 passes."""
+    a = as_accessor(a)
+    _validate(a, l)
+    if p < 0:
+        raise ValueError("p must be >= 0")
+    checks = RankChecks()
+    om = core.omega(seed, a.shape[1], l, a.device)
+    q = qr_basis_(a.matmul(om), checks)
+    passes = 1
+    for _ in range(p):
+        q = qr_basis_(a.rmatmul(q), checks)
+        q = qr_basis_(a.matmul(q), checks)
+        passes += 2
+    checks.raise_if_collapsed()
+    return RangeBasis(q, passes)
+
+
+def power_basis_lu_l(a, l, p, seed, *, _checks=None):
+    """rlra/rangefinder.py:106-126: LU-stabilised sketch of A (A^T A)^p Omega
+    for randlu -- (L, U, p) of the final pivoted LU (bit-exact GEPP, K3),
+    interior renormalisations by the row-unpermuted L; 2p + 1 passes."""
+    a = as_accessor(a)
+    _validate(a, l)
+    if p < 0:
+        raise ValueError("p must be >= 0")
+    checks = _checks if _checks is not None else RankChecks()
+    om = core.omega(seed, a.shape[1], l, a.device)
+    y = a.matmul(om)
+    if p == 0:
+        out = final_sketch_lu_(y, checks)
+    else:
+        w = lu_basis_(y, checks)
+        for i in range(1, p + 1):
+            w = lu_basis_(a.rmatmul(w), checks)
+            y = a.matmul(w)
+            if i == p:
+                out = final_sketch_lu_(y, checks)
+                break
+            w = lu_basis_(y, checks)
+    if _checks is None:
+        checks.raise_if_collapsed()
+    return out
