@@ -12,6 +12,7 @@ from .backend import BACKEND, plu_inplace
 from .core import gaussian, set_omega_cache
 from .device import (
     DenseColumnStream,
+    RlraFileColumnStream,
     DeviceColumnStream,
     DeviceMatrix,
     InstrumentedAccessor,
@@ -41,6 +42,7 @@ from .fixedrank import (LowRankLU, LowRankSVD, lu_from_projection, powerlu, rand
 from .rangefinder import (PowerParams, RangeBasis, SketchLU, general_power_basis_v, power_basis_lu_l,
                           power_basis_q, power_basis_v)
 from .singlepass import SketchPair, single_pass_lu, stream_sketch
+from .streams import read_rlra, read_rlra_header, write_rlra
 
 __version__ = "0.1.0"
 
@@ -55,4 +57,6 @@ __all__ = [
     # paper's comparison baselines
     "LowRankSVD", "PowerParams", "SketchLU", "power_basis_lu_l", "power_basis_q", "randlu",
     "randlu_noreorth", "randsvd", "range_agreement",
+    # out-of-core streams
+    "RlraFileColumnStream", "read_rlra", "read_rlra_header", "write_rlra",
 ]

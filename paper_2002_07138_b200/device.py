@@ -329,15 +329,4 @@ class DeviceColumnStream(_StreamBase):
         return self._m.tensor[:, j0:j1]
 
 
-class DenseColumnStream(_StreamBase):
-    """Streams an in-memory HOST matrix (rlra/singlepass.py:49-57); each panel
-    is uploaded when pulled (out-of-core style)."""
-
-    def __init__(self, a):
-        self._a = np.asfortranarray(np.asarray(a, dtype=np.float64))
-        if self._a.ndim != 2:
-            raise ValueError(f"expected a 2-d array, got ndim={self._a.ndim}")
-        super().__init__(self._a.shape)
-
-    def _panel(self, j0, j1):
-        return self._a[:, j0:j1]
+from .streams import DenseColumnStream, RlraFileColumnStream  # noqa: E402  (host streams: pinned pipeline)

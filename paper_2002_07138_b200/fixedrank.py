@@ -37,9 +37,11 @@ class LowRankLU:
     rank: int
 
     def to_numpy(self):
-        conv = lambda t: ops.to_numpy(t) if isinstance(t, torch.Tensor) else t
-        torch.cuda.synchronize() if self.on_device else None
-        return LowRankLU(conv(self.p), conv(self.q), conv(self.L), conv(self.U), self.rank)
+        flds = [self.p, self.q, self.L, self.U]
+        dev = [i for i, t in enumerate(flds) if isinstance(t, torch.Tensor)]
+        for i, h in zip(dev, ops.to_numpy_many([flds[i] for i in dev])):
+            flds[i] = h
+        return LowRankLU(*flds, self.rank)
 
     @property
     def on_device(self):

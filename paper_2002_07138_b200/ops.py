@@ -127,14 +127,34 @@ def from_numpy(a, device):
     return out
 
 
+PINNED_MIN_BYTES = 1 << 20  # results at least this large come back through pinned buffers
+
+
+def _host_like(t):
+    pin = t.numel() * t.element_size() >= PINNED_MIN_BYTES
+    if t.dim() == 1:
+        return torch.empty(t.shape, dtype=t.dtype, pin_memory=pin)
+    m, n = t.shape
+    return torch.empty((n, m), dtype=t.dtype, pin_memory=pin).t()
+
+
+def to_numpy_many(ts):
+    """Download several device tensors (column-major matrices or vectors) with
+    asynchronous copies into pinned host buffers and ONE synchronisation;
+    returns F-ordered ndarrays viewing those buffers."""
+    hosts = []
+    for t in ts:
+        h = _host_like(t)
+        h.copy_(t, non_blocking=True)
+        hosts.append(h)
+    if ts:
+        torch.cuda.current_stream(ts[0].device).synchronize()
+    return [h.numpy() for h in hosts]
+
+
 def to_numpy(t):
     """Download a column-major device matrix as an F-ordered ndarray."""
-    if t.dim() == 1:
-        return t.cpu().numpy()
-    m, n = t.shape
-    host = torch.empty((n, m), dtype=t.dtype).t()
-    host.copy_(t)
-    return host.numpy()
+    return to_numpy_many([t])[0]
 
 
 def ptr(t):

@@ -50,7 +50,7 @@ def stream_sketch(stream, k, seed, panel=DEFAULT_PANEL):
 
 def single_pass_lu(stream, k, seed, q_os=0, panel=DEFAULT_PANEL):
     """rlra/singlepass.py:123-144."""
-    host = isinstance(stream, DenseColumnStream) or not isinstance(stream, DeviceColumnStream)
+    host = not isinstance(stream, DeviceColumnStream)  # host streams return NumPy factors
     l = k + q_os
     g, h = stream_sketch(stream, l, seed, panel=panel)
     f1 = plu_(h)  # L1 m x l, U1 l x l, p
