@@ -22,6 +22,7 @@ from __future__ import annotations
 import os
 import struct
 import threading
+from concurrent.futures import ThreadPoolExecutor
 
 import numpy as np
 import torch
@@ -31,6 +32,20 @@ from . import ops
 RLRA_MAGIC = b"RLRA"  # rlra/fileio.py:14-15
 RLRA_HEADER_BYTES = 4 + 8 + 8
 PIPELINE_SLOTS = 3
+IO_THREADS = int(os.environ.get("RLRA_B200_IO_THREADS", "8"))  # parallel preads / copies per panel
+_POOL = None
+
+
+def _pool():
+    global _POOL
+    if _POOL is None:
+        _POOL = ThreadPoolExecutor(max_workers=max(1, IO_THREADS), thread_name_prefix="rlra-b200-io")
+    return _POOL
+
+
+def _split_cols(j0, j1, parts):
+    step = max(1, -(-(j1 - j0) // parts))
+    return [(c, min(j1, c + step)) for c in range(j0, j1, step)]
 
 
 # ---------------------------------------------------------------- .rlm container
@@ -196,13 +211,17 @@ class DenseColumnStream(_HostStreamBase):
         super().__init__(self._a.shape, device)
 
     def _fill(self, j0, j1, out):
-        np.copyto(out, self._a[:, j0:j1])
+        def cp(c0, c1):
+            np.copyto(out[:, c0 - j0:c1 - j0], self._a[:, c0:c1])
+
+        list(_pool().map(lambda r: cp(*r), _split_cols(j0, j1, IO_THREADS)))
 
 
 class RlraFileColumnStream(_HostStreamBase):
     """Streams a column-major ``.rlm`` file without loading it whole
-    (rlra/singlepass.py:60-74): each panel is ONE contiguous pread straight
-    into pinned memory, then uploaded asynchronously."""
+    (rlra/singlepass.py:60-74): each panel is a contiguous byte range, read
+    by IO_THREADS parallel preads straight into pinned memory, then uploaded
+    asynchronously."""
 
     def __init__(self, path, device=None):
         self._path = os.fspath(path)
@@ -210,19 +229,24 @@ class RlraFileColumnStream(_HostStreamBase):
 
     def _fill(self, j0, j1, out):
         m = self.shape[0]
-        want = 8 * m * (j1 - j0)
         buf = memoryview(out.T.reshape(-1)).cast("B")  # out is F-ordered: its bytes are contiguous
         fd = os.open(self._path, os.O_RDONLY)
-        try:
-            got = 0
-            while got < want:
-                r = os.preadv(fd, [buf[got:want]], RLRA_HEADER_BYTES + 8 * m * j0 + got)
+
+        def rd(c0, c1):  # columns [c0, c1): one contiguous byte range of file and buffer
+            lo, hi = 8 * m * (c0 - j0), 8 * m * (c1 - j0)
+            got = lo
+            while got < hi:
+                r = os.preadv(fd, [buf[got:hi]], RLRA_HEADER_BYTES + 8 * m * j0 + got)
                 if r <= 0:
                     break
                 got += r
+            return got == hi
+
+        try:
+            ok = all(_pool().map(lambda r: rd(*r), _split_cols(j0, j1, IO_THREADS)))
         finally:
             os.close(fd)
-        if got != want:
+        if not ok:
             raise IOError(f"{self._path}: truncated column data")
         if np.little_endian is False:  # pragma: no cover - the format is little-endian
             out.byteswap(inplace=True)
