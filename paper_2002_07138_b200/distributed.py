@@ -8,10 +8,18 @@ Per pass (rlra/rangefinder.py:144-176 control flow, unchanged):
   ||A||_F^2   local compensated sum, then all-reduce     1 double
   column energies of G: local, then all-reduce           l doubles
 Sketch factorizations:
-  interior LU of the row-sharded Y and the final LU of G are EXACT GEPP on the
-  all-gathered matrix (every rank redundantly, bit-exact kernel) so pivots are
-  those of the single-GPU / reference algorithm; LU / QR of the replicated
-  n x l sketches run redundantly with no communication.
+  interior LU of the row-sharded Y: TSLU (tournament pivoting, SURVEY.md
+  §8(e)) -- local GEPP of Y_i names l candidate rows per rank, one all-gather
+  of the world*l x l candidates, a redundant GEPP of those gives U, and
+  W_i = Y_i U^{-1} locally.  Any pivoting gives W = Y U^{-1} with U upper
+  triangular, so range(W) is that of the exact GEPP's P^T L and the final QR
+  absorbs the difference (V equal up to column signs and rounding); traffic is
+  world*l*l doubles instead of the whole m x l sketch.  RLRA_B200_DIST_INTERIOR
+  =gather selects the all-gathered exact GEPP instead.
+  final LU of G: EXACT GEPP on the all-gathered matrix (every rank
+  redundantly, bit-exact kernel), so p and q are those of the single-GPU /
+  reference algorithm; LU / QR of the replicated n x l sketches run
+  redundantly with no communication.
 
 The orchestration is written against a small ops interface so the same code
 runs on CUDA tensors with NCCL (CudaOps, the product) and -- in the CPU test
@@ -91,6 +99,17 @@ class CudaOps:
 
     def colsumsq(self, a):
         return self.o.colsumsq(a)
+
+    def gather_rows(self, x, idx):
+        return self.o.as_fmat(x.index_select(0, idx))
+
+    def right_solve_upper(self, x, u):
+        """X U^{-1} (U upper l x l): transposes around the K6 solve U^T Z = X^T."""
+        if x.shape[0] == 0:
+            return x
+        xt = self.o.transpose(x)
+        self.o.trsm_rt_(u, xt)
+        return self.o.transpose(xt)
 
 
 @dataclass
@@ -185,6 +204,37 @@ class ShardedMatrix:
         return full[self.r0:self.r1, :]
 
 
+INTERIOR = os.environ.get("RLRA_B200_DIST_INTERIOR", "tslu")  # "tslu" | "gather"
+
+
+def tslu_basis_rows(A, y_local, l):
+    """Interior renormalisation of the row-sharded sketch by tournament
+    pivoting; returns this rank's rows of W = Y U^{-1}."""
+    ops = A.ops
+    rows = y_local.shape[0]
+    c = min(rows, l)
+    dev = y_local.device
+    cand = torch.zeros((l, l), dtype=torch.float64, device=dev)  # row-major candidate rows
+    gidx = torch.full((l,), -1, dtype=torch.int64, device=dev)
+    if rows:
+        work = ops.empty(rows, l)
+        work.copy_(y_local)
+        piv, _ = ops.getrf_(work)
+        sel = piv[:c].to(dev)
+        cand[:c].copy_(y_local.index_select(0, sel))
+        gidx[:c] = sel + A.r0
+    cands = [torch.empty_like(cand) for _ in range(A.world)]
+    idxs = [torch.empty_like(gidx) for _ in range(A.world)]
+    dist.all_gather(cands, cand, group=A.group)
+    dist.all_gather(idxs, gidx, group=A.group)
+    full = ops.empty(A.world * l, l)
+    full.copy_(torch.cat(cands, 0))
+    _, cnt = ops.getrf_(full)  # redundant on every rank: identical U everywhere
+    _check(cnt, l)
+    _, u = ops.lu_extract(full)
+    return ops.right_solve_upper(y_local, u)
+
+
 def _check(count, requested):
     achieved = int(count.item())
     if achieved < requested:
@@ -202,6 +252,8 @@ def general_power_basis_v(A: ShardedMatrix, l, v, seed, omega_fn):
     ops = A.ops
 
     def lu_basis_rows(y_local):
+        if INTERIOR == "tslu" and A.world > 1:
+            return tslu_basis_rows(A, y_local, l)
         full = A.gather_rows(y_local)
         piv, cnt = ops.getrf_(full)
         _check(cnt, l)

@@ -76,6 +76,14 @@ class OracleOps:
         an = a.numpy()
         return torch.tensor([float(an[:, j] @ an[:, j]) for j in range(an.shape[1])], dtype=torch.float64)
 
+    def gather_rows(self, x, idx):
+        return self.upload(x.numpy()[idx.numpy()])
+
+    def right_solve_upper(self, x, u):
+        from scipy.linalg import solve_triangular
+
+        return self.upload(solve_triangular(u.numpy(), x.numpy().T, trans="T", lower=False).T)
+
 
 def _free_port():
     s = socket.socket()
@@ -91,6 +99,7 @@ def _worker(rank, world, port, case, q):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     from paper_2002_07138_b200 import distributed as D
 
+    D.INTERIOR = case.get("interior", "tslu")
     try:
         a = case["a"]
         m = a.shape[0]
@@ -151,3 +160,24 @@ def test_sharded_powerlu_fp_rank_matches():
     for rank, (p, q, L, U, r) in res.items():
         assert r == ref_o.rank
         assert np.array_equal(p, ref_f.p) and np.array_equal(q, ref_f.q)
+
+
+def test_sharded_interior_gather_path_matches():
+    """RLRA_B200_DIST_INTERIOR=gather: all-gathered exact interior GEPPs."""
+    a = decay_matrix(203, 150, seed=4)
+    res = run_dist({"kind": "powerlu", "a": a, "k": 20, "q_os": 8, "v": 4, "seed": 1, "interior": "gather"})
+    ref = O.powerlu(a, 20, 8, 4, 1)
+    for rank, (p, q, L, U, passes) in res.items():
+        assert np.array_equal(p, ref.p) and np.array_equal(q, ref.q)
+
+
+def test_sharded_tslu_shards_shorter_than_sketch():
+    """world 4, 62 rows: shards of 16 / 16 / 16 / 14 rows < l = 20 (zero-padded
+    candidate blocks in the tournament)."""
+    a = decay_matrix(62, 40, seed=8)
+    res = run_dist({"kind": "powerlu", "a": a, "k": 12, "q_os": 8, "v": 5, "seed": 2}, world=4)
+    ref = O.powerlu(a, 12, 8, 5, 2)
+    for rank, (p, q, L, U, passes) in res.items():
+        assert np.array_equal(p, ref.p) and np.array_equal(q, ref.q)
+        f = O.LowRankLU(p, q, L, U, 12)
+        assert abs(O.rel_fro_error_factor(a, f) - O.rel_fro_error_factor(a, ref)) <= 1e-12

@@ -253,6 +253,14 @@ def test_distributed_path_single_rank_nccl(cuda_dev):
         fp, r = D.powerlu_fp(B, 1e-3, 5, 60, 4, 0, O.gaussian)
         assert r == META["drivers"]["fp"]["rank"]
         assert np.array_equal(fp.p.cpu().numpy(), DRV["fpfac/p"])
+        # TSLU interior step on the CUDA ops (the multi-rank tournament: gloo tests):
+        # W = Y U^{-1} with W unit lower at the tournament's pivot rows
+        y = np.asfortranarray(O.gaussian(3, 500, 40))
+        Y = D.ShardedMatrix(ops.from_numpy(y, cuda_dev), 500, 0, 500, D.CudaOps(cuda_dev))
+        w = ops.to_numpy(D.tslu_basis_rows(Y, Y.local, 40))
+        ref = O.plu(y)
+        w_ref = O.apply_inv_row_perm(ref.p, ref.L)  # exact GEPP's P^T L: same U for one rank
+        assert np.abs(w - w_ref).max() <= 1e-12 * np.abs(w_ref).max()
     finally:
         dist.destroy_process_group()
 
