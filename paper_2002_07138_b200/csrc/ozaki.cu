@@ -124,38 +124,58 @@ static Crt make_crt(int nmod) {
 // ----------------------------------------------------------------- residues
 // x = rint(v * 2^e), |x| < 2^55, as four float parts x = p3 2^42 + p2 2^28 +
 // p1 2^14 + p0 with p0..p2 in [0, 2^14) and p3 signed (two's complement split).
-struct Parts {
-  float p0, p1, p2, p3;
+// Residue modulo m: v = p3 (2^42 mod m) + p2 (2^28 mod m) + p1 (2^14 mod m) + p0
+// (exact in fp32, |v| < 2^24), q ~ rint(v / m), r = v - q m exact in
+// [-m/2-1, m/2+1] (|r| <= 126), returned as the low byte of the float r + 1.5*2^23.
+__device__ __forceinline__ unsigned pack4(unsigned b0, unsigned b1, unsigned b2, unsigned b3) {
+  return __byte_perm(__byte_perm(b0, b1, 0x0040), __byte_perm(b2, b3, 0x0040), 0x5410);
+}
+
+// ---- the same arithmetic on PAIRS of values with the packed fp32x2 pipe
+// (FFMA2 / FADD2, sm_100): two values per instruction, half the instruction
+// count of scalar fp32 -- the residue kernel is issue-bound, not HBM-bound,
+// without it.
+typedef unsigned long long f2_t;  // (lo = element 2i, hi = element 2i+1)
+__device__ __forceinline__ f2_t f2_ffma(f2_t a, f2_t b, f2_t c) {
+  f2_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ f2_t f2_fadd(f2_t a, f2_t b) {
+  f2_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ f2_t f2_bits(unsigned lo, unsigned hi) { return ((f2_t)hi << 32) | lo; }
+__device__ __forceinline__ f2_t f2_dup(float v) { return f2_bits(__float_as_uint(v), __float_as_uint(v)); }
+
+struct Parts2 {
+  f2_t p0, p1, p2, p3;
 };
-__device__ __forceinline__ Parts split_parts(double v, double scale) {
-  const long long xi = __double2ll_rn(v * scale);
-  const unsigned lo = (unsigned)xi;
-  const unsigned hi = (unsigned)(xi >> 28);  // bits 28..59 (sign-extended)
-  Parts p;
-  p.p0 = __int_as_float(0x4B000000 | (lo & 0x3FFF)) - 8388608.0f;
-  p.p1 = __int_as_float(0x4B000000 | ((lo >> 14) & 0x3FFF)) - 8388608.0f;
-  p.p2 = __int_as_float(0x4B000000 | (hi & 0x3FFF)) - 8388608.0f;
-  p.p3 = __int_as_float(0x4B400000 + ((int)hi >> 14)) - 12582912.0f;  // signed, |p3| < 2^13
+__device__ __forceinline__ Parts2 split_parts2(double va, double vb, double scale) {
+  const long long xa = __double2ll_rn(va * scale), xb = __double2ll_rn(vb * scale);
+  const unsigned la = (unsigned)xa, lb = (unsigned)xb;
+  const unsigned ha = (unsigned)(xa >> 28), hb = (unsigned)(xb >> 28);
+  const f2_t m23 = f2_dup(-8388608.0f);
+  Parts2 p;
+  p.p0 = f2_fadd(f2_bits(0x4B000000 | (la & 0x3FFF), 0x4B000000 | (lb & 0x3FFF)), m23);
+  p.p1 = f2_fadd(f2_bits(0x4B000000 | ((la >> 14) & 0x3FFF), 0x4B000000 | ((lb >> 14) & 0x3FFF)), m23);
+  p.p2 = f2_fadd(f2_bits(0x4B000000 | (ha & 0x3FFF), 0x4B000000 | (hb & 0x3FFF)), m23);
+  p.p3 = f2_fadd(f2_bits(0x4B400000 + ((int)ha >> 14), 0x4B400000 + ((int)hb >> 14)), f2_dup(-12582912.0f));
   return p;
 }
 
-// Residue of the part-encoded integer modulo kModuli[L], in [-m/2-1, m/2+1]
-// (|r| <= 126), returned as the low byte of a float-encoded integer.
+// residue_byte<L> of both values of a pair: the two floats' low bytes
 template <int L>
-__device__ __forceinline__ unsigned residue_byte(const Parts& x) {
+__device__ __forceinline__ f2_t residue_pair(const Parts2& x) {
   constexpr int m = kModuli[L];
-  constexpr float c1 = (float)pow2mod(14, m);
-  constexpr float c2 = (float)pow2mod(28, m);
-  constexpr float c3 = (float)pow2mod(42, m);
-  constexpr float inv = 1.0f / (float)m;
-  const float v = fmaf(x.p3, c3, fmaf(x.p2, c2, fmaf(x.p1, c1, x.p0)));  // exact, |v| < 2^24
-  const float q = __fadd_rn(fmaf(v, inv, 12582912.0f), -12582912.0f);  // ~rint(v / m)
-  const float r = fmaf(-q, (float)m, v);                                // exact
-  return (unsigned)__float_as_int(__fadd_rn(r, 12582912.0f));           // low byte = r (two's compl.)
-}
-
-__device__ __forceinline__ unsigned pack4(unsigned b0, unsigned b1, unsigned b2, unsigned b3) {
-  return __byte_perm(__byte_perm(b0, b1, 0x0040), __byte_perm(b2, b3, 0x0040), 0x5410);
+  const f2_t c1 = f2_dup((float)pow2mod(14, m)), c2 = f2_dup((float)pow2mod(28, m));
+  const f2_t c3 = f2_dup((float)pow2mod(42, m)), inv = f2_dup(1.0f / (float)m);
+  const f2_t big = f2_dup(12582912.0f), nbig = f2_dup(-12582912.0f), nm = f2_dup(-(float)m);
+  const f2_t v = f2_ffma(x.p3, c3, f2_ffma(x.p2, c2, f2_ffma(x.p1, c1, x.p0)));  // exact, |v| < 2^24
+  const f2_t q = f2_fadd(f2_ffma(v, inv, big), nbig);                             // ~rint(v / m)
+  const f2_t r = f2_ffma(q, nm, v);                                               // exact
+  return f2_fadd(r, big);                                                         // low bytes = r
 }
 
 template <int N>
@@ -169,14 +189,15 @@ struct Bytes<8> {
   typedef uint2 T;
 };
 
-// N (8 or 16) consecutive values -> N residue bytes for modulus L.
+// N (8 or 16) consecutive values (N/2 pairs) -> N residue bytes for modulus L.
 template <int L, int N>
-__device__ __forceinline__ typename Bytes<N>::T residue_chunk(const Parts (&x)[N]) {
+__device__ __forceinline__ typename Bytes<N>::T residue_chunk(const Parts2 (&x)[N / 2]) {
   unsigned w[N / 4];
 #pragma unroll
-  for (int q = 0; q < N / 4; ++q)
-    w[q] = pack4(residue_byte<L>(x[4 * q]), residue_byte<L>(x[4 * q + 1]), residue_byte<L>(x[4 * q + 2]),
-                 residue_byte<L>(x[4 * q + 3]));
+  for (int q = 0; q < N / 4; ++q) {
+    const f2_t a = residue_pair<L>(x[2 * q]), b = residue_pair<L>(x[2 * q + 1]);
+    w[q] = pack4((unsigned)a, (unsigned)(a >> 32), (unsigned)b, (unsigned)(b >> 32));
+  }
   typename Bytes<N>::T o;
   if constexpr (N == 16) {
     o.x = w[0]; o.y = w[1]; o.z = w[2]; o.w = w[3];
@@ -188,14 +209,14 @@ __device__ __forceinline__ typename Bytes<N>::T residue_chunk(const Parts (&x)[N
 
 template <int L, int NMOD, int N>
 struct ChunkWriter {
-  __device__ __forceinline__ static void run(const Parts (&x)[N], int8_t* base, size_t mod_stride) {
+  __device__ __forceinline__ static void run(const Parts2 (&x)[N / 2], int8_t* base, size_t mod_stride) {
     *reinterpret_cast<typename Bytes<N>::T*>(base + (size_t)L * mod_stride) = residue_chunk<L, N>(x);
     ChunkWriter<L + 1, NMOD, N>::run(x, base, mod_stride);
   }
 };
 template <int NMOD, int N>
 struct ChunkWriter<NMOD, NMOD, N> {
-  __device__ __forceinline__ static void run(const Parts (&)[N], int8_t*, size_t) {}
+  __device__ __forceinline__ static void run(const Parts2 (&)[N / 2], int8_t*, size_t) {}
 };
 
 __device__ __forceinline__ int swz(int r, int c) {  // byte offset of 16-byte chunk c of row r
@@ -235,9 +256,9 @@ __global__ void __launch_bounds__(256, 2) residue_a_kernel(const double* __restr
     if (s + 1 < 8) load(s + 1, nxt);
     const int ch = threadIdx.x + 256 * s;
     const int r = ch >> 4, h = ch & 15;
-    Parts x[8];
+    Parts2 x[4];
 #pragma unroll
-    for (int t = 0; t < 8; ++t) x[t] = split_parts(cur[t], scale);
+    for (int t = 0; t < 4; ++t) x[t] = split_parts2(cur[2 * t], cur[2 * t + 1], scale);
     ChunkWriter<0, NMOD, 8>::run(x, tile + swz(r, h >> 1) + (h & 1) * 8, mod_stride);
 #pragma unroll
     for (int t = 0; t < 8; ++t) cur[t] = nxt[t];
@@ -300,13 +321,15 @@ __global__ void __launch_bounds__(256) residue_b_kernel(const double* __restrict
   const int64_t kb = ch >> 3;
   const int c = (int)(ch & 7);
   const int64_t i0 = kb * kTile + c * 16;
-  Parts x[16];
+  double v[16];
 #pragma unroll
   for (int t = 0; t < 16; ++t) {
     const int64_t i = i0 + t;
-    const double v = (jj < ncols && i < k) ? b[i + jj * ldb] : 0.0;
-    x[t] = split_parts(v, scale);
+    v[t] = (jj < ncols && i < k) ? b[i + jj * ldb] : 0.0;
   }
+  Parts2 x[8];
+#pragma unroll
+  for (int t = 0; t < 8; ++t) x[t] = split_parts2(v[2 * t], v[2 * t + 1], scale);
   ChunkWriter<0, NMOD, 16>::run(x, tile0 + (size_t)kb * n_g * kTile + swz(r, c), mod_stride);
 }
 
