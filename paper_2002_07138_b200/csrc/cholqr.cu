@@ -168,12 +168,23 @@ __global__ void __launch_bounds__(CHOL_THREADS, 1)
         for (int q = 0; q < 4; q++)
 #pragma unroll
           for (int w = 0; w < 4; w++) acc[q][w] = 0.0;
+        // packed column c holds rows 0..c contiguously: the block row's entries
+        // (k0 + s2, c) sit at c(c+1)/2 + k0 + s2 (columns past l are clamped:
+        // their products are never stored)
+        int ba[4], bb[4];
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+          const int ca = min(ja + q, l - 1), cb = min(jb + q, l - 1);
+          ba[q] = ca * (ca + 1) / 2 + k0;
+          bb[q] = cb * (cb + 1) / 2 + k0;
+        }
+#pragma unroll 4
         for (int s2 = 0; s2 < b; s2++) {
           double ra[4], rb[4];
 #pragma unroll
           for (int q = 0; q < 4; q++) {
-            ra[q] = (ja + q < l) ? P[pk(k0 + s2, ja + q)] : 0.0;
-            rb[q] = (jb + q < l) ? P[pk(k0 + s2, jb + q)] : 0.0;
+            ra[q] = P[ba[q] + s2];
+            rb[q] = P[bb[q] + s2];
           }
 #pragma unroll
           for (int q = 0; q < 4; q++)
