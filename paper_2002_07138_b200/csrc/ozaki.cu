@@ -227,7 +227,7 @@ __device__ __forceinline__ int swz(int r, int c) {  // byte offset of 16-byte ch
 // converts 8 x 8 consecutive rows of one column (half swizzle chunks), with the
 // next group's loads in flight while the current one is converted.
 template <int NMOD>
-__global__ void __launch_bounds__(256, 2) residue_a_kernel(const double* __restrict__ a, int64_t lda, int64_t m,
+__global__ void __launch_bounds__(256, 3) residue_a_kernel(const double* __restrict__ a, int64_t lda, int64_t m,
                                                            int64_t n, const int* __restrict__ e_a,
                                                            int8_t* __restrict__ tiles, int64_t nib, int64_t njb) {
   const int64_t ib = blockIdx.x, jb = blockIdx.y;
