@@ -128,6 +128,7 @@ RLRA_B200_API int rlra_b200_oz_gemm(int trans, const void* prep, int64_t m, int6
  * bit-identical to the one-block product. */
 #define RLRA_B200_OZ_ACCUMULATE 1
 #define RLRA_B200_OZ_NO_CRT 2
+#define RLRA_B200_OZ_ADD_TO_C 4 /* C += A B (the single-pass H += panel G_j) */
 RLRA_B200_API size_t rlra_b200_oz_scale_workspace(int64_t m, int64_t n);
 RLRA_B200_API int rlra_b200_oz_scale(const double* a, int64_t lda, int64_t m, int64_t n, int nmod, int* e_a,
                                      void* ws, size_t ws_bytes, void* stream);

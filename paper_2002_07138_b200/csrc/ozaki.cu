@@ -675,7 +675,7 @@ __device__ __forceinline__ double u128_to_double(u128 x) {
 __global__ void __launch_bounds__(256) crt_kernel(const uint8_t* __restrict__ t, int64_t rows_pad, int64_t cols_pad,
                                                   int64_t mrows, int64_t ncols, const int* __restrict__ e_a,
                                                   const int* __restrict__ e_b, const Crt crt, double* __restrict__ c,
-                                                  int64_t ldc) {
+                                                  int64_t ldc, int add) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t j = blockIdx.y;
   if (i >= mrows) return;
@@ -711,7 +711,8 @@ __global__ void __launch_bounds__(256) crt_kernel(const uint8_t* __restrict__ t,
   }
   const u128 mag = (s > H) ? M - s : s;
   const double v = fma((double)(uint64_t)(mag >> 64), 0x1p64, (double)(uint64_t)mag);  // within 1 ulp
-  c[i + j * ldc] = ((s > H) ? -v : v) * scalbn(1.0, -(e_a[0] + e_b[j]));
+  const double r = ((s > H) ? -v : v) * scalbn(1.0, -(e_a[0] + e_b[j]));
+  c[i + j * ldc] = add ? c[i + j * ldc] + r : r;  // add: C += A B (one rounding of the sum, like beta = 1)
 }
 
 // ----------------------------------------------------------------- host side
@@ -954,7 +955,7 @@ int oz_gemm_ex(int trans, const void* prep, int64_t m, int64_t n, int nmod, cons
   if (flags & 2) return 0;  // RLRA_B200_OZ_NO_CRT: more K blocks follow
   ktimer_mark(KT_OZ_CRT, st, false);
   oz::crt_kernel<<<dim3((unsigned)ceil_div(mrows, 256), (unsigned)ncols), 256, 0, st>>>(
-      tout, g.rows_pad, g.cols_pad, mrows, ncols, e_a, e_b, crt, c, ldc);
+      tout, g.rows_pad, g.cols_pad, mrows, ncols, e_a, e_b, crt, c, ldc, (flags & 4) ? 1 : 0);
   ktimer_mark(KT_OZ_CRT, st, true);
   RLRA_LAUNCHED();
   return 0;

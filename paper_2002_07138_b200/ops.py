@@ -195,25 +195,29 @@ class OzPrep:
         _call("rlra_b200_oz_prep", a.device, ptr(a), ld_of(a), self.m, self.n, self.nmod, ptr(self.ws), wsb,
               _stream(a.device))
 
-    def gemm(self, b, trans=False, keep_ws=False):
-        """C = A B (trans=False, b n x l) or A^T B (trans=True, b m x l)."""
+    def gemm(self, b, trans=False, keep_ws=False, out=None, add=False):
+        """C = A B (trans=False, b n x l) or A^T B (trans=True, b m x l); with
+        `out`, the product is written into it (add=True: out += A B)."""
         k, rows = (self.m, self.n) if trans else (self.n, self.m)
         if b.shape[0] != k:
             raise ValueError(f"oz gemm shape mismatch: A {(self.m, self.n)} trans={trans}, B {tuple(b.shape)}")
         ncols = int(b.shape[1])
-        c = fmat(rows, ncols, self.device)
+        c = fmat(rows, ncols, self.device) if out is None else out
+        if tuple(c.shape) != (rows, ncols):
+            raise ValueError(f"oz gemm output shape {tuple(c.shape)}, expected {(rows, ncols)}")
         if ncols == 0:
             return (c, None) if keep_ws else c
         b = as_fmat(b)
         wsb = _native.query("rlra_b200_oz_gemm_workspace", int(trans), self.m, self.n, ncols, self.nmod)
         ws = torch.empty(max(wsb, 8), dtype=torch.uint8, device=self.device)
-        _call("rlra_b200_oz_gemm", self.device, int(trans), ptr(self.ws), self.m, self.n, self.nmod, ptr(b),
-              ld_of(b), ncols, ptr(c), ld_of(c), ptr(ws), wsb, _stream(self.device))
+        _call("rlra_b200_oz_gemm_ex", self.device, int(trans), ptr(self.ws), self.m, self.n, self.nmod, ptr(b),
+              ld_of(b), ncols, ptr(c), ld_of(c), ptr(ws), wsb, None, OZ_ADD_TO_C if add else 0,
+              _stream(self.device))
         return (c, ws) if keep_ws else c
 
 
 OZ_BLOCK_K = 133120  # largest multiple of 256 inside the exact int32 K range (133144)
-OZ_ACCUMULATE, OZ_NO_CRT = 1, 2  # include/rlra_b200.h
+OZ_ACCUMULATE, OZ_NO_CRT, OZ_ADD_TO_C = 1, 2, 4  # include/rlra_b200.h
 
 
 def _split(total, cap):

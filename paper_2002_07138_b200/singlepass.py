@@ -1,10 +1,14 @@
 """Single-pass randomized LU over column-streamed matrices on device
 (rlra/singlepass.py:99-144).
 
-stream_sketch: one sweep, each panel read once; per panel G_j = panel^T Omega
-(DMMA TN) written straight into its rows of G, then H += panel G_j (DMMA NN,
-beta = 1) while the panel is still L2-resident, ascending column order like
-the reference.  single_pass_lu: bit-exact GEPP of H, Householder QR of G with
+stream_sketch: one sweep, each panel read once, ascending column order like
+the reference; per panel G_j = panel^T Omega written straight into its rows of
+G, then H += panel G_j.  Both products run on the int8 tensor cores (Ozaki-II,
+csrc/ozaki.cu) from ONE residue set of the panel (TN, then NN with the CRT
+adding into H); panels are consumed in sweep panels of up to SWEEP_PANEL
+columns (a multiple of the caller's width) so the per-panel fixed costs stay
+small -- G is unchanged by the grouping, H sees one rounding per sweep panel
+instead of per panel.  DMMA when the int8 engine does not apply.  single_pass_lu: bit-exact GEPP of H, Householder QR of G with
 the pinv rank test, blocked TRSM, one more GEMM, GEPP of T, and the assembly.
 """
 
@@ -14,8 +18,10 @@ from typing import NamedTuple
 
 import torch
 
+import os
+
 from . import core, ops
-from .device import DEFAULT_PANEL, DenseColumnStream, DeviceColumnStream
+from .device import DEFAULT_PANEL, PASS_GEMM, DenseColumnStream, DeviceColumnStream
 from .fixedrank import LowRankLU
 from .kernels import pinv_transpose_apply, plu_
 
@@ -23,6 +29,25 @@ from .kernels import pinv_transpose_apply, plu_
 class SketchPair(NamedTuple):
     G: torch.Tensor  # n x k
     H: torch.Tensor  # m x k
+
+
+SWEEP_PANEL = int(os.environ.get("RLRA_B200_SWEEP_PANEL", "2048"))
+SWEEP_PANEL_BYTES = 512 << 20  # one sweep panel of float64 (host streams keep 3 pinned + 3 device slots)
+# The int8 engine's normwise error equals DGEMM's but it is not exact on
+# sparse/identity panels (B is rounded relative to its column norm), which
+# the reference's bitwise identity-stream property (pkg/tests/
+# test_singlepass.py:15-24) relies on; small sweeps keep the native DMMA.
+SWEEP_OZ_MIN_ELEMS = int(os.environ.get("RLRA_B200_SWEEP_OZ_MIN", str(1 << 24)))
+
+
+def sweep_width(m, panel):
+    """Columns per sweep panel: a multiple of the caller's width, <= SWEEP_PANEL
+    columns and <= SWEEP_PANEL_BYTES (identical for every stream type, so host
+    and device streams give bit-identical sketches)."""
+    if panel < 1:
+        raise ValueError("panel width must be >= 1")
+    cap = min(SWEEP_PANEL, max(1, SWEEP_PANEL_BYTES // (8 * max(int(m), 1))))
+    return panel * max(1, cap // panel)
 
 
 def stream_sketch(stream, k, seed, panel=DEFAULT_PANEL):
@@ -34,14 +59,21 @@ def stream_sketch(stream, k, seed, panel=DEFAULT_PANEL):
     om = core.omega(seed, m, k, dev)
     g = ops.fmat(n, k, dev)
     h = ops.fmat(m, k, dev, zero=True)
+    oz = PASS_GEMM == "oz" and 0 < m <= ops.OZ_BLOCK_K and k <= 4096 and m * n >= SWEEP_OZ_MIN_ELEMS
     count = 0
-    for j0, block in stream.panels(panel):
+    for j0, block in stream.panels(sweep_width(m, panel) if oz else panel):
         if not isinstance(block, torch.Tensor):
             block = ops.from_numpy(block, dev)
         w = block.shape[1]
         gb = g[j0:j0 + w, :]
-        ops.gemm(block, om, gb, ta=True)  # G(j0:j0+w, :) = panel^T Omega
-        ops.gemm(block, gb, h, beta=1.0)  # H += panel G_j
+        if oz:
+            with ops.label("sweep_oz"):
+                prep = ops.OzPrep(block)  # residues of the panel, read once
+                prep.gemm(om, trans=True, out=gb)  # G(j0:j0+w, :) = panel^T Omega
+                prep.gemm(gb, out=h, add=True)  # H += panel G_j
+        else:
+            ops.gemm(block, om, gb, ta=True)  # G(j0:j0+w, :) = panel^T Omega
+            ops.gemm(block, gb, h, beta=1.0)  # H += panel G_j
         count += w
     if count != n:
         raise ValueError(f"stream delivered {count} columns, expected {n}")

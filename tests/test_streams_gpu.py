@@ -64,3 +64,33 @@ def test_file_stream_truncated(cuda_dev, tmp_path):
         fh.truncate(20 + 8 * 50 * 30)
     with pytest.raises(IOError, match="truncated"):
         P.stream_sketch(s, 5, 0, panel=16)
+
+
+@pytest.mark.parametrize("panel", [64, 256])
+def test_int8_sweep_matches_products_and_streams_agree(cuda_dev, tmp_path, monkeypatch, panel):
+    """The int8 (Ozaki-II) sweep, forced at a small size: G = A^T Omega and
+    H = A G within DGEMM-level normwise error of the float64 products, and the
+    file / host / device streams bit-identical to each other."""
+    import torch
+
+    import paper_2002_07138_b200 as P
+    from paper_2002_07138_b200 import ops, singlepass
+
+    monkeypatch.setattr(singlepass, "SWEEP_OZ_MIN_ELEMS", 0)
+    monkeypatch.setattr(singlepass, "SWEEP_PANEL", 512)
+    rng = np.random.default_rng(7)
+    a = np.asfortranarray(rng.standard_normal((1500, 1300)) * np.exp(rng.uniform(-3, 3, size=(1, 1300))))
+    path = tmp_path / "a.rlm"
+    P.write_rlra(path, a)
+    ref = P.stream_sketch(P.DeviceColumnStream(a), 40, 2, panel=panel)
+    g, h = ops.to_numpy(ref.G), ops.to_numpy(ref.H)
+    om = O.gaussian(2, 1500, 40)
+    g64 = a.T @ om
+    h64 = a @ g64
+    na = np.linalg.norm(a)
+    assert np.abs(g - g64).max() <= 1e-13 * na * np.linalg.norm(om, axis=0).max()
+    assert np.abs(h - h64).max() <= 1e-12 * na * np.linalg.norm(g64, axis=0).max()
+    for s in (P.RlraFileColumnStream(path), P.DenseColumnStream(a)):
+        got = P.stream_sketch(s, 40, 2, panel=panel)
+        torch.cuda.synchronize()
+        assert torch.equal(got.G, ref.G) and torch.equal(got.H, ref.H)
