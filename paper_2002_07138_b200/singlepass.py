@@ -31,8 +31,8 @@ class SketchPair(NamedTuple):
     H: torch.Tensor  # m x k
 
 
-SWEEP_PANEL = int(os.environ.get("RLRA_B200_SWEEP_PANEL", "2048"))
-SWEEP_PANEL_BYTES = 512 << 20  # one sweep panel of float64 (host streams keep 3 pinned + 3 device slots)
+SWEEP_PANEL = int(os.environ.get("RLRA_B200_SWEEP_PANEL", "8192"))
+SWEEP_PANEL_BYTES = int(os.environ.get("RLRA_B200_SWEEP_BYTES", str(2 << 30)))  # one sweep panel of float64 (host streams keep 3 pinned + 3 device slots)
 # The int8 engine's normwise error equals DGEMM's but it is not exact on
 # sparse/identity panels (B is rounded relative to its column norm), which
 # the reference's bitwise identity-stream property (pkg/tests/
