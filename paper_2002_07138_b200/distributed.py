@@ -91,6 +91,15 @@ class CudaOps:
         qr = self.o.QR(x)
         return qr.q(), self.o.count_nonzero_diag(qr.r_view())
 
+    def qr_q_fast(self, x):
+        """powerlu's final basis as on one GPU: CholeskyQR2, Householder when
+        the Cholesky declines (rangefinder.qr_basis_ with method="chol")."""
+        if x.shape[0] >= x.shape[1] and 0 < x.shape[1] <= self.o.cholqr_max_l():
+            q, flag = self.o.cholqr2(x)
+            if not int(flag.item()):
+                return q, None
+        return self.qr_q(x)
+
     def transpose(self, a):
         return self.o.transpose(a)
 
@@ -204,7 +213,7 @@ class ShardedMatrix:
         return full[self.r0:self.r1, :]
 
 
-INTERIOR = os.environ.get("RLRA_B200_DIST_INTERIOR", "tslu")  # "tslu" | "gather"
+INTERIOR = os.environ.get("RLRA_B200_DIST_INTERIOR", "tslu")  # "tslu" | "gather" | "tslu_always" (also 1 rank)
 
 
 def tslu_basis_rows(A, y_local, l):
@@ -241,9 +250,22 @@ def _check(count, requested):
         raise RankCollapse(achieved, requested)
 
 
-def general_power_basis_v(A: ShardedMatrix, l, v, seed, omega_fn):
+def _use_tslu(A, l):
+    """Interior LU of a row-sharded sketch: TSLU at 4+ ranks or tall sketches
+    (the all-gather of m x l and the replicated m x l GEPP grow with m, the
+    tournament does not); the all-gathered exact GEPP at 2 ranks."""
+    if INTERIOR == "tslu_always":
+        return True
+    if INTERIOR != "tslu" or A.world < 2:
+        return False
+    return A.world >= 4 or A.m > 131072
+
+
+def general_power_basis_v(A: ShardedMatrix, l, v, seed, omega_fn, fast_qr=False):
     """rlra/rangefinder.py:144-176 over a row-sharded A.  omega_fn(seed, rows, l)
-    returns the full host Omega (bit-exact rlra.core.gaussian)."""
+    returns the full Omega (bit-exact rlra.core.gaussian): a host array, or a
+    device tensor (core.omega) that is sliced in place.  fast_qr: powerlu's
+    final basis by CholeskyQR2 (as on one GPU)."""
     m, n = A.shape
     if not 1 <= l <= min(m, n):
         raise ValueError(f"sketch width l={l} outside 1..min{(m, n)}")
@@ -252,7 +274,7 @@ def general_power_basis_v(A: ShardedMatrix, l, v, seed, omega_fn):
     ops = A.ops
 
     def lu_basis_rows(y_local):
-        if INTERIOR == "tslu" and A.world > 1:
+        if _use_tslu(A, l):
             return tslu_basis_rows(A, y_local, l)
         full = A.gather_rows(y_local)
         piv, cnt = ops.getrf_(full)
@@ -265,19 +287,24 @@ def general_power_basis_v(A: ShardedMatrix, l, v, seed, omega_fn):
         return ops.lu_basis(z, piv)
 
     def qr_basis(z):
-        q, cnt = ops.qr_q(z)
-        _check(cnt, l)
+        q, cnt = (ops.qr_q_fast if fast_qr and hasattr(ops, "qr_q_fast") else ops.qr_q)(z)
+        if cnt is not None:
+            _check(cnt, l)
         return q
 
+    def omega_rows(rows, r0, r1):
+        om = omega_fn(seed, rows, l)
+        if isinstance(om, torch.Tensor):  # device Omega (core.omega): slice, no copy
+            return om[r0:r1]
+        return ops.upload(np.asfortranarray(om[r0:r1]))
+
     if v % 2 == 0:
-        om = omega_fn(seed, m, l)
-        om_local = ops.upload(np.asfortranarray(om[A.r0:A.r1]))
-        x = A.rmatmul(om_local)
+        x = A.rmatmul(omega_rows(m, A.r0, A.r1))
         if v == 2:
             return qr_basis(x), 1
         w = lu_basis_repl(x)
     else:
-        w = ops.upload(omega_fn(seed, n, l))
+        w = omega_rows(n, 0, n)
     half = (v - 1) // 2
     passes = 1 if v % 2 == 0 else 0
     basis = None
@@ -319,7 +346,7 @@ def powerlu(A: ShardedMatrix, k, q_os=10, v=3, seed=0, omega_fn=None):
     if k + q_os > min(m, n):
         raise ValueError(f"sketch width {k + q_os} exceeds min{(m, n)}")
     with A.products():
-        V, _ = general_power_basis_v(A, k + q_os, v, seed, omega_fn)
+        V, _ = general_power_basis_v(A, k + q_os, v, seed, omega_fn, fast_qr=True)
         vk = V[:, :k]
         g_local = A.matmul(vk)
     return lu_from_projection(A, g_local, vk)
@@ -361,8 +388,6 @@ def bench_main(args):
     import time
 
     from . import configs
-    from .core import gaussian
-
     rank = int(os.environ["RANK"])
     world = int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
@@ -374,18 +399,24 @@ def bench_main(args):
     passes, fact = configs.powerlu_flops(w.m, w.n, w.k, w.k + w.q_os, v)
     flops = passes + fact
     r0, r1 = row_range(w.m, world, rank)
-    gen = {"C1": configs.gen_c1, "C2": configs.gen_c2, "C5": configs.gen_c5}[w.name]
-    a = gen()
     ops = CudaOps(dev)
-    A = ShardedMatrix(ops.upload(np.asfortranarray(a[r0:r1])), w.m, r0, r1, ops)
-    del a
-    cache = {}
+    if w.name in ("C1", "C2"):
+        a = {"C1": configs.gen_c1, "C2": configs.gen_c2}[w.name]()
+        shard = ops.upload(np.asfortranarray(a[r0:r1]))
+    else:  # C5 (68.7 GB): built in HBM (configs.gen_device), this rank keeps its rows
+        full = configs.gen_device(w.name, dev)
+        shard = ops.empty(r1 - r0, w.n)
+        shard.copy_(full[r0:r1])
+        del full
+        torch.cuda.empty_cache()
+    A = ShardedMatrix(shard, w.m, r0, r1, ops)
+    a = None
+    from . import core as _core
+
+    _core.set_omega_cache(True)  # as the single-GPU bench: Omega is an input, drawn once on the device
 
     def omega(seed, rows, l):
-        key = (seed, rows, l)
-        if key not in cache:
-            cache[key] = gaussian(seed, rows, l)
-        return cache[key]
+        return _core.omega(seed, rows, l, dev)
 
     for _ in range(args.warmup):
         powerlu(A, w.k, w.q_os, v, w.seed, omega)

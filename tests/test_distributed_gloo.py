@@ -143,7 +143,7 @@ def decay_matrix(m, n, seed, r=None):
 @pytest.mark.parametrize("v", [2, 3, 4, 5])
 def test_sharded_powerlu_matches_single_process(v):
     a = decay_matrix(203, 150, seed=v)  # 203 rows: uneven shards
-    res = run_dist({"kind": "powerlu", "a": a, "k": 20, "q_os": 8, "v": v, "seed": 1})
+    res = run_dist({"kind": "powerlu", "a": a, "k": 20, "q_os": 8, "v": v, "seed": 1, "interior": "tslu_always"})
     ref = O.powerlu(a, 20, 8, v, 1)
     for rank, (p, q, L, U, passes) in res.items():
         assert np.array_equal(p, ref.p) and np.array_equal(q, ref.q)
