@@ -3,7 +3,8 @@
 // rlra/kernels.py:57-61) used by rangefinder._qr_basis (rlra/rangefinder.py:67-70)
 // and kernels.pinv_factor (rlra/kernels.py:64-79).
 //
-// Blocked right-looking Householder (panel width QR_NB = 32), LAPACK dlarfg sign
+// Blocked right-looking Householder (panel width QR_NB = 32, two-level: outer
+// blocks of QR_NBO = 128 columns carry the trailing update), LAPACK dlarfg sign
 // convention (beta = -sign(alpha) * ||x||, tau = (beta - alpha) / beta, v(1) = 1),
 // so R's diagonal signs and Q's column signs follow NumPy's.  CholeskyQR2 is not
 // used: the final-QR inputs reach cond 6.7e8.
@@ -369,6 +370,35 @@ __global__ void qr_larft_kernel(const double* __restrict__ gram, int nb, const d
   for (int e = threadIdx.x; e < nb * nb; e += blockDim.x) T[e] = Ts[e % nb][e / nb];
 }
 
+// dlarft for an outer block of nbo <= QR_NBO columns: the same recurrence with
+// T in shared memory (dynamic) and S read from global memory; one CTA, thread
+// t owns row t of T.
+constexpr int QR_NBO = 128;
+__global__ void __launch_bounds__(QR_NBO) qr_larft_big_kernel(const double* __restrict__ gram, int nb,
+                                                             const double* __restrict__ tau,
+                                                             double* __restrict__ T) {
+  extern __shared__ double Tsb[];  // [QR_NBO][QR_NBO + 1], row t at t * (QR_NBO + 1)
+  __shared__ double y[QR_NBO];
+  const int t = threadIdx.x;
+  constexpr int LD = QR_NBO + 1;
+  for (int c = 0; c < nb; c++) Tsb[t * LD + c] = 0.0;
+  __syncthreads();
+  for (int i = 0; i < nb; i++) {
+    const double ti = tau[i];
+    if (t < i) y[t] = -ti * gram[t + (int64_t)i * nb];
+    __syncthreads();
+    if (t < i) {
+      double acc = 0.0;
+      for (int k = t; k < i; k++) acc += Tsb[t * LD + k] * y[k];
+      Tsb[t * LD + i] = acc;
+    }
+    if (t == i) Tsb[t * LD + i] = ti;
+    __syncthreads();
+  }
+  if (t < nb)
+    for (int c = 0; c < nb; c++) T[t + (int64_t)c * nb] = Tsb[t * LD + c];
+}
+
 __global__ void set_identity_kernel(double* q, int64_t ldq, int64_t m, int64_t n) {
   const int64_t total = m * n;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
@@ -391,7 +421,7 @@ static int qr_pw(int64_t m, int sms) {
 }
 
 struct QrLayout {
-  size_t part, diag, bar, recg, gramp, vbuf, gram, tblocks, wbuf, w2buf, gemm_ws, total;
+  size_t part, diag, bar, recg, gramp, vbuf, gram, tblocks, tbig, wbuf, w2buf, gemm_ws, total;
 };
 
 static QrLayout qr_layout(int64_t m, int64_t n, int G) {
@@ -404,14 +434,15 @@ static QrLayout qr_layout(int64_t m, int64_t n, int G) {
   take(L.bar, 2 * sizeof(unsigned));
   take(L.recg, (size_t)(2 * 16 * (2 + QR_NB) + 2 * QR_NB) * sizeof(double));
   take(L.gramp, (size_t)16 * QR_NB * QR_NB * sizeof(double));
-  take(L.vbuf, (size_t)m * QR_NB * sizeof(double));
-  take(L.gram, QR_NB * QR_NB * sizeof(double));
+  take(L.vbuf, (size_t)m * QR_NBO * sizeof(double));
+  take(L.gram, QR_NBO * QR_NBO * sizeof(double));
   take(L.tblocks, (size_t)npan * QR_NB * QR_NB * sizeof(double));
-  take(L.wbuf, (size_t)QR_NB * n * sizeof(double));
-  take(L.w2buf, (size_t)QR_NB * n * sizeof(double));
-  // split-K partials of the skinny (QR_NB-row) GEMMs: at most 32 splits
-  size_t g = (size_t)32 * QR_NB * std::max<int64_t>(n, QR_NB) * sizeof(double);
-  g = std::max(g, gemm_workspace_bytes(m, n, QR_NB));
+  take(L.tbig, (size_t)ceil_div(n, QR_NBO) * QR_NBO * QR_NBO * sizeof(double));
+  take(L.wbuf, (size_t)QR_NBO * n * sizeof(double));
+  take(L.w2buf, (size_t)QR_NBO * n * sizeof(double));
+  // split-K partials of the skinny GEMMs: at most 32 splits
+  size_t g = (size_t)32 * QR_NBO * std::max<int64_t>(n, QR_NBO) * sizeof(double);
+  g = std::max(g, gemm_workspace_bytes(m, n, QR_NBO));
   take(L.gemm_ws, g);
   L.total = o;
   return L;
@@ -490,11 +521,21 @@ int geqrf(double* a, int64_t lda, int64_t m, int64_t n, double* tau, void* ws, s
   double* vbuf = reinterpret_cast<double*>(base + L.vbuf);
   double* gram = reinterpret_cast<double*>(base + L.gram);
   double* tbl = reinterpret_cast<double*>(base + L.tblocks);
+  double* tbig = reinterpret_cast<double*>(base + L.tbig);
   double* wbuf = reinterpret_cast<double*>(base + L.wbuf);
   double* w2buf = reinterpret_cast<double*>(base + L.w2buf);
   void* gws = base + L.gemm_ws;
   const size_t gws_bytes = L.total - L.gemm_ws;
   RLRA_CHECK_CUDA(cudaMemsetAsync(bar, 0, 2 * sizeof(unsigned), st));
+  {
+    static std::once_flag once;
+    static cudaError_t e = cudaSuccess;
+    std::call_once(once, [] {
+      e = cudaFuncSetAttribute(qr_larft_big_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)((size_t)QR_NBO * (QR_NBO + 1) * sizeof(double)));
+    });
+    RLRA_CHECK_CUDA(e);
+  }
   // Panel: one thread-block cluster (DSMEM multicast exchange) while the rows
   // fit 16 CTAs' shared memory, else one CTA per SM with a grid barrier.
   const int cmax = qr_max_cluster();
@@ -546,13 +587,37 @@ int geqrf(double* a, int64_t lda, int64_t m, int64_t n, double* tau, void* ws, s
     if (gemm(true, false, nb, nb, rows, 1.0, vbuf, rows, vbuf, rows, 0.0, gram, nb, gws, gws_bytes, st)) return -1;
     qr_larft_kernel<<<1, 256, 0, st>>>(gram, nb, tau + j0, T);
     RLRA_LAUNCHED();
-    // trailing update C = (I - V T^T V^T) C on columns [j0+nb, n)
-    const int64_t nc = n - j0 - nb;
+    // two-level blocking: the panel's update C = (I - V T^T V^T) C reaches the
+    // columns of its outer block of QR_NBO only; a completed outer block is
+    // applied to everything right of it at once with its own block reflector
+    // (V_b, T_b: GEMMs with a 128-deep inner dimension instead of 16)
+    const int64_t ob0 = (j0 / QR_NBO) * QR_NBO, oend = std::min<int64_t>(n, ob0 + QR_NBO);
+    const int64_t nc = oend - j0 - nb;
     if (nc > 0) {
       double* C = a + cm(j0, j0 + nb, lda);
       if (gemm(true, false, nb, nc, rows, 1.0, vbuf, rows, C, lda, 0.0, wbuf, nb, gws, gws_bytes, st)) return -1;
       if (gemm(true, false, nb, nc, nb, 1.0, T, nb, wbuf, nb, 0.0, w2buf, nb, gws, gws_bytes, st)) return -1;
       if (gemm(false, false, rows, nc, nb, -1.0, vbuf, rows, w2buf, nb, 1.0, C, lda, gws, gws_bytes, st)) return -1;
+    }
+    if (j0 + nb == oend) {  // outer block complete: V_b, T_b (kept for orgqr), update the rest
+      const int64_t rb = m - ob0;
+      const int nbo = (int)(oend - ob0);
+      double* Tb = tbig + (ob0 / QR_NBO) * QR_NBO * QR_NBO;
+      qr_make_v_kernel<<<grid_for_q(rb * nbo), 256, 0, st>>>(a, lda, ob0, rb, nbo, vbuf, rb);
+      RLRA_LAUNCHED();
+      if (gemm(true, false, nbo, nbo, rb, 1.0, vbuf, rb, vbuf, rb, 0.0, gram, nbo, gws, gws_bytes, st)) return -1;
+      qr_larft_big_kernel<<<1, QR_NBO, (size_t)QR_NBO * (QR_NBO + 1) * sizeof(double), st>>>(gram, nbo, tau + ob0,
+                                                                                           Tb);
+      RLRA_LAUNCHED();
+      const int64_t ncb = n - oend;
+      if (ncb > 0) {
+        double* C = a + cm(ob0, oend, lda);
+        if (gemm(true, false, nbo, ncb, rb, 1.0, vbuf, rb, C, lda, 0.0, wbuf, nbo, gws, gws_bytes, st)) return -1;
+        if (gemm(true, false, nbo, ncb, nbo, 1.0, Tb, nbo, wbuf, nbo, 0.0, w2buf, nbo, gws, gws_bytes, st))
+          return -1;
+        if (gemm(false, false, rb, ncb, nbo, -1.0, vbuf, rb, w2buf, nbo, 1.0, C, lda, gws, gws_bytes, st))
+          return -1;
+      }
     }
   }
   return 0;
@@ -575,23 +640,23 @@ int orgqr(const double* a, int64_t lda, int64_t m, int64_t n, double* q, int64_t
   const size_t gws_bytes = L.total - L.gemm_ws;
   set_identity_kernel<<<grid_for_q(m * n), 256, 0, st>>>(q, ldq, m, n);
   RLRA_LAUNCHED();
-  const int cmax = qr_max_cluster();
-  const bool use_cluster = cmax > 1 && m <= cmax * qr_rows_cap(16);
-  const int pw = use_cluster ? (m <= cmax * qr_rows_cap(32) ? 32 : 16) : qr_pw(m, sms);
-  const int64_t npan = ceil_div(n, pw);
-  for (int64_t pidx = npan - 1; pidx >= 0; pidx--) {
-    const int64_t j0 = pidx * pw;
-    const int nb = (int)std::min<int64_t>(pw, n - j0);
-    const int64_t rows = m - j0;
-    const int64_t nc = n - j0;
-    qr_make_v_kernel<<<grid_for_q(rows * nb), 256, 0, st>>>(a, lda, j0, rows, nb, vbuf, rows);
+  double* tbig = reinterpret_cast<double*>(base + L.tbig);
+  (void)tbl;
+  // outer blocks (V_b, T_b from geqrf), last to first
+  for (int64_t ob = ceil_div(n, QR_NBO) - 1; ob >= 0; ob--) {
+    const int64_t ob0 = ob * QR_NBO;
+    const int nbo = (int)std::min<int64_t>(QR_NBO, n - ob0);
+    const int64_t rows = m - ob0;
+    const int64_t nc = n - ob0;
+    qr_make_v_kernel<<<grid_for_q(rows * nbo), 256, 0, st>>>(a, lda, ob0, rows, nbo, vbuf, rows);
     RLRA_LAUNCHED();
-    const double* T = tbl + pidx * QR_NB * QR_NB;
-    double* Qs = q + cm(j0, j0, ldq);
+    const double* Tb = tbig + ob * QR_NBO * QR_NBO;
+    double* Qs = q + cm(ob0, ob0, ldq);
     // Qs = (I - V T V^T) Qs
-    if (gemm(true, false, nb, nc, rows, 1.0, vbuf, rows, Qs, ldq, 0.0, wbuf, nb, gws, gws_bytes, st)) return -1;
-    if (gemm(false, false, nb, nc, nb, 1.0, T, nb, wbuf, nb, 0.0, w2buf, nb, gws, gws_bytes, st)) return -1;
-    if (gemm(false, false, rows, nc, nb, -1.0, vbuf, rows, w2buf, nb, 1.0, Qs, ldq, gws, gws_bytes, st)) return -1;
+    if (gemm(true, false, nbo, nc, rows, 1.0, vbuf, rows, Qs, ldq, 0.0, wbuf, nbo, gws, gws_bytes, st)) return -1;
+    if (gemm(false, false, nbo, nc, nbo, 1.0, Tb, nbo, wbuf, nbo, 0.0, w2buf, nbo, gws, gws_bytes, st)) return -1;
+    if (gemm(false, false, rows, nc, nbo, -1.0, vbuf, rows, w2buf, nbo, 1.0, Qs, ldq, gws, gws_bytes, st))
+      return -1;
   }
   return 0;
 }
