@@ -109,16 +109,18 @@ __global__ void __launch_bounds__(CHOL_THREADS, 1)
         s_rmax = fmax(s_rmax, rmax);
       }
   };
-  if (warp == 0) diag(0, min(CHOL_NB, l));
-  __syncthreads();
-  for (int k0 = 0; k0 < l; k0 += CHOL_NB) {
-    const int b = min(CHOL_NB, l - k0);
+  // iteration it applies block it (k0 = it * NB) and factors block it + 1;
+  // it = -1 only factors block 0 -- ONE inlined copy of diag() (code size:
+  // the unrolled register factorization is the bulk of the kernel's SASS)
+  for (int it = -1;; it++) {
+    const int k0 = it * CHOL_NB;
+    const int b = it < 0 ? 0 : min(CHOL_NB, l - k0);
     if (s_bad) break;
-    const int c0 = k0 + b, m = l - c0;
+    const int c0 = it < 0 ? 0 : k0 + b, m = l - c0;
     if (m <= 0) break;
     // ---- (2) block row: R(k0.., j) = R_kk^{-T} G(k0.., j) = Xkk^T g, one warp
     // per column: lane u accumulates sum_{s <= u} Xkk[s][u] g_s (no recurrence)
-    for (int jj = warp; jj < m; jj += NW) {
+    for (int jj = warp; it >= 0 && jj < m; jj += NW) {
       const int j = c0 + jj, cj = j * (j + 1) / 2;
       const double gl = (lane < b) ? P[cj + k0 + lane] : 0.0;
       double acc = 0.0;
@@ -136,7 +138,7 @@ __global__ void __launch_bounds__(CHOL_THREADS, 1)
     // the rest of the triangle in 4 x 4 tiles.
     const int bn = min(CHOL_NB, m);
     if (warp == 0) {
-      const int ne = bn * (bn + 1) / 2;
+      const int ne = it < 0 ? 0 : bn * (bn + 1) / 2;
       for (int e = lane; e < ne; e += 32) {
         int jj = (int)((sqrtf(8.0f * (float)e + 1.0f) - 1.0f) * 0.5f);
         while (jj * (jj + 1) / 2 > e) --jj;
@@ -152,7 +154,7 @@ __global__ void __launch_bounds__(CHOL_THREADS, 1)
 #ifdef CHOL_EXP_NOTRAIL
       const int mt = 0;
 #else
-      const int mt = (m + 3) >> 2;
+      const int mt = it < 0 ? 0 : (m + 3) >> 2;
 #endif
       const int ntiles = mt * (mt + 1) / 2;
       const int lim = c0 + bn;  // entries with i, j < lim belong to warp 0
