@@ -116,7 +116,14 @@ def powerlu(a, k, q_os=10, v=3, seed=0):
         basis = general_power_basis_v(a, k + q_os, v, seed, _checks=checks, _qr=POWERLU_QR)
         vk = basis.V[:, :k]
         g = a.matmul(vk)
-    f = lu_from_projection_(g, vk)
+        f = lu_from_projection_(g, vk)
+        declined = checks.cholqr_declined()  # the only mid-call host sync, after all the work is queued
+        if declined is not None and declined[0]:  # rare: redo the final basis by Householder, then G and LU
+            from .rangefinder import qr_basis_
+
+            v_h = qr_basis_(declined[1], checks, "householder")
+            vk = v_h[:, :k]
+            f = lu_from_projection_(a.matmul(vk), vk)
     checks.raise_if_collapsed()
     return f.to_numpy() if host else f
 

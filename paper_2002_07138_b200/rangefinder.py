@@ -62,9 +62,22 @@ class RankChecks:
 
     def __init__(self):
         self._items = []
+        self._cholqr = None  # (flag, Z) of a deferred CholeskyQR2 basis
 
     def add(self, count, requested):
         self._items.append((count, int(requested)))
+
+    def defer_cholqr(self, flag, z):
+        self._cholqr = (flag, z)
+
+    def cholqr_declined(self):
+        """The parked CholeskyQR2 flag (host sync): None when no basis was
+        deferred, else (declined, Z)."""
+        if self._cholqr is None:
+            return None
+        flag, z = self._cholqr
+        self._cholqr = None
+        return bool(int(flag.item())), z
 
     def raise_if_collapsed(self):
         if not self._items:
@@ -85,16 +98,19 @@ def _validate(a, l, lower=1):
 
 
 def qr_basis_(x, checks, method="householder"):
-    """rlra/rangefinder.py:67-70 (destroys x).
+    """rlra/rangefinder.py:67-70 (destroys x, except on the CholeskyQR2 path).
 
     method="chol" (powerlu's internal basis): CholeskyQR2 -- same range as the
     Householder Q, columns possibly of opposite sign, which no powerlu output
-    depends on -- with the Householder path as the fallback whenever the
-    Cholesky declines (rank collapse keeps the reference's exception)."""
+    depends on.  Its decline flag (non-SPD Gram / condition bound) is NOT read
+    here: the flag and x are parked in `checks` (checks.cholqr_declined(), one
+    host sync at the end of the driver) and the caller redoes the basis on the
+    Householder path if it was raised -- rank collapse keeps the reference's
+    exception there.  method="householder_now": Householder unconditionally."""
     if method == "chol" and x.shape[0] >= x.shape[1] and 0 < x.shape[1] <= ops.cholqr_max_l():
         q, flag = ops.cholqr2(x)
-        if not int(flag.item()):
-            return q
+        checks.defer_cholqr(flag, x)
+        return q
     qr = ops.QR(x)
     checks.add(ops.count_nonzero_diag(qr.r_view()), x.shape[1])
     return qr.q()

@@ -288,3 +288,24 @@ def test_pipelined_upload_matches_resident(cuda_dev, monkeypatch):
     from paper_2002_07138_b200 import ops
 
     np.testing.assert_allclose(ops.to_numpy(z), a.T @ np.eye(200)[:, :5], rtol=0, atol=1e-14)
+
+
+@pytest.mark.parametrize("v", [2, 3, 4])
+def test_powerlu_cholqr_decline_falls_back_to_householder(cuda_dev, monkeypatch, v):
+    """Exact-rank input: the CholeskyQR2 basis declines (singular Gram); the
+    deferred flag makes powerlu redo the basis, G and the assembly on the
+    Householder path -- identical to running Householder from the start."""
+    import paper_2002_07138_b200 as P
+    from paper_2002_07138_b200 import fixedrank, ops
+
+    a = DRV["exact_a"]
+    calls = []
+    orig = ops.cholqr2
+    monkeypatch.setattr(ops, "cholqr2", lambda z: calls.append(1) or orig(z))
+    f = P.powerlu(a, 8, q_os=4, v=v, seed=0)
+    assert calls, "CholeskyQR2 path not taken"
+    monkeypatch.setattr(fixedrank, "POWERLU_QR", "householder")
+    g = P.powerlu(a, 8, q_os=4, v=v, seed=0)
+    assert np.array_equal(f.p, g.p) and np.array_equal(f.q, g.q)
+    assert np.array_equal(f.p, DRV[f"exact_v{v}/p"]) and np.array_equal(f.q, DRV[f"exact_v{v}/q"])
+    assert np.abs(f.L @ f.U - g.L @ g.U).max() <= 1e-12 * np.abs(g.L @ g.U).max()
