@@ -39,7 +39,7 @@ constexpr int NW = T / 32;    // warps per CTA
 constexpr int CS = 16;        // cluster size
 constexpr int RECD = 2 + W;   // record: {|v|, row bits, row[W]} (<= 144 B)
 constexpr int MAXRPT = 6;     // rows per thread
-constexpr int MAXN = 256;     // widest sketch handled (trailing work runs on 16 SMs)
+constexpr int MAXN = 512;     // widest sketch handled (wider: the blocked path, whose trailing update uses every SM, wins)
 constexpr double ZTOL = 1e-14;  // rlra/_lu_cython.pyx:11
 constexpr unsigned NONE = 0xffffffffu;
 
@@ -221,7 +221,7 @@ struct Handoff {
   unsigned u12done[MAXP];    // helper CTAs done with panel b's far U12 rows
   unsigned nextdone[MAXP];   // helper CTAs done with the next panel's columns (update by panel b)
   unsigned u12read[MAXP];    // helper CTAs (other than 0) done reading the next columns' rows j0..ce
-  unsigned pad[128 - 1 - 4 * MAXP];
+  unsigned pad[(1 + 4 * MAXP + 127) / 128 * 128 - 1 - 4 * MAXP];  // counters on their own lines
   unsigned long long cmax[MAXN];
   int64_t prow[MAXP][2 * 16], psrc[MAXP][2 * 16];
   int pcnt[MAXP];

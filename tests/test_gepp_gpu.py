@@ -67,7 +67,7 @@ def test_host_seam_plu_inplace_bit_exact(cuda_dev, name):
                                       (100000, 70, 6), (200000, 45, 7),
                                       # one-launch cluster GEPP (csrc/getrf_full.cu): edges of its range
                                       (24576, 256, 10), (8193, 33, 11), (2000, 60, 12), (520, 256, 13),
-                                      (16385, 200, 14)])
+                                      (16385, 200, 14), (8192, 300, 15), (24576, 512, 16)])
 def test_device_gepp_bit_exact_vs_oracle_sketch_shapes(cuda_dev, m, n, seed):
     a = np.random.default_rng(seed).standard_normal((m, n))
     if n > 40:
