@@ -292,10 +292,8 @@ def our_arm(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
-        from paper_2002_07138_b200 import distributed as D
-
-        return D.bench_main(args)
+    if world > 1 or os.environ.get("RLRA_B200_BENCH_DIST") == "1":
+        return dist_arm(args)
     torch.cuda.set_device(local)
     import paper_2002_07138_b200 as P
     from paper_2002_07138_b200 import _native, ops
@@ -420,6 +418,121 @@ def our_arm(args):
         "host_prep": {"generate_A_s": gen_s, "upload_A_s": upload_s},
     }
     print(json.dumps(line), flush=True)
+    return 0
+
+
+def dist_arm(args):
+    """N GPUs under torchrun: A row-sharded (one shard per rank, NCCL over
+    NVLink; paper_2002_07138_b200/distributed.py), the same workload and
+    metric as N=1 (strong scaling).  value: device-resident shards, max over
+    ranks of the CUDA-event time; e2e: every step uploads each rank's shard
+    from pinned host memory and rank 0 downloads the factors."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2002_07138_b200 import _native, configs, core, ops
+    from paper_2002_07138_b200 import distributed as D
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29541")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
+    w, v, gen, passes, fact, desc = workload(args)
+    flops = passes + fact
+    r0, r1 = D.row_range(w.m, world, rank)
+    cops = D.CudaOps(dev)
+    host_shard = None
+    if gen is not None:
+        a = gen()
+        host_shard = torch.empty((w.n, r1 - r0), dtype=torch.float64, pin_memory=True)  # column-major shard
+        host_shard.numpy().T[...] = a[r0:r1]
+        del a
+        shard = cops.empty(r1 - r0, w.n)
+        shard.copy_(host_shard.t())
+    else:  # C5: built in HBM, this rank keeps its rows
+        full = configs.gen_device(w.name, dev)
+        shard = cops.empty(r1 - r0, w.n)
+        shard.copy_(full[r0:r1])
+        del full
+        torch.cuda.empty_cache()
+    A = D.ShardedMatrix(shard, w.m, r0, r1, cops)
+    core.set_omega_cache(True)
+    omega = lambda seed, rows, l: core.omega(seed, rows, l, dev)  # noqa: E731
+    for _ in range(args.warmup):
+        D.powerlu(A, w.k, w.q_os, v, w.seed, omega)
+    torch.cuda.synchronize()
+    dist.barrier()
+    lib = _native.load()
+    clocks = Clocks(local)
+    clocks.start()
+    l0 = lib.rlra_b200_launch_count()
+    st = torch.cuda.current_stream(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    dist.barrier()
+    e0.record(st)
+    for _ in range(args.steps):
+        D.powerlu(A, w.k, w.q_os, v, w.seed, omega)
+    e1.record(st)
+    torch.cuda.synchronize()
+    dist.barrier()
+    launches = lib.rlra_b200_launch_count() - l0
+    clk = clocks.stop()
+    ms = torch.tensor([e0.elapsed_time(e1) / args.steps], device=dev)
+    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    nl = torch.tensor([float(launches)], device=dev)
+    dist.all_reduce(nl, op=dist.ReduceOp.SUM)
+    clks = [None] * world
+    dist.all_gather_object(clks, clk)
+
+    e2e = None
+    if host_shard is not None and not args.no_e2e:
+        ksteps = max(1, min(args.steps, 5))
+        d2h = 0
+        dist.barrier()
+        torch.cuda.synchronize()
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s0.record(st)
+        for _ in range(ksteps):
+            sh = cops.empty(r1 - r0, w.n)
+            sh.copy_(host_shard.t(), non_blocking=True)
+            f = D.powerlu(D.ShardedMatrix(sh, w.m, r0, r1, cops), w.k, w.q_os, v, w.seed, omega)
+            if rank == 0:
+                hp = ops.to_numpy_many([f.p, f.q, f.L, f.U])
+                d2h = sum(x.nbytes for x in hp)
+        s1.record(st)
+        torch.cuda.synchronize()
+        em = torch.tensor([s0.elapsed_time(s1) / ksteps], device=dev)
+        dist.all_reduce(em, op=dist.ReduceOp.MAX)
+        e2e_ms = float(em.item())
+        e2e = {"value": flops / (e2e_ms / 1e3) / 1e9, "unit": "GFLOP/s", "ms_per_step": e2e_ms,
+               "h2d_bytes_per_step": int(8 * w.m * w.n), "d2h_bytes_per_step": int(d2h), "steps": ksteps,
+               "path": "distributed.powerlu over pinned host row shards -> NumPy factors on rank 0"}
+    if rank == 0:
+        msv = float(ms.item())
+        sm = [c.get("sm_mhz") for c in clks if c and c.get("sm_mhz")]
+        reasons = sorted({r for c in clks if c for r in c.get("reasons", [])})
+        line = {"metric": f"PowerLU FP64 GFLOP/s ({w.name}, v={v})", "value": flops / (msv / 1e3) / 1e9,
+                "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": msv, "s_per_factorization": msv / 1e3, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": {"workload": desc, "m": w.m, "n": w.n, "k": w.k, "l": w.k + w.q_os, "v": v,
+                           "parallelism": f"A row-sharded over {world} GPUs; NCCL all-reduce of A^T Y, "
+                                          f"all-gather for the exact final GEPP, TSLU interior from 4 ranks",
+                           "l2": "inputs larger than L2"},
+                "gpu_launches": int(nl.item()),
+                "clocks": {"sm_mhz": min(sm) if sm else None,
+                           "sm_max_mhz": clks[0].get("sm_max_mhz") if clks[0] else None,
+                           "reasons": reasons, "per_rank": clks},
+                "roofline": None, "e2e": e2e, "cpu_baseline": None,
+                "note": "roofline and cpu_baseline are reported by the N=1 run"}
+        print(json.dumps(line), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
     return 0
 
 

@@ -379,70 +379,3 @@ def powerlu_fp(A: ShardedMatrix, eps, b, l, v, seed, omega_fn):
         raise NotConverged(AdaptiveOutcome(rank, V, g_local, resid, conv))
     # lu_from_projection factors the all-gathered copy, g_local stays intact
     return lu_from_projection(A, g_local[:, :rank], V[:, :rank]), rank
-
-
-# ---------------------------------------------------------------- bench entry
-def bench_main(args):
-    """bench.py under torchrun (N > 1): row-sharded C2 / C5 powerlu over NCCL."""
-    import json
-    import time
-
-    from . import configs
-    rank = int(os.environ["RANK"])
-    world = int(os.environ["WORLD_SIZE"])
-    local = int(os.environ.get("LOCAL_RANK", rank))
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    dist.init_process_group("nccl", device_id=dev)
-    w = configs.WORKLOADS[args.config]
-    v = args.v if args.v is not None else w.v
-    passes, fact = configs.powerlu_flops(w.m, w.n, w.k, w.k + w.q_os, v)
-    flops = passes + fact
-    r0, r1 = row_range(w.m, world, rank)
-    ops = CudaOps(dev)
-    if w.name in ("C1", "C2"):
-        a = {"C1": configs.gen_c1, "C2": configs.gen_c2}[w.name]()
-        shard = ops.upload(np.asfortranarray(a[r0:r1]))
-    else:  # C5 (68.7 GB): built in HBM (configs.gen_device), this rank keeps its rows
-        full = configs.gen_device(w.name, dev)
-        shard = ops.empty(r1 - r0, w.n)
-        shard.copy_(full[r0:r1])
-        del full
-        torch.cuda.empty_cache()
-    A = ShardedMatrix(shard, w.m, r0, r1, ops)
-    a = None
-    from . import core as _core
-
-    _core.set_omega_cache(True)  # as the single-GPU bench: Omega is an input, drawn once on the device
-
-    def omega(seed, rows, l):
-        return _core.omega(seed, rows, l, dev)
-
-    for _ in range(args.warmup):
-        powerlu(A, w.k, w.q_os, v, w.seed, omega)
-    torch.cuda.synchronize()
-    dist.barrier()
-    st = torch.cuda.current_stream(dev)
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    e0.record(st)
-    for _ in range(args.steps):
-        powerlu(A, w.k, w.q_os, v, w.seed, omega)
-    e1.record(st)
-    torch.cuda.synchronize()
-    ms = torch.tensor([e0.elapsed_time(e1) / args.steps], device=dev)
-    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
-    dist.barrier()
-    if rank == 0:
-        msv = float(ms.item())
-        line = {"metric": f"PowerLU FP64 GFLOP/s ({w.name}, v={v})", "value": flops / (msv / 1e3) / 1e9,
-                "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-                "ms_per_step": msv, "s_per_factorization": msv / 1e3, "higher_is_better": True,
-                "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-                "config": {"workload": f"{w.name} powerlu m={w.m} n={w.n} k={w.k} l={w.k + w.q_os} v={v}",
-                           "parallelism": f"row-sharded A over {world} GPUs, NCCL all-reduce/all-gather",
-                           "l2": "inputs larger than L2"},
-                "roofline": None, "e2e": None, "cpu_baseline": None}
-        print(json.dumps(line), flush=True)
-    dist.destroy_process_group()
-    return 0
