@@ -29,6 +29,7 @@
  *   rlra_b200_trsm_un          solve_triangular(R, C^T)       fixedrank.py:113 (randlu assembly)
  *   rlra_b200_apply_inv_row_perm core.apply_inv_row_perm      core.py:103-109, fixedrank.py:111
  *   rlra_b200_svd_jacobi       np.linalg.svd of the l x l     fixedrank.py:71 (randsvd)
+ *   rlra_b200_resid_sumsq_block reconstruct + rel_fro_error    fixedrank.py:149-155, core.py:56-65
  *                              triangular factor of B = Q^T A
  *   rlra_b200_diag_absmin      pinv_factor rank test          kernels.py:75-79
  *   rlra_b200_sumsq            DenseAccessor.fro_norm()**2    accessors.py:33-34, fixedprec.py:72
@@ -170,6 +171,16 @@ RLRA_B200_API int rlra_b200_trsm_un(const double* r, int64_t ldr, int64_t l, dou
 RLRA_B200_API int rlra_b200_apply_inv_row_perm(const int64_t* p, int64_t m, int64_t n, const double* x,
                                                int64_t ldx, int64_t* pinv_ws, double* out, int64_t ldo,
                                                void* stream);
+
+/* ---- K9 validation residual ||A[p, :][:, q] - L U||_F^2 (rlra/fixedrank.py:149-155,
+ * rlra/core.py:56-65) without materialising the m x n reconstruction: per block
+ * of w columns of L U (m x w, caller-computed), partial[2j..2j+1] = the
+ * double-double sum over i of (A[p[i], q_blk[j]] - LU[i, j])^2; dd_finish sums
+ * nparts such pairs in a fixed order into out[0]. */
+RLRA_B200_API int rlra_b200_resid_sumsq_block(const double* a, int64_t lda, int64_t m, const int64_t* p,
+                                              const int64_t* q_blk, int64_t w, const double* lu, int64_t ldlu,
+                                              double* partial, void* stream);
+RLRA_B200_API int rlra_b200_dd_finish(const double* partial, int64_t nparts, double* out, void* stream);
 
 /* ---- randsvd's small SVD: one-sided Jacobi, A (m x l, m >= l, l <= max_l)
  * = U diag(s) V^T, s nonincreasing (ties by column index); sweeps_out

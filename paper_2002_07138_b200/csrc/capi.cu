@@ -85,6 +85,9 @@ int geqrf(double* a, int64_t lda, int64_t m, int64_t n, double* tau, void* ws, s
           cudaStream_t st);
 int orgqr(const double* a, int64_t lda, int64_t m, int64_t n, double* q, int64_t ldq, void* ws,
           size_t ws_bytes, cudaStream_t st);
+int resid_sumsq_block(const double* a, int64_t lda, int64_t m, const int64_t* p, const int64_t* qb, int64_t w,
+                      const double* lu, int64_t ldlu, double* partial, cudaStream_t st);
+int dd_finish(const double* partial, int64_t nparts, double* out_dev, cudaStream_t st);
 int trsm_un(const double* r, int64_t ldr, int64_t l, double* x, int64_t ldx, int64_t ncols, void* ws,
             size_t ws_bytes, cudaStream_t st);
 int apply_inv_row_perm(const int64_t* p, int64_t m, int64_t n, const double* x, int64_t ldx, int64_t* pinv_ws,
@@ -335,6 +338,15 @@ int rlra_b200_trsm_un(const double* r, int64_t ldr, int64_t l, double* x, int64_
 int rlra_b200_apply_inv_row_perm(const int64_t* p, int64_t m, int64_t n, const double* x, int64_t ldx,
                                  int64_t* pinv_ws, double* out, int64_t ldo, void* stream) {
   return apply_inv_row_perm(p, m, n, x, ldx, pinv_ws, out, ldo, S(stream));
+}
+
+int rlra_b200_resid_sumsq_block(const double* a, int64_t lda, int64_t m, const int64_t* p, const int64_t* q_blk,
+                                int64_t w, const double* lu, int64_t ldlu, double* partial, void* stream) {
+  return resid_sumsq_block(a, lda, m, p, q_blk, w, lu, ldlu, partial, S(stream));
+}
+
+int rlra_b200_dd_finish(const double* partial, int64_t nparts, double* out, void* stream) {
+  return dd_finish(partial, nparts, out, S(stream));
 }
 
 int rlra_b200_svd_jacobi_max_l(void) { return svd_jacobi_max_l(); }

@@ -104,6 +104,43 @@ int sumsq(const double* a, int64_t lda, int64_t m, int64_t n, double* out_dev, v
   return 0;
 }
 
+// ---------------------------------------------------------------- K9 validation residual
+// ||A[p, :][:, q] - L U||_F^2 over one block of w columns of L U (rlra/
+// fixedrank.py:149-155 with rlra/core.py:56-65, without materialising the
+// m x n reconstruction): CTA j takes column j of the block, reads A's column
+// q_blk[j] gathered through p (the column, <= 2 MB, stays in L2) and the
+// block's column j contiguously; compensated sums, one partial per column.
+__global__ void resid_sumsq_kernel(const double* __restrict__ a, int64_t lda, int64_t m,
+                                   const int64_t* __restrict__ p, const int64_t* __restrict__ qb,
+                                   const double* __restrict__ lu, int64_t ldlu, double* partial) {
+  const int64_t j = blockIdx.x;
+  const double* acol = a + cm(0, __ldg(qb + j), lda);
+  const double* lcol = lu + cm(0, j, ldlu);
+  DD acc{0.0, 0.0};
+  for (int64_t i = threadIdx.x; i < m; i += blockDim.x) acc = dd_add_sq(acc, __ldg(acol + __ldg(p + i)) - lcol[i]);
+  acc = dd_block_reduce(acc);
+  if (threadIdx.x == 0) {
+    partial[2 * j] = acc.hi;
+    partial[2 * j + 1] = acc.lo;
+  }
+}
+
+int resid_sumsq_block(const double* a, int64_t lda, int64_t m, const int64_t* p, const int64_t* qb, int64_t w,
+                      const double* lu, int64_t ldlu, double* partial, cudaStream_t st) {
+  if (w <= 0) return 0;
+  RLRA_REQUIRE(w <= 2147483647 && m >= 1, "resid_sumsq_block: bad shape");
+  resid_sumsq_kernel<<<(unsigned)w, 512, 0, st>>>(a, lda, m, p, qb, lu, ldlu, partial);
+  RLRA_LAUNCHED();
+  return 0;
+}
+
+int dd_finish(const double* partial, int64_t nparts, double* out_dev, cudaStream_t st) {
+  RLRA_REQUIRE(nparts >= 1 && nparts <= 2147483647, "dd_finish: bad count");
+  dd_finish_kernel<<<1, 1024, 0, st>>>(partial, (int)nparts, out_dev);
+  RLRA_LAUNCHED();
+  return 0;
+}
+
 // ---------------------------------------------------------------- column energies
 __global__ void colsumsq_kernel(const double* __restrict__ a, int64_t lda, int64_t m, int64_t n,
                                 double* out) {

@@ -309,3 +309,18 @@ def test_powerlu_cholqr_decline_falls_back_to_householder(cuda_dev, monkeypatch,
     assert np.array_equal(f.p, g.p) and np.array_equal(f.q, g.q)
     assert np.array_equal(f.p, DRV[f"exact_v{v}/p"]) and np.array_equal(f.q, DRV[f"exact_v{v}/q"])
     assert np.abs(f.L @ f.U - g.L @ g.U).max() <= 1e-12 * np.abs(g.L @ g.U).max()
+
+
+@pytest.mark.parametrize("block", [7, 2048])
+def test_device_validation_metric_matches_oracle(cuda_dev, block):
+    """K9 (validate.rel_err_device: L U per column block on the DMMA GEMM, the
+    fused gather/difference/double-double kernel) against the oracle's
+    ||A - P^T (L U) Q^T||_F / ||A||_F (rlra/fixedrank.py:149-155)."""
+    import paper_2002_07138_b200 as P
+    from paper_2002_07138_b200 import ops, validate
+
+    a = DRV["pl_a"]
+    f = P.powerlu(a, 30, q_os=10, v=4, seed=1)
+    ref = O.rel_fro_error_factor(a, f)
+    got = validate.rel_err_device(ops.from_numpy(a, cuda_dev), f, block=block)
+    assert abs(got - ref) <= 1e-13 * ref
