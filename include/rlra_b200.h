@@ -30,6 +30,7 @@
  *   rlra_b200_apply_inv_row_perm core.apply_inv_row_perm      core.py:103-109, fixedrank.py:111
  *   rlra_b200_svd_jacobi       np.linalg.svd of the l x l     fixedrank.py:71 (randsvd)
  *   rlra_b200_resid_sumsq_block reconstruct + rel_fro_error    fixedrank.py:149-155, core.py:56-65
+ *   rlra_b200_spmm_csr         SparseAccessor.matmul/rmatmul   accessors.py:40-64
  *                              triangular factor of B = Q^T A
  *   rlra_b200_diag_absmin      pinv_factor rank test          kernels.py:75-79
  *   rlra_b200_sumsq            DenseAccessor.fro_norm()**2    accessors.py:33-34, fixedprec.py:72
@@ -181,6 +182,13 @@ RLRA_B200_API int rlra_b200_resid_sumsq_block(const double* a, int64_t lda, int6
                                               const int64_t* q_blk, int64_t w, const double* lu, int64_t ldlu,
                                               double* partial, void* stream);
 RLRA_B200_API int rlra_b200_dd_finish(const double* partial, int64_t nparts, double* out, void* stream);
+
+/* ---- sparse operands (SparseAccessor, rlra/accessors.py:40-64): Y = S X for S
+ * (rows x K) in CSR with int64 indices, X (K x l) and Y (rows x l) column-major;
+ * A X uses the CSR of A, A^T X the CSR of A^T (the CSC arrays of A). */
+RLRA_B200_API int rlra_b200_spmm_csr(const int64_t* rowptr, const int64_t* colidx, const double* vals,
+                                     int64_t rows, const double* x, int64_t ldx, int64_t l, double* y,
+                                     int64_t ldy, void* stream);
 
 /* ---- randsvd's small SVD: one-sided Jacobi, A (m x l, m >= l, l <= max_l)
  * = U diag(s) V^T, s nonincreasing (ties by column index); sweeps_out

@@ -16,6 +16,7 @@ from .device import (
     DeviceColumnStream,
     DeviceMatrix,
     InstrumentedAccessor,
+    SparseDeviceMatrix,
     as_accessor,
 )
 from .errors import (
@@ -59,4 +60,6 @@ __all__ = [
     "randlu_noreorth", "randsvd", "range_agreement",
     # out-of-core streams
     "RlraFileColumnStream", "read_rlra", "read_rlra_header", "write_rlra",
+    # sparse operands
+    "SparseDeviceMatrix",
 ]

@@ -63,6 +63,7 @@ SIGNATURES = {
     "rlra_b200_apply_inv_row_perm": (_c_i, [_c_p, _c_i64, _c_i64, _c_p, _c_i64, _c_p, _c_p, _c_i64, _c_p]),
     "rlra_b200_resid_sumsq_block": (_c_i, [_c_p, _c_i64, _c_i64, _c_p, _c_p, _c_i64, _c_p, _c_i64, _c_p, _c_p]),
     "rlra_b200_dd_finish": (_c_i, [_c_p, _c_i64, _c_p, _c_p]),
+    "rlra_b200_spmm_csr": (_c_i, [_c_p, _c_p, _c_p, _c_i64, _c_p, _c_i64, _c_i64, _c_p, _c_i64, _c_p]),
     "rlra_b200_svd_jacobi_max_l": (_c_i, []),
     "rlra_b200_svd_jacobi_workspace": (_c_sz, [_c_i64, _c_i64]),
     "rlra_b200_svd_jacobi": (_c_i, [_c_p, _c_i64, _c_i64, _c_i64, _c_p, _c_i64, _c_p, _c_p, _c_i64, _c_p, _c_p,

@@ -88,6 +88,8 @@ int orgqr(const double* a, int64_t lda, int64_t m, int64_t n, double* q, int64_t
 int resid_sumsq_block(const double* a, int64_t lda, int64_t m, const int64_t* p, const int64_t* qb, int64_t w,
                       const double* lu, int64_t ldlu, double* partial, cudaStream_t st);
 int dd_finish(const double* partial, int64_t nparts, double* out_dev, cudaStream_t st);
+int spmm_csr(const int64_t* rowptr, const int64_t* colidx, const double* vals, int64_t rows, const double* x,
+             int64_t ldx, int64_t l, double* y, int64_t ldy, cudaStream_t st);
 int trsm_un(const double* r, int64_t ldr, int64_t l, double* x, int64_t ldx, int64_t ncols, void* ws,
             size_t ws_bytes, cudaStream_t st);
 int apply_inv_row_perm(const int64_t* p, int64_t m, int64_t n, const double* x, int64_t ldx, int64_t* pinv_ws,
@@ -347,6 +349,11 @@ int rlra_b200_resid_sumsq_block(const double* a, int64_t lda, int64_t m, const i
 
 int rlra_b200_dd_finish(const double* partial, int64_t nparts, double* out, void* stream) {
   return dd_finish(partial, nparts, out, S(stream));
+}
+
+int rlra_b200_spmm_csr(const int64_t* rowptr, const int64_t* colidx, const double* vals, int64_t rows,
+                       const double* x, int64_t ldx, int64_t l, double* y, int64_t ldy, void* stream) {
+  return spmm_csr(rowptr, colidx, vals, rows, x, ldx, l, y, ldy, S(stream));
 }
 
 int rlra_b200_svd_jacobi_max_l(void) { return svd_jacobi_max_l(); }

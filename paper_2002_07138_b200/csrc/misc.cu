@@ -141,6 +141,38 @@ int dd_finish(const double* partial, int64_t nparts, double* out_dev, cudaStream
   return 0;
 }
 
+// ---------------------------------------------------------------- sparse products
+static int grid_for(int64_t total);
+
+// Y (rows x l, column-major) = S X for S in CSR (rowptr/colidx/vals) and X
+// column-major -- SparseAccessor.matmul / rmatmul (rlra/accessors.py:40-64)
+// with the CSR of A for A X and the CSR of A^T (= CSC of A) for A^T X.  One
+// thread per (row, column of X): consecutive threads take consecutive rows
+// (coalesced Y), the row's nonzeros are read in ascending order (fixed
+// summation order, deterministic).
+__global__ void spmm_csr_kernel(const int64_t* __restrict__ rowptr, const int64_t* __restrict__ colidx,
+                                const double* __restrict__ vals, int64_t rows, const double* __restrict__ x,
+                                int64_t ldx, int64_t l, double* __restrict__ y, int64_t ldy) {
+  const int64_t total = rows * l;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e % rows, c = e / rows;
+    const double* xc = x + c * ldx;
+    double acc = 0.0;
+    const int64_t k1 = __ldg(rowptr + r + 1);
+    for (int64_t k = __ldg(rowptr + r); k < k1; k++) acc = fma(__ldg(vals + k), __ldg(xc + __ldg(colidx + k)), acc);
+    y[r + c * ldy] = acc;
+  }
+}
+
+int spmm_csr(const int64_t* rowptr, const int64_t* colidx, const double* vals, int64_t rows, const double* x,
+             int64_t ldx, int64_t l, double* y, int64_t ldy, cudaStream_t st) {
+  if (rows <= 0 || l <= 0) return 0;
+  spmm_csr_kernel<<<grid_for(rows * l), 256, 0, st>>>(rowptr, colidx, vals, rows, x, ldx, l, y, ldy);
+  RLRA_LAUNCHED();
+  return 0;
+}
+
 // ---------------------------------------------------------------- column energies
 __global__ void colsumsq_kernel(const double* __restrict__ a, int64_t lda, int64_t m, int64_t n,
                                 double* out) {

@@ -277,10 +277,74 @@ def as_accessor(a, device=None):
         import scipy.sparse as sp
 
         if sp.issparse(a):
-            raise TypeError("sparse operands are outside the B200 path (SURVEY.md §8(f) row 4)")
+            return SparseDeviceMatrix(a, device)
     except ImportError:  # pragma: no cover
         pass
     return DeviceMatrix(a, device)
+
+
+class SparseDeviceMatrix:
+    """HBM-resident sparse operand (rlra/accessors.py:40-64, SparseAccessor):
+    products never densify A.  Both CSR(A) (for A X) and CSR(A^T) = CSC(A)
+    (for A^T X) are kept, int64 indices, so each product is a gather SpMM with
+    a fixed per-row summation order (csrc/misc.cu spmm_csr_kernel)."""
+
+    is_device_accessor = True
+
+    def __init__(self, a, device=None):
+        import scipy.sparse as sp
+
+        dev = ops.check_device(device)
+        self._dev = dev
+        csr = sp.csr_matrix(a, dtype=np.float64)
+        csr.sum_duplicates()
+        csc = sp.csc_matrix(csr)
+        self._shape = tuple(int(x) for x in csr.shape)
+        up = lambda x, dt: torch.as_tensor(np.ascontiguousarray(x, dtype=dt), device=dev)  # noqa: E731
+        self._r = (up(csr.indptr, np.int64), up(csr.indices, np.int64), up(csr.data, np.float64))
+        self._c = (up(csc.indptr, np.int64), up(csc.indices, np.int64), up(csc.data, np.float64))
+        self._host = csc
+
+    @property
+    def shape(self):
+        return self._shape
+
+    @property
+    def device(self):
+        return self._dev
+
+    def _spmm(self, mats, rows, x):
+        x = _dev(x, self._dev)
+        y = ops.fmat(rows, x.shape[1], self._dev)
+        rp, ci, va = mats
+        ops._call("rlra_b200_spmm_csr", self._dev, ops.ptr(rp), ops.ptr(ci), ops.ptr(va), rows, ops.ptr(x),
+                  ops.ld_of(x), x.shape[1], ops.ptr(y), ops.ld_of(y), ops._stream(self._dev))
+        return y
+
+    def matmul(self, x):
+        """A @ X, one pass (rlra/accessors.py:50-51)."""
+        with ops.label("pass_nn_sparse"):
+            return self._spmm(self._r, self._shape[0], x)
+
+    def rmatmul(self, x):
+        """A^T @ X, one pass (rlra/accessors.py:53-54)."""
+        with ops.label("pass_tn_sparse"):
+            return self._spmm(self._c, self._shape[1], x)
+
+    def fro_norm_sq_device(self):
+        v = self._r[2]
+        return ops.sumsq(v.view(-1, 1)) if v.numel() else torch.zeros(1, dtype=torch.float64, device=self._dev)
+
+    def fro_norm(self):
+        """rlra/accessors.py:56-57."""
+        return math.sqrt(float(self.fro_norm_sq_device().item()))
+
+    def to_dense(self):
+        return np.asarray(self._host.todense(), dtype=np.float64)
+
+    @property
+    def sparse(self):
+        return self._host
 
 
 def _dev(x, device):
