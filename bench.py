@@ -367,7 +367,8 @@ def our_arm(args):
         pinned = torch.empty((w.n, w.m), dtype=torch.float64, pin_memory=True)
         ah = pinned.numpy().T  # F-ordered m x n view of pinned memory
         ah[...] = a
-        fh = P.powerlu(ah, w.k, w.q_os, v, w.seed)  # warm
+        for _ in range(max(2, args.warmup)):  # warm-up: pinned result buffers reach their steady-state reuse
+            fh = P.powerlu(ah, w.k, w.q_os, v, w.seed)
         ksteps = max(1, min(args.steps, 5))
         torch.cuda.synchronize()
         s0 = torch.cuda.Event(enable_timing=True)
@@ -493,17 +494,22 @@ def dist_arm(args):
     if host_shard is not None and not args.no_e2e:
         ksteps = max(1, min(args.steps, 5))
         d2h = 0
+
+        def e2e_step():
+            sh = cops.empty(r1 - r0, w.n)
+            sh.copy_(host_shard.t(), non_blocking=True)
+            f = D.powerlu(D.ShardedMatrix(sh, w.m, r0, r1, cops), w.k, w.q_os, v, w.seed, omega)
+            return ops.to_numpy_many([f.p, f.q, f.L, f.U]) if rank == 0 else []
+
+        for _ in range(max(2, args.warmup)):
+            e2e_step()
         dist.barrier()
         torch.cuda.synchronize()
         s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s0.record(st)
         for _ in range(ksteps):
-            sh = cops.empty(r1 - r0, w.n)
-            sh.copy_(host_shard.t(), non_blocking=True)
-            f = D.powerlu(D.ShardedMatrix(sh, w.m, r0, r1, cops), w.k, w.q_os, v, w.seed, omega)
-            if rank == 0:
-                hp = ops.to_numpy_many([f.p, f.q, f.L, f.U])
-                d2h = sum(x.nbytes for x in hp)
+            hp = e2e_step()
+            d2h = sum(x.nbytes for x in hp)
         s1.record(st)
         torch.cuda.synchronize()
         em = torch.tensor([s0.elapsed_time(s1) / ksteps], device=dev)
