@@ -774,7 +774,7 @@ __global__ void lu_trsm_kernel(double* a, int64_t lda, int64_t j0, int nb, int64
 
 // A22 -= L21 * U12 with the panel's steps applied in ascending order, DMUL+DSUB.
 constexpr int UPD_TM = 64, UPD_TN = 64;
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 4)
 lu_update_kernel(double* a, int64_t lda, int64_t j0, int nb, int64_t r0, int64_t m, int64_t c0,
                  int64_t n, const int* zflag) {
   __shared__ double Ls[LU_NB][UPD_TM];
