@@ -70,6 +70,9 @@ struct Crt {
   int m[kMaxMod];
   float inv_m[kMaxMod];
   uint32_t limb[kCrtLimbs][kMaxMod];  // 20-bit limbs of M / m_l
+  uint32_t d28[4][kMaxMod];           // 28-bit limbs of M / m_l (nmod <= 14: M < 2^112)
+  uint32_t M28[4];                    // 28-bit limbs of M
+  uint32_t H28[4];                    // 28-bit limbs of floor(M / 2)
   double inv_M;                     // ~1 / M
   int nmod;
 };
@@ -115,7 +118,10 @@ static Crt make_crt(int nmod) {
     c.m[l] = m;
     c.inv_m[l] = 1.0f / (float)m;
     for (int q = 0; q < kCrtLimbs; ++q) c.limb[q][l] = (uint32_t)((md >> (20 * q)) & 0xFFFFF);
+    for (int q = 0; q < 4; ++q) c.d28[q][l] = (uint32_t)((md >> (28 * q)) & 0xFFFFFFF);
   }
+  for (int q = 0; q < 4; ++q) c.M28[q] = (uint32_t)((M >> (28 * q)) & 0xFFFFFFF);
+  for (int q = 0; q < 4; ++q) c.H28[q] = (uint32_t)((H >> (28 * q)) & 0xFFFFFFF);
   c.inv_M = 1.0 / (double)M;
   c.nmod = nmod;
   return c;
@@ -672,21 +678,69 @@ __device__ __forceinline__ double u128_to_double(u128 x) {
 // CRT: s = sum_l t'_l (M / m_l) (t'_l < m_l, so every term is < M and the sum
 // of nmod <= 15 terms stays below 2^122), in two 64-bit words; then one
 // reduction modulo M and the signed representative as a double.
-__global__ void __launch_bounds__(256) crt_kernel(const uint8_t* __restrict__ t, int64_t rows_pad, int64_t cols_pad,
-                                                  int64_t mrows, int64_t ncols, const int* __restrict__ e_a,
-                                                  const int* __restrict__ e_b, const Crt crt, double* __restrict__ c,
-                                                  int64_t ldc, int add) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t j = blockIdx.y;
-  if (i >= mrows) return;
+// One element of the CRT: residues tv[0..nmod) -> the signed integer A''B'' as a
+// double (within 1 ulp; the sign in `neg`).
+__device__ __forceinline__ double crt_value(const unsigned (&tv)[kMaxMod], const Crt& crt, bool& neg) {
+  const int nm = crt.nmod;
   const u128 M = ((u128)crt.M_hi << 64) | crt.M_lo;
   const u128 H = ((u128)crt.H_hi << 64) | crt.H_lo;
-  const size_t lstride = (size_t)cols_pad * rows_pad;
-  const uint8_t* tp = t + (size_t)j * rows_pad + i;
-  const int nm = crt.nmod;
-  unsigned tv[kMaxMod];
+  double v;
+  if (nm <= 14) {
+    // 28-bit limbs: every product t d < 2^36 and the 14-term sums < 2^40, one
+    // 32x32->64 multiply-add each (IMAD.WIDE); then carries, one quotient
+    // estimate (s < 14 * 256 * M / 181 < 20 M) and an exact limb subtraction
+    constexpr int64_t MASK = (1ll << 28) - 1;
+    uint64_t a0 = 0, a1 = 0, a2 = 0, a3 = 0;
 #pragma unroll
-  for (int l = 0; l < kMaxMod; ++l) tv[l] = (l < nm) ? (unsigned)__ldcs(tp + (size_t)l * lstride) : 0u;
+    for (int l = 0; l < 14; ++l) {
+      const uint64_t tl = tv[l];
+      a0 += tl * crt.d28[0][l];
+      a1 += tl * crt.d28[1][l];
+      a2 += tl * crt.d28[2][l];
+      a3 += tl * crt.d28[3][l];
+    }
+    a1 += a0 >> 28;
+    a2 += a1 >> 28;
+    a3 += a2 >> 28;
+    int64_t s0 = (int64_t)(a0 & MASK), s1 = (int64_t)(a1 & MASK), s2 = (int64_t)(a2 & MASK), s3 = (int64_t)a3;
+    const double sd = fma((double)s3, 0x1p84, (double)s2 * 0x1p56);
+    const int64_t q = (int64_t)(sd * crt.inv_M);  // floor(s / M) or one off
+    s0 -= q * (int64_t)crt.M28[0];
+    s1 -= q * (int64_t)crt.M28[1];
+    s2 -= q * (int64_t)crt.M28[2];
+    s3 -= q * (int64_t)crt.M28[3];
+    auto norm = [&]() {  // signed limbs -> limbs in [0, 2^28) except the top
+      s1 += s0 >> 28;
+      s0 &= MASK;
+      s2 += s1 >> 28;
+      s1 &= MASK;
+      s3 += s2 >> 28;
+      s2 &= MASK;
+    };
+    norm();
+    if (s3 < 0) {  // q one too large
+      s0 += crt.M28[0]; s1 += crt.M28[1]; s2 += crt.M28[2]; s3 += crt.M28[3];
+      norm();
+    }
+    const bool ge = s3 != (int64_t)crt.M28[3] ? s3 > (int64_t)crt.M28[3]
+                    : s2 != (int64_t)crt.M28[2] ? s2 > (int64_t)crt.M28[2]
+                    : s1 != (int64_t)crt.M28[1] ? s1 > (int64_t)crt.M28[1] : s0 >= (int64_t)crt.M28[0];
+    if (ge) {  // q one too small
+      s0 -= crt.M28[0]; s1 -= crt.M28[1]; s2 -= crt.M28[2]; s3 -= crt.M28[3];
+      norm();
+    }
+    // s in [0, M): the signed representative is s - M when s > floor(M / 2)
+    neg = s3 != (int64_t)crt.H28[3] ? s3 > (int64_t)crt.H28[3]
+          : s2 != (int64_t)crt.H28[2] ? s2 > (int64_t)crt.H28[2]
+          : s1 != (int64_t)crt.H28[1] ? s1 > (int64_t)crt.H28[1] : s0 > (int64_t)crt.H28[0];
+    if (neg) {  // magnitude M - s
+      s0 = crt.M28[0] - s0; s1 = crt.M28[1] - s1; s2 = crt.M28[2] - s2; s3 = crt.M28[3] - s3;
+      norm();
+    }
+    const uint64_t top = ((uint64_t)s3 << 28) | (uint64_t)s2;  // < 2^54: exact in a double
+    const uint64_t low = ((uint64_t)s1 << 28) | (uint64_t)s0;  // < 2^56
+    v = fma((double)top, 0x1p56, (double)low);                  // within 1 ulp
+  } else {
   u128 s = 0;
   if (nm <= 15) {
     uint64_t lo = 0, hi = 0;
@@ -710,9 +764,39 @@ __global__ void __launch_bounds__(256) crt_kernel(const uint8_t* __restrict__ t,
     }
   }
   const u128 mag = (s > H) ? M - s : s;
-  const double v = fma((double)(uint64_t)(mag >> 64), 0x1p64, (double)(uint64_t)mag);  // within 1 ulp
-  const double r = ((s > H) ? -v : v) * scalbn(1.0, -(e_a[0] + e_b[j]));
-  c[i + j * ldc] = add ? c[i + j * ldc] + r : r;  // add: C += A B (one rounding of the sum, like beta = 1)
+  v = fma((double)(uint64_t)(mag >> 64), 0x1p64, (double)(uint64_t)mag);  // within 1 ulp
+  neg = s > H;
+  }
+  return v;
+}
+
+// 4 consecutive rows per thread: one 32-bit load per residue plane.
+__global__ void __launch_bounds__(256) crt_kernel(const uint8_t* __restrict__ t, int64_t rows_pad, int64_t cols_pad,
+                                                  int64_t mrows, int64_t ncols, const int* __restrict__ e_a,
+                                                  const int* __restrict__ e_b, const Crt crt, double* __restrict__ c,
+                                                  int64_t ldc, int add) {
+  const int64_t i0 = 4 * ((int64_t)blockIdx.x * blockDim.x + threadIdx.x);
+  const int64_t j = blockIdx.y;
+  if (i0 >= mrows) return;
+  const size_t lstride = (size_t)cols_pad * rows_pad;
+  const uint32_t* tp = reinterpret_cast<const uint32_t*>(t + (size_t)j * rows_pad + i0);  // rows_pad % 256 == 0
+  const int nm = crt.nmod;
+  uint32_t w[kMaxMod];
+#pragma unroll
+  for (int l = 0; l < kMaxMod; ++l) w[l] = (l < nm) ? __ldcs(tp + (size_t)l * (lstride / 4)) : 0u;
+  const double sc = scalbn(1.0, -(e_a[0] + e_b[j]));
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    if (i0 + e >= mrows) break;
+    unsigned tv[kMaxMod];
+#pragma unroll
+    for (int l = 0; l < kMaxMod; ++l) tv[l] = (w[l] >> (8 * e)) & 0xFFu;
+    bool neg;
+    const double v = crt_value(tv, crt, neg);
+    const double r = (neg ? -v : v) * sc;
+    double* cp = c + (i0 + e) + j * ldc;
+    *cp = add ? *cp + r : r;  // add: C += A B (one rounding of the sum, like beta = 1)
+  }
 }
 
 // ----------------------------------------------------------------- host side
@@ -954,7 +1038,7 @@ int oz_gemm_ex(int trans, const void* prep, int64_t m, int64_t n, int nmod, cons
 
   if (flags & 2) return 0;  // RLRA_B200_OZ_NO_CRT: more K blocks follow
   ktimer_mark(KT_OZ_CRT, st, false);
-  oz::crt_kernel<<<dim3((unsigned)ceil_div(mrows, 256), (unsigned)ncols), 256, 0, st>>>(
+  oz::crt_kernel<<<dim3((unsigned)ceil_div(mrows, 1024), (unsigned)ncols), 256, 0, st>>>(
       tout, g.rows_pad, g.cols_pad, mrows, ncols, e_a, e_b, crt, c, ldc, (flags & 4) ? 1 : 0);
   ktimer_mark(KT_OZ_CRT, st, true);
   RLRA_LAUNCHED();
