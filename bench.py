@@ -356,6 +356,15 @@ def our_arm(args):
     ops.PROF.records.clear()
     pass_ms = sum(summ.get(k, (0.0, 0))[0] for k in ("pass_nn", "pass_tn"))
     roofline = roofline_line(w, v, passes, reps, kt, pass_ms, ms)
+    # the exact GEPPs: latency-bound (one cluster-wide pivot exchange per column),
+    # no HBM / tensor roofline applies; reported with their share of the step
+    l_ = w.k + w.q_os
+    gepp_cols = (v - 2) * l_ + 2 * w.k  # v - 2 interior sketch LUs of width l, the two final LUs of width k
+    gepp_ms = summ.get("rlra_b200_getrf", (0.0, 0))[0] / reps
+    roofline["latency_bound"] = {
+        "kernel": "lu_coop_kernel (bit-exact GEPP, csrc/getrf_full.cu)", "ms_per_step": gepp_ms,
+        "share_of_step": gepp_ms / ms, "calls_per_step": summ.get("rlra_b200_getrf", (0.0, 0))[1] / reps,
+        "us_per_column": 1e3 * gepp_ms / max(1, gepp_cols), "columns_per_step": gepp_cols}
     if args.breakdown:
         for k2, (t, c) in sorted(summ.items(), key=lambda kv: -kv[1][0]):
             print(f"  {k2:32s} {t / reps:9.3f} ms/step  {c / reps:6.1f} calls/step", file=sys.stderr)
