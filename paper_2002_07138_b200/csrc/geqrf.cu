@@ -30,7 +30,6 @@ int gemm(bool ta, bool tb, int64_t M, int64_t N, int64_t K, double alpha, const 
 size_t gemm_workspace_bytes(int64_t M, int64_t N, int64_t K);
 
 constexpr int QR_NB = 32;
-constexpr int QR_THREADS = 256;
 
 struct QrPanelArgs {
   double* a;
@@ -633,7 +632,6 @@ int orgqr(const double* a, int64_t lda, int64_t m, int64_t n, double* q, int64_t
   RLRA_REQUIRE(ws && ws_bytes >= L.total, "orgqr: workspace too small");
   char* base = static_cast<char*>(ws);
   double* vbuf = reinterpret_cast<double*>(base + L.vbuf);
-  double* tbl = reinterpret_cast<double*>(base + L.tblocks);
   double* wbuf = reinterpret_cast<double*>(base + L.wbuf);
   double* w2buf = reinterpret_cast<double*>(base + L.w2buf);
   void* gws = base + L.gemm_ws;
@@ -641,7 +639,6 @@ int orgqr(const double* a, int64_t lda, int64_t m, int64_t n, double* q, int64_t
   set_identity_kernel<<<grid_for_q(m * n), 256, 0, st>>>(q, ldq, m, n);
   RLRA_LAUNCHED();
   double* tbig = reinterpret_cast<double*>(base + L.tbig);
-  (void)tbl;
   // outer blocks (V_b, T_b from geqrf), last to first
   for (int64_t ob = ceil_div(n, QR_NBO) - 1; ob >= 0; ob--) {
     const int64_t ob0 = ob * QR_NBO;

@@ -276,7 +276,7 @@ struct Panel {
 template <int RPT, int W, int SC>
 __device__ __forceinline__ unsigned publish(const Ctx& x, Panel<RPT, W>& P, int jj, int nb, int jn, bool fin,
                                             const double* su, unsigned par) {
-  const int j0 = SC == 0 ? 1 : jn - 1 - jj;  // for STEP_TRACE (panel 0 steps only)
+  [[maybe_unused]] const int j0 = SC == 0 ? 1 : jn - 1 - jj;  // for STEP_TRACE (panel 0 steps only)
   constexpr int RECD = 2 + W;
   constexpr int RS = Plan<RPT, W>::RS;
   Shared& S = *x.S;
