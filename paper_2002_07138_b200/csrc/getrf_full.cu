@@ -925,7 +925,12 @@ static int launch_full(lufull::Args a, cudaStream_t st) {
   }
   const int ncl = nclusters[dev & 63][RPT];
   if (ncl < 2) return 1;
-  const int nh = ncl - 1 < 6 ? ncl - 1 : 6;  // helper clusters
+  static int nh_cap = -1;  // helper clusters (RLRA_B200_LU_HELPERS overrides the default 6)
+  if (nh_cap < 0) {
+    const char* e = getenv("RLRA_B200_LU_HELPERS");
+    nh_cap = (e && atoi(e) > 0) ? atoi(e) : 6;
+  }
+  const int nh = ncl - 1 < nh_cap ? ncl - 1 : nh_cap;
   a.nhelpers = (unsigned)(nh * lufull::CS);
   RLRA_CHECK_CUDA(cudaMemsetAsync(a.recg, 0, sizeof(lufull::Handoff), st));
   cfg.gridDim = dim3(lufull::CS * (1 + nh));
