@@ -25,6 +25,13 @@ constexpr int CHOL_THREADS = 512;
 
 __host__ __device__ __forceinline__ int pk(int i, int j) { return j * (j + 1) / 2 + i; }  // i <= j
 
+// global -> shared staging with every element in flight at once (LDGSTS): the
+// plain load/store loops waited one global latency per handful of elements
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
 // Blocked (32) right-looking Cholesky in shared memory, one CTA:
 //   diagonal block by warp 0 in registers (shuffles), the block row by a
 //   forward substitution per column (one thread each), the trailing triangle
@@ -32,26 +39,42 @@ __host__ __device__ __forceinline__ int pk(int i, int j) { return j * (j + 1) / 
 // Then X = R^{-1} column by column (one warp each, back substitution, R read
 // only), written straight to global memory.
 constexpr int CHOL_NB = 16;
+
+#ifdef CHOL_TRACE  // tools/chol_probe.cu: globaltimer stamps [iteration][8]
+__device__ unsigned long long* g_chol_trace;
+void chol_set_trace(unsigned long long* p) { cudaMemcpyToSymbol(g_chol_trace, &p, sizeof(p)); }
+#define CTRACE(slot)                                                                           \
+  do {                                                                                         \
+    unsigned long long t_;                                                                     \
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                                     \
+    if (g_chol_trace && it + 1 < 20) g_chol_trace[(it + 1) * 8 + (slot)] = t_;                 \
+  } while (0)
+#else
+#define CTRACE(slot) \
+  do {               \
+  } while (0)
+#endif
 constexpr int CHOL_MAXL = 256;
 
 __global__ void __launch_bounds__(CHOL_THREADS, 1)
     chol_kernel(double* __restrict__ g, int64_t ldg, int l, int* __restrict__ flag, double cond_limit) {
   extern __shared__ double P[];
   double* dinv = P + (size_t)l * (l + 1) / 2;  // 1 / R_ii
-  __shared__ double Xkk[CHOL_NB][CHOL_NB + 1];  // inverse of the current diagonal block (row-major)
+  __shared__ double Xkk[CHOL_NB][CHOL_NB + 1];  // current diagonal block R_kk (row-major)
   __shared__ int s_bad;
   __shared__ double s_rmin, s_rmax;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int NW = CHOL_THREADS / 32;
   for (int j = warp; j < l; j += NW)
-    for (int i = lane; i <= j; i += 32) P[pk(i, j)] = g[i + (int64_t)j * ldg];
+    for (int i = lane; i <= j; i += 32) cp_async8(&P[pk(i, j)], &g[i + (int64_t)j * ldg]);
+  cp_async_wait_all();
   if (tid == 0) {
     s_bad = 0;
     s_rmin = INFINITY;
     s_rmax = 0.0;
   }
   __syncthreads();
-  // (1) factor + invert the diagonal block at k0 (warp 0): lane c holds column k0 + c
+  // (1) factor the diagonal block at k0 (warp 0): lane c holds column k0 + c
   auto diag = [&](const int k0, const int b) {
       double gg[CHOL_NB];
 #pragma unroll
@@ -82,27 +105,12 @@ __global__ void __launch_bounds__(CHOL_THREADS, 1)
 #pragma unroll
       for (int i = 0; i < CHOL_NB; i++)
         if (i == lane) dl = gg[i];
-      const double dil = 1.0 / dl;  // lane i: 1 / R_ii, all lanes at once
-      if (lane < b) dinv[k0 + lane] = dil;
-      // inverse of the diagonal block: lane c back-substitutes its own column
-      // (R_kk staged row-major in Xkk first; rows / columns >= b are identity)
+      if (lane < b) dinv[k0 + lane] = 1.0 / dl;
+      // R_kk staged row-major for the block-row substitution (zero outside
+      // the b x b triangle)
 #pragma unroll
       for (int i = 0; i < CHOL_NB; i++)
-        if (lane < CHOL_NB) Xkk[i][lane] = (i <= lane && lane < b) ? gg[i] : (i == lane ? 1.0 : 0.0);
-      __syncwarp();
-      double xc[CHOL_NB];
-#pragma unroll
-      for (int i = CHOL_NB - 1; i >= 0; i--) {
-        double acc = (i == lane) ? 1.0 : 0.0;
-#pragma unroll
-        for (int t = i + 1; t < CHOL_NB; t++) acc = fma(-Xkk[i][t], (t <= lane && lane < CHOL_NB) ? xc[t] : 0.0, acc);
-        const double di = __shfl_sync(0xffffffffu, dil, i);  // every lane participates
-        xc[i] = (i <= lane) ? acc * di : 0.0;
-      }
-      __syncwarp();
-#pragma unroll
-      for (int i = 0; i < CHOL_NB; i++)
-        if (lane < CHOL_NB) Xkk[i][lane] = xc[i];
+        if (lane < CHOL_NB) Xkk[i][lane] = (i <= lane && lane < b) ? gg[i] : 0.0;
       if (lane == 0) {
         if (bad) s_bad = 1;
         s_rmin = fmin(s_rmin, rmin);
@@ -115,54 +123,86 @@ __global__ void __launch_bounds__(CHOL_THREADS, 1)
   for (int it = -1;; it++) {
     const int k0 = it * CHOL_NB;
     const int b = it < 0 ? 0 : min(CHOL_NB, l - k0);
+    if (tid == 0) CTRACE(0);
     if (s_bad) break;
     const int c0 = it < 0 ? 0 : k0 + b, m = l - c0;
     if (m <= 0) break;
-    // ---- (2) block row: R(k0.., j) = R_kk^{-T} G(k0.., j) = Xkk^T g, one warp
-    // per column: lane u accumulates sum_{s <= u} Xkk[s][u] g_s (no recurrence)
-    for (int jj = warp; it >= 0 && jj < m; jj += NW) {
-      const int j = c0 + jj, cj = j * (j + 1) / 2;
-      const double gl = (lane < b) ? P[cj + k0 + lane] : 0.0;
-      double acc = 0.0;
+    // ---- (2) block row: R(k0.., j) = R_kk^{-T} G(k0.., j), one thread per
+    // column: forward substitution with the column's 16 entries in registers
+    // (R_kk reads are warp broadcasts; no inverse of R_kk on the warp-0 chain)
+#ifdef CHOL_EXP_NOBLKROW
+    for (int jj = tid; false; jj += CHOL_THREADS) {
+#else
+    for (int jj = tid; it >= 0 && jj < m; jj += CHOL_THREADS) {
+#endif
+      const int j = c0 + jj, cj = j * (j + 1) / 2 + k0;
+      double x[CHOL_NB];
+#pragma unroll
+      for (int u = 0; u < CHOL_NB; u++) x[u] = (u < b) ? P[cj + u] : 0.0;
 #pragma unroll
       for (int s2 = 0; s2 < CHOL_NB; s2++) {
-        const double gs = __shfl_sync(0xffffffffu, gl, s2);
-        if (s2 <= lane && lane < CHOL_NB) acc = fma(Xkk[s2][lane], gs, acc);
+        x[s2] *= (s2 < b) ? dinv[k0 + s2] : 1.0;
+#pragma unroll
+        for (int u = s2 + 1; u < CHOL_NB; u++) x[u] = fma(-Xkk[s2][u], x[s2], x[u]);
+        asm volatile("" ::: "memory");  // keep the R_kk row loads per step (no hoisting / spills)
       }
-      __syncwarp();
-      if (lane < b) P[cj + k0 + lane] = acc;
+#pragma unroll
+      for (int u = 0; u < CHOL_NB; u++)
+        if (u < b) P[cj + u] = x[u];
     }
+    if (tid == 0) CTRACE(1);
+    if (tid == 32) CTRACE(5);
     __syncthreads();
+    if (tid == 0) CTRACE(2);
     // ---- (3) trailing triangle -= R(k0.., :)^T R(k0.., :).  Look-ahead: warp 0
     // updates the NEXT diagonal block and factors it while warps 1.. update
     // the rest of the triangle in 4 x 4 tiles.
     const int bn = min(CHOL_NB, m);
-    if (warp == 0) {
+    if (warp < 4) {
+      // the next diagonal block's update, one entry per thread of warps 0..3
+#ifdef CHOL_EXP_NONEXT
+      const int ne = 0;
+#else
       const int ne = it < 0 ? 0 : bn * (bn + 1) / 2;
-      for (int e = lane; e < ne; e += 32) {
+#endif
+      for (int e = tid; e < ne; e += 128) {
         int jj = (int)((sqrtf(8.0f * (float)e + 1.0f) - 1.0f) * 0.5f);
         while (jj * (jj + 1) / 2 > e) --jj;
         while ((jj + 1) * (jj + 2) / 2 <= e) ++jj;
         const int i = c0 + (e - jj * (jj + 1) / 2), j = c0 + jj;
+        const int bi = i * (i + 1) / 2 + k0, bj = j * (j + 1) / 2 + k0;
         double acc = 0.0;
-        for (int s2 = 0; s2 < b; s2++) acc = fma(P[pk(k0 + s2, i)], P[pk(k0 + s2, j)], acc);
+#pragma unroll
+        for (int s2 = 0; s2 < CHOL_NB; s2++)
+          if (s2 < b) acc = fma(P[bi + s2], P[bj + s2], acc);
         P[pk(i, j)] -= acc;
       }
-      __syncwarp();
+      asm volatile("bar.sync 1, 128;\n" ::: "memory");
+    }
+    if (warp == 0) {
+      if (lane == 0) CTRACE(3);
+#ifdef CHOL_EXP_NODIAG
+      if (it < 0)
+#endif
       diag(c0, bn);
+      if (lane == 0) CTRACE(4);
     } else {
 #ifdef CHOL_EXP_NOTRAIL
       const int mt = 0;
 #else
       const int mt = it < 0 ? 0 : (m + 3) >> 2;
 #endif
-      const int ntiles = mt * (mt + 1) / 2;
-      const int lim = c0 + bn;  // entries with i, j < lim belong to warp 0
-      for (int t = tid - 32; t < ntiles; t += CHOL_THREADS - 32) {
-        int tb = (int)((sqrtf(8.0f * (float)t + 1.0f) - 1.0f) * 0.5f);
-        while (tb * (tb + 1) / 2 > t) --tb;
-        while ((tb + 1) * (tb + 2) / 2 <= t) ++tb;
-        const int ta = t - tb * (tb + 1) / 2;
+      // 4 x 4 register tiles, grouped per warp into 4 (ta) x 8 (tb) super-tiles:
+      // a block-row load touches 4 (ra) or 8 (rb) distinct addresses per warp
+      // instead of 32 scattered columns (the former 1-D tile order ran the
+      // trailing update at ~5-way shared-memory bank conflicts)
+      const int nsa = (mt + 3) >> 2, nsb = (mt + 7) >> 3;
+      const int lim = c0 + bn;  // entries with i, j < lim belong to warps 0..3
+      for (int st = warp - 1; st < nsa * nsb; st += NW - 1) {
+        const int sa = st % nsa, sb = st / nsa;
+        if (4 * sa > 8 * sb + 7) continue;  // whole super-tile below the diagonal
+        const int ta = 4 * sa + (lane & 3), tb = 8 * sb + (lane >> 2);
+        if (ta > tb || tb >= mt) continue;
         const int ja = c0 + 4 * ta, jb = c0 + 4 * tb;
         if (jb + 3 < lim) continue;  // whole tile inside the next diagonal block
         double acc[4][4];
@@ -202,6 +242,8 @@ __global__ void __launch_bounds__(CHOL_THREADS, 1)
           }
       }
     }
+    if (tid == 32) CTRACE(6);
+    if (tid == CHOL_THREADS - 1) CTRACE(7);
     __syncthreads();
   }
   __syncthreads();
@@ -233,7 +275,8 @@ __global__ void __launch_bounds__(INV_COLS * 32, 1)
     return;
   }
   const int np = l * (l + 1) / 2;
-  for (int e = tid; e < np; e += blockDim.x) P[e] = rp[e];
+  for (int e = tid; e < np; e += blockDim.x) cp_async8(&P[e], &rp[e]);
+  cp_async_wait_all();
   __syncthreads();
   for (int t = tid; t < l; t += blockDim.x) dinv[t] = 1.0 / P[pk(t, t)];
   __syncthreads();
