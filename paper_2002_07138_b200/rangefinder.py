@@ -63,6 +63,7 @@ class RankChecks:
     def __init__(self):
         self._items = []
         self._cholqr = None  # (flag, Z) of a deferred CholeskyQR2 basis
+        self._resolved = []  # host values of the first len(_resolved) counts
 
     def add(self, count, requested):
         self._items.append((count, int(requested)))
@@ -70,21 +71,36 @@ class RankChecks:
     def defer_cholqr(self, flag, z):
         self._cholqr = (flag, z)
 
+    def _fetch(self, extra=None):
+        """Every unresolved count (and `extra`) in ONE device->host transfer."""
+        pend = [c.view(-1) for c, _ in self._items[len(self._resolved):]]
+        if extra is not None:
+            pend.append(extra.view(-1).to(torch.int64))
+        if not pend:
+            return []
+        vals = (torch.cat(pend) if len(pend) > 1 else pend[0]).cpu().tolist()
+        n = len(vals) - (extra is not None)
+        self._resolved.extend(int(v) for v in vals[:n])
+        return vals[n:]
+
     def cholqr_declined(self):
-        """The parked CholeskyQR2 flag (host sync): None when no basis was
-        deferred, else (declined, Z)."""
+        """The parked CholeskyQR2 flag: None when no basis was deferred, else
+        (declined, Z).  The counts queued so far come back in the same host
+        round trip, so a call that does not decline syncs exactly once."""
         if self._cholqr is None:
             return None
         flag, z = self._cholqr
         self._cholqr = None
-        return bool(int(flag.item())), z
+        return bool(int(self._fetch(flag)[0])), z
 
     def raise_if_collapsed(self):
+        """Raise RankCollapse for the first count (in call order) below its
+        requested width; only counts not yet resolved cost a transfer."""
         if not self._items:
             return
-        counts = torch.cat([c for c, _ in self._items]).cpu().tolist()
-        items = self._items
-        self._items = []
+        self._fetch()
+        items, counts = self._items, self._resolved
+        self._items, self._resolved = [], []
         for achieved, (_, requested) in zip(counts, items):
             if achieved < requested:
                 raise RankCollapse(int(achieved), requested)
