@@ -84,6 +84,29 @@ def test_cholqr2_flags_rank_collapse_and_ill_conditioning(cuda_dev):
     assert int(flag.item()) == 1
 
 
+@pytest.mark.parametrize("l", [1, 2, 15, 16, 17, 31, 32, 33, 47, 100, 129, 220, -1])
+def test_chol_inv_block_edges(cuda_dev, l):
+    """chol_kernel's 16-column blocks, the 4-warp next-block update and the
+    4 x 8 super-tiles of the trailing update at every ragged edge (l = -1: the
+    largest l the shared-memory layout takes)."""
+    import torch
+
+    from paper_2002_07138_b200 import ops
+
+    l = ops.cholqr_max_l() if l < 0 else l
+    rng = np.random.default_rng(100 + l)
+    z = rng.standard_normal((3 * l + 5, l)) * np.logspace(0, -3, l)[None, :]
+    g = z.T @ z
+    out = ops.fmat(l, l, cuda_dev)
+    flag = torch.zeros(1, dtype=torch.int32, device=cuda_dev)
+    ops.chol_inv(ops.from_numpy(g, cuda_dev), out, flag, 1e8)
+    assert int(flag.item()) == 0
+    rinv = ops.to_numpy(out)
+    assert np.all(np.tril(rinv, -1) == 0)
+    # R^{-T} G R^{-1} = I to working precision (cond(G) ~ 1e6 here)
+    assert np.abs(rinv.T @ g @ rinv - np.eye(l)).max() < 1e-9
+
+
 def test_chol_inv_matches_numpy(cuda_dev):
     import torch
 
