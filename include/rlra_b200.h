@@ -105,13 +105,33 @@ RLRA_B200_API int rlra_b200_dgemm(int transa, int transb, int64_t m, int64_t n, 
  * rounded to integers (A'' = rint(2^eA A), B'' = rint(2^eB[j] B[:, j])), the
  * integer product is computed exactly modulo nmod pairwise-coprime moduli with
  * tcgen05 kind::i8 MMAs and reassembled by Chinese remaindering, then rounded
- * once to double.  Accuracy: |error| <~ 2^-53 ||A_i|| ||B_j|| for nmod = 14
- * (the DGEMM-level bound); results are exact functions of the inputs.
+ * once to double.  Accuracy (nmod = 14, PA = 54, PB = 53): with N_A the
+ * largest row or column 2-norm of A and A_i the i-th row of op(A),
+ *   |error_ij| <= 2^-PA sqrt(K) N_A ||B_j|| + 2^-PB sqrt(K) ||A_i|| ||B_j|| + 2^-52 ||A_i|| ||B_j||,
+ * normwise in N_A (one scale for all of A).  rlra_b200_oz_guard admits an
+ * orientation when N_A / min ||A_i|| <= rlra_b200_oz_guard_limit(K), which
+ * makes this at most K 2^-53 ||A_i|| ||B_j||, the classical DGEMM bound; the
+ * drivers run the other products (graded rows / columns, NaN / Inf, norms
+ * outside [2^-480, 2^512)) on the DMMA GEMM.  Results are exact functions of
+ * the inputs.  A column of B holding NaN / Inf yields a NaN output column.
  * prep: residues of A, built once per A by rlra_b200_oz_prep (both
  * orientations); then any number of
  *   trans = 0: C (m x ncols) = A   B,  B n x ncols
  *   trans = 1: C (n x ncols) = A^T B,  B m x ncols
- * nmod in [12, 16] (14 = DGEMM accuracy); K (= n or m) <= 133144. */
+ * nmod in [12, 16] (14 = DGEMM accuracy); K (= n or m) <= 133144.
+ * The first RLRA_B200_OZ_HEADER_BYTES of a prep (or oz_scale) workspace are
+ * the guard header: int e_a, int pad, then three uint64 holding the double
+ * bits of the largest row/column sum of squares, the smallest non-zero row
+ * sum and the smallest non-zero column sum (all ones: none), then uint32
+ * non-finite flag.  rlra_b200_oz_norms fills it (and e_a) without building
+ * residues; copy it to the host and pass it to rlra_b200_oz_guard (host-only,
+ * no GPU); then rlra_b200_oz_prep_ex(e_a = the prep's own header) builds the
+ * residues. */
+#define RLRA_B200_OZ_HEADER_BYTES 64
+RLRA_B200_API int rlra_b200_oz_norms(const double* a, int64_t lda, int64_t m, int64_t n, int nmod, void* prep,
+                                     size_t prep_bytes, void* stream);
+RLRA_B200_API double rlra_b200_oz_guard_limit(int64_t k);
+RLRA_B200_API int rlra_b200_oz_guard(const void* header, int64_t m, int64_t n, int* ok_nn, int* ok_tn);
 RLRA_B200_API size_t rlra_b200_oz_prep_workspace(int64_t m, int64_t n, int nmod);
 RLRA_B200_API int rlra_b200_oz_prep(const double* a, int64_t lda, int64_t m, int64_t n, int nmod, void* prep,
                                     size_t prep_bytes, void* stream);

@@ -49,6 +49,9 @@ SIGNATURES = {
     "rlra_b200_oz_scale": (_c_i, [_c_p, _c_i64, _c_i64, _c_i64, _c_i, _c_p, _c_p, _c_sz, _c_p]),
     "rlra_b200_oz_prep_ex": (_c_i, [_c_p, _c_i64, _c_i64, _c_i64, _c_i, _c_p, _c_p, _c_sz, _c_p]),
     "rlra_b200_oz_cols_pad": (_c_i64, [_c_i64]),
+    "rlra_b200_oz_norms": (_c_i, [_c_p, _c_i64, _c_i64, _c_i64, _c_i, _c_p, _c_sz, _c_p]),
+    "rlra_b200_oz_guard_limit": (_c_d, [_c_i64]),
+    "rlra_b200_oz_guard": (_c_i, [_c_p, _c_i64, _c_i64, _c_p, _c_p]),
     "rlra_b200_oz_bscale": (_c_i, [_c_p, _c_i64, _c_i64, _c_i64, _c_i, _c_p, _c_p]),
     "rlra_b200_oz_gemm_ex": (_c_i, [_c_i, _c_p, _c_i64, _c_i64, _c_i, _c_p, _c_i64, _c_i64, _c_p, _c_i64,
                                     _c_p, _c_sz, _c_p, _c_i, _c_p]),

@@ -121,6 +121,10 @@ int oz_scale(const double* a, int64_t lda, int64_t m, int64_t n, int nmod, int* 
              cudaStream_t st);
 int oz_prep_ex(const double* a, int64_t lda, int64_t m, int64_t n, int nmod, const int* e_a_ext, void* prep,
                size_t prep_bytes, cudaStream_t st);
+int oz_norms_prep(const double* a, int64_t lda, int64_t m, int64_t n, int nmod, void* prep, size_t prep_bytes,
+                  cudaStream_t st);
+double oz_guard_limit(int64_t k);
+int oz_guard(const void* hdr_host, int64_t m, int64_t n, int* ok_nn, int* ok_tn);
 int64_t oz_cols_pad(int64_t ncols);
 int oz_bscale(const double* b, int64_t ldb, int64_t k, int64_t ncols, int nmod, int* e_b, cudaStream_t st);
 int oz_gemm_ex(int trans, const void* prep, int64_t m, int64_t n, int nmod, const double* b, int64_t ldb,
@@ -285,6 +289,17 @@ int rlra_b200_oz_scale(const double* a, int64_t lda, int64_t m, int64_t n, int n
 int rlra_b200_oz_prep_ex(const double* a, int64_t lda, int64_t m, int64_t n, int nmod, const int* e_a,
                          void* prep, size_t prep_bytes, void* stream) {
   return oz_prep_ex(a, lda, m, n, nmod, e_a, prep, prep_bytes, static_cast<cudaStream_t>(stream));
+}
+
+int rlra_b200_oz_norms(const double* a, int64_t lda, int64_t m, int64_t n, int nmod, void* prep,
+                       size_t prep_bytes, void* stream) {
+  return oz_norms_prep(a, lda, m, n, nmod, prep, prep_bytes, static_cast<cudaStream_t>(stream));
+}
+
+double rlra_b200_oz_guard_limit(int64_t k) { return oz_guard_limit(k); }
+
+int rlra_b200_oz_guard(const void* header, int64_t m, int64_t n, int* ok_nn, int* ok_tn) {
+  return oz_guard(header, m, n, ok_nn, ok_tn);
 }
 
 int64_t rlra_b200_oz_cols_pad(int64_t ncols) { return oz_cols_pad(ncols); }

@@ -14,10 +14,23 @@
 //   3. t_l = C_l mod m_l (uint8), and A''B'' = CRT(t_1..t_NMOD) in (-M/2, M/2)
 //      is reconstructed exactly in 128-bit integers, rounded once to double
 //      and unscaled by 2^-(eA+eB[j]).
-// The only rounding is the scaling step (|error| <= 2^-PA relative to the row /
-// column norm of A, 2^-PB for B), which for NMOD = 14 (PA = 54, PB = 53) is
-// below DGEMM's own accumulation error; results are exact functions of the
-// inputs (tiling- and order-independent, so bitwise deterministic).
+// The only roundings are the scaling steps and the final conversion: with
+// N_A = max over all row AND column 2-norms of A (one scale for both
+// orientations), for C = A B
+//   |C_ij - (AB)_ij| <= 2^-PA sqrt(K) N_A ||B_j|| + 2^-PB sqrt(K) ||A_i|| ||B_j||
+//                       + 2^-52 ||A_i|| ||B_j||
+// (K = contraction length; A_i the i-th row of op(A)).  This is NORMWISE in
+// N_A, not per row: a row i with ||A_i|| << N_A gets a larger relative error
+// than DGEMM would give it.  The dynamic-range guard (oz_guard below,
+// rlra_b200_oz_guard) therefore admits an orientation only when
+//   rho = N_A / min_i ||A_i|| <= T(K) = 2 (K - 2) / sqrt(K) - 2
+// (min over the non-zero rows of op(A)), which makes the bound above at most
+// K u ||A_i|| ||B_j||, u = 2^-53 -- the classical DGEMM bound (every inner
+// product of length K in floating point).  Inputs that fail it (graded rows /
+// columns, non-finite or out-of-range entries) take the FP64 DMMA GEMM
+// instead (ops.OzPrep / ops.OzBlocked route them).  Results are exact
+// functions of the inputs (tiling- and order-independent, so bitwise
+// deterministic).
 //
 // Data layout.  The residues of A are written once per PowerLU call into
 // 128 x 128-byte tiles (16 KB), tile (jb, ib) holding A''[ib*128 .. +128,
@@ -35,6 +48,7 @@
 // accumulators live in TMEM (2 x N_g <= 512 columns).
 #include <algorithm>
 #include <cmath>
+#include <cstring>
 #include <mutex>
 
 #include "common.cuh"
@@ -271,42 +285,69 @@ __global__ void __launch_bounds__(256, 3) residue_a_kernel(const double* __restr
   }
 }
 
-// Per-column scale of the skinny operand B (K x ncols): one CTA per (padded) column.
+// Per-column scale of the skinny operand B (K x ncols): one CTA per (padded)
+// column.  Two passes over the column (it is L1/L2 resident): max |b|, then the
+// sum of squares of b 2^-s (s = exponent of the max) so neither overflow nor
+// underflow of the squares can misplace the scale.  A column holding NaN/Inf
+// gets kEbNonFinite: its residues are zero and the CRT writes NaN into the
+// output column (every BLAS output touching it is non-finite too).  Columns
+// with norm below 2^-947 keep e <= kEbMax (relative accuracy degrades there).
+constexpr int kEbNonFinite = -0x40000000;
+constexpr int kEbMax = 1000;
 __global__ void __launch_bounds__(256) bscale_kernel(const double* __restrict__ b, int64_t ldb, int64_t k,
                                                      int64_t ncols, int64_t cols_pad, int pb, int* __restrict__ e_b) {
   const int64_t jj = blockIdx.x;
   __shared__ double red[8];
-  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+  __shared__ double s_mx;
+  const double* col = b + jj * ldb;
+  double mx = 0.0;
+  bool bad = false;
   if (jj < ncols) {
-    const double* col = b + jj * ldb;
-    int64_t i = threadIdx.x;
-    for (; i + 768 < k; i += 1024) {
-      const double v0 = __ldg(col + i), v1 = __ldg(col + i + 256), v2 = __ldg(col + i + 512), v3 = __ldg(col + i + 768);
-      s0 = fma(v0, v0, s0);
-      s1 = fma(v1, v1, s1);
-      s2 = fma(v2, v2, s2);
-      s3 = fma(v3, v3, s3);
-    }
-    for (; i < k; i += 256) {
-      const double v0 = __ldg(col + i);
-      s0 = fma(v0, v0, s0);
+    for (int64_t i = threadIdx.x; i < k; i += 256) {
+      const double v = fabs(__ldg(col + i));
+      bad |= !(v <= 1.7976931348623157e308);
+      mx = fmax(mx, v);
     }
   }
-  double ss = (s0 + s1) + (s2 + s3);
+  bad = __syncthreads_or(bad);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < 8; ++w) t = fmax(t, red[w]);
+    s_mx = t;
+  }
+  __syncthreads();
+  mx = s_mx;
+  if (bad || mx == 0.0) {
+    if (threadIdx.x == 0) e_b[jj] = bad ? kEbNonFinite : 0;
+    return;
+  }
+  int s;
+  frexp(mx, &s);  // mx < 2^s
+  double s0 = 0.0, s1 = 0.0;
+  for (int64_t i = threadIdx.x; i < k; i += 512) {
+    const double v0 = scalbn(__ldg(col + i), -s);
+    s0 = fma(v0, v0, s0);
+    if (i + 256 < k) {
+      const double v1 = scalbn(__ldg(col + i + 256), -s);
+      s1 = fma(v1, v1, s1);
+    }
+  }
+  double ss = s0 + s1;
 #pragma unroll
   for (int o = 16; o; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+  __syncthreads();
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
   __syncthreads();
   if (threadIdx.x == 0) {
     double tot = 0.0;
     for (int w = 0; w < 8; ++w) tot += red[w];
-    int e = 0;
-    if (tot > 0.0) {
-      int ex;
-      frexp(sqrt(tot) * (1.0 + 0x1p-40), &ex);  // ||b_j|| < 2^ex
-      e = pb - ex;
-    }
-    e_b[jj] = e;
+    int ex;
+    frexp(sqrt(tot) * (1.0 + 0x1p-40), &ex);  // ||b_j|| < 2^(ex + s)
+    e_b[jj] = min(pb - (ex + s), kEbMax);
   }
 }
 
@@ -319,7 +360,9 @@ __global__ void __launch_bounds__(256) residue_b_kernel(const double* __restrict
                                                         int ng) {
   const int64_t jj = blockIdx.x;
   const int g = (int)(jj / n_g), r = (int)(jj % n_g);
-  const double scale = scalbn(1.0, e_b[jj]);
+  const int eb = e_b[jj];
+  const bool dead = eb == kEbNonFinite;  // NaN/Inf column: zero residues, NaN output (crt_kernel)
+  const double scale = scalbn(1.0, dead ? 0 : eb);
   const size_t mod_stride = (size_t)ng * nkb * n_g * kTile;
   int8_t* tile0 = tiles + (size_t)g * nkb * n_g * kTile;
   const int64_t ch = (int64_t)blockIdx.y * 256 + threadIdx.x;
@@ -331,7 +374,7 @@ __global__ void __launch_bounds__(256) residue_b_kernel(const double* __restrict
 #pragma unroll
   for (int t = 0; t < 16; ++t) {
     const int64_t i = i0 + t;
-    v[t] = (jj < ncols && i < k) ? b[i + jj * ldb] : 0.0;
+    v[t] = (jj < ncols && i < k && !dead) ? b[i + jj * ldb] : 0.0;
   }
   Parts2 x[8];
 #pragma unroll
@@ -341,17 +384,38 @@ __global__ void __launch_bounds__(256) residue_b_kernel(const double* __restrict
 
 // ----------------------------------------------------------------- A scale
 // Row and column 2-norms of A in ONE read: CTA = 2048 rows x 256 columns;
-// partial sums in fixed order (deterministic), then max -> eA.
+// partial sums in fixed order (deterministic), then max -> eA, plus the
+// guard statistics (header below); NaN / Inf propagate through the sums.  A
+// row or column whose sum of squares is below DBL_MIN -- all zero, or tiny
+// entries whose squares underflow -- is reported through the minimum as is
+// (0 or subnormal), so the guard rejects that orientation: exact zero rows are
+// rare in dense operands and only cost the faster engine.
 constexpr int kNormRows = 2048, kNormCols = 256, kNormBlk = 8;
 constexpr size_t kNormSmem = (8 * kNormCols + 8 * 32 * (kNormBlk + 1)) * sizeof(double);
 
+// Header of the scale and prep workspaces (device, first 64 bytes).
+struct OzHeader {
+  int e_a;                       // scale of A (prep workspaces only)
+  int pad;
+  unsigned long long maxbits;    // max over rows and columns of the sum of squares (double bits)
+  unsigned long long minrow;     // min over rows (~0ull: none)
+  unsigned long long mincol;     // min over columns (~0ull: none)
+  unsigned nonfinite;            // a row or column sum is NaN / Inf
+};
+
 __global__ void __launch_bounds__(256, 4) norms_partial_kernel(const double* __restrict__ a, int64_t lda, int64_t m,
                                                             int64_t n, double* __restrict__ part_row,
-                                                            double* __restrict__ part_col) {
+                                                            double* __restrict__ part_col, OzHeader* hdr) {
   // warp w owns rows r0 + 256 w + [0, 256) (8 chunks of 32, lane = row in
   // chunk); column blocks of 32: lane keeps its rows' partial sums per column,
   // then one shared-memory transpose per block sums them over the lanes
   const int64_t rb = blockIdx.x, cb = blockIdx.y;
+  if (rb == 0 && cb == 0 && threadIdx.x == 0) {  // statistics reset (norms_final runs after this kernel)
+    hdr->maxbits = 0ull;
+    hdr->minrow = ~0ull;
+    hdr->mincol = ~0ull;
+    hdr->nonfinite = 0u;
+  }
   const int64_t r0 = rb * kNormRows, c0 = cb * kNormCols;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   extern __shared__ double nsm[];
@@ -403,13 +467,9 @@ __global__ void __launch_bounds__(256, 4) norms_partial_kernel(const double* __r
   }
 }
 
-__device__ __forceinline__ void atomic_max_pos(unsigned long long* p, double v) {
-  atomicMax(p, (unsigned long long)__double_as_longlong(v));  // v >= 0: bit order = value order
-}
-
 __global__ void norms_final_kernel(const double* __restrict__ part_row, int64_t ncb, int64_t m,
                                    const double* __restrict__ part_col, int64_t nrb, int64_t n,
-                                   unsigned long long* __restrict__ maxbits) {
+                                   OzHeader* __restrict__ hdr) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   double v = 0.0;
   if (t < m) {
@@ -417,15 +477,30 @@ __global__ void norms_final_kernel(const double* __restrict__ part_row, int64_t 
   } else if (t < m + n) {
     for (int64_t rb = 0; rb < nrb; ++rb) v += part_col[rb * n + (t - m)];
   }
+  const bool bad = !(v <= 1.7976931348623157e308);  // NaN, Inf (or an overflowing sum of squares)
+  const double inf = __longlong_as_double(0x7FF0000000000000ll);
+  double mx = bad ? 0.0 : v;
+  double mnr = (!bad && t < m) ? v : inf;
+  double mnc = (!bad && t >= m && t < m + n) ? v : inf;
 #pragma unroll
-  for (int o = 16; o; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
-  if ((threadIdx.x & 31) == 0) atomic_max_pos(maxbits, v);
+  for (int o = 16; o; o >>= 1) {
+    mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    mnr = fmin(mnr, __shfl_xor_sync(0xffffffffu, mnr, o));
+    mnc = fmin(mnc, __shfl_xor_sync(0xffffffffu, mnc, o));
+  }
+  const bool anybad = __any_sync(0xffffffffu, bad);
+  if ((threadIdx.x & 31) == 0) {  // v >= 0: bit order = value order
+    atomicMax(&hdr->maxbits, (unsigned long long)__double_as_longlong(mx));
+    if (mnr < inf) atomicMin(&hdr->minrow, (unsigned long long)__double_as_longlong(mnr));
+    if (mnc < inf) atomicMin(&hdr->mincol, (unsigned long long)__double_as_longlong(mnc));
+    if (anybad) atomicOr(&hdr->nonfinite, 1u);
+  }
 }
 
-__global__ void scale_a_kernel(const unsigned long long* __restrict__ maxbits, int pa, int* __restrict__ e_a) {
-  const double t = __longlong_as_double((long long)maxbits[0]);
+__global__ void scale_a_kernel(const OzHeader* __restrict__ hdr, int pa, int* __restrict__ e_a) {
+  const double t = __longlong_as_double((long long)hdr->maxbits);
   int e = 0;
-  if (t > 0.0) {
+  if (t > 0.0 && hdr->nonfinite == 0u) {
     int ex;
     frexp(sqrt(t) * (1.0 + 0x1p-40), &ex);
     e = pa - ex;
@@ -784,7 +859,9 @@ __global__ void __launch_bounds__(256) crt_kernel(const uint8_t* __restrict__ t,
   uint32_t w[kMaxMod];
 #pragma unroll
   for (int l = 0; l < kMaxMod; ++l) w[l] = (l < nm) ? __ldcs(tp + (size_t)l * (lstride / 4)) : 0u;
-  const double sc = scalbn(1.0, -(e_a[0] + e_b[j]));
+  const int eb = e_b[j];
+  const bool dead = eb == kEbNonFinite;  // non-finite column of B: NaN, like every BLAS output it touches
+  const int sc = -(e_a[0] + (dead ? 0 : eb));
 #pragma unroll
   for (int e = 0; e < 4; ++e) {
     if (i0 + e >= mrows) break;
@@ -793,7 +870,7 @@ __global__ void __launch_bounds__(256) crt_kernel(const uint8_t* __restrict__ t,
     for (int l = 0; l < kMaxMod; ++l) tv[l] = (w[l] >> (8 * e)) & 0xFFu;
     bool neg;
     const double v = crt_value(tv, crt, neg);
-    const double r = (neg ? -v : v) * sc;
+    const double r = dead ? __longlong_as_double(0x7FF8000000000000ll) : scalbn(neg ? -v : v, sc);
     double* cp = c + (i0 + e) + j * ldc;
     *cp = add ? *cp + r : r;  // add: C += A B (one rounding of the sum, like beta = 1)
   }
@@ -880,11 +957,10 @@ size_t oz_prep_workspace(int64_t m, int64_t n, int nmod) {
   return oz::prep_layout(m, n, nmod).total;
 }
 
-static int oz_norms(const double* a, int64_t lda, int64_t m, int64_t n, int nmod, int* e_a,
-                    unsigned long long* maxbits, double* prow, double* pcol, cudaStream_t st) {
+static int oz_norms(const double* a, int64_t lda, int64_t m, int64_t n, int nmod, int* e_a, oz::OzHeader* hdr,
+                    double* prow, double* pcol, cudaStream_t st) {
   const int64_t ncb = ceil_div(n, oz::kNormCols), nrb = ceil_div(m, oz::kNormRows);
   RLRA_REQUIRE(nrb <= 2147483647 && ncb <= 65535, "oz: A too large for the norm grid");
-  RLRA_CHECK_CUDA(cudaMemsetAsync(maxbits, 0, sizeof(unsigned long long), st));
   {
     static int attr_dev = -1;
     int dev = 0;
@@ -897,12 +973,12 @@ static int oz_norms(const double* a, int64_t lda, int64_t m, int64_t n, int nmod
   }
   ktimer_mark(KT_OZ_NORMS, st, false);
   oz::norms_partial_kernel<<<dim3((unsigned)nrb, (unsigned)ncb), 256, oz::kNormSmem, st>>>(a, lda, m, n, prow,
-                                                                                           pcol);
+                                                                                           pcol, hdr);
   ktimer_mark(KT_OZ_NORMS, st, true);
   RLRA_LAUNCHED();
-  oz::norms_final_kernel<<<(unsigned)ceil_div(m + n, 256), 256, 0, st>>>(prow, ncb, m, pcol, nrb, n, maxbits);
+  oz::norms_final_kernel<<<(unsigned)ceil_div(m + n, 256), 256, 0, st>>>(prow, ncb, m, pcol, nrb, n, hdr);
   RLRA_LAUNCHED();
-  oz::scale_a_kernel<<<1, 1, 0, st>>>(maxbits, oz::budget(nmod).pa, e_a);
+  oz::scale_a_kernel<<<1, 1, 0, st>>>(hdr, oz::budget(nmod).pa, e_a);
   RLRA_LAUNCHED();
   return 0;
 }
@@ -921,7 +997,37 @@ int oz_scale(const double* a, int64_t lda, int64_t m, int64_t n, int nmod, int* 
   uint8_t* base = static_cast<uint8_t*>(ws);
   double* prow = reinterpret_cast<double*>(base + 256);
   double* pcol = prow + (size_t)ceil_div(n, oz::kNormCols) * m;
-  return oz_norms(a, lda, m, n, nmod, e_a, reinterpret_cast<unsigned long long*>(base), prow, pcol, st);
+  return oz_norms(a, lda, m, n, nmod, e_a, reinterpret_cast<oz::OzHeader*>(base), prow, pcol, st);
+}
+
+// Dynamic-range guard (see the accuracy note at the top): T(K) = 2 (K-2)/sqrt(K) - 2.
+double oz_guard_limit(int64_t k) { return k > 4 ? 2.0 * (double)(k - 2) / std::sqrt((double)k) - 2.0 : 0.0; }
+
+int oz_guard(const void* hdr_host, int64_t m, int64_t n, int* ok_nn, int* ok_tn) {
+  RLRA_REQUIRE(hdr_host && ok_nn && ok_tn && m >= 1 && n >= 1, "oz_guard: bad arguments");
+  oz::OzHeader h;
+  std::memcpy(&h, hdr_host, sizeof(h));
+  double mx, mr, mc;
+  std::memcpy(&mx, &h.maxbits, 8);
+  std::memcpy(&mr, &h.minrow, 8);
+  std::memcpy(&mc, &h.mincol, 8);
+  *ok_nn = *ok_tn = 0;
+  if (h.nonfinite) return 0;  // NaN / Inf (or |a| > ~1e154): the DMMA GEMM propagates them like BLAS
+  if (mx == 0.0) {            // A = 0: exact either way
+    *ok_nn = *ok_tn = 1;
+    return 0;
+  }
+  if (mx < 0x1p-960) return 0;  // every row and column norm below 2^-480: the scale would leave the normal range
+  // rho^2 = max / min of the sums of squares; a minimum below DBL_MIN (a zero
+  // row, or squares that underflow) is rejected
+  auto ok = [&](unsigned long long minbits, double mn, int64_t k) {
+    if (minbits == ~0ull) return 1;
+    const double lim = oz_guard_limit(k);
+    return (mn >= 2.2250738585072014e-308 && mx <= lim * lim * mn) ? 1 : 0;
+  };
+  *ok_nn = ok(h.minrow, mr, n);  // C = A B: rows of A, K = n
+  *ok_tn = ok(h.mincol, mc, m);  // C = A^T B: columns of A, K = m
+  return 0;
 }
 
 int oz_prep_ex(const double* a, int64_t lda, int64_t m, int64_t n, int nmod, const int* e_a_ext, void* prep,
@@ -933,15 +1039,15 @@ int oz_prep_ex(const double* a, int64_t lda, int64_t m, int64_t n, int nmod, con
   RLRA_REQUIRE(prep && prep_bytes >= p.total, "oz_prep: workspace too small (%zu < %zu)", prep_bytes, p.total);
   RLRA_REQUIRE(p.njb <= 65535, "oz_prep: n too large (%lld)", (long long)n);
   uint8_t* base = static_cast<uint8_t*>(prep);
-  int* e_a = reinterpret_cast<int*>(base + p.off_hdr);
-  unsigned long long* maxbits = reinterpret_cast<unsigned long long*>(base + p.off_hdr + 8);
+  oz::OzHeader* hdr = reinterpret_cast<oz::OzHeader*>(base + p.off_hdr);
+  int* e_a = &hdr->e_a;
   double* prow = reinterpret_cast<double*>(base + p.off_prow);
   double* pcol = reinterpret_cast<double*>(base + p.off_pcol);
   int8_t* tiles = reinterpret_cast<int8_t*>(base + p.off_tiles);
-  if (e_a_ext) {  // scale of an enclosing matrix (block-wise residues)
-    RLRA_CHECK_CUDA(cudaMemcpyAsync(e_a, e_a_ext, sizeof(int), cudaMemcpyDeviceToDevice, st));
+  if (e_a_ext) {  // scale of an enclosing matrix (block-wise residues), or of this prep (oz_norms_prep)
+    if (e_a_ext != e_a) RLRA_CHECK_CUDA(cudaMemcpyAsync(e_a, e_a_ext, sizeof(int), cudaMemcpyDeviceToDevice, st));
   } else {
-    const int rc = oz_norms(a, lda, m, n, nmod, e_a, maxbits, prow, pcol, st);
+    const int rc = oz_norms(a, lda, m, n, nmod, e_a, hdr, prow, pcol, st);
     if (rc) return rc;
   }
   ktimer_mark(KT_OZ_RESIDUE_A, st, false);
@@ -949,6 +1055,22 @@ int oz_prep_ex(const double* a, int64_t lda, int64_t m, int64_t n, int nmod, con
   ktimer_mark(KT_OZ_RESIDUE_A, st, true);
   RLRA_LAUNCHED();
   return 0;
+}
+
+// Norms, scale and guard statistics into a prep workspace, without residues
+// (the caller reads the header, then calls oz_prep_ex(e_a = the header's) for
+// the residues only when an orientation passes the guard).
+int oz_norms_prep(const double* a, int64_t lda, int64_t m, int64_t n, int nmod, void* prep, size_t prep_bytes,
+                  cudaStream_t st) {
+  RLRA_REQUIRE(nmod >= 12 && nmod <= oz::kMaxMod, "oz_norms: nmod must be in [12, 16], got %d", nmod);
+  RLRA_REQUIRE(m >= 1 && n >= 1 && lda >= m, "oz_norms: bad shape m=%lld n=%lld lda=%lld", (long long)m,
+               (long long)n, (long long)lda);
+  const oz::PrepLayout p = oz::prep_layout(m, n, nmod);
+  RLRA_REQUIRE(prep && prep_bytes >= p.total, "oz_norms: workspace too small (%zu < %zu)", prep_bytes, p.total);
+  uint8_t* base = static_cast<uint8_t*>(prep);
+  oz::OzHeader* hdr = reinterpret_cast<oz::OzHeader*>(base + p.off_hdr);
+  return oz_norms(a, lda, m, n, nmod, &hdr->e_a, hdr, reinterpret_cast<double*>(base + p.off_prow),
+                  reinterpret_cast<double*>(base + p.off_pcol), st);
 }
 
 int oz_prep(const double* a, int64_t lda, int64_t m, int64_t n, int nmod, void* prep, size_t prep_bytes,

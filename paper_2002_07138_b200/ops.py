@@ -179,21 +179,66 @@ def gemm(a, b, c, *, ta=False, tb=False, alpha=1.0, beta=0.0):
 
 
 OZ_NMOD = int(os.environ.get("RLRA_B200_OZ_NMOD", "14"))
+OZ_HEADER_BYTES = 64  # include/rlra_b200.h RLRA_B200_OZ_HEADER_BYTES
+
+
+def oz_guard(header, m, n):
+    """(ok_nn, ok_tn) from a workspace header (rlra_b200_oz_guard, host only):
+    an orientation may take the emulated product only when its error bound is
+    within DGEMM's classical bound (csrc/ozaki.cu accuracy note)."""
+    import ctypes
+
+    raw = bytes(header.cpu().numpy().tobytes()) if isinstance(header, torch.Tensor) else bytes(header)
+    if len(raw) < OZ_HEADER_BYTES:
+        raise ValueError("oz header must hold RLRA_B200_OZ_HEADER_BYTES bytes")
+    buf = ctypes.create_string_buffer(raw, len(raw))
+    ok_nn, ok_tn = ctypes.c_int(0), ctypes.c_int(0)
+    _native.call("rlra_b200_oz_guard", ctypes.cast(buf, ctypes.c_void_p), int(m), int(n), ctypes.byref(ok_nn),
+                 ctypes.byref(ok_tn))
+    return bool(ok_nn.value), bool(ok_tn.value)
+
+
+def oz_guard_stats(header):
+    """Decoded guard header: (max norm, min non-zero row norm, min non-zero
+    column norm, non-finite) -- diagnostics only."""
+    h = header.cpu().numpy() if isinstance(header, torch.Tensor) else np.frombuffer(bytes(header), np.uint8)
+    mx, mr, mc = h[8:32].view(np.uint64)
+    nf = int(h[32:36].view(np.uint32)[0])
+    f = lambda b: float("inf") if b == np.uint64(0xFFFFFFFFFFFFFFFF) else float(np.sqrt(np.array([b]).view(np.float64)[0]))  # noqa: E731
+    return f(mx), f(mr), f(mc), bool(nf)
 
 
 class OzPrep:
     """Int8 residues of A for the emulated pass products (csrc/ozaki.cu): built
-    once per A, they serve both C = A B (trans=False) and C = A^T B."""
+    once per A, they serve both C = A B (trans=False) and C = A^T B.
 
-    def __init__(self, a, nmod=None):
+    guard=True (the product path): the norms and guard statistics are computed
+    first and read back (one small device->host transfer); an orientation the
+    guard rejects (graded rows / columns beyond rlra_b200_oz_guard_limit(K),
+    NaN / Inf, extreme exponent range) runs on the FP64 DMMA GEMM instead, and
+    the residues are built only if some orientation is admitted.  guard=False
+    exercises the raw engine (tests)."""
+
+    def __init__(self, a, nmod=None, guard=True):
         m, n = a.shape
+        self.a = a
         self.m, self.n = int(m), int(n)
         self.nmod = OZ_NMOD if nmod is None else int(nmod)
         self.device = a.device
         wsb = _native.query("rlra_b200_oz_prep_workspace", self.m, self.n, self.nmod)
         self.ws = torch.empty(max(wsb, 8), dtype=torch.uint8, device=a.device)
-        _call("rlra_b200_oz_prep", a.device, ptr(a), ld_of(a), self.m, self.n, self.nmod, ptr(self.ws), wsb,
-              _stream(a.device))
+        st = _stream(a.device)
+        if guard:
+            _call("rlra_b200_oz_norms", a.device, ptr(a), ld_of(a), self.m, self.n, self.nmod, ptr(self.ws), wsb, st)
+            self.header = self.ws[:OZ_HEADER_BYTES].cpu()
+            self.ok = oz_guard(self.header, self.m, self.n)
+            if any(self.ok):
+                _call("rlra_b200_oz_prep_ex", a.device, ptr(a), ld_of(a), self.m, self.n, self.nmod, ptr(self.ws),
+                      ptr(self.ws), wsb, st)
+        else:
+            self.header = None
+            self.ok = (True, True)
+            _call("rlra_b200_oz_prep", a.device, ptr(a), ld_of(a), self.m, self.n, self.nmod, ptr(self.ws), wsb, st)
 
     def gemm(self, b, trans=False, keep_ws=False, out=None, add=False):
         """C = A B (trans=False, b n x l) or A^T B (trans=True, b m x l); with
@@ -208,6 +253,9 @@ class OzPrep:
         if ncols == 0:
             return (c, None) if keep_ws else c
         b = as_fmat(b)
+        if not self.ok[int(bool(trans))]:  # guard: DGEMM-class accuracy needs the native FP64 GEMM
+            gemm(self.a, b, c, ta=bool(trans), beta=1.0 if add else 0.0)
+            return (c, None) if keep_ws else c
         wsb = _native.query("rlra_b200_oz_gemm_workspace", int(trans), self.m, self.n, ncols, self.nmod)
         ws = torch.empty(max(wsb, 8), dtype=torch.uint8, device=self.device)
         _call("rlra_b200_oz_gemm_ex", self.device, int(trans), ptr(self.ws), self.m, self.n, self.nmod, ptr(b),
@@ -240,7 +288,7 @@ class OzBlocked:
     scratch workspace (8 B read + nmod B written per element)."""
 
     def __init__(self, a, nmod=None, block_bytes=None, cache_bytes=None, row_cap=OZ_BLOCK_K,
-                 col_cap=OZ_BLOCK_K):
+                 col_cap=OZ_BLOCK_K, guard=True):
         m, n = a.shape
         self.a = a
         self.m, self.n = int(m), int(n)
@@ -252,6 +300,8 @@ class OzBlocked:
         self.e_a = torch.empty(1, dtype=torch.int32, device=dev)
         _call("rlra_b200_oz_scale", dev, ptr(a), ld_of(a), self.m, self.n, self.nmod, ptr(self.e_a), ptr(ws), wsb,
               _stream(dev))
+        self.header = ws[:OZ_HEADER_BYTES].cpu() if guard else None
+        self.ok = oz_guard(self.header, self.m, self.n) if guard else (True, True)
         del ws
         if block_bytes is None:
             block_bytes = int(os.environ.get("RLRA_B200_OZ_BLOCK_BYTES", str(16 << 30)))
@@ -276,12 +326,14 @@ class OzBlocked:
             cache_bytes -= biggest  # room for the scratch block
         self.cache = {}
         used = 0
+        if not any(self.ok):  # every product goes to the DMMA GEMM: no residues at all
+            self.blocks = []
         for ij in self.blocks:
             if used + self.block_ws[ij] <= cache_bytes:
                 self.cache[ij] = self._build(ij, None)
                 used += self.block_ws[ij]
         self.scratch = None
-        if len(self.cache) < len(self.blocks):
+        if self.blocks and len(self.cache) < len(self.blocks):
             self.scratch = torch.empty(biggest, dtype=torch.uint8, device=dev)
         self.rebuilt = len(self.blocks) - len(self.cache)
 
@@ -308,6 +360,8 @@ class OzBlocked:
         if ncols == 0:
             return c
         b = as_fmat(b)
+        if not self.ok[int(bool(trans))]:  # guard (OzPrep): the native FP64 GEMM
+            return gemm(self.a, b, c, ta=bool(trans))
         dev, st = self.device, _stream(self.device)
         cp = int(_native.load().rlra_b200_oz_cols_pad(ncols))
         e_b = torch.empty(cp, dtype=torch.int32, device=dev)

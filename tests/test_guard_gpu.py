@@ -1,0 +1,183 @@
+"""The int8 pass engine's dynamic-range guard and non-finite handling on the
+device (csrc/ozaki.cu accuracy note, ops.OzPrep / ops.OzBlocked).
+
+* Graded rows / columns beyond rlra_b200_oz_guard_limit(K): the product takes
+  the DMMA GEMM and every ROW of the result is as accurate as NumPy's DGEMM
+  (per-row relative error within 4x DGEMM's).
+* Moderate grading inside the limit stays on the int8 engine and obeys the
+  classical per-row bound K u ||A_i|| ||B_j||.
+* NaN / Inf in A propagate to exactly the outputs BLAS makes non-finite; a
+  NaN column of B gives a NaN output column.
+* Driver parity on the reference's integer exact-rank input
+  (pkg/tests/test_cli.py:76-89), sketches wider than the rank (pass-through vs
+  RankCollapse, rlra/rangefinder.py:55-64), graded and extreme-magnitude
+  inputs: same outcome, p, q and rel_err as the unmodified reference
+  (tests/golden/make_golden_guard.py).
+"""
+
+import json
+import os
+
+import numpy as np
+import pytest
+
+from oracle import rlra_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+GCASES = np.load(os.path.join(HERE, "golden", "guard_cases.npz"))
+GMETA = json.load(open(os.path.join(HERE, "golden", "guard_cases.json")))
+U = 2.0 ** -53
+
+
+def _exact(opa, b):
+    return opa.astype(np.longdouble) @ b.astype(np.longdouble)
+
+
+def _row_err(c, ref, opa, b):
+    """Per row i: max_j |C_ij - ref_ij| / (||A_i|| ||B_j||)."""
+    ra = np.sqrt((opa * opa).sum(1))
+    nb = np.sqrt((b * b).sum(0))
+    scale = ra[:, None] * nb[None, :]
+    return (np.abs(c - ref).astype(np.float64) / np.where(scale > 0, scale, 1.0)).max(1)
+
+
+def _product(a, b, trans, **kw):
+    from paper_2002_07138_b200 import ops
+
+    dev = ops.check_device()
+    prep = ops.OzPrep(ops.from_numpy(a, dev), **kw)
+    return prep, ops.to_numpy(prep.gemm(ops.from_numpy(b, dev), trans=trans))
+
+
+@pytest.mark.parametrize("trans", [False, True])
+def test_graded_over_ten_decades_takes_dmma_and_matches_dgemm_per_row(cuda_dev, trans):
+    rng = np.random.default_rng(21)
+    m, n, l = 1500, 1100, 64
+    a = rng.standard_normal((m, n)) * 10.0 ** rng.uniform(-10, 0, size=(m, 1)) * 10.0 ** rng.uniform(-10, 0, size=(1, n))
+    b = rng.standard_normal((m if trans else n, l))
+    prep, c = _product(a, b, trans)
+    assert prep.ok == (False, False)
+    opa = a.T if trans else a
+    ref = _exact(opa, b)
+    e_gpu = _row_err(c, ref, opa, b)
+    e_np = _row_err(opa @ b, ref, opa, b)
+    assert np.all(e_gpu <= 4 * e_np + 4 * U), float((e_gpu / (e_np + U)).max())
+
+
+@pytest.mark.parametrize("trans", [False, True])
+def test_moderate_grading_stays_on_int8_within_classical_bound(cuda_dev, trans):
+    rng = np.random.default_rng(22)
+    m, n, l = 2000, 1600, 96
+    a = rng.standard_normal((m, n)) * np.exp(rng.uniform(-1.5, 1.5, size=(m, 1))) * np.exp(
+        rng.uniform(-1.5, 1.5, size=(1, n)))
+    b = rng.standard_normal((m if trans else n, l)) * np.exp(rng.uniform(-5, 5, size=(1, l)))
+    prep, c = _product(a, b, trans)
+    assert prep.ok == (True, True)
+    opa = a.T if trans else a
+    k = opa.shape[1]
+    e = _row_err(c, _exact(opa, b), opa, b)
+    assert np.all(e <= k * U), float(e.max() / (k * U))
+
+
+def test_raw_engine_is_normwise_only(cuda_dev):
+    """Why the guard exists: with the guard off, a row 1e-8 below N_A loses
+    ~8 digits against DGEMM (normwise bound only)."""
+    rng = np.random.default_rng(23)
+    a = rng.standard_normal((800, 600))
+    a[:10] *= 1e-8
+    b = rng.standard_normal((600, 32))
+    prep, c = _product(a, b, False, guard=False)
+    ok_prep, c_ok = _product(a, b, False)
+    assert ok_prep.ok[0] is False
+    ref = _exact(a, b)
+    e_raw = _row_err(c, ref, a, b)[:10]
+    e_guard = _row_err(c_ok, ref, a, b)[:10]
+    e_np = _row_err(a @ b, ref, a, b)[:10]
+    assert e_raw.max() > 1e4 * e_np.max()
+    assert np.all(e_guard <= 4 * e_np + 4 * U)
+
+
+def test_nonfinite_entries_propagate_like_blas(cuda_dev):
+    rng = np.random.default_rng(24)
+    a = rng.standard_normal((500, 400))
+    a[3, 5] = np.nan
+    a[7, 2] = np.inf
+    b = rng.standard_normal((400, 20))
+    prep, c = _product(a, b, False)
+    assert prep.ok == (False, False)
+    assert np.array_equal(~np.isfinite(c), ~np.isfinite(a @ b))
+    bt = rng.standard_normal((500, 20))
+    _, ct = _product(a, bt, True)
+    assert np.array_equal(~np.isfinite(ct), ~np.isfinite(a.T @ bt))
+
+
+def test_nonfinite_column_of_b_gives_nan_column(cuda_dev):
+    rng = np.random.default_rng(25)
+    a = rng.standard_normal((300, 200))
+    b = rng.standard_normal((200, 12))
+    b[17, 4] = np.nan
+    b[3, 9] = -np.inf
+    _, c = _product(a, b, False, guard=False)
+    assert np.all(np.isnan(c[:, 4])) and np.all(np.isnan(c[:, 9]))
+    keep = [j for j in range(12) if j not in (4, 9)]
+    ref = _exact(a, b[:, keep])
+    assert np.abs(c[:, keep] - ref).max() <= 1e-13 * np.abs(ref).max()
+
+
+@pytest.mark.parametrize("scale", [1e-300, 1e-160, 1e150, 1e250])
+def test_extreme_column_scales_of_b(cuda_dev, scale):
+    """bscale's two-pass norm: no overflow / underflow of the squares."""
+    rng = np.random.default_rng(26)
+    a = rng.standard_normal((300, 200))
+    b = rng.standard_normal((200, 8))
+    b[:, 2] *= scale
+    _, c = _product(a, b, False, guard=False)
+    ref = _exact(a, b)
+    err = np.abs(c - ref).astype(np.float64).max(0) / np.abs(ref).astype(np.float64).max(0)
+    assert np.all(err <= 1e-13), err
+
+
+@pytest.mark.parametrize("scale", [1e-140, 1e-100, 1e120, 1e150])
+def test_extreme_magnitudes_of_a(cuda_dev, scale):
+    rng = np.random.default_rng(27)
+    a = rng.standard_normal((400, 300)) * scale
+    b = rng.standard_normal((300, 16))
+    prep, c = _product(a, b, False)
+    ref = _exact(a, b)
+    e = _row_err(c, ref, a, b)
+    assert np.all(e <= 300 * U), (prep.ok, float(e.max()))
+
+
+@pytest.mark.parametrize("name", sorted(GMETA))
+def test_driver_outcome_matches_reference(cuda_dev, name):
+    import paper_2002_07138_b200 as P
+
+    meta = GMETA[name]
+    a = GCASES[f"{name}/a"]
+    args = (a, meta["k"], meta["q_os"], meta["v"], meta["seed"])
+    if meta["outcome"] == "RankCollapse":
+        with pytest.raises(P.RankCollapse) as ei:
+            P.powerlu(*args)
+        assert (ei.value.achieved, ei.value.requested) == (meta["achieved"], meta["requested"])
+        return
+    f = P.powerlu(*args)
+    assert np.array_equal(f.p, GCASES[f"{name}/p"]), name
+    assert np.array_equal(f.q, GCASES[f"{name}/q"]), name
+    err = O.rel_fro_error_factor(a, f)
+    assert abs(err - meta["rel_err"]) <= 1e-10 * max(1.0, meta["rel_err"]), (err, meta["rel_err"])
+
+
+def test_powerlu_nan_input_gives_nonfinite_factors(cuda_dev):
+    """The reference's BLAS propagates NaN into its factors; so must we --
+    never plausible-looking finite factors (ozaki.cu:421)."""
+    import paper_2002_07138_b200 as P
+
+    a = np.array(GCASES["int_rank7_v3/a"])
+    a[10, 20] = np.nan
+    try:
+        f = P.powerlu(a, 7, 3, 3, 2)
+    except P.RankCollapse:
+        return  # an exactly-zero pivot count is also a loud outcome
+    assert not (np.all(np.isfinite(f.L)) and np.all(np.isfinite(f.U)))
