@@ -2,7 +2,11 @@
 """PowerLU FP64 benchmark (BASELINE.json metric) on B200.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                  [--config C2|C1|C3|C5] [--v 4] [--breakdown]
+                  [--config C2|C1|C5] [--v 4] [--breakdown] [--no-c5]
+
+--gpus N > 1 outside torchrun re-launches this script under
+`torch.distributed.run --nproc-per-node N` (one rank per GPU, NCCL); under
+torchrun (WORLD_SIZE set) every rank runs the distributed arm.
 
 One step = one complete factorization of the workload (default C2:
 powerlu(A 20000x10000, k=200, q_os=20, v=4, seed=0), BASELINE.json configs[1]).
@@ -58,6 +62,8 @@ def parse():
     ap.add_argument("--breakdown", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-c5", action="store_true", help="skip the C5 (262144 x 32768) sub-record")
+    ap.add_argument("--c5-steps", type=int, default=2)
     return ap.parse_args()
 
 
@@ -286,6 +292,99 @@ def cpu_baseline_analogue(w, v):
             "sample": f"1 factorization of the C5 analogue {m}x{n} (SURVEY Appendix A), {sec:.1f} s"}
 
 
+GOLDEN = os.path.join(REPO, "tests", "golden")
+
+
+def golden_pq(name, v):
+    """Reference pivots of a config (tests/golden/*_pq.npz, written by the
+    unmodified reference; SURVEY.md Appendix A recipes), or None."""
+    try:
+        if name == "C2":
+            d = np.load(os.path.join(GOLDEN, "c2_pq.npz"))
+            return d[f"v{v}_p"], d[f"v{v}_q"]
+        if name == "C5" and v == 4:
+            d = np.load(os.path.join(GOLDEN, "c5_pq.npz"))
+            return d["p"], d["q"]
+    except (OSError, KeyError):
+        return None
+    return None
+
+
+def pq_parity(name, v, p, q):
+    g = golden_pq(name, v)
+    if g is None:
+        return None
+    return {"p_identical_to_reference": bool(np.array_equal(np.asarray(p), g[0])),
+            "q_identical_to_reference": bool(np.array_equal(np.asarray(q), g[1])),
+            "golden": f"tests/golden/{name.lower()}_pq.npz"}
+
+
+def c5_record(args, dist_ctx=None):
+    """The north-star config on the same N GPUs: C5 = powerlu(A 262144 x 32768
+    (68.7 GB, built in HBM by configs.gen_device), k=512, q_os=32, v=4).  One
+    warm-up, then `--c5-steps` timed factorizations (CUDA events; max over
+    ranks), pivots checked against the reference's (tests/golden/c5_pq.npz).
+    dist_ctx: (rank, world, local) under torchrun, else None (one GPU)."""
+    import torch
+
+    from paper_2002_07138_b200 import configs, core
+
+    w = configs.WORKLOADS["C5"]
+    passes, fact = configs.powerlu_flops(w.m, w.n, w.k, w.k + w.q_os, w.v)
+    flops = passes + fact
+    local = dist_ctx[2] if dist_ctx else int(os.environ.get("LOCAL_RANK", "0"))
+    dev = torch.device("cuda", local)
+    core.set_omega_cache(True)
+    t0 = time.perf_counter()
+    if dist_ctx is None:
+        import paper_2002_07138_b200 as P
+
+        A = P.DeviceMatrix(configs.gen_device("C5", dev), local)
+        run = lambda: P.powerlu(A, w.k, w.q_os, w.v, w.seed)  # noqa: E731
+    else:
+        import torch.distributed as dist
+
+        from paper_2002_07138_b200 import distributed as D
+
+        rank, world, _ = dist_ctx
+        r0, r1 = D.row_range(w.m, world, rank)
+        full = configs.gen_device("C5", dev)
+        shard = D.CudaOps(dev).empty(r1 - r0, w.n)
+        shard.copy_(full[r0:r1])
+        del full
+        torch.cuda.empty_cache()
+        A = D.ShardedMatrix(shard, w.m, r0, r1, D.CudaOps(dev))
+        om = lambda seed, rows, l: core.omega(seed, rows, l, dev)  # noqa: E731
+        run = lambda: D.powerlu(A, w.k, w.q_os, w.v, w.seed, om)  # noqa: E731
+    gen_s = time.perf_counter() - t0
+    f = run()
+    torch.cuda.synchronize()
+    st = torch.cuda.current_stream(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if dist_ctx is not None:
+        torch.distributed.barrier()
+    e0.record(st)
+    for _ in range(max(1, args.c5_steps)):
+        f = run()
+    e1.record(st)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / max(1, args.c5_steps)
+    if dist_ctx is not None:
+        t = torch.tensor([ms], device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    p = f.p.cpu().numpy() if hasattr(f.p, "cpu") else f.p
+    q = f.q.cpu().numpy() if hasattr(f.q, "cpu") else f.q
+    rec = {"workload": "C5: powerlu(A 262144x32768 float64 (68.7 GB, device-built), k=512, q_os=32, v=4, seed=0)",
+           "ms_per_step": ms, "gflops": flops / (ms / 1e3) / 1e9, "steps": max(1, args.c5_steps), "warmup": 1,
+           "algorithmic_gflop": flops / 1e9, "input_build_s": gen_s,
+           "parity": pq_parity("C5", 4, p, q)}
+    del A, f, run
+    core.set_omega_cache(False)
+    torch.cuda.empty_cache()
+    return rec
+
+
 def our_arm(args):
     import torch
 
@@ -412,6 +511,21 @@ def our_arm(args):
             parity.update({"rel_err_gpu": e_gpu, "rel_err_ref": e_ref, "abs_diff": abs(e_gpu - e_ref)})
     elif not args.no_cpu_baseline:
         cpu = cpu_baseline_analogue(w, v)
+    fd = f.to_numpy() if hasattr(f, "to_numpy") else f
+    gpar = pq_parity(w.name, v, fd.p, fd.q)
+    if gpar is not None:
+        parity = dict(parity or {}, **gpar)
+
+    c5 = None
+    if not args.no_c5 and w.name != "C5":
+        del dm, f, fd
+        a = None  # the host copy is no longer needed either
+        P.set_omega_cache(False)
+        torch.cuda.empty_cache()
+        try:
+            c5 = c5_record(args)
+        except Exception as exc:  # the sub-record must never cost the headline line
+            c5 = {"error": f"{type(exc).__name__}: {exc}"}
 
     line = {
         "metric": f"PowerLU FP64 GFLOP/s ({w.name}, v={v})", "value": value, "unit": "GFLOP/s",
@@ -420,12 +534,14 @@ def our_arm(args):
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": desc, "m": w.m, "n": w.n, "k": w.k, "l": w.k + w.q_os, "v": v,
                    "algorithmic_gflop": flops / 1e9, "pass_gflop": passes / 1e9,
-                   "l2": f"inputs larger than L2 (A = {a.nbytes / 1e9:.2f} GB > 126 MB L2)",
-                   "omega": "host NumPy PCG64 draw (bit-exact rlra.core.gaussian), device-cached for value",
+                   "l2": f"inputs larger than L2 (A = {8 * w.m * w.n / 1e9:.2f} GB > 126 MB L2)",
+                   "omega": "device replay of NumPy's PCG64 + ziggurat stream (bit-exact rlra.core.gaussian); "
+                            "cached across steps for value, redrawn every step for e2e",
                    "parallelism": "single GPU"},
         "gpu_launches": int(launches), "gpu_launches_per_step": launches / args.steps,
         "clocks": clk, "roofline": roofline, "e2e": e2e, "cpu_baseline": cpu, "parity": parity,
         "host_prep": {"generate_A_s": gen_s, "upload_A_s": upload_s},
+        "comm": None, "C5": c5,
     }
     print(json.dumps(line), flush=True)
     return 0
@@ -448,9 +564,21 @@ def dist_arm(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
     os.environ.setdefault("MASTER_PORT", "29541")
+    if os.environ.get("RLRA_B200_BENCH_DRYRUN") == "1":  # launcher test (CPU, gloo): report and leave
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        print(json.dumps({"dryrun": True, "arm": "dist", "rank": rank, "world": dist.get_world_size()}), flush=True)
+        dist.destroy_process_group()
+        return 0
+    # communicator evidence: NCCL's init lines (rank r nranks N) on stderr, so
+    # stdout keeps exactly one JSON line
+    os.environ.setdefault("NCCL_DEBUG", "INFO")
+    os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
+    comm = {"backend": dist.get_backend(), "world_size": dist.get_world_size(),
+            "nccl_version": ".".join(str(x) for x in torch.cuda.nccl.version())}
     w, v, gen, passes, fact, desc = workload(args)
     flops = passes + fact
     r0, r1 = D.row_range(w.m, world, rank)
@@ -504,6 +632,8 @@ def dist_arm(args):
         ksteps = max(1, min(args.steps, 5))
         d2h = 0
 
+        core.set_omega_cache(False)  # as at N=1: Omega is redrawn every e2e step
+
         def e2e_step():
             sh = cops.empty(r1 - r0, w.n)
             sh.copy_(host_shard.t(), non_blocking=True)
@@ -527,6 +657,18 @@ def dist_arm(args):
         e2e = {"value": flops / (e2e_ms / 1e3) / 1e9, "unit": "GFLOP/s", "ms_per_step": e2e_ms,
                "h2d_bytes_per_step": int(8 * w.m * w.n), "d2h_bytes_per_step": int(d2h), "steps": ksteps,
                "path": "distributed.powerlu over pinned host row shards -> NumPy factors on rank 0"}
+        core.set_omega_cache(True)
+    fin = D.powerlu(A, w.k, w.q_os, v, w.seed, omega)
+    parity = pq_parity(w.name, v, fin.p.cpu().numpy(), fin.q.cpu().numpy()) if rank == 0 else None
+    del fin, A, shard
+    core.set_omega_cache(False)
+    torch.cuda.empty_cache()
+    c5 = None
+    if not args.no_c5 and w.name != "C5":
+        try:
+            c5 = c5_record(args, (rank, world, local))
+        except Exception as exc:
+            c5 = {"error": f"{type(exc).__name__}: {exc}"}
     if rank == 0:
         msv = float(ms.item())
         sm = [c.get("sm_mhz") for c in clks if c and c.get("sm_mhz")]
@@ -543,7 +685,7 @@ def dist_arm(args):
                 "clocks": {"sm_mhz": min(sm) if sm else None,
                            "sm_max_mhz": clks[0].get("sm_max_mhz") if clks[0] else None,
                            "reasons": reasons, "per_rank": clks},
-                "roofline": None, "e2e": e2e, "cpu_baseline": None,
+                "roofline": None, "e2e": e2e, "cpu_baseline": None, "parity": parity, "comm": comm, "C5": c5,
                 "note": "roofline and cpu_baseline are reported by the N=1 run"}
         print(json.dumps(line), flush=True)
     dist.barrier()
@@ -551,10 +693,30 @@ def dist_arm(args):
     return 0
 
 
+def torchrun_cmd(argv, nproc, port):
+    """The driver's multi-GPU launch line for this script (one rank per GPU)."""
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
+            "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + list(argv)
+
+
+def _free_port():
+    import socket
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         return reference_arm(args)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # `python bench.py --gpus N`: start N ranks ourselves (same as the driver's torchrun)
+        return subprocess.call(torchrun_cmd(sys.argv[1:], args.gpus, _free_port()))
+    if os.environ.get("RLRA_B200_BENCH_DRYRUN") == "1" and int(os.environ.get("WORLD_SIZE", "1")) == 1:
+        print(json.dumps({"dryrun": True, "arm": "single", "rank": 0, "world": 1}), flush=True)
+        return 0
     return our_arm(args)
 
 

@@ -112,7 +112,7 @@ RLRA_B200_API int rlra_b200_dgemm(int transa, int transb, int64_t m, int64_t n, 
  * orientation when N_A / min ||A_i|| <= rlra_b200_oz_guard_limit(K), which
  * makes this at most K 2^-53 ||A_i|| ||B_j||, the classical DGEMM bound; the
  * drivers run the other products (graded rows / columns, NaN / Inf, norms
- * outside [2^-480, 2^512)) on the DMMA GEMM.  Results are exact functions of
+ * outside [2^-480, 2^512), integer-valued A) on the DMMA GEMM.  Results are exact functions of
  * the inputs.  A column of B holding NaN / Inf yields a NaN output column.
  * prep: residues of A, built once per A by rlra_b200_oz_prep (both
  * orientations); then any number of
@@ -123,7 +123,9 @@ RLRA_B200_API int rlra_b200_dgemm(int transa, int transb, int64_t m, int64_t n, 
  * the guard header: int e_a, int pad, then three uint64 holding the double
  * bits of the largest row/column sum of squares, the smallest non-zero row
  * sum and the smallest non-zero column sum (all ones: none), then uint32
- * non-finite flag.  rlra_b200_oz_norms fills it (and e_a) without building
+ * non-finite flag and uint32 "some entry is not an integer" flag
+ * (integer-valued A is routed to DMMA: exact products turn exact linear
+ * dependencies into exact zero pivots where BLAS leaves rounding noise).  rlra_b200_oz_norms fills it (and e_a) without building
  * residues; copy it to the host and pass it to rlra_b200_oz_guard (host-only,
  * no GPU); then rlra_b200_oz_prep_ex(e_a = the prep's own header) builds the
  * residues. */

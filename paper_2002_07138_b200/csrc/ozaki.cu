@@ -290,10 +290,10 @@ __global__ void __launch_bounds__(256, 3) residue_a_kernel(const double* __restr
 // sum of squares of b 2^-s (s = exponent of the max) so neither overflow nor
 // underflow of the squares can misplace the scale.  A column holding NaN/Inf
 // gets kEbNonFinite: its residues are zero and the CRT writes NaN into the
-// output column (every BLAS output touching it is non-finite too).  Columns
-// with norm below 2^-947 keep e <= kEbMax (relative accuracy degrades there).
+// output column (every BLAS output touching it is non-finite too).  The scale
+// may exceed 2^1023 (columns of norm < 2^-970): residue_b applies it with
+// scalbn, the CRT unscales with scalbn.
 constexpr int kEbNonFinite = -0x40000000;
-constexpr int kEbMax = 1000;
 __global__ void __launch_bounds__(256) bscale_kernel(const double* __restrict__ b, int64_t ldb, int64_t k,
                                                      int64_t ncols, int64_t cols_pad, int pb, int* __restrict__ e_b) {
   const int64_t jj = blockIdx.x;
@@ -347,7 +347,7 @@ __global__ void __launch_bounds__(256) bscale_kernel(const double* __restrict__ 
     for (int w = 0; w < 8; ++w) tot += red[w];
     int ex;
     frexp(sqrt(tot) * (1.0 + 0x1p-40), &ex);  // ||b_j|| < 2^(ex + s)
-    e_b[jj] = min(pb - (ex + s), kEbMax);
+    e_b[jj] = pb - (ex + s);
   }
 }
 
@@ -362,7 +362,6 @@ __global__ void __launch_bounds__(256) residue_b_kernel(const double* __restrict
   const int g = (int)(jj / n_g), r = (int)(jj % n_g);
   const int eb = e_b[jj];
   const bool dead = eb == kEbNonFinite;  // NaN/Inf column: zero residues, NaN output (crt_kernel)
-  const double scale = scalbn(1.0, dead ? 0 : eb);
   const size_t mod_stride = (size_t)ng * nkb * n_g * kTile;
   int8_t* tile0 = tiles + (size_t)g * nkb * n_g * kTile;
   const int64_t ch = (int64_t)blockIdx.y * 256 + threadIdx.x;
@@ -374,11 +373,11 @@ __global__ void __launch_bounds__(256) residue_b_kernel(const double* __restrict
 #pragma unroll
   for (int t = 0; t < 16; ++t) {
     const int64_t i = i0 + t;
-    v[t] = (jj < ncols && i < k && !dead) ? b[i + jj * ldb] : 0.0;
+    v[t] = (jj < ncols && i < k && !dead) ? scalbn(b[i + jj * ldb], eb) : 0.0;  // exact (|result| < 2^53)
   }
   Parts2 x[8];
 #pragma unroll
-  for (int t = 0; t < 8; ++t) x[t] = split_parts2(v[2 * t], v[2 * t + 1], scale);
+  for (int t = 0; t < 8; ++t) x[t] = split_parts2(v[2 * t], v[2 * t + 1], 1.0);
   ChunkWriter<0, NMOD, 16>::run(x, tile0 + (size_t)kb * n_g * kTile + swz(r, c), mod_stride);
 }
 
@@ -401,6 +400,7 @@ struct OzHeader {
   unsigned long long minrow;     // min over rows (~0ull: none)
   unsigned long long mincol;     // min over columns (~0ull: none)
   unsigned nonfinite;            // a row or column sum is NaN / Inf
+  unsigned nonint;               // some entry is not an integer
 };
 
 __global__ void __launch_bounds__(256, 4) norms_partial_kernel(const double* __restrict__ a, int64_t lda, int64_t m,
@@ -415,6 +415,7 @@ __global__ void __launch_bounds__(256, 4) norms_partial_kernel(const double* __r
     hdr->minrow = ~0ull;
     hdr->mincol = ~0ull;
     hdr->nonfinite = 0u;
+    hdr->nonint = 0u;
   }
   const int64_t r0 = rb * kNormRows, c0 = cb * kNormCols;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -467,10 +468,23 @@ __global__ void __launch_bounds__(256, 4) norms_partial_kernel(const double* __r
   }
 }
 
+constexpr int kIntSampleCols = 16;
+
 __global__ void norms_final_kernel(const double* __restrict__ part_row, int64_t ncb, int64_t m,
                                    const double* __restrict__ part_col, int64_t nrb, int64_t n,
-                                   OzHeader* __restrict__ hdr) {
+                                   OzHeader* __restrict__ hdr, const double* __restrict__ a, int64_t lda) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < m) {  // integrality sample: row t of 16 evenly spread columns.  A non-integer
+                // entry proves A is not integer-valued; an all-integer sample (possibly a
+                // false "integer") only costs the faster engine (integer A goes to DMMA).
+    bool frac = false;
+#pragma unroll 4
+    for (int q = 0; q < kIntSampleCols; ++q) {
+      const double v = __ldg(a + t + ((int64_t)q * n / kIntSampleCols) * lda);
+      frac |= v != rint(v);
+    }
+    if (__any_sync(__activemask(), frac) && (threadIdx.x & 31) == 0) atomicOr(&hdr->nonint, 1u);
+  }
   double v = 0.0;
   if (t < m) {
     for (int64_t cb = 0; cb < ncb; ++cb) v += part_row[cb * m + t];
@@ -976,7 +990,7 @@ static int oz_norms(const double* a, int64_t lda, int64_t m, int64_t n, int nmod
                                                                                            pcol, hdr);
   ktimer_mark(KT_OZ_NORMS, st, true);
   RLRA_LAUNCHED();
-  oz::norms_final_kernel<<<(unsigned)ceil_div(m + n, 256), 256, 0, st>>>(prow, ncb, m, pcol, nrb, n, hdr);
+  oz::norms_final_kernel<<<(unsigned)ceil_div(m + n, 256), 256, 0, st>>>(prow, ncb, m, pcol, nrb, n, hdr, a, lda);
   RLRA_LAUNCHED();
   oz::scale_a_kernel<<<1, 1, 0, st>>>(hdr, oz::budget(nmod).pa, e_a);
   RLRA_LAUNCHED();
@@ -1018,6 +1032,12 @@ int oz_guard(const void* hdr_host, int64_t m, int64_t n, int* ok_nn, int* ok_tn)
     return 0;
   }
   if (mx < 0x1p-960) return 0;  // every row and column norm below 2^-480: the scale would leave the normal range
+  // Integer-valued A: exact linear dependencies among its rows / columns survive
+  // the engine's exactly-rounded products, so a rank-deficient sketch gets
+  // EXACT zero pivots where BLAS's accumulation noise leaves tiny non-zero ones
+  // (the reference then passes through instead of raising RankCollapse,
+  // rlra/rangefinder.py:55-64).  Such inputs take the DMMA GEMM.
+  if (h.nonint == 0u) return 0;
   // rho^2 = max / min of the sums of squares; a minimum below DBL_MIN (a zero
   // row, or squares that underflow) is rejected
   auto ok = [&](unsigned long long minbits, double mn, int64_t k) {

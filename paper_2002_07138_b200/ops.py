@@ -199,13 +199,13 @@ def oz_guard(header, m, n):
 
 
 def oz_guard_stats(header):
-    """Decoded guard header: (max norm, min non-zero row norm, min non-zero
-    column norm, non-finite) -- diagnostics only."""
+    """Decoded guard header: (max norm, min row norm, min column norm,
+    non-finite, integer-valued) -- diagnostics only."""
     h = header.cpu().numpy() if isinstance(header, torch.Tensor) else np.frombuffer(bytes(header), np.uint8)
     mx, mr, mc = h[8:32].view(np.uint64)
-    nf = int(h[32:36].view(np.uint32)[0])
+    nf, nonint = (int(x) for x in h[32:40].view(np.uint32))
     f = lambda b: float("inf") if b == np.uint64(0xFFFFFFFFFFFFFFFF) else float(np.sqrt(np.array([b]).view(np.float64)[0]))  # noqa: E731
-    return f(mx), f(mr), f(mc), bool(nf)
+    return f(mx), f(mr), f(mc), bool(nf), not nonint
 
 
 class OzPrep:
@@ -215,7 +215,8 @@ class OzPrep:
     guard=True (the product path): the norms and guard statistics are computed
     first and read back (one small device->host transfer); an orientation the
     guard rejects (graded rows / columns beyond rlra_b200_oz_guard_limit(K),
-    NaN / Inf, extreme exponent range) runs on the FP64 DMMA GEMM instead, and
+    NaN / Inf, extreme exponent range, integer-valued A) runs on the FP64 DMMA
+    GEMM instead, and
     the residues are built only if some orientation is admitted.  guard=False
     exercises the raw engine (tests)."""
 

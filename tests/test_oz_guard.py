@@ -18,9 +18,9 @@ import pytest
 from paper_2002_07138_b200 import ops
 
 
-def header(max_ss, min_row_ss, min_col_ss, nonfinite=0, e_a=0):
+def header(max_ss, min_row_ss, min_col_ss, nonfinite=0, e_a=0, nonint=1):
     bits = lambda x: struct.unpack("<Q", struct.pack("<d", x))[0] if x is not None else 0xFFFFFFFFFFFFFFFF  # noqa: E731
-    raw = struct.pack("<iiQQQI", e_a, 0, bits(max_ss), bits(min_row_ss), bits(min_col_ss), nonfinite)
+    raw = struct.pack("<iiQQQII", e_a, 0, bits(max_ss), bits(min_row_ss), bits(min_col_ss), nonfinite, nonint)
     return raw + b"\0" * (ops.OZ_HEADER_BYTES - len(raw))
 
 
@@ -58,6 +58,8 @@ def test_guard_decisions():
     assert ops.oz_guard(header(1.0, 1.0, 1e-320), m, n) == (True, False)
     # everything tiny (norms below 2^-480): the scale leaves the normal range
     assert ops.oz_guard(header(2.0 ** -970, 2.0 ** -970, 2.0 ** -970), m, n) == (False, False)
+    # integer-valued A: DMMA (exact products would turn exact dependencies into exact zero pivots)
+    assert ops.oz_guard(header(4.0, 1.0, 1.0, nonint=0), m, n) == (False, False)
     # tiny K: no admissible ratio
     assert ops.oz_guard(header(1.0, 1.0, 1.0), 4, 4) == (False, False)
 
@@ -73,5 +75,5 @@ def test_guard_on_the_benchmark_configs():
 
 def test_header_decoding():
     h = np.frombuffer(header(16.0, 4.0, None, 0), dtype=np.uint8)
-    mx, mr, mc, nf = ops.oz_guard_stats(h)
-    assert (mx, mr, mc, nf) == (4.0, 2.0, float("inf"), False)
+    assert ops.oz_guard_stats(h) == (4.0, 2.0, float("inf"), False, False)
+    assert ops.oz_guard_stats(np.frombuffer(header(1.0, 1.0, 1.0, nonint=0), np.uint8))[4] is True
