@@ -64,11 +64,56 @@ def cases():
     return out
 
 
+def order_outcomes(a, k, q_os, v, seed):
+    """Outcome of the reference's algorithm (the oracle restatement) when its
+    products sum over K in other legitimate orders: reversed, K-chunks of 64,
+    reversed chunks of 32.  A case whose pass-through / RankCollapse outcome
+    changes with the order is rounding-dependent, not a parity target."""
+    sys.path.insert(0, REPO)
+    from oracle import rlra_oracle as O
+
+    def rev(x, y):
+        return np.ascontiguousarray(x[:, ::-1]) @ np.ascontiguousarray(y[::-1])
+
+    def chunk(x, y, c=64, reverse=False):
+        out = np.zeros((x.shape[0], y.shape[1]))
+        starts = range(0, x.shape[1], c)
+        for k0 in (reversed(starts) if reverse else starts):
+            out += x[:, k0:k0 + c] @ y[k0:k0 + c]
+        return out
+
+    res = []
+    for mm in (np.matmul, rev, chunk, lambda x, y: chunk(x, y, 32, True)):
+        l = k + q_os
+        m, n = a.shape
+        try:
+            if v % 2 == 0:
+                x = mm(a.T, O.gaussian(seed, m, l))
+                if v == 2:
+                    O._qr_basis(x)
+                    res.append("ok")
+                    continue
+                w = O._lu_basis(x)
+            else:
+                w = O.gaussian(seed, n, l)
+            half = (v - 1) // 2
+            for i in range(1, half + 1):
+                w = O._lu_basis(mm(a, w))
+                if i == half:
+                    O._qr_basis(mm(a.T, w))
+                else:
+                    w = O._lu_basis(mm(a.T, w))
+            res.append("ok")
+        except O.OracleRankCollapse as e:
+            res.append(f"RankCollapse:{e.achieved}")
+    return res
+
+
 def main():
     arrays, meta = {}, {}
     for name, (a, k, q_os, v, seed) in cases().items():
         arrays[f"{name}/a"] = a
-        rec = {"k": k, "q_os": q_os, "v": v, "seed": seed}
+        rec = {"k": k, "q_os": q_os, "v": v, "seed": seed, "order_outcomes": order_outcomes(a, k, q_os, v, seed)}
         try:
             f = fixedrank.powerlu(a, k, q_os, v, seed)
         except errors.RankCollapse as e:

@@ -152,17 +152,32 @@ def test_extreme_magnitudes_of_a(cuda_dev, scale):
 
 @pytest.mark.parametrize("name", sorted(GMETA))
 def test_driver_outcome_matches_reference(cuda_dev, name):
+    """Same outcome as the reference.  For rank-deficient sketches the
+    pass-through / RankCollapse outcome hinges on whether an eliminated column
+    is EXACTLY zero, i.e. on the last-bit rounding of the products: the
+    generator records the reference algorithm's outcome under four legitimate
+    summation orders (order_outcomes).  Order-stable cases must match the
+    reference exactly; an order-sensitive case must give one of the outcomes a
+    legitimate order gives."""
     import paper_2002_07138_b200 as P
 
     meta = GMETA[name]
     a = GCASES[f"{name}/a"]
     args = (a, meta["k"], meta["q_os"], meta["v"], meta["seed"])
-    if meta["outcome"] == "RankCollapse":
-        with pytest.raises(P.RankCollapse) as ei:
-            P.powerlu(*args)
-        assert (ei.value.achieved, ei.value.requested) == (meta["achieved"], meta["requested"])
+    allowed = set(meta["order_outcomes"])
+    try:
+        f = P.powerlu(*args)
+        got = "ok"
+    except P.RankCollapse as e:
+        got, f = f"RankCollapse:{e.achieved}", None
+        assert e.requested == meta["k"] + meta["q_os"]
+    if len(allowed) == 1:
+        ref = "ok" if meta["outcome"] == "ok" else f"RankCollapse:{meta['achieved']}"
+        assert got == ref, (got, ref)
+    else:
+        assert got in allowed, (got, allowed)
+    if f is None:
         return
-    f = P.powerlu(*args)
     if not name.startswith("int_"):
         # integer inputs repeat columns: exact ties in |B^T| whose tie-break
         # follows the last-bit rounding of the BLAS used (the reference's own
@@ -170,7 +185,16 @@ def test_driver_outcome_matches_reference(cuda_dev, name):
         assert np.array_equal(f.p, GCASES[f"{name}/p"]), name
         assert np.array_equal(f.q, GCASES[f"{name}/q"]), name
     err = O.rel_fro_error_factor(a, f)
-    assert abs(err - meta["rel_err"]) <= 1e-10 * max(1.0, meta["rel_err"]), (err, meta["rel_err"])
+    if meta["outcome"] == "ok":
+        assert abs(err - meta["rel_err"]) <= 1e-10 * max(1.0, meta["rel_err"]), (err, meta["rel_err"])
+    else:
+        assert err <= 1e-10
+
+
+def test_order_stable_cases_exist():
+    stable = [n for n, m in GMETA.items() if len(set(m["order_outcomes"])) == 1]
+    assert len(stable) >= len(GMETA) - 1
+    assert any(m["outcome"] == "RankCollapse" for n, m in GMETA.items() if n in stable)
 
 
 def test_powerlu_nan_input_gives_nonfinite_factors(cuda_dev):
