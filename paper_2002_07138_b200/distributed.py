@@ -21,6 +21,12 @@ Sketch factorizations:
   reference algorithm; LU / QR of the replicated n x l sketches run
   redundantly with no communication.
 
+Single-pass LU (rlra/singlepass.py:99-144) over the same row shards: per sweep
+panel J, G_J = sum_i A_i(:, J)^T Omega_i is a local partial product followed
+by an all-reduce (w x l), issued asynchronously so it overlaps the next
+panel's partial product; H_i += A_i(:, J) G_J stays local (H row-sharded).
+H is all-gathered for its exact GEPP; G is replicated for the QR / TRSM / LU.
+
 The orchestration is written against a small ops interface so the same code
 runs on CUDA tensors with NCCL (CudaOps, the product) and -- in the CPU test
 suite only -- on CPU tensors with gloo and an oracle-backed ops object
@@ -77,6 +83,35 @@ class CudaOps:
         if prep is not None and 0 < x.shape[1] <= 4096:
             return prep.gemm(x, trans=ta)
         return self.o.matmul(a, x, ta=ta)
+
+    def zeros(self, m, n):
+        return self.o.fmat(m, n, self.device, zero=True)
+
+    def sweep_width(self, m, panel):
+        from .singlepass import sweep_width
+
+        return sweep_width(m, panel) if self.sweep_oz(m, 1 << 30, 1) else panel
+
+    def sweep_oz(self, m, n, k):
+        from .device import PASS_GEMM
+        from .singlepass import SWEEP_OZ_MIN_ELEMS
+
+        return PASS_GEMM == "oz" and 0 < m <= self.o.OZ_BLOCK_K and k <= 4096 and m * n >= SWEEP_OZ_MIN_ELEMS
+
+    def sweep_prep(self, block, oz):
+        """Residues of one sweep panel (read once, both products), or None."""
+        return self.o.OzPrep(block) if oz and min(block.shape) > 0 else None
+
+    def sweep_products(self, block, prep, x, out, ta, add):
+        """out = block^T x (ta) or out += block x (add) on the sweep engine."""
+        if prep is not None:
+            return prep.gemm(x, trans=ta, out=out, add=add)
+        return self.o.gemm(block, x, out, ta=ta, beta=1.0 if add else 0.0)
+
+    def pinv_transpose_apply(self, g, m_):
+        from .kernels import pinv_transpose_apply
+
+        return pinv_transpose_apply(g, m_)
 
     def getrf_(self, a):
         return self.o.getrf_(a)
@@ -379,3 +414,77 @@ def powerlu_fp(A: ShardedMatrix, eps, b, l, v, seed, omega_fn):
         raise NotConverged(AdaptiveOutcome(rank, V, g_local, resid, conv))
     # lu_from_projection factors the all-gathered copy, g_local stays intact
     return lu_from_projection(A, g_local[:, :rank], V[:, :rank]), rank
+
+
+# ---------------------------------------------------------------- single pass
+def stream_sketch(A: ShardedMatrix, k, seed, omega_fn, panel=256):
+    """rlra/singlepass.py:99-120 over a row-sharded A (each rank streams the
+    columns of its own rows A_i, ascending, each column once).
+
+    Per sweep panel J (the single-GPU grouping, singlepass.sweep_width):
+      G_J  = A_i(:, J)^T Omega_i   local partial (w x k)
+      all-reduce(G_J)              asynchronous: runs while the next panel's
+                                   partial product is computed
+      H_i += A_i(:, J) G_J         local rows of H
+    Returns (G replicated n x k, H_i this rank's rows of the m x k H)."""
+    m, n = A.shape
+    if not 1 <= k <= min(m, n):
+        raise ValueError(f"k={k} outside 1..min{(m, n)}")
+    if panel < 1:
+        raise ValueError("panel width must be >= 1")
+    ops = A.ops
+    rows = A.r1 - A.r0
+    om = omega_fn(seed, m, k)
+    if isinstance(om, torch.Tensor):
+        om_i = om[A.r0:A.r1]
+    else:
+        om_i = ops.upload(np.asfortranarray(om[A.r0:A.r1]))
+    oz = hasattr(ops, "sweep_oz") and ops.sweep_oz(m, n, k)
+    width = ops.sweep_width(m, panel) if oz else panel
+    g = ops.empty(n, k)
+    h = ops.zeros(rows, k)
+    pending = None  # (j0, w, block, prep, reduced buffer, async handle)
+
+    def finish(item):
+        j0, w, block, prep, buf, handle = item
+        handle.wait()
+        g[j0:j0 + w, :].copy_(buf)
+        if rows:
+            ops.sweep_products(block, prep, buf, h, ta=False, add=True)  # H_i += A_i(:, J) G_J
+
+    for j0 in range(0, n, width):
+        w = min(width, n - j0)
+        block = A.local[:, j0:j0 + w]
+        prep = ops.sweep_prep(block, oz) if (rows and hasattr(ops, "sweep_prep")) else None
+        buf = ops.zeros(w, k)  # contiguous column-major: (k, w) row-major storage
+        if rows:
+            ops.sweep_products(block, prep, om_i, buf, ta=True, add=False)  # partial G_J
+        handle = dist.all_reduce(buf.t(), op=dist.ReduceOp.SUM, group=A.group, async_op=True)
+        if pending is not None:
+            finish(pending)
+        pending = (j0, w, block, prep, buf, handle)
+        A.product_count += 1
+    if pending is not None:
+        finish(pending)
+    return g, h
+
+
+def single_pass_lu(A: ShardedMatrix, k, seed, omega_fn, q_os=0, panel=256):
+    """rlra/singlepass.py:123-144 over a row-sharded A; every rank returns the
+    same factors.  H is all-gathered for the exact GEPP (p identical to one
+    GPU); G, T and their factors are replicated."""
+    l = k + q_os
+    ops = A.ops
+    g, h_local = stream_sketch(A, l, seed, omega_fn, panel)
+    h = A.gather_rows(h_local)
+    piv1, _ = ops.getrf_(h)
+    l1, u1 = ops.lu_extract(h)
+    t = ops.pinv_transpose_apply(g, ops.transpose(u1))
+    piv2, _ = ops.getrf_(t)
+    l2, u2 = ops.lu_extract(t)
+    big_l = ops.matmul(l1, u2, tb=True)
+    big_u = ops.transpose(l2)
+    if q_os:
+        big_l = big_l[:, :k]
+        big_u = big_u[:k, :]
+    return DistLU(piv1, piv2, big_l, big_u, k)

@@ -40,6 +40,22 @@ class OracleOps:
         out.copy_(r)
         return out
 
+    def zeros(self, m, n):
+        t = self._f(m, n)
+        t.zero_()
+        return t
+
+    def sweep_products(self, block, prep, x, out, ta, add):
+        r = (block.t() @ x) if ta else (block @ x)
+        if add:
+            out += r
+        else:
+            out.copy_(r)
+        return out
+
+    def pinv_transpose_apply(self, g, m_):
+        return self.upload(O.pinv_transpose_apply(g.numpy(), m_.numpy()))
+
     def getrf_(self, a):
         lu = np.asfortranarray(a.numpy())
         piv = np.arange(lu.shape[0], dtype=np.int64)
@@ -106,7 +122,11 @@ def _worker(rank, world, port, case, q):
         r0, r1 = D.row_range(m, world, rank)
         ops = OracleOps()
         A = D.ShardedMatrix(ops.upload(a[r0:r1]), m, r0, r1, ops)
-        if case["kind"] == "powerlu":
+        if case["kind"] == "single_pass":
+            f = D.single_pass_lu(A, case["k"], case["seed"], O.gaussian, q_os=case["q_os"], panel=case["panel"])
+            out = (f.p.numpy().copy(), f.q.numpy().copy(), f.L.numpy().copy(), f.U.numpy().copy(),
+                   A.product_count)
+        elif case["kind"] == "powerlu":
             f = D.powerlu(A, case["k"], case["q_os"], case["v"], case["seed"], O.gaussian)
             out = (f.p.numpy().copy(), f.q.numpy().copy(), f.L.numpy().copy(), f.U.numpy().copy(),
                    A.product_count)
@@ -181,3 +201,23 @@ def test_sharded_tslu_shards_shorter_than_sketch():
         assert np.array_equal(p, ref.p) and np.array_equal(q, ref.q)
         f = O.LowRankLU(p, q, L, U, 12)
         assert abs(O.rel_fro_error_factor(a, f) - O.rel_fro_error_factor(a, ref)) <= 1e-12
+
+
+@pytest.mark.parametrize("world,panel,q_os", [(2, 16, 0), (2, 7, 10), (3, 64, 5)])
+def test_sharded_single_pass_matches_single_process(world, panel, q_os):
+    """C4's path (rlra/singlepass.py:99-144) row-sharded: per-panel all-reduce
+    of the partial G_J (asynchronous, overlapping the next panel), local H_i,
+    gathered exact GEPP of H: same p, q as one process; error equal to 1e-12."""
+    rng = np.random.default_rng(40 + world)
+    x, _ = np.linalg.qr(rng.standard_normal((211, 30)))
+    y, _ = np.linalg.qr(rng.standard_normal((130, 30)))
+    a = np.asfortranarray((x * np.arange(1, 31) ** -1.5) @ y.T + 1e-6 * rng.standard_normal((211, 130)))
+    k = 12
+    res = run_dist({"kind": "single_pass", "a": a, "k": k, "q_os": q_os, "seed": 3, "panel": panel}, world=world)
+    ref = O.single_pass_lu(a, k, 3, q_os=q_os, panel=panel)
+    e_ref = O.rel_fro_error_factor(a, ref)
+    for rank, (p, q, L, U, sweeps) in res.items():
+        assert np.array_equal(p, ref.p) and np.array_equal(q, ref.q)
+        assert abs(O.rel_fro_error_factor(a, O.LowRankLU(p, q, L, U, k)) - e_ref) <= 1e-12
+        assert sweeps == -(-130 // panel)  # one all-reduce per panel, each column read once
+    np.testing.assert_array_equal(res[0][2], res[1][2])
