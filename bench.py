@@ -72,12 +72,44 @@ def workload(args):
 
     w = configs.WORKLOADS[args.config]
     v = args.v if args.v is not None else w.v
-    if w.kind != "powerlu":
-        raise SystemExit(f"bench supports the fixed-rank powerlu configs (C1, C2, C5); got {args.config}")
-    gen = {"C1": configs.gen_c1, "C2": configs.gen_c2, "C5": None}[w.name]  # C5: built in HBM
-    passes, fact = configs.powerlu_flops(w.m, w.n, w.k, w.k + w.q_os, v)
-    desc = (f"{w.name}: powerlu(A {w.m}x{w.n} float64, k={w.k}, q_os={w.q_os}, v={v}, seed={w.seed})")
+    gen = {"C1": configs.gen_c1, "C2": configs.gen_c2}.get(w.name)  # C3-C5: built in HBM (configs.gen_device)
+    if w.kind == "powerlu":
+        passes, fact = configs.powerlu_flops(w.m, w.n, w.k, w.k + w.q_os, v)
+        desc = f"{w.name}: powerlu(A {w.m}x{w.n} float64, k={w.k}, q_os={w.q_os}, v={v}, seed={w.seed})"
+    elif w.kind == "powerlu_fp":
+        passes, fact = configs.powerlu_fp_flops(w.m, w.n, FP_WIDTH, v, FP_RANK)
+        desc = (f"{w.name}: powerlu_fp(A {w.m}x{w.n} float64, PrecisionParams(eps={w.eps}, b={w.b}, "
+                f"l={FP_WIDTH}, v={v}), seed={w.seed}) (flops at the reference's rank {FP_RANK})")
+    else:
+        passes, fact = configs.single_pass_flops(w.m, w.n, w.k + w.q_os)
+        desc = (f"{w.name}: single_pass_lu(DeviceColumnStream(A {w.m}x{w.n} float64), k={w.k}, "
+                f"seed={w.seed}, q_os={w.q_os})")
     return w, v, gen, passes, fact, desc
+
+
+FP_WIDTH, FP_RANK = 1024, 843  # C3: sketch width and the reference's chosen rank (tests/golden/golden_configs.json)
+
+
+def single_runner(w, v, dm):
+    """The drop-in call of config w on one GPU (DeviceMatrix operand)."""
+    import paper_2002_07138_b200 as P
+
+    if w.kind == "powerlu":
+        return lambda: P.powerlu(dm, w.k, w.q_os, v, w.seed)
+    if w.kind == "powerlu_fp":
+        return lambda: P.powerlu_fp(dm, P.PrecisionParams(w.eps, w.b, FP_WIDTH, v), w.seed)[0]
+    return lambda: P.single_pass_lu(P.DeviceColumnStream(dm), w.k, w.seed, q_os=w.q_os)
+
+
+def dist_runner(w, v, A, omega):
+    """The same call over a row-sharded A (distributed.py)."""
+    from paper_2002_07138_b200 import distributed as D
+
+    if w.kind == "powerlu":
+        return lambda: D.powerlu(A, w.k, w.q_os, v, w.seed, omega)
+    if w.kind == "powerlu_fp":
+        return lambda: D.powerlu_fp(A, w.eps, w.b, FP_WIDTH, v, w.seed, omega)[0]
+    return lambda: D.single_pass_lu(A, w.k, w.seed, omega, q_os=w.q_os)
 
 
 def ref_module():
@@ -176,10 +208,19 @@ def roofline_line(w, v, passes, reps, kt, pass_ms, step_ms):
     from paper_2002_07138_b200 import ops
 
     nmod = ops.OZ_NMOD
-    l_ = w.k + w.q_os
-    widths = [l_] * (v - 1) + [w.k]
-    bytes_step = sum(nmod * (w.m * w.n + (w.m + w.n) * x) for x in widths)
-    i8ops_step = sum(nmod * 2.0 * w.m * w.n * x for x in widths)
+    if w.kind == "single_pass":  # two products per sweep panel (TN then NN), K or rows = m
+        from paper_2002_07138_b200.singlepass import sweep_width
+
+        l_ = w.k + w.q_os
+        sw = sweep_width(w.m, 256)
+        panels = [min(sw, w.n - j0) for j0 in range(0, w.n, sw)]
+        bytes_step = sum(2 * nmod * (w.m * x + (w.m + x) * l_) for x in panels)
+        i8ops_step = sum(2 * nmod * 2.0 * w.m * x * l_ for x in panels)
+    else:
+        l_ = FP_WIDTH if w.kind == "powerlu_fp" else w.k + w.q_os
+        widths = [l_] * v if w.kind == "powerlu_fp" else [l_] * (v - 1) + [w.k]
+        bytes_step = sum(nmod * (w.m * w.n + (w.m + w.n) * x) for x in widths)
+        i8ops_step = sum(nmod * 2.0 * w.m * w.n * x for x in widths)
     g_ms, g_cnt = kt["oz_gemm_i8"]
     hbm_peak = MEASURED.get("hbm_gbs")
     if g_cnt == 0:  # DMMA pass (RLRA_B200_PASS_GEMM=dmma or operands too large for the residues)
@@ -225,28 +266,41 @@ def reference_arm(args):
     w, v, gen, passes, fact, desc = workload(args)
     mod, kind = ref_module()
     sample = f"{args.steps} full {w.name} factorizations (mean)"
-    if gen is None:  # C5 (68.7 GB): the survey's C5 analogue is the bounded host sample
-        from paper_2002_07138_b200 import configs
+    from paper_2002_07138_b200 import configs
 
+    call = lambda a_: mod.powerlu(a_, w.k, w.q_os, v, w.seed)  # noqa: E731
+    steps, warm = args.steps, args.warmup
+    if w.name == "C5":  # 68.7 GB: the survey's C5 analogue is the bounded host sample
         a = configs.gen_lowrank_plus_noise(32768, 8192, 640, 10.0 ** (-8.0 * np.arange(640) / 639), 1e-10, 5)
         passes, fact = configs.powerlu_flops(32768, 8192, w.k, w.k + w.q_os, v)
-        sample = f"{args.steps} factorizations of the C5 analogue 32768x8192 (SURVEY Appendix A), mean"
+        sample = f"{steps} factorizations of the C5 analogue 32768x8192 (SURVEY Appendix A), mean"
+    elif w.name == "C4":  # 20 GB, ~100 s per call on the host: the survey's 20000^2 analogue
+        a = configs.gen_lowrank_plus_noise(20000, 20000, 300, np.arange(1, 301) ** -1.5, 1e-6, 4)
+        passes, fact = configs.single_pass_flops(20000, 20000, w.k + w.q_os)
+        steps, warm = min(steps, 2), min(warm, 1)
+        call = lambda a_: mod.single_pass_lu(mod.DenseColumnStream(a_), w.k, w.seed, q_os=w.q_os)  # noqa: E731
+        sample = f"{steps} single_pass_lu of the C4 analogue 20000x20000 (SURVEY Appendix A), mean"
+    elif w.name == "C3":  # ~37 s per call on the host: one warm-up-free sample
+        a = configs.gen_c3()
+        steps, warm = min(steps, 2), 0
+        call = lambda a_: mod.powerlu_fp(a_, mod.PrecisionParams(w.eps, w.b, FP_WIDTH, v), w.seed)  # noqa: E731
+        sample = f"{steps} full C3 powerlu_fp calls (mean)"
     else:
         a = gen()
     flops = passes + fact
-    for _ in range(args.warmup):
-        mod.powerlu(a, w.k, w.q_os, v, w.seed)
+    for _ in range(warm):
+        call(a)
     times = []
-    for _ in range(args.steps):
+    for _ in range(steps):
         t0 = time.perf_counter()
-        mod.powerlu(a, w.k, w.q_os, v, w.seed)
+        call(a)
         times.append(time.perf_counter() - t0)
     sec = sum(times) / len(times)
     val = flops / sec / 1e9
     cores = os.cpu_count()
     line = {
         "impl": "reference", "metric": f"PowerLU FP64 GFLOP/s ({w.name}, v={v})", "value": val,
-        "unit": "GFLOP/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "unit": "GFLOP/s", "n_gpus": args.gpus, "steps": steps, "warmup": warm,
         "ms_per_step": sec * 1e3, "s_per_factorization": sec, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": desc, "m": w.m, "n": w.n, "k": w.k, "l": w.k + w.q_os, "v": v},
@@ -276,20 +330,33 @@ def cpu_baseline(a, w, v, flops, budget_s=30.0):
 
 
 def cpu_baseline_analogue(w, v):
-    """Bounded CPU sample for the 68.7 GB C5: the reference on the survey's
-    C5 analogue (32768 x 8192, same k, q_os, v and spectrum recipe; SURVEY.md
-    Appendix A) -- GFLOP/s of the same algorithm at a host-feasible size."""
+    """Bounded CPU sample for the device-built configs: the reference on the
+    survey's host-feasible analogues -- C5: 32768 x 8192,
+    same k, q_os, v and spectrum recipe; C4: 20000 x 20000 single pass, same
+    widths; C3: the full C3 (one call) -- GFLOP/s of the same algorithm."""
     from paper_2002_07138_b200 import configs
 
-    m, n = 32768, 8192
-    a = configs.gen_lowrank_plus_noise(m, n, 640, 10.0 ** (-8.0 * np.arange(640) / 639), 1e-10, 5)
     mod, kind = ref_module()
-    p_, f_ = configs.powerlu_flops(m, n, w.k, w.k + w.q_os, v)
+    if w.name == "C3":
+        m, n = w.m, w.n
+        a = configs.gen_c3()
+        p_, f_ = configs.powerlu_fp_flops(m, n, FP_WIDTH, v, FP_RANK)
+        call = lambda: mod.powerlu_fp(a, mod.PrecisionParams(w.eps, w.b, FP_WIDTH, v), w.seed)  # noqa: E731
+    elif w.name == "C4":
+        m, n = 20000, 20000
+        a = configs.gen_lowrank_plus_noise(m, n, 300, np.arange(1, 301) ** -1.5, 1e-6, 4)
+        p_, f_ = configs.single_pass_flops(m, n, w.k + w.q_os)
+        call = lambda: mod.single_pass_lu(mod.DenseColumnStream(a), w.k, w.seed, q_os=w.q_os)  # noqa: E731
+    else:
+        m, n = 32768, 8192
+        a = configs.gen_lowrank_plus_noise(m, n, 640, 10.0 ** (-8.0 * np.arange(640) / 639), 1e-10, 5)
+        p_, f_ = configs.powerlu_flops(m, n, w.k, w.k + w.q_os, v)
+        call = lambda: mod.powerlu(a, w.k, w.q_os, v, w.seed)  # noqa: E731
     t0 = time.perf_counter()
-    mod.powerlu(a, w.k, w.q_os, v, w.seed)
+    call()
     sec = time.perf_counter() - t0
     return {"value": (p_ + f_) / sec / 1e9, "unit": "GFLOP/s", "cores": os.cpu_count(), "kind": kind,
-            "sample": f"1 factorization of the C5 analogue {m}x{n} (SURVEY Appendix A), {sec:.1f} s"}
+            "sample": f"1 call on the {w.name} analogue {m}x{n} (SURVEY Appendix A), {sec:.1f} s"}
 
 
 GOLDEN = os.path.join(REPO, "tests", "golden")
@@ -302,8 +369,10 @@ def golden_pq(name, v):
         if name == "C2":
             d = np.load(os.path.join(GOLDEN, "c2_pq.npz"))
             return d[f"v{v}_p"], d[f"v{v}_q"]
-        if name == "C5" and v == 4:
-            d = np.load(os.path.join(GOLDEN, "c5_pq.npz"))
+        from paper_2002_07138_b200 import configs
+
+        if name in ("C1", "C3", "C4", "C5") and v == configs.WORKLOADS[name].v:
+            d = np.load(os.path.join(GOLDEN, f"{name.lower()}_pq.npz"))
             return d["p"], d["q"]
     except (OSError, KeyError):
         return None
@@ -408,17 +477,18 @@ def our_arm(args):
         dm = P.DeviceMatrix(a, local)
         torch.cuda.synchronize()
         upload_s = time.perf_counter() - t0
-    else:  # C5 (68.7 GB): same recipe, built directly in HBM (configs.gen_device)
+    else:  # C3-C5 (2-69 GB): same recipe, built directly in HBM (configs.gen_device)
         from paper_2002_07138_b200 import configs as _cfg
 
         a = None
         dm = P.DeviceMatrix(_cfg.gen_device(w.name, dev), local)
         gen_s, upload_s = time.perf_counter() - t0, 0.0
         args.no_e2e = True
+    run = single_runner(w, v, dm)
     P.set_omega_cache(True)
     st = torch.cuda.current_stream(dev)
     for _ in range(args.warmup):
-        P.powerlu(dm, w.k, w.q_os, v, w.seed)
+        run()
     torch.cuda.synchronize()
 
     # ---- timed region: device-resident inputs and outputs
@@ -431,7 +501,7 @@ def our_arm(args):
     torch.cuda.synchronize()
     e0.record(st)
     for _ in range(args.steps):
-        f = P.powerlu(dm, w.k, w.q_os, v, w.seed)
+        f = run()
     e1.record(st)
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / args.steps
@@ -446,19 +516,23 @@ def our_arm(args):
     _ktimer_reset(lib)
     lib.rlra_b200_ktimer_enable(1)
     for _ in range(reps):
-        P.powerlu(dm, w.k, w.q_os, v, w.seed)
+        run()
     torch.cuda.synchronize()
     lib.rlra_b200_ktimer_enable(0)
     kt = {nm: _ktimer_read(lib, nm) for nm in KTIMERS}
     summ = ops.PROF.summary()
     ops.PROF.on = False
     ops.PROF.records.clear()
-    pass_ms = sum(summ.get(k, (0.0, 0))[0] for k in ("pass_nn", "pass_tn"))
+    pass_ms = sum(summ.get(k, (0.0, 0))[0] for k in ("pass_nn", "pass_tn", "sweep_oz"))
     roofline = roofline_line(w, v, passes, reps, kt, pass_ms, ms)
     # the exact GEPPs: latency-bound (one cluster-wide pivot exchange per column),
     # no HBM / tensor roofline applies; reported with their share of the step
     l_ = w.k + w.q_os
     gepp_cols = (v - 2) * l_ + 2 * w.k  # v - 2 interior sketch LUs of width l, the two final LUs of width k
+    if w.kind == "single_pass":
+        gepp_cols = 2 * l_  # GEPP of H (m x l) and of T (n x l)
+    elif w.kind == "powerlu_fp":
+        gepp_cols = (v - 2) * FP_WIDTH + 2 * FP_RANK
     gepp_ms = summ.get("rlra_b200_getrf", (0.0, 0))[0] / reps
     roofline["latency_bound"] = {
         "kernel": "lu_coop_kernel (bit-exact GEPP, csrc/getrf_full.cu)", "ms_per_step": gepp_ms,
@@ -600,8 +674,9 @@ def dist_arm(args):
     A = D.ShardedMatrix(shard, w.m, r0, r1, cops)
     core.set_omega_cache(True)
     omega = lambda seed, rows, l: core.omega(seed, rows, l, dev)  # noqa: E731
+    run = dist_runner(w, v, A, omega)
     for _ in range(args.warmup):
-        D.powerlu(A, w.k, w.q_os, v, w.seed, omega)
+        run()
     torch.cuda.synchronize()
     dist.barrier()
     lib = _native.load()
@@ -614,7 +689,7 @@ def dist_arm(args):
     dist.barrier()
     e0.record(st)
     for _ in range(args.steps):
-        D.powerlu(A, w.k, w.q_os, v, w.seed, omega)
+        run()
     e1.record(st)
     torch.cuda.synchronize()
     dist.barrier()
@@ -637,7 +712,7 @@ def dist_arm(args):
         def e2e_step():
             sh = cops.empty(r1 - r0, w.n)
             sh.copy_(host_shard.t(), non_blocking=True)
-            f = D.powerlu(D.ShardedMatrix(sh, w.m, r0, r1, cops), w.k, w.q_os, v, w.seed, omega)
+            f = dist_runner(w, v, D.ShardedMatrix(sh, w.m, r0, r1, cops), omega)()
             return ops.to_numpy_many([f.p, f.q, f.L, f.U]) if rank == 0 else []
 
         for _ in range(max(2, args.warmup)):
@@ -658,9 +733,9 @@ def dist_arm(args):
                "h2d_bytes_per_step": int(8 * w.m * w.n), "d2h_bytes_per_step": int(d2h), "steps": ksteps,
                "path": "distributed.powerlu over pinned host row shards -> NumPy factors on rank 0"}
         core.set_omega_cache(True)
-    fin = D.powerlu(A, w.k, w.q_os, v, w.seed, omega)
+    fin = run()
     parity = pq_parity(w.name, v, fin.p.cpu().numpy(), fin.q.cpu().numpy()) if rank == 0 else None
-    del fin, A, shard
+    del fin, A, shard, run
     core.set_omega_cache(False)
     torch.cuda.empty_cache()
     c5 = None

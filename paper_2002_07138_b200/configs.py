@@ -111,6 +111,34 @@ def powerlu_flops(m, n, k, l, v):
     return passes, fact
 
 
+def single_pass_flops(m, n, l):
+    """Algorithmic flops of one single_pass_lu of sketch width l (SURVEY.md
+    Appendix B): sweep 4mnl; GEPP(m x l of H) + QR(n x l of G) + 2nl^2 (T = Q X)
+    + GEPP(n x l of T) + 2ml^2 (L = L1 U2^T) + l^3 (TRSM)."""
+    gepp = lambda a, b: a * b * b - b ** 3 / 3.0
+    qr = lambda a, b: 4.0 * a * b * b - 4.0 * b ** 3 / 3.0
+    sweep = 4.0 * m * n * l
+    fact = gepp(m, l) + qr(n, l) + 2.0 * n * l * l + gepp(n, l) + 2.0 * m * l * l + float(l) ** 3
+    return sweep, fact
+
+
+def powerlu_fp_flops(m, n, l, v, rank):
+    """Algorithmic flops of one powerlu_fp: v passes of
+    width l (the G pass uses the full l) + 2mn for ||A||_F^2; interior LUs and
+    the final QR as in powerlu; the assembly at the chosen rank."""
+    gepp = lambda a, b: a * b * b - b ** 3 / 3.0
+    qr = lambda a, b: 4.0 * a * b * b - 4.0 * b ** 3 / 3.0
+    passes = 2.0 * m * n * v * l + 2.0 * m * n
+    fact = qr(n, l) + gepp(m, rank) + gepp(n, rank) + 2.0 * n * rank * rank + 2.0 * m * rank * rank
+    if v % 2:
+        h = (v - 1) // 2
+        fact += h * gepp(m, l) + (h - 1) * gepp(n, l)
+    elif v >= 4:
+        h = (v - 2) // 2
+        fact += h * (gepp(m, l) + gepp(n, l))
+    return passes, fact
+
+
 # ---------------------------------------------------------------- device builds
 def gen_device(name, device):
     """Build config `name`'s A directly in HBM (column-major torch tensor).

@@ -261,6 +261,13 @@ def test_distributed_path_single_rank_nccl(cuda_dev):
         ref = O.plu(y)
         w_ref = O.apply_inv_row_perm(ref.p, ref.L)  # exact GEPP's P^T L: same U for one rank
         assert np.abs(w - w_ref).max() <= 1e-12 * np.abs(w_ref).max()
+        # single-pass (C4's path): sharded sweep with the per-panel all-reduce
+        sa = DRV["sp_a"]
+        S = D.ShardedMatrix(ops.from_numpy(sa, cuda_dev), sa.shape[0], 0, sa.shape[0], D.CudaOps(cuda_dev))
+        sp = D.single_pass_lu(S, 20, 0, O.gaussian, q_os=5)
+        assert np.array_equal(sp.p.cpu().numpy(), DRV["sp/p"]) and np.array_equal(sp.q.cpu().numpy(), DRV["sp/q"])
+        spd = P.LowRankLU(sp.p.cpu().numpy(), sp.q.cpu().numpy(), ops.to_numpy(sp.L), ops.to_numpy(sp.U), 20)
+        assert abs(O.rel_fro_error_factor(sa, spd) - META["drivers"]["sp"]["rel_err"]) <= REL_ERR_TOL
     finally:
         dist.destroy_process_group()
 
