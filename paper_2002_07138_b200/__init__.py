@@ -2,10 +2,14 @@
 package ``rlra``'s PowerLU / PowerLU_FP / single-pass API.
 
 All factorization arithmetic runs in hand-written sm_100a kernels in
-librlra_b200.so (FP64 DMMA GEMMs, bit-exact GEPP, Householder QR, TRSM,
-compensated reductions) called through its C ABI (include/rlra_b200.h).
-There is no CPU fallback: without the library or a CUDA device every entry
-point raises NativeUnavailable.
+librlra_b200.so called through its C ABI (include/rlra_b200.h): the pass
+products as FP64 emulated on the int8 tensor cores (tcgen05 kind::i8,
+Ozaki scheme II, with a dynamic-range guard that sends inputs outside its
+DGEMM-class error bound to the FP64 DMMA GEMM), bit-exact GEPP, CholeskyQR2 /
+Householder QR, TRSM, compensated reductions.  There is no CPU fallback:
+without the library or a CUDA device every entry point raises
+NativeUnavailable.  A ``ShardedMatrix`` (distributed.shard_rows) passed to the
+same entry points runs the row-sharded multi-GPU algorithm (NCCL).
 """
 
 from .backend import BACKEND, plu_inplace
@@ -43,6 +47,7 @@ from .fixedrank import (LowRankLU, LowRankSVD, lu_from_projection, powerlu, rand
 from .rangefinder import (PowerParams, RangeBasis, SketchLU, general_power_basis_v, power_basis_lu_l,
                           power_basis_q, power_basis_v)
 from .singlepass import SketchPair, single_pass_lu, stream_sketch
+from .distributed import ShardedMatrix, shard_rows
 from .streams import read_rlra, read_rlra_header, write_rlra
 
 __version__ = "0.1.0"
@@ -62,4 +67,6 @@ __all__ = [
     "RlraFileColumnStream", "read_rlra", "read_rlra_header", "write_rlra",
     # sparse operands
     "SparseDeviceMatrix",
+    # multi-GPU operands
+    "ShardedMatrix", "shard_rows",
 ]

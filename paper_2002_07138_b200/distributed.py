@@ -166,10 +166,20 @@ class DistLU:
 
 
 class ShardedMatrix:
-    """Row shard A_i (rows [r0, r1) of the m x n operand) on this rank."""
+    """Row shard A_i (rows [r0, r1) of the m x n operand) on this rank.
 
-    def __init__(self, local, m, r0, r1, ops, group=None):
+    Passing it to the drop-in API (powerlu, powerlu_fp, adaptive_rank,
+    general_power_basis_v, single_pass_lu, stream_sketch -- the reference
+    signatures, rlra/fixedrank.py:120, rlra/fixedprec.py:152, ...) runs the
+    row-sharded algorithm over `group`; every rank gets the same factors.
+    omega_fn(seed, rows, l) draws Omega (default: the device replay of
+    rlra.core.gaussian)."""
+
+    is_sharded = True
+
+    def __init__(self, local, m, r0, r1, ops, group=None, omega_fn=None):
         self.local = local
+        self.omega_fn = omega_fn
         self.m, self.n = int(m), int(local.shape[1])
         self.r0, self.r1 = r0, r1
         self.ops = ops
@@ -411,7 +421,7 @@ def powerlu_fp(A: ShardedMatrix, eps, b, l, v, seed, omega_fn):
     if not conv:
         from .fixedprec import AdaptiveOutcome
 
-        raise NotConverged(AdaptiveOutcome(rank, V, g_local, resid, conv))
+        raise NotConverged(AdaptiveOutcome(rank, V[:, :rank], g_local[:, :rank], resid, conv))
     # lu_from_projection factors the all-gathered copy, g_local stays intact
     return lu_from_projection(A, g_local[:, :rank], V[:, :rank]), rank
 
@@ -488,3 +498,89 @@ def single_pass_lu(A: ShardedMatrix, k, seed, omega_fn, q_os=0, panel=256):
         big_l = big_l[:, :k]
         big_u = big_u[:k, :]
     return DistLU(piv1, piv2, big_l, big_u, k)
+
+
+# ---------------------------------------------------------------- drop-in API glue
+def _omega(A):
+    if A.omega_fn is not None:
+        return A.omega_fn
+    from . import core
+
+    dev = A.local.device
+    return lambda seed, rows, l: core.omega(seed, rows, l, dev)
+
+
+def shard_rows(a, group=None, device=None, ops=None):
+    """This rank's row shard of an m x n matrix (host ndarray or tensor, the
+    same full matrix on every rank, or already only this rank's rows with
+    `rows_only`): rows row_range(m, world, rank), column-major in HBM."""
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    m = int(a.shape[0])
+    r0, r1 = row_range(m, world, rank)
+    if ops is None:
+        import torch as _t
+
+        dev = device if device is not None else _t.device("cuda", _t.cuda.current_device())
+        ops = CudaOps(dev)
+    if isinstance(a, torch.Tensor):
+        local = ops.empty(r1 - r0, a.shape[1])
+        local.copy_(a[r0:r1])
+    else:
+        local = ops.upload(np.asfortranarray(np.asarray(a, dtype=np.float64)[r0:r1]))
+    return ShardedMatrix(local, m, r0, r1, ops, group)
+
+
+def api_powerlu(A, k, q_os, v, seed):
+    """powerlu(a, k, q_os, v, seed) for a ShardedMatrix (rlra/fixedrank.py:120)."""
+    from .fixedrank import LowRankLU
+
+    f = powerlu(A, k, q_os, v, seed, _omega(A))
+    return LowRankLU(f.p, f.q, f.L, f.U, f.rank)
+
+
+def api_adaptive_rank(A, params, seed):
+    """adaptive_rank(a, params, seed) (rlra/fixedprec.py:57): G holds this
+    rank's rows of A V."""
+    from .fixedprec import AdaptiveOutcome
+
+    rank, V, g_local, resid, conv = adaptive_rank(A, params.eps, params.b, params.l, params.v, seed, _omega(A))
+    return AdaptiveOutcome(rank, V[:, :rank], g_local[:, :rank], resid, conv)
+
+
+def api_powerlu_fp(A, params, seed):
+    """powerlu_fp(a, params, seed) (rlra/fixedprec.py:152): (LowRankLU,
+    AdaptiveOutcome) or NotConverged."""
+    from .fixedprec import AdaptiveOutcome
+    from .fixedrank import LowRankLU
+
+    rank, V, g_local, resid, conv = adaptive_rank(A, params.eps, params.b, params.l, params.v, seed, _omega(A))
+    out = AdaptiveOutcome(rank, V[:, :rank], g_local[:, :rank], resid, conv)
+    if not conv:
+        raise NotConverged(out)
+    f = lu_from_projection(A, g_local[:, :rank], V[:, :rank])
+    return LowRankLU(f.p, f.q, f.L, f.U, f.rank), out
+
+
+def api_general_power_basis_v(A, l, v, seed):
+    """general_power_basis_v(a, l, v, seed) (rlra/rangefinder.py:144)."""
+    from .rangefinder import RangeBasis
+
+    basis, passes = general_power_basis_v(A, l, v, seed, _omega(A))
+    return RangeBasis(basis, passes)
+
+
+def api_stream_sketch(A, k, seed, panel):
+    """stream_sketch(stream, k, seed, panel) (rlra/singlepass.py:99): H holds
+    this rank's rows."""
+    from .singlepass import SketchPair
+
+    g, h = stream_sketch(A, k, seed, _omega(A), panel)
+    return SketchPair(g, h)
+
+
+def api_single_pass_lu(A, k, seed, q_os, panel):
+    """single_pass_lu(stream, k, seed, q_os, panel) (rlra/singlepass.py:123)."""
+    from .fixedrank import LowRankLU
+
+    f = single_pass_lu(A, k, seed, _omega(A), q_os=q_os, panel=panel)
+    return LowRankLU(f.p, f.q, f.L, f.U, f.rank)

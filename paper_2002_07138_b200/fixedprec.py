@@ -125,6 +125,10 @@ def _adaptive(a, params, seed):
 
 def adaptive_rank(a, params, seed):
     """rlra/fixedprec.py:57-94."""
+    if getattr(a, "is_sharded", False):
+        from .distributed import api_adaptive_rank
+
+        return api_adaptive_rank(a, params, seed)
     host = _host_input(a)
     out = _adaptive(as_accessor(a), params, seed)
     if host:
@@ -135,6 +139,10 @@ def adaptive_rank(a, params, seed):
 
 def powerlu_fp(a, params, seed):
     """rlra/fixedprec.py:152-163: (LowRankLU, AdaptiveOutcome) or NotConverged."""
+    if getattr(a, "is_sharded", False):
+        from .distributed import api_powerlu_fp
+
+        return api_powerlu_fp(a, params, seed)
     host = _host_input(a)
     out = _adaptive(as_accessor(a), params, seed)
     if not out.converged:

@@ -105,7 +105,12 @@ POWERLU_QR = os.environ.get("RLRA_B200_POWERLU_QR", "chol")
 
 
 def powerlu(a, k, q_os=10, v=3, seed=0):
-    """Pass-parameterised randomized LU (rlra/fixedrank.py:120-133)."""
+    """Pass-parameterised randomized LU (rlra/fixedrank.py:120-133).  A
+    distributed.ShardedMatrix runs the row-sharded multi-GPU algorithm."""
+    if getattr(a, "is_sharded", False):
+        from .distributed import api_powerlu
+
+        return api_powerlu(a, k, q_os, v, seed)
     host = _host_input(a)
     a = as_accessor(a)
     _validate_rank(a, k, q_os)

@@ -141,6 +141,10 @@ def lu_basis_(x, checks):
 
 def general_power_basis_v(a, l, v, seed, *, _checks=None, _qr="householder"):
     """rlra/rangefinder.py:144-176; consumes exactly v - 1 passes."""
+    if getattr(a, "is_sharded", False):
+        from .distributed import api_general_power_basis_v
+
+        return api_general_power_basis_v(a, l, v, seed)
     a = as_accessor(a)
     _validate(a, l)
     if v < 2:

@@ -51,7 +51,12 @@ def sweep_width(m, panel):
 
 
 def stream_sketch(stream, k, seed, panel=DEFAULT_PANEL):
-    """rlra/singlepass.py:99-120."""
+    """rlra/singlepass.py:99-120 (a distributed.ShardedMatrix as the stream:
+    the row-sharded sweep)."""
+    if getattr(stream, "is_sharded", False):
+        from .distributed import api_stream_sketch
+
+        return api_stream_sketch(stream, k, seed, panel)
     m, n = stream.shape
     if not 1 <= k <= min(m, n):
         raise ValueError(f"k={k} outside 1..min{(m, n)}")
@@ -81,7 +86,12 @@ def stream_sketch(stream, k, seed, panel=DEFAULT_PANEL):
 
 
 def single_pass_lu(stream, k, seed, q_os=0, panel=DEFAULT_PANEL):
-    """rlra/singlepass.py:123-144."""
+    """rlra/singlepass.py:123-144 (a distributed.ShardedMatrix as the stream:
+    the row-sharded sweep, every rank gets the factors)."""
+    if getattr(stream, "is_sharded", False):
+        from .distributed import api_single_pass_lu
+
+        return api_single_pass_lu(stream, k, seed, q_os, panel)
     host = not isinstance(stream, DeviceColumnStream)  # host streams return NumPy factors
     l = k + q_os
     g, h = stream_sketch(stream, l, seed, panel=panel)

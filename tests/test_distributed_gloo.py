@@ -122,7 +122,20 @@ def _worker(rank, world, port, case, q):
         r0, r1 = D.row_range(m, world, rank)
         ops = OracleOps()
         A = D.ShardedMatrix(ops.upload(a[r0:r1]), m, r0, r1, ops)
-        if case["kind"] == "single_pass":
+        if case["kind"] == "api":
+            # the reference signatures on a ShardedMatrix (rlra/fixedrank.py:120,
+            # rlra/fixedprec.py:152, rlra/singlepass.py:123, rlra/rangefinder.py:144)
+            import paper_2002_07138_b200 as P
+
+            A.omega_fn = O.gaussian
+            f = P.powerlu(A, case["k"], case["q_os"], case["v"], case["seed"])
+            fp, outc = P.powerlu_fp(A, P.PrecisionParams(1e-3, 5, 60, 4), 0)
+            sp = P.single_pass_lu(A, case["k"], case["seed"], q_os=4, panel=16)
+            basis = P.general_power_basis_v(A, 20, 3, 1)
+            out = ([x.numpy().copy() for x in (f.p, f.q, f.L, f.U)], outc.rank, outc.G.shape,
+                   [x.numpy().copy() for x in (fp.p, fp.q)], [x.numpy().copy() for x in (sp.p, sp.q)],
+                   basis.V.numpy().copy(), basis.passes_used)
+        elif case["kind"] == "single_pass":
             f = D.single_pass_lu(A, case["k"], case["seed"], O.gaussian, q_os=case["q_os"], panel=case["panel"])
             out = (f.p.numpy().copy(), f.q.numpy().copy(), f.L.numpy().copy(), f.U.numpy().copy(),
                    A.product_count)
@@ -221,3 +234,21 @@ def test_sharded_single_pass_matches_single_process(world, panel, q_os):
         assert abs(O.rel_fro_error_factor(a, O.LowRankLU(p, q, L, U, k)) - e_ref) <= 1e-12
         assert sweeps == -(-130 // panel)  # one all-reduce per panel, each column read once
     np.testing.assert_array_equal(res[0][2], res[1][2])
+
+
+def test_reference_signatures_accept_a_sharded_matrix():
+    """the multi-GPU path behind the drop-in API."""
+    a = decay_matrix(190, 140, seed=13)
+    res = run_dist({"kind": "api", "a": a, "k": 18, "q_os": 6, "v": 4, "seed": 2})
+    ref = O.powerlu(a, 18, 6, 4, 2)
+    ref_fp, ref_o = O.powerlu_fp(a, 1e-3, 5, 60, 4, 0)
+    ref_sp = O.single_pass_lu(a, 18, 2, q_os=4, panel=16)
+    ref_v = O.general_power_basis_v(a, 20, 3, 1)
+    for rank, (f, r, gshape, fp, sp, v, passes) in res.items():
+        assert np.array_equal(f[0], ref.p) and np.array_equal(f[1], ref.q)
+        assert r == ref_o.rank and gshape[1] == r
+        assert np.array_equal(fp[0], ref_fp.p) and np.array_equal(fp[1], ref_fp.q)
+        assert np.array_equal(sp[0], ref_sp.p) and np.array_equal(sp[1], ref_sp.q)
+        assert passes == ref_v.passes_used
+        # same basis up to column signs
+        assert np.allclose(np.abs(np.sum(v * ref_v.V, axis=0)), 1.0, atol=1e-10)
