@@ -22,6 +22,10 @@ cp -r "$SRC" "$TMP/pkg"
 rm -f "$TMP/pkg/src/rlra/_lu_cython.c"
 rm -rf "$OUT"
 python -m pip install --quiet --no-index --no-build-isolation --no-deps --target "$OUT" "$TMP/pkg"
+# the reference's own test files, next to the build (git-ignored, not
+# committed): tests/test_reference_suite_gpu.py runs them against the B200
+# backend and the aliased hot path on the GPU box, where /root/reference is absent
+cp -r "$SRC/tests" "$OUT/tests"
 python - "$OUT" <<'PY'
 import os, sys
 sys.path.insert(0, sys.argv[1])
