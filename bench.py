@@ -713,7 +713,8 @@ def dist_arm(args):
             sh = cops.empty(r1 - r0, w.n)
             sh.copy_(host_shard.t(), non_blocking=True)
             f = dist_runner(w, v, D.ShardedMatrix(sh, w.m, r0, r1, cops), omega)()
-            return ops.to_numpy_many([f.p, f.q, f.L, f.U]) if rank == 0 else []
+            big_l = f.full_L()  # row blocks of L -> rank 0 (collective)
+            return ops.to_numpy_many([f.p, f.q, big_l, f.U]) if rank == 0 else []
 
         for _ in range(max(2, args.warmup)):
             e2e_step()

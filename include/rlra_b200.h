@@ -179,6 +179,19 @@ RLRA_B200_API int rlra_b200_orgqr(const double* a, int64_t lda, int64_t m, int64
  * max_i R_ii > cond_limit * min_i R_ii (rinv is then zero); it is never
  * cleared.  l <= rlra_b200_chol_inv_max_l() (one CTA, shared memory). */
 RLRA_B200_API int rlra_b200_chol_inv_max_l(void);
+/* Shifted CholeskyQR (sCholQR3's first step, sketches wider than
+ * rlra_b200_chol_inv_max_l are factored by blocks of chol_inv + DMMA GEMMs in
+ * ops.chol_inv_blocked): g_ii += c * trace(g).  Replaces rlra/kernels.py:57-61's
+ * Householder QR for powerlu's final basis (rlra/rangefinder.py:67-70). */
+RLRA_B200_API int rlra_b200_chol_shift_diag(double* g, int64_t ldg, int64_t l, double c, void* stream);
+/* *flag := 1 when max |d_ii| > cond_limit * min |d_ii| (or a zero / non-finite
+ * diagonal entry); never cleared. */
+/* *flag := 1 when max |g_ij - delta_ij| > tol: CholeskyQR's second Gram far
+ * from I means cond(Z) beyond ~u^-1/2 (the diagonal ratio is only a lower bound). */
+RLRA_B200_API int rlra_b200_gram_identity_flag(const double* g, int64_t ldg, int64_t l, double tol, int* flag,
+                                               void* stream);
+RLRA_B200_API int rlra_b200_diag_ratio_flag(const double* d, int64_t ldd, int64_t l, double cond_limit, int* flag,
+                                            void* stream);
 RLRA_B200_API int rlra_b200_chol_inv(double* g, int64_t ldg, int64_t l, double* rinv, int64_t ldr, int* flag,
                                      double cond_limit, void* stream);
 

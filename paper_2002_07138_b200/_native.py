@@ -59,6 +59,9 @@ SIGNATURES = {
     "rlra_b200_geqrf": (_c_i, [_c_p, _c_i64, _c_i64, _c_i64, _c_p, _c_p, _c_sz, _c_p]),
     "rlra_b200_orgqr": (_c_i, [_c_p, _c_i64, _c_i64, _c_i64, _c_p, _c_i64, _c_p, _c_sz, _c_p]),
     "rlra_b200_chol_inv_max_l": (_c_i, []),
+    "rlra_b200_chol_shift_diag": (_c_i, [_c_p, _c_i64, _c_i64, _c_d, _c_p]),
+    "rlra_b200_diag_ratio_flag": (_c_i, [_c_p, _c_i64, _c_i64, _c_d, _c_p, _c_p]),
+    "rlra_b200_gram_identity_flag": (_c_i, [_c_p, _c_i64, _c_i64, _c_d, _c_p, _c_p]),
     "rlra_b200_chol_inv": (_c_i, [_c_p, _c_i64, _c_i64, _c_p, _c_i64, _c_p, _c_d, _c_p]),
     "rlra_b200_trsm_workspace": (_c_sz, [_c_i64, _c_i64]),
     "rlra_b200_trsm_rt": (_c_i, [_c_p, _c_i64, _c_i64, _c_p, _c_i64, _c_i64, _c_p, _c_sz, _c_p]),

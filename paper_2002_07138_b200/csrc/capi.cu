@@ -108,6 +108,9 @@ int colsumsq(const double* a, int64_t lda, int64_t m, int64_t n, double* out_dev
 int transpose(const double* in, int64_t ldi, int64_t m, int64_t n, double* out, int64_t ldo,
               cudaStream_t st);
 int chol_inv_max_l();
+int chol_shift_diag(double* g, int64_t ldg, int64_t l, double c, cudaStream_t st);
+int diag_ratio_flag(const double* d, int64_t ldd, int64_t l, double cond_limit, int* flag, cudaStream_t st);
+int gram_identity_flag(const double* g, int64_t ldg, int64_t l, double tol, int* flag, cudaStream_t st);
 int chol_inv(double* g, int64_t ldg, int64_t l, double* x, int64_t ldx, int* flag, double cond_limit,
              cudaStream_t st);
 size_t oz_prep_workspace(int64_t m, int64_t n, int nmod);
@@ -256,6 +259,19 @@ int rlra_b200_lu_extract(const double* lu, int64_t ldlu, int64_t m, int64_t n, d
 }
 
 int rlra_b200_chol_inv_max_l(void) { return chol_inv_max_l(); }
+
+int rlra_b200_chol_shift_diag(double* g, int64_t ldg, int64_t l, double c, void* stream) {
+  return chol_shift_diag(g, ldg, l, c, static_cast<cudaStream_t>(stream));
+}
+
+int rlra_b200_gram_identity_flag(const double* g, int64_t ldg, int64_t l, double tol, int* flag, void* stream) {
+  return gram_identity_flag(g, ldg, l, tol, flag, static_cast<cudaStream_t>(stream));
+}
+
+int rlra_b200_diag_ratio_flag(const double* d, int64_t ldd, int64_t l, double cond_limit, int* flag,
+                              void* stream) {
+  return diag_ratio_flag(d, ldd, l, cond_limit, flag, static_cast<cudaStream_t>(stream));
+}
 
 int rlra_b200_chol_inv(double* g, int64_t ldg, int64_t l, double* rinv, int64_t ldr, int* flag,
                        double cond_limit, void* stream) {

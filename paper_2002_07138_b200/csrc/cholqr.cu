@@ -17,6 +17,8 @@
 // chol_kernel: one CTA, the l x l matrix packed (upper triangle) in shared
 // memory, blocked right-looking Cholesky G = R^T R; R (packed) replaces G.
 // inv_upper_kernel: X = R^{-1}, one warp per column, ceil(l/16) CTAs.
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace rlra {
@@ -304,6 +306,96 @@ __global__ void __launch_bounds__(INV_COLS * 32, 1)
     const int i = lane + 32 * q;
     if (i < l) x[i + (int64_t)j * ldx] = (i <= j) ? a[q] : 0.0;
   }
+}
+
+// Shifted CholeskyQR (Fukaya, Kannan, Nakatsukasa, Yamamoto, Yanagisawa 2020):
+// G + s I with s = c * trace(G) (trace(Z^T Z) = ||Z||_F^2 >= ||Z||_2^2), so
+// the Cholesky of the first step of sCholQR3 succeeds for cond(Z) up to ~u^-1.
+// One CTA: fixed-order trace reduction, then the diagonal update.
+__global__ void __launch_bounds__(256) shift_diag_kernel(double* __restrict__ g, int64_t ldg, int l, double c) {
+  __shared__ double red[8];
+  double t = 0.0;
+  for (int i = threadIdx.x; i < l; i += 256) t += g[i + (int64_t)i * ldg];
+#pragma unroll
+  for (int o = 16; o; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = t;
+  __syncthreads();
+  double tr = 0.0;
+#pragma unroll
+  for (int w = 0; w < 8; ++w) tr += red[w];
+  const double s = c * tr;
+  for (int i = threadIdx.x; i < l; i += 256) g[i + (int64_t)i * ldg] += s;
+}
+
+// flag := 1 when max_i |d_ii| > cond_limit * min_i |d_ii| (or a zero / NaN
+// diagonal): the condition bound of a blocked Cholesky across its blocks (the
+// one-CTA kernel checks it inside a block).
+__global__ void __launch_bounds__(256) diag_ratio_flag_kernel(const double* __restrict__ d, int64_t ldd, int l,
+                                                              double cond_limit, int* __restrict__ flag) {
+  __shared__ double rmax[8], rmin[8];
+  double mx = 0.0, mn = __longlong_as_double(0x7FF0000000000000ll);
+  bool bad = false;
+  for (int i = threadIdx.x; i < l; i += 256) {
+    const double v = fabs(d[i + (int64_t)i * ldd]);
+    bad |= !(v > 0.0) || !(v <= 1.7976931348623157e308);
+    mx = fmax(mx, v);
+    mn = fmin(mn, v);
+  }
+  bad = __syncthreads_or(bad);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    rmax[threadIdx.x >> 5] = mx;
+    rmin[threadIdx.x >> 5] = mn;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 0; w < 8; ++w) {
+      mx = fmax(mx, rmax[w]);
+      mn = fmin(mn, rmin[w]);
+    }
+    if (bad || !(mx <= cond_limit * mn)) atomicExch(flag, 1);
+  }
+}
+
+// flag := 1 when max_ij |g_ij - delta_ij| > tol (or non-finite): the Gram of
+// CholeskyQR's first Q deviates from I by ~u cond(Z)^2, so this declines
+// sketches beyond ~u^-1/2 whatever their R diagonal ratio says.
+__global__ void __launch_bounds__(256) gram_identity_flag_kernel(const double* __restrict__ g, int64_t ldg, int l,
+                                                                 double tol, int* __restrict__ flag) {
+  bool bad = false;
+  const int64_t total = (int64_t)l * l;
+  for (int64_t e = (int64_t)blockIdx.x * 256 + threadIdx.x; e < total; e += (int64_t)gridDim.x * 256) {
+    const int i = (int)(e % l), j = (int)(e / l);
+    const double d = fabs(g[i + (int64_t)j * ldg] - (i == j ? 1.0 : 0.0));
+    bad |= !(d <= tol);
+  }
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicExch(flag, 1);
+}
+
+int gram_identity_flag(const double* g, int64_t ldg, int64_t l, double tol, int* flag, cudaStream_t st) {
+  RLRA_REQUIRE(l >= 1 && ldg >= l && flag, "gram_identity_flag: bad arguments");
+  const int64_t blocks = std::min<int64_t>(ceil_div(l * l, 256), 148);
+  gram_identity_flag_kernel<<<(unsigned)blocks, 256, 0, st>>>(g, ldg, (int)l, tol, flag);
+  RLRA_LAUNCHED();
+  return 0;
+}
+
+int chol_shift_diag(double* g, int64_t ldg, int64_t l, double c, cudaStream_t st) {
+  RLRA_REQUIRE(l >= 1 && ldg >= l, "chol_shift_diag: bad shape");
+  shift_diag_kernel<<<1, 256, 0, st>>>(g, ldg, (int)l, c);
+  RLRA_LAUNCHED();
+  return 0;
+}
+
+int diag_ratio_flag(const double* d, int64_t ldd, int64_t l, double cond_limit, int* flag, cudaStream_t st) {
+  RLRA_REQUIRE(l >= 1 && ldd >= l && flag, "diag_ratio_flag: bad arguments");
+  diag_ratio_flag_kernel<<<1, 256, 0, st>>>(d, ldd, (int)l, cond_limit, flag);
+  RLRA_LAUNCHED();
+  return 0;
 }
 
 int chol_inv_max_l() {

@@ -27,10 +27,11 @@ DEFAULT_PANEL = 256  # rlra/singlepass.py:19
 # FP64 DMMA GEMM (csrc/gemm_tma.cu).
 PASS_GEMM = os.environ.get("RLRA_B200_PASS_GEMM", "oz")
 OZ_MAX_K = 133144
-# residues take nmod bytes per element of A (14 B vs 8 B of float64); larger
-# operands (C5: 68.7 GB A would need 120 GB of residues) use block-wise
-# residues (ops.OzBlocked), bit-identical to the one-block product
-OZ_MAX_RESIDUE_BYTES = int(os.environ.get("RLRA_B200_OZ_MAX_BYTES", str(48 << 30)))
+# residues take nmod bytes per element of A (14 B vs 8 B of float64); operands
+# whose residues do not fit in the free HBM (ops.oz_residue_budget; C5 on one
+# GPU: 120 GB next to its 68.7 GB A) use block-wise residues (ops.OzBlocked),
+# bit-identical to the one-block product
+OZ_MAX_RESIDUE_BYTES = None  # None: ops.oz_residue_budget (free memory); RLRA_B200_OZ_MAX_BYTES overrides
 
 
 _ENGINE = [None]  # per-call override of PASS_GEMM (pass_engine)

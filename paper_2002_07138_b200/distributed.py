@@ -138,6 +138,46 @@ class CudaOps:
     def transpose(self, a):
         return self.o.transpose(a)
 
+    def chol_inv(self, g, cond_limit, flag=None):
+        """R^{-1} of chol(g) (upper, any l: blocked beyond the one-CTA kernel)
+        and the device decline flag (csrc/cholqr.cu)."""
+        l = g.shape[0]
+        if flag is None:
+            flag = torch.zeros(1, dtype=torch.int32, device=self.device)
+        rinv = self.o.fmat(l, l, self.device)
+        self.o.chol_inv_blocked(g, rinv, flag, cond_limit)
+        return rinv, flag
+
+    def shift_gram(self, g, n, flag):
+        """sCholQR3's first step: flag an exactly zero column, g += s I."""
+        l = g.shape[0]
+        st = self.o._stream(self.device)
+        self.o._call("rlra_b200_diag_ratio_flag", self.device, self.o.ptr(g), self.o.ld_of(g), l,
+                     self.o.NO_COND_LIMIT, self.o.ptr(flag), st)
+        self.o._call("rlra_b200_chol_shift_diag", self.device, self.o.ptr(g), self.o.ld_of(g), l,
+                     self.o.SCHOL_C * (n * l + l * (l + 1)), st)
+
+    def gram_identity_flag(self, g, flag):
+        self.o.gram_identity_flag(g, flag)
+
+    def cholqr_wide(self, l):
+        return l > self.o.cholqr_max_l()
+
+    def cholqr_ok(self, x):
+        return x.shape[0] >= x.shape[1] > 0
+
+    def qr_qr(self, x):
+        """Householder Q (m x l) and R (l x l) of x (destroyed)."""
+        qr = self.o.QR(x)
+        _, r = self.o.lu_extract(qr.r_view(), want_l=False)
+        return qr.q(), r
+
+    def flag_value(self, flag):
+        return int(flag.item())
+
+    def nonzero_diag(self, r):
+        return self.o.count_nonzero_diag(r)
+
     def sumsq(self, a):
         return self.o.sumsq(a)
 
@@ -158,11 +198,42 @@ class CudaOps:
 
 @dataclass
 class DistLU:
+    """Factors of a distributed call: p, q, U replicated on every rank; L
+    row-sharded by position -- this rank holds rows [l0, l1) of the m x k L
+    (L = L1 U2^T is the largest GEMM of the assembly, 2 m k^2 flops: each rank
+    forms only its block).  full_L() all-gathers it."""
     p: object
     q: object
     L: object
     U: object
     rank: int
+    l0: int = 0
+    l1: int = -1
+    m: int = 0
+    group: object = None
+    ops: object = None
+
+    @property
+    def sharded(self):
+        return self.l1 >= 0 and (self.l0, self.l1) != (0, self.m)
+
+    def full_L(self):
+        if not self.sharded:
+            return self.L
+        world = dist.get_world_size(self.group)
+        k = self.L.shape[1]
+        per = -(-self.m // world)
+        buf = torch.zeros((k, per), dtype=self.L.dtype, device=self.L.device)
+        if self.l1 > self.l0:
+            buf[:, : self.l1 - self.l0].copy_(self.L.t())
+        out = [torch.empty_like(buf) for _ in range(world)]
+        dist.all_gather(out, buf, group=self.group)
+        full = self.ops.empty(self.m, k)
+        for r in range(world):
+            a0, a1 = row_range(self.m, world, r)
+            if a1 > a0:
+                full[a0:a1, :].copy_(out[r][:, : a1 - a0].t())
+        return full
 
 
 class ShardedMatrix:
@@ -326,13 +397,24 @@ def general_power_basis_v(A: ShardedMatrix, l, v, seed, omega_fn, fast_qr=False)
         _check(cnt, l)
         return A.local_rows(ops.lu_basis(full, piv))
 
+    n_rows = A.shape[1]
+    shard = SHARD_REPLICATED and _block_ok(A, n_rows, l)
+
     def lu_basis_repl(z):
+        # the tournament only pays for very tall sketches: its local and
+        # candidate GEPPs are latency bound like the replicated one
+        # (profiles/r02_time_getrf.txt: 4096 x 544 and 32768 x 544 both ~2-4 ms)
+        if shard and _use_tslu(A, l) and n_rows > REPL_TSLU_MIN_ROWS:
+            return sharded_lu_basis(A, z, l)
         piv, cnt = ops.getrf_(z)
         _check(cnt, l)
         return ops.lu_basis(z, piv)
 
     def qr_basis(z):
-        q, cnt = (ops.qr_q_fast if fast_qr and hasattr(ops, "qr_q_fast") else ops.qr_q)(z)
+        if shard and fast_qr:
+            q, cnt = sharded_qr_basis(A, z)
+        else:
+            q, cnt = (ops.qr_q_fast if fast_qr and hasattr(ops, "qr_q_fast") else ops.qr_q)(z)
         if cnt is not None:
             _check(cnt, l)
         return q
@@ -365,8 +447,28 @@ def general_power_basis_v(A: ShardedMatrix, l, v, seed, omega_fn, fast_qr=False)
     return basis, passes
 
 
+SHARD_L = os.environ.get("RLRA_B200_DIST_SHARD_L", "1") == "1"
+
+
+def _assemble(A, l1, u2, l2, piv1, piv2, k, cut=None):
+    """L = L1 U2^T (row block of this rank when SHARD_L), U = L2^T."""
+    ops = A.ops
+    m = l1.shape[0]
+    if SHARD_L and A.world > 1:
+        p0, p1 = row_range(m, A.world, A.rank)
+        big_l = ops.matmul(l1[p0:p1], u2, tb=True)
+    else:
+        p0, p1 = 0, m
+        big_l = ops.matmul(l1, u2, tb=True)
+    big_u = ops.transpose(l2)
+    if cut is not None:
+        big_l, big_u = big_l[:, :cut], big_u[:cut, :]
+    return DistLU(piv1, piv2, big_l, big_u, k, p0, p1, m, A.group, ops)
+
+
 def lu_from_projection(A: ShardedMatrix, g_local, vk):
-    """rlra/fixedrank.py:136-146 with G gathered for the exact GEPP."""
+    """rlra/fixedrank.py:136-146 with G gathered for the exact GEPP (p, q
+    identical to one GPU); L = L1 U2^T formed by row blocks (DistLU)."""
     ops = A.ops
     k = g_local.shape[1]
     g = A.gather_rows(g_local)
@@ -375,10 +477,106 @@ def lu_from_projection(A: ShardedMatrix, g_local, vk):
     bt = ops.matmul(vk, u1, tb=True)
     piv2, _ = ops.getrf_(bt)
     l2, u2 = ops.lu_extract(bt)
-    big_l = ops.matmul(l1, u2, tb=True)
-    big_u = ops.transpose(l2)
-    return DistLU(piv1, piv2, big_l, big_u, k)
+    return _assemble(A, l1, u2, l2, piv1, piv2, k)
 
+
+
+# ---------------------------------------------------------------- sharded factorizations of replicated sketches
+# Z = A^T W is replicated after its all-reduce (n x l).  Its factorizations run
+# on row blocks of Z, one per rank, instead of redundantly on every rank
+# (the replicated n x l QR / LU capped the 8-GPU efficiency).
+def _row_block(A, rows):
+    return row_range(rows, A.world, A.rank)
+
+
+def _all_gather_rows(A, local, rows):
+    """Column-major (rows x w) from the ranks' row blocks (row_range(rows))."""
+    w = local.shape[1]
+    per = -(-rows // A.world)
+    buf = torch.zeros((w, per), dtype=local.dtype, device=local.device)
+    if local.shape[0]:
+        buf[:, :local.shape[0]].copy_(local.t())
+    out = [torch.empty_like(buf) for _ in range(A.world)]
+    dist.all_gather(out, buf, group=A.group)
+    full = A.ops.empty(rows, w)
+    for r in range(A.world):
+        a0, a1 = row_range(rows, A.world, r)
+        if a1 > a0:
+            full[a0:a1, :].copy_(out[r][:, : a1 - a0].t())
+    return full
+
+
+def _block_ok(A, rows, l):
+    """Every rank's row block of a rows x l matrix has at least l rows."""
+    return A.world > 1 and rows // A.world >= l and row_range(rows, A.world, A.world - 1)[1] - \
+        row_range(rows, A.world, A.world - 1)[0] >= l
+
+
+def sharded_qr_basis(A, z):
+    """Orthonormal basis of range(z), z replicated n x l, computed on row
+    blocks: CholeskyQR2 with all-reduced l x l Grams (Q_r = Z_r R^{-1}, twice),
+    then one all-gather of Q.  When the Cholesky declines (cond(Z) beyond its
+    bound -- the decision is identical on every rank, the Gram is replicated),
+    TSQR: local Householder QR of each block, the stacked R factors
+    all-gathered and factored, Q_r = Q_r,local Q_s[r].  Same range and column
+    signs up to +-1 as the Householder Q of the whole z (which no powerlu
+    output depends on).  Returns (Q replicated, nonzero-diagonal count or None)."""
+    ops = A.ops
+    n, l = z.shape
+    c0, c1 = _row_block(A, n)
+    zr = z[c0:c1]
+    if hasattr(ops, "chol_inv") and ops.cholqr_ok(z):
+        from .ops import CHOLQR_COND
+
+        # CholeskyQR2, or shifted CholeskyQR3 for sketches wider than the
+        # one-CTA Cholesky (ops.scholqr3): all-reduced Grams, local Q_r updates
+        wide = ops.cholqr_wide(l)
+        steps = [(True, 1e300), (False, 1e7), (False, 2.0)] if wide else [(False, CHOLQR_COND), (False, 2.0)]
+        flag = _new_flag(z)
+        q = zr
+        for i, (shifted, limit) in enumerate(steps):
+            g = ops.matmul(q, q, ta=True)
+            dist.all_reduce(g.t(), op=dist.ReduceOp.SUM, group=A.group)
+            if shifted:
+                ops.shift_gram(g, n, flag)
+            if i == len(steps) - 1:
+                ops.gram_identity_flag(g, flag)
+            rinv, flag = ops.chol_inv(g, limit, flag)
+            q = ops.matmul(q, rinv)
+        if not ops.flag_value(flag):
+            return _all_gather_rows(A, q, n), None
+    # TSQR
+    work = ops.empty(c1 - c0, l)
+    work.copy_(zr)
+    q_loc, r_loc = ops.qr_qr(work)
+    rs = [torch.empty((l, l), dtype=z.dtype, device=z.device) for _ in range(A.world)]
+    dist.all_gather(rs, r_loc.contiguous(), group=A.group)  # R_r, row-major
+    stacked = ops.empty(A.world * l, l)
+    stacked.copy_(torch.cat(rs, 0))
+    q_s, r = ops.qr_qr(stacked)
+    q_r = ops.matmul(q_loc, q_s[A.rank * l:(A.rank + 1) * l])
+    return _all_gather_rows(A, q_r, n), ops.nonzero_diag(r)
+
+
+def _new_flag(like):
+    return torch.zeros(1, dtype=torch.int32, device=like.device)
+
+
+def sharded_lu_basis(A, z, l):
+    """Interior LU basis of a REPLICATED n x l sketch by tournament pivoting
+    over row blocks (like tslu_basis_rows for the row-sharded m x l sketch):
+    local GEPP of Z_r names l candidates, one all-gather of the world*l x l
+    candidates, a redundant GEPP gives U, W_r = Z_r U^{-1}, W all-gathered.
+    W = Z U^{-1} with U upper triangular."""
+    n = z.shape[0]
+    c0, c1 = _row_block(A, n)
+    sub = ShardedMatrix(z[c0:c1], n, c0, c1, A.ops, A.group)
+    w_r = tslu_basis_rows(sub, z[c0:c1], l)
+    return _all_gather_rows(A, w_r, n)
+
+
+SHARD_REPLICATED = os.environ.get("RLRA_B200_DIST_SHARD_REPL", "1") == "1"  # 0: redundant n x l QR / LU
+REPL_TSLU_MIN_ROWS = int(os.environ.get("RLRA_B200_DIST_REPL_TSLU_ROWS", "131072"))
 
 def powerlu(A: ShardedMatrix, k, q_os=10, v=3, seed=0, omega_fn=None):
     """rlra/fixedrank.py:120-133 over a row-sharded A; every rank returns the
@@ -492,12 +690,7 @@ def single_pass_lu(A: ShardedMatrix, k, seed, omega_fn, q_os=0, panel=256):
     t = ops.pinv_transpose_apply(g, ops.transpose(u1))
     piv2, _ = ops.getrf_(t)
     l2, u2 = ops.lu_extract(t)
-    big_l = ops.matmul(l1, u2, tb=True)
-    big_u = ops.transpose(l2)
-    if q_os:
-        big_l = big_l[:, :k]
-        big_u = big_u[:k, :]
-    return DistLU(piv1, piv2, big_l, big_u, k)
+    return _assemble(A, l1, u2, l2, piv1, piv2, k, cut=k if q_os else None)
 
 
 # ---------------------------------------------------------------- drop-in API glue
@@ -535,7 +728,7 @@ def api_powerlu(A, k, q_os, v, seed):
     from .fixedrank import LowRankLU
 
     f = powerlu(A, k, q_os, v, seed, _omega(A))
-    return LowRankLU(f.p, f.q, f.L, f.U, f.rank)
+    return LowRankLU(f.p, f.q, f.full_L(), f.U, f.rank)
 
 
 def api_adaptive_rank(A, params, seed):
@@ -558,7 +751,7 @@ def api_powerlu_fp(A, params, seed):
     if not conv:
         raise NotConverged(out)
     f = lu_from_projection(A, g_local[:, :rank], V[:, :rank])
-    return LowRankLU(f.p, f.q, f.L, f.U, f.rank), out
+    return LowRankLU(f.p, f.q, f.full_L(), f.U, f.rank), out
 
 
 def api_general_power_basis_v(A, l, v, seed):
@@ -583,4 +776,4 @@ def api_single_pass_lu(A, k, seed, q_os, panel):
     from .fixedrank import LowRankLU
 
     f = single_pass_lu(A, k, seed, _omega(A), q_os=q_os, panel=panel)
-    return LowRankLU(f.p, f.q, f.L, f.U, f.rank)
+    return LowRankLU(f.p, f.q, f.full_L(), f.U, f.rank)

@@ -11,6 +11,7 @@ sqrt(sum)**2, refinement by per-column `col @ col`).
 from __future__ import annotations
 
 import math
+import os
 from dataclasses import dataclass, replace
 from typing import Any
 
@@ -105,14 +106,26 @@ def scan_energies(total, col_energy, eps, b, l):
     return l, max(e, 0.0), False
 
 
+# Final basis of powerlu_fp: "chol" (CholeskyQR2 / shifted CholeskyQR3, the
+# Householder redo when it declines) or "householder".
+POWERLU_FP_QR = os.environ.get("RLRA_B200_POWERLU_FP_QR", "chol")
+
+
 def _adaptive(a, params, seed):
     m, n = a.shape
     if params.l > min(m, n):
         raise ValueError(f"sketch width {params.l} exceeds min{(m, n)}")
     checks = RankChecks()
     with product_session(a):
-        basis = general_power_basis_v(a, params.l, params.v, seed, _checks=checks)
-        g = a.matmul(basis.V)
+        basis = general_power_basis_v(a, params.l, params.v, seed, _checks=checks, _qr=POWERLU_FP_QR)
+        V = basis.V
+        g = a.matmul(V)
+        declined = checks.cholqr_declined()  # one host round trip (the counts ride along)
+        if declined is not None and declined[0]:  # rare: Householder basis, then G again
+            from .rangefinder import qr_basis_
+
+            V = qr_basis_(declined[1], checks, "householder")
+            g = a.matmul(V)
     fro2 = a.fro_norm_sq_device()
     energies = ops.colsumsq(g)
     checks.raise_if_collapsed()
@@ -120,7 +133,7 @@ def _adaptive(a, params, seed):
     # total = fro_norm(a) ** 2 (rlra/fixedprec.py:72): norm then square, as there
     total = math.sqrt(float(host[0])) ** 2
     rank, resid, conv = scan_energies(total, host[1:], params.eps, params.b, params.l)
-    return AdaptiveOutcome(rank, basis.V[:, :rank], g[:, :rank], resid, conv)
+    return AdaptiveOutcome(rank, V[:, :rank], g[:, :rank], resid, conv)
 
 
 def adaptive_rank(a, params, seed):

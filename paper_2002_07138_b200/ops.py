@@ -320,8 +320,7 @@ class OzBlocked:
         if cache_bytes is None:
             free, _ = torch.cuda.mem_get_info(dev)
             free += torch.cuda.memory_reserved(dev) - torch.cuda.memory_allocated(dev)  # allocator cache
-            reserve = int(os.environ.get("RLRA_B200_OZ_RESERVE_BYTES", str(12 << 30)))
-            cache_bytes = free - reserve
+            cache_bytes = free - OZ_RESERVE_BYTES
         total = sum(self.block_ws.values())
         if total > cache_bytes:
             cache_bytes -= biggest  # room for the scratch block
@@ -382,9 +381,27 @@ class OzBlocked:
         return c
 
 
-def oz_engine(a, max_residue_bytes):
+OZ_RESERVE_BYTES = int(os.environ.get("RLRA_B200_OZ_RESERVE_BYTES", str(12 << 30)))
+
+
+def oz_residue_budget(device):
+    """Bytes the residues of one operand may take: RLRA_B200_OZ_MAX_BYTES, else
+    the device's free memory (allocator cache included) minus a reserve for the
+    sketches and workspaces (C5 on one GPU: 120 GB of residues next to its
+    68.7 GB A do not fit -> block-wise; a C5 row shard at 2+ GPUs does)."""
+    env = os.environ.get("RLRA_B200_OZ_MAX_BYTES")
+    if env:
+        return int(env)
+    free, _ = torch.cuda.mem_get_info(device)
+    free += torch.cuda.memory_reserved(device) - torch.cuda.memory_allocated(device)
+    return max(0, free - OZ_RESERVE_BYTES)
+
+
+def oz_engine(a, max_residue_bytes=None):
     """OzPrep when the residues of all of A fit (and K is in range), else OzBlocked."""
     m, n = a.shape
+    if max_residue_bytes is None:
+        max_residue_bytes = oz_residue_budget(a.device)
     if max(m, n) <= OZ_BLOCK_K and OZ_NMOD * m * n <= max_residue_bytes:
         return OzPrep(a)
     return OzBlocked(a)
@@ -463,6 +480,77 @@ def chol_inv(g, out, flag, cond_limit):
     return out
 
 
+def _diag_blocks(l, cap):
+    nb = max(1, -(-l // cap))
+    step = -(-l // nb)
+    return [(j, min(l, j + step)) for j in range(0, l, step)]
+
+
+def chol_inv_blocked(g, out, flag, cond_limit):
+    """out = chol(g)^{-1} (upper) for any l; g (full symmetric) is consumed.
+
+    l <= chol_inv_max_l: the one-CTA kernel.  Wider: diagonal blocks by the
+    one-CTA kernel (R_JJ^{-1}, condition bound inside the block), block rows
+    R_J,rest = R_JJ^{-T} G_J,rest and trailing updates G_rest -= R_J,rest^T
+    R_J,rest on the DMMA GEMM, then R^{-1} assembled block column by block
+    column (Rinv_0J = -Rinv_00 R_0J Rinv_JJ) and the condition bound across
+    blocks on its diagonal (|Rinv_ii| = 1 / |R_ii|)."""
+    l = g.shape[0]
+    cap = cholqr_max_l()
+    if l <= cap:
+        return chol_inv(g, out, flag, cond_limit)
+    dev = g.device
+    blocks = _diag_blocks(l, cap)
+    r = fmat(l, l, dev, zero=True)  # off-diagonal blocks of R
+    out.zero_()
+    for j0, j1 in blocks:
+        gjj = fmat(j1 - j0, j1 - j0, dev)
+        gjj.copy_(g[j0:j1, j0:j1])
+        chol_inv(gjj, out[j0:j1, j0:j1], flag, cond_limit)
+        if j1 < l:
+            gemm(out[j0:j1, j0:j1], g[j0:j1, j1:], r[j0:j1, j1:], ta=True)
+            gemm(r[j0:j1, j1:], r[j0:j1, j1:], g[j1:, j1:], ta=True, alpha=-1.0, beta=1.0)
+    for j0, j1 in blocks[1:]:
+        t = matmul(out[:j0, :j0], r[:j0, j0:j1])
+        gemm(t, out[j0:j1, j0:j1], out[:j0, j0:j1], alpha=-1.0)
+    _call("rlra_b200_diag_ratio_flag", dev, ptr(out), ld_of(out), l, float(cond_limit), ptr(flag), _stream(dev))
+    return out
+
+
+SCHOL_C = 11.0 * 2.0 ** -53  # shift constant of shifted CholeskyQR (Fukaya et al. 2020)
+NO_COND_LIMIT = 1e300
+
+
+def scholqr3(z):
+    """Orthonormal basis of range(z) by shifted CholeskyQR3 (csrc/cholqr.cu
+    notes): step 1 factors Z^T Z + s I, s = 11 (n l + l (l + 1)) u ||Z||_F^2,
+    which succeeds for cond(Z) up to ~u^-1 and leaves cond(Q1) ~ 1e4; steps 2
+    and 3 are CholeskyQR2 on Q1 with the usual condition bounds.  All six
+    products are DMMA GEMMs, the factorizations blocked Choleskys (any l).
+    The device flag is raised when step 2 or 3 declines, or when z has an
+    exactly zero column (the structural rank collapse the reference's
+    Householder R reports as an exact zero diagonal, rlra/rangefinder.py:55-64):
+    the caller then redoes the basis on the Householder path."""
+    n, l = z.shape
+    dev = z.device
+    flag = torch.zeros(1, dtype=torch.int32, device=dev)
+    with label("scholqr3"):
+        # exactly zero column -> flag (diag_ratio_flag sees a zero diagonal of Z^T Z)
+        q = z
+        for step, limit in enumerate((NO_COND_LIMIT, 1e7, 2.0)):
+            g = matmul(q, q, ta=True)
+            if step == 0:
+                _call("rlra_b200_diag_ratio_flag", dev, ptr(g), ld_of(g), l, NO_COND_LIMIT, ptr(flag), _stream(dev))
+                _call("rlra_b200_chol_shift_diag", dev, ptr(g), ld_of(g), l,
+                      SCHOL_C * (n * l + l * (l + 1)), _stream(dev))
+            if step == 2:
+                gram_identity_flag(g, flag)
+            rinv = fmat(l, l, dev)
+            chol_inv_blocked(g, rinv, flag, limit)
+            q = matmul(q, rinv)
+    return q, flag
+
+
 def cholqr2(z):
     """Orthonormal basis of range(z) by CholeskyQR2 (csrc/cholqr.cu) and a device
     int32 flag that is 1 when the Cholesky declined (rank collapse or cond(z)
@@ -476,9 +564,18 @@ def cholqr2(z):
         chol_inv(g, rinv, flag, CHOLQR_COND)
         q1 = matmul(z, rinv)
         g2 = matmul(q1, q1, ta=True)
+        gram_identity_flag(g2, flag)  # cond(Z) beyond ~u^-1/2 whatever the diagonal ratio said
         chol_inv(g2, rinv, flag, 2.0)
         q = matmul(q1, rinv)
     return q, flag
+
+
+GRAM_IDENTITY_TOL = 0.1
+
+
+def gram_identity_flag(g, flag, tol=GRAM_IDENTITY_TOL):
+    _call("rlra_b200_gram_identity_flag", g.device, ptr(g), ld_of(g), g.shape[0], float(tol), ptr(flag),
+          _stream(g.device))
 
 
 class QR:

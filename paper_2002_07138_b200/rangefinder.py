@@ -123,8 +123,15 @@ def qr_basis_(x, checks, method="householder"):
     host sync at the end of the driver) and the caller redoes the basis on the
     Householder path if it was raised -- rank collapse keeps the reference's
     exception there.  method="householder_now": Householder unconditionally."""
-    if method == "chol" and x.shape[0] >= x.shape[1] and 0 < x.shape[1] <= ops.cholqr_max_l():
-        q, flag = ops.cholqr2(x)
+    if method == "chol" and x.shape[0] >= x.shape[1] > 0:
+        # CholeskyQR2 for l <= chol_inv_max_l (one-CTA Cholesky); wider sketches
+        # (C3 l = 1024, C5 l = 544, whose cond(Z) reaches 1e9+) by shifted
+        # CholeskyQR3 with blocked Choleskys -- Householder panels are latency
+        # bound (one cluster exchange per column, 13-17 ms at those widths)
+        if x.shape[1] <= ops.cholqr_max_l():
+            q, flag = ops.cholqr2(x)
+        else:
+            q, flag = ops.scholqr3(x)
         checks.defer_cholqr(flag, x)
         return q
     qr = ops.QR(x)
@@ -149,6 +156,8 @@ def general_power_basis_v(a, l, v, seed, *, _checks=None, _qr="householder"):
     _validate(a, l)
     if v < 2:
         raise ValueError("pass budget v must be >= 2")
+    if _qr == "chol" and _checks is None:
+        _qr = "householder"  # the CholeskyQR decline flag needs a caller that resolves it
     checks = _checks if _checks is not None else RankChecks()
     m, n = a.shape
     dev = a.device

@@ -45,6 +45,51 @@ class OracleOps:
         t.zero_()
         return t
 
+    # sharded factorizations of the replicated sketches (CholeskyQR2 / TSQR)
+    decline = False  # force the CholeskyQR2 decline -> TSQR path
+
+    def chol_inv(self, g, cond_limit, flag=None):
+        flag = torch.zeros(1, dtype=torch.int32) if flag is None else flag
+        gn = g.numpy()
+        try:
+            r = np.linalg.cholesky(gn).T
+            d = np.abs(np.diag(r))
+            if self.decline or d.max() > cond_limit * d.min():
+                raise np.linalg.LinAlgError
+            return self.upload(np.linalg.inv(r)), flag
+        except np.linalg.LinAlgError:
+            flag[0] = 1
+            return self.upload(np.zeros_like(gn)), flag
+
+    def cholqr_ok(self, x):
+        return x.shape[0] >= x.shape[1] > 0
+
+    wide_at = 10 ** 9  # sketches wider than this take the shifted CholeskyQR3 steps
+
+    def cholqr_wide(self, l):
+        return l > self.wide_at
+
+    def shift_gram(self, g, n, flag):
+        gn = g.numpy()
+        l = gn.shape[0]
+        if np.any(np.diag(gn) == 0):
+            flag[0] = 1
+        g += torch.eye(l, dtype=torch.float64) * (11.0 * 2.0 ** -53 * (n * l + l * (l + 1)) * np.trace(gn))
+
+    def gram_identity_flag(self, g, flag):
+        if np.abs(g.numpy() - np.eye(g.shape[0])).max() > 0.1:
+            flag[0] = 1
+
+    def flag_value(self, flag):
+        return int(flag[0])
+
+    def qr_qr(self, x):
+        q, r = np.linalg.qr(x.numpy())
+        return self.upload(q), self.upload(r)
+
+    def nonzero_diag(self, r):
+        return torch.tensor([int(np.count_nonzero(np.diag(r.numpy())))])
+
     def sweep_products(self, block, prep, x, out, ta, add):
         r = (block.t() @ x) if ta else (block @ x)
         if add:
@@ -116,11 +161,14 @@ def _worker(rank, world, port, case, q):
     from paper_2002_07138_b200 import distributed as D
 
     D.INTERIOR = case.get("interior", "tslu")
+    D.REPL_TSLU_MIN_ROWS = case.get("repl_tslu_min_rows", 0)  # exercise the sharded n x l tournament on small cases
     try:
         a = case["a"]
         m = a.shape[0]
         r0, r1 = D.row_range(m, world, rank)
         ops = OracleOps()
+        ops.decline = case.get("decline", False)
+        ops.wide_at = case.get("wide_at", 10 ** 9)
         A = D.ShardedMatrix(ops.upload(a[r0:r1]), m, r0, r1, ops)
         if case["kind"] == "api":
             # the reference signatures on a ShardedMatrix (rlra/fixedrank.py:120,
@@ -137,15 +185,15 @@ def _worker(rank, world, port, case, q):
                    basis.V.numpy().copy(), basis.passes_used)
         elif case["kind"] == "single_pass":
             f = D.single_pass_lu(A, case["k"], case["seed"], O.gaussian, q_os=case["q_os"], panel=case["panel"])
-            out = (f.p.numpy().copy(), f.q.numpy().copy(), f.L.numpy().copy(), f.U.numpy().copy(),
+            out = (f.p.numpy().copy(), f.q.numpy().copy(), f.full_L().numpy().copy(), f.U.numpy().copy(),
                    A.product_count)
         elif case["kind"] == "powerlu":
             f = D.powerlu(A, case["k"], case["q_os"], case["v"], case["seed"], O.gaussian)
-            out = (f.p.numpy().copy(), f.q.numpy().copy(), f.L.numpy().copy(), f.U.numpy().copy(),
+            out = (f.p.numpy().copy(), f.q.numpy().copy(), f.full_L().numpy().copy(), f.U.numpy().copy(),
                    A.product_count)
         else:
             f, rank_ = D.powerlu_fp(A, case["eps"], case["b"], case["l"], case["v"], case["seed"], O.gaussian)
-            out = (f.p.numpy().copy(), f.q.numpy().copy(), f.L.numpy().copy(), f.U.numpy().copy(), rank_)
+            out = (f.p.numpy().copy(), f.q.numpy().copy(), f.full_L().numpy().copy(), f.U.numpy().copy(), rank_)
         q.put((rank, out))
     finally:
         dist.destroy_process_group()
@@ -252,3 +300,21 @@ def test_reference_signatures_accept_a_sharded_matrix():
         assert passes == ref_v.passes_used
         # same basis up to column signs
         assert np.allclose(np.abs(np.sum(v * ref_v.V, axis=0)), 1.0, atol=1e-10)
+
+
+@pytest.mark.parametrize("v,decline,wide_at", [(4, False, 10 ** 9), (5, False, 16), (4, True, 10 ** 9),
+                                               (6, True, 10 ** 9)])
+def test_sharded_replicated_factorizations_world4(v, decline, wide_at):
+    """the n x l sketch factorizations on row blocks of the
+    replicated Z (sharded CholeskyQR2 with all-reduced Grams, TSQR when the
+    Cholesky declines, tournament LU for the interior n x l LU) and L = L1 U2^T
+    by row blocks (full_L all-gathers): p, q identical, error equal to 1e-12."""
+    a = decay_matrix(400, 240, seed=20 + v)
+    res = run_dist({"kind": "powerlu", "a": a, "k": 20, "q_os": 8, "v": v, "seed": 5, "decline": decline,
+                    "wide_at": wide_at}, world=4)
+    ref = O.powerlu(a, 20, 8, v, 5)
+    e_ref = O.rel_fro_error_factor(a, ref)
+    for rank, (p, q, L, U, passes) in res.items():
+        assert np.array_equal(p, ref.p) and np.array_equal(q, ref.q), rank
+        assert abs(O.rel_fro_error_factor(a, O.LowRankLU(p, q, L, U, 20)) - e_ref) <= 1e-12
+        np.testing.assert_allclose(L, ref.L, rtol=0, atol=1e-9)
