@@ -5,6 +5,7 @@ All arithmetic runs in librlra_b200.so; nothing here computes on the host.
 
 from __future__ import annotations
 
+import os
 from typing import NamedTuple
 
 import torch
@@ -47,6 +48,23 @@ def eqr_(a):
     return qr.q(), qr
 
 
+class _CholFactor:
+    """QR factor from CholeskyQR (pinv_factor_): q() and r_view() like ops.QR."""
+
+    def __init__(self, q, r):
+        self._q, self._r = q, r
+
+    def q(self):
+        return self._q
+
+    def r_view(self):
+        return self._r
+
+
+PINV_QR = os.environ.get("RLRA_B200_PINV_QR", "chol")
+PINV_CHOL_MARGIN = 1e4  # CholeskyQR's R is trusted for the rank test only this far above PINV_RTOL
+
+
 def pinv_factor_(l):
     """kernels.pinv_factor (rlra/kernels.py:64-79) on a scratch copy of `l`.
 
@@ -55,6 +73,19 @@ def pinv_factor_(l):
     if m < n:
         raise ValueError(f"need a tall matrix, got {(m, n)}")
     fro2 = ops.sumsq(l)
+    if PINV_QR == "chol" and n > 0:
+        # CholeskyQR2 / shifted CholeskyQR3 (tall products on the int8 engine)
+        # instead of the latency-bound Householder panels (C4: G 50000 x 720).
+        # R = Q^T L; the reference's rank test on its diagonal is decided here
+        # only when min |R_ii| clears the threshold by PINV_CHOL_MARGIN (Cholesky
+        # R is accurate to ~u cond); otherwise -- or when the Cholesky declined
+        # -- the Householder path below decides exactly as rlra/kernels.py:64-79.
+        q, flag = ops.cholqr2(l) if n <= ops.cholqr_max_l() else ops.scholqr3(l)
+        _, r = ops.lu_extract(ops.matmul(q, l, ta=True), want_l=False)
+        dmin = ops.diag_absmin(r)
+        vals = torch.cat([dmin, fro2, flag.to(torch.float64)]).cpu()
+        if not int(vals[2]) and float(vals[0]) > PINV_CHOL_MARGIN * PINV_RTOL * float(vals[1]) ** 0.5:
+            return _CholFactor(q, r)
     work = _copy(l)
     qr = ops.QR(work)
     dmin = ops.diag_absmin(qr.r_view())

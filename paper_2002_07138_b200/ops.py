@@ -518,6 +518,20 @@ def chol_inv_blocked(g, out, flag, cond_limit):
 
 
 SCHOL_C = 11.0 * 2.0 ** -53  # shift constant of shifted CholeskyQR (Fukaya et al. 2020)
+CHOLQR_OZ_MIN_ELEMS = int(os.environ.get("RLRA_B200_CHOLQR_OZ_MIN", str(1 << 24)))
+
+
+def _tall_products(z):
+    """(gram, times) for a tall sketch z: Z^T Z and Z R.  Large sketches (C3-C5
+    final bases, C4's pinv) take the int8 tensor-core engine -- ONE residue set
+    of z serves both products (TN with B = z, NN with B = R) -- under its
+    dynamic-range guard; small ones the DMMA GEMM."""
+    n, l = z.shape
+    if (os.environ.get("RLRA_B200_PASS_GEMM", "oz") == "oz" and n * l >= CHOLQR_OZ_MIN_ELEMS
+            and n <= OZ_BLOCK_K and l <= 4096):
+        prep = OzPrep(z)
+        return (lambda: prep.gemm(z, trans=True)), (lambda r: prep.gemm(r, trans=False))
+    return (lambda: matmul(z, z, ta=True)), (lambda r: matmul(z, r))
 NO_COND_LIMIT = 1e300
 
 
@@ -538,7 +552,8 @@ def scholqr3(z):
         # exactly zero column -> flag (diag_ratio_flag sees a zero diagonal of Z^T Z)
         q = z
         for step, limit in enumerate((NO_COND_LIMIT, 1e7, 2.0)):
-            g = matmul(q, q, ta=True)
+            gram, times = _tall_products(q)
+            g = gram()
             if step == 0:
                 _call("rlra_b200_diag_ratio_flag", dev, ptr(g), ld_of(g), l, NO_COND_LIMIT, ptr(flag), _stream(dev))
                 _call("rlra_b200_chol_shift_diag", dev, ptr(g), ld_of(g), l,
@@ -547,7 +562,7 @@ def scholqr3(z):
                 gram_identity_flag(g, flag)
             rinv = fmat(l, l, dev)
             chol_inv_blocked(g, rinv, flag, limit)
-            q = matmul(q, rinv)
+            q = times(rinv)
     return q, flag
 
 
@@ -560,13 +575,15 @@ def cholqr2(z):
     flag = torch.zeros(1, dtype=torch.int32, device=dev)
     rinv = fmat(l, l, dev)
     with label("cholqr2"):
-        g = matmul(z, z, ta=True)
-        chol_inv(g, rinv, flag, CHOLQR_COND)
-        q1 = matmul(z, rinv)
-        g2 = matmul(q1, q1, ta=True)
+        gram, times = _tall_products(z)
+        g = gram()
+        chol_inv_blocked(g, rinv, flag, CHOLQR_COND)
+        q1 = times(rinv)
+        gram, times = _tall_products(q1)
+        g2 = gram()
         gram_identity_flag(g2, flag)  # cond(Z) beyond ~u^-1/2 whatever the diagonal ratio said
-        chol_inv(g2, rinv, flag, 2.0)
-        q = matmul(q1, rinv)
+        chol_inv_blocked(g2, rinv, flag, 2.0)
+        q = times(rinv)
     return q, flag
 
 
