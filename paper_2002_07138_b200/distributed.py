@@ -188,12 +188,16 @@ class CudaOps:
         return self.o.as_fmat(x.index_select(0, idx))
 
     def right_solve_upper(self, x, u):
-        """X U^{-1} (U upper l x l): transposes around the K6 solve U^T Z = X^T."""
+        """X U^{-1} (U upper l x l): U^{-1} by the K6 solve U X = I (l^3, small),
+        then one DMMA GEMM over the tall X (the transposed TRSM took 3.4 ms on
+        a 32768 x 544 shard, profiles/r02_scale_model_C5.json)."""
         if x.shape[0] == 0:
             return x
-        xt = self.o.transpose(x)
-        self.o.trsm_rt_(u, xt)
-        return self.o.transpose(xt)
+        l = u.shape[0]
+        inv = self.o.fmat(l, l, self.device)
+        inv.copy_(torch.eye(l, dtype=torch.float64, device=self.device))
+        self.o.trsm_un_(u, inv)
+        return self.o.matmul(x, inv)
 
 
 @dataclass

@@ -317,24 +317,26 @@ class OzBlocked:
                                         self.cols[ij[1]][1] - self.cols[ij[1]][0], self.nmod)
         self.block_ws = {ij: size(ij) for ij in self.blocks}
         biggest = max(self.block_ws.values())
-        if cache_bytes is None:
-            free, _ = torch.cuda.mem_get_info(dev)
-            free += torch.cuda.memory_reserved(dev) - torch.cuda.memory_allocated(dev)  # allocator cache
-            cache_bytes = free - OZ_RESERVE_BYTES
-        total = sum(self.block_ws.values())
-        if total > cache_bytes:
-            cache_bytes -= biggest  # room for the scratch block
-        self.cache = {}
-        used = 0
         if not any(self.ok):  # every product goes to the DMMA GEMM: no residues at all
             self.blocks = []
+        total = sum(self.block_ws.values())
+        if cache_bytes is None:
+            torch.cuda.empty_cache()  # the allocator's cached segments are fragmented: hand them back first
+            free, _ = torch.cuda.mem_get_info(dev)
+            cache_bytes = free - OZ_RESERVE_BYTES
+        self.scratch = None
+        if self.blocks and total > cache_bytes:
+            # the scratch block first, while the largest contiguous range is free
+            self.scratch = torch.empty(biggest, dtype=torch.uint8, device=dev)
+            cache_bytes -= biggest
+        self.cache = {}
+        used = 0
         for ij in self.blocks:
             if used + self.block_ws[ij] <= cache_bytes:
                 self.cache[ij] = self._build(ij, None)
                 used += self.block_ws[ij]
-        self.scratch = None
-        if self.blocks and len(self.cache) < len(self.blocks):
-            self.scratch = torch.empty(biggest, dtype=torch.uint8, device=dev)
+        if self.scratch is not None and len(self.cache) == len(self.blocks):
+            self.scratch = None
         self.rebuilt = len(self.blocks) - len(self.cache)
 
     def _build(self, ij, into):
