@@ -82,6 +82,14 @@ RLRA_B200_API size_t rlra_b200_getrf_workspace(int64_t m, int64_t n);
 /* nonzero_diag (device int64*, nullable) receives count_nonzero(diag(U)) */
 RLRA_B200_API int rlra_b200_getrf(double* a, int64_t lda, int64_t m, int64_t n, int64_t* piv,
                     int64_t* nonzero_diag, void* ws, size_t ws_bytes, void* stream);
+/* Same, with flags: RLRA_B200_GETRF_FAST_UPDATE -- the blocked path's
+ * trailing updates on the DMMA GEMM (FMA rounding; same pivot rule, pivots
+ * equal the exact kernel's except at rounding-level ties).  The drivers'
+ * sketch LUs use it (rlra/rangefinder.py:73-77, rlra/fixedrank.py:144-146);
+ * rlra_b200_plu_inplace and flags = 0 stay bit-exact. */
+#define RLRA_B200_GETRF_FAST_UPDATE 1
+RLRA_B200_API int rlra_b200_getrf_ex(double* a, int64_t lda, int64_t m, int64_t n, int64_t* piv,
+                                     int64_t* nonzero_diag, void* ws, size_t ws_bytes, int flags, void* stream);
 RLRA_B200_API int rlra_b200_iota(int64_t* p, int64_t m, void* stream);
 /* count_nonzero(diag(a)) over the leading r x r block -> device int64 *out
  * (rangefinder._check_width, rangefinder.py:55-64) */
@@ -123,7 +131,9 @@ RLRA_B200_API int rlra_b200_dgemm(int transa, int transb, int64_t m, int64_t n, 
  * the guard header: int e_a, int pad, then three uint64 holding the double
  * bits of the largest row/column sum of squares, the smallest non-zero row
  * sum and the smallest non-zero column sum (all ones: none), then uint32
- * non-finite flag and uint32 "some entry is not an integer" flag
+ * non-finite flag, uint32 "some entry is not an integer" flag and the double
+ * ||A||_F^2 (fixed-order double-double sum of the column partials: the
+ * Frobenius norm of rlra/fixedprec.py:72 fused into the norms pass)
  * (integer-valued A is routed to DMMA: exact products turn exact linear
  * dependencies into exact zero pivots where BLAS leaves rounding noise).  rlra_b200_oz_norms fills it (and e_a) without building
  * residues; copy it to the host and pass it to rlra_b200_oz_guard (host-only,

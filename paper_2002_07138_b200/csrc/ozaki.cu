@@ -401,6 +401,7 @@ struct OzHeader {
   unsigned long long mincol;     // min over columns (~0ull: none)
   unsigned nonfinite;            // a row or column sum is NaN / Inf
   unsigned nonint;               // some entry is not an integer
+  double fro2;                   // ||A||_F^2 from the column partials (fro2_kernel)
 };
 
 __global__ void __launch_bounds__(256, 4) norms_partial_kernel(const double* __restrict__ a, int64_t lda, int64_t m,
@@ -508,6 +509,54 @@ __global__ void norms_final_kernel(const double* __restrict__ part_row, int64_t 
     if (mnr < inf) atomicMin(&hdr->minrow, (unsigned long long)__double_as_longlong(mnr));
     if (mnc < inf) atomicMin(&hdr->mincol, (unsigned long long)__double_as_longlong(mnc));
     if (anybad) atomicOr(&hdr->nonfinite, 1u);
+  }
+}
+
+// ||A||_F^2 as a by-product of the norms pass (rlra/accessors.py:33-34 at
+// rlra/fixedprec.py:72; north star (d): the Frobenius-norm reduction fused with
+// the pass): the column partial sums (each over <= 2048 rows) are added in a
+// fixed order in double-double, so no extra read of A.
+__device__ __forceinline__ void oz_two_sum(double a, double b, double& s, double& e) {
+  s = a + b;
+  const double bb = s - a;
+  e = (a - (s - bb)) + (b - bb);
+}
+
+__global__ void __launch_bounds__(1024) fro2_kernel(const double* __restrict__ part, int64_t count,
+                                                    OzHeader* __restrict__ hdr) {
+  __shared__ double sh[32], sl[32];
+  double hi = 0.0, lo = 0.0;
+  for (int64_t i = threadIdx.x; i < count; i += 1024) {
+    double s, e;
+    oz_two_sum(hi, part[i], s, e);
+    hi = s;
+    lo += e;
+  }
+  auto merge = [](double& h, double& l, double h2, double l2) {
+    double s, e;
+    oz_two_sum(h, h2, s, e);
+    h = s;
+    l = l + l2 + e;
+  };
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    const double h2 = __shfl_down_sync(0xffffffffu, hi, o), l2 = __shfl_down_sync(0xffffffffu, lo, o);
+    merge(hi, lo, h2, l2);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    sh[threadIdx.x >> 5] = hi;
+    sl[threadIdx.x >> 5] = lo;
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    hi = sh[threadIdx.x];
+    lo = sl[threadIdx.x];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      const double h2 = __shfl_down_sync(0xffffffffu, hi, o), l2 = __shfl_down_sync(0xffffffffu, lo, o);
+      merge(hi, lo, h2, l2);
+    }
+    if (threadIdx.x == 0) hdr->fro2 = hi + lo;
   }
 }
 
@@ -993,6 +1042,8 @@ static int oz_norms(const double* a, int64_t lda, int64_t m, int64_t n, int nmod
   oz::norms_final_kernel<<<(unsigned)ceil_div(m + n, 256), 256, 0, st>>>(prow, ncb, m, pcol, nrb, n, hdr, a, lda);
   RLRA_LAUNCHED();
   oz::scale_a_kernel<<<1, 1, 0, st>>>(hdr, oz::budget(nmod).pa, e_a);
+  RLRA_LAUNCHED();
+  oz::fro2_kernel<<<1, 1024, 0, st>>>(pcol, nrb * n, hdr);
   RLRA_LAUNCHED();
   return 0;
 }

@@ -184,8 +184,14 @@ class DeviceMatrix:
             return ops.matmul(self._a, x, ta=True)
 
     def fro_norm_sq_device(self):
-        """Compensated ||A||_F^2 as a device scalar (no host sync)."""
+        """||A||_F^2 as a device scalar (no host sync): inside a product session
+        whose residues are built, the by-product of their norms pass (fixed-
+        order double-double over the column partials -- no extra read of A);
+        otherwise the compensated K2b reduction."""
         self._finish_upload()
+        prep = self._oz_prep
+        if prep is not None and getattr(prep, "fro2", None) is not None:
+            return prep.fro2
         return ops.sumsq(self._a)
 
     def fro_norm(self):

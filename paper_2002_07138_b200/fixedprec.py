@@ -126,7 +126,7 @@ def _adaptive(a, params, seed):
 
             V = qr_basis_(declined[1], checks, "householder")
             g = a.matmul(V)
-    fro2 = a.fro_norm_sq_device()
+        fro2 = a.fro_norm_sq_device()  # inside the session: fused into the pass's norms read
     energies = ops.colsumsq(g)
     checks.raise_if_collapsed()
     host = torch.cat([fro2, energies]).cpu().numpy()

@@ -180,6 +180,7 @@ def gemm(a, b, c, *, ta=False, tb=False, alpha=1.0, beta=0.0):
 
 OZ_NMOD = int(os.environ.get("RLRA_B200_OZ_NMOD", "14"))
 OZ_HEADER_BYTES = 64  # include/rlra_b200.h RLRA_B200_OZ_HEADER_BYTES
+OZ_FRO2_OFFSET = 40  # double ||A||_F^2 in the header
 
 
 def oz_guard(header, m, n):
@@ -240,6 +241,8 @@ class OzPrep:
             self.header = None
             self.ok = (True, True)
             _call("rlra_b200_oz_prep", a.device, ptr(a), ld_of(a), self.m, self.n, self.nmod, ptr(self.ws), wsb, st)
+        # ||A||_F^2 of the norms pass (header bytes 40..48): device scalar, no extra read of A
+        self.fro2 = self.ws[OZ_FRO2_OFFSET:OZ_FRO2_OFFSET + 8].view(torch.float64)
 
     def gemm(self, b, trans=False, keep_ws=False, out=None, add=False):
         """C = A B (trans=False, b n x l) or A^T B (trans=True, b m x l); with
@@ -303,6 +306,7 @@ class OzBlocked:
               _stream(dev))
         self.header = ws[:OZ_HEADER_BYTES].cpu() if guard else None
         self.ok = oz_guard(self.header, self.m, self.n) if guard else (True, True)
+        self.fro2 = ws[OZ_FRO2_OFFSET:OZ_FRO2_OFFSET + 8].view(torch.float64).clone()
         del ws
         if block_bytes is None:
             block_bytes = int(os.environ.get("RLRA_B200_OZ_BLOCK_BYTES", str(16 << 30)))
@@ -321,8 +325,8 @@ class OzBlocked:
             self.blocks = []
         total = sum(self.block_ws.values())
         if cache_bytes is None:
-            torch.cuda.empty_cache()  # the allocator's cached segments are fragmented: hand them back first
             free, _ = torch.cuda.mem_get_info(dev)
+            free += torch.cuda.memory_reserved(dev) - torch.cuda.memory_allocated(dev)  # allocator cache
             cache_bytes = free - OZ_RESERVE_BYTES
         self.scratch = None
         if self.blocks and total > cache_bytes:
@@ -333,7 +337,12 @@ class OzBlocked:
         used = 0
         for ij in self.blocks:
             if used + self.block_ws[ij] <= cache_bytes:
-                self.cache[ij] = self._build(ij, None)
+                try:
+                    self.cache[ij] = self._build(ij, None)
+                except torch.OutOfMemoryError:  # fragmented allocator: rebuild the rest per product
+                    if self.scratch is None:
+                        self.scratch = torch.empty(biggest, dtype=torch.uint8, device=dev)
+                    break
                 used += self.block_ws[ij]
         if self.scratch is not None and len(self.cache) == len(self.blocks):
             self.scratch = None
@@ -423,8 +432,15 @@ def iota(m, device):
     return p
 
 
-def getrf_(a, piv=None):
-    """In-place packed GEPP of a (bit-exact with rlra/_lu_cython.pyx:14-55).
+# The drivers' sketch LUs: trailing updates of the blocked path on the DMMA
+# GEMM (RLRA_B200_GETRF_FAST_UPDATE); RLRA_B200_GEPP_EXACT=1 keeps them bit-exact.
+DRIVER_GEPP_FAST = os.environ.get("RLRA_B200_GEPP_EXACT", "0") != "1"
+
+
+def getrf_(a, piv=None, exact=True):
+    """In-place packed GEPP of a.  exact=True: bit-exact with
+    rlra/_lu_cython.pyx:14-55; exact=False: same pivot rule, the blocked path's
+    trailing updates on the DMMA GEMM (csrc/getrf.cu getrf_ex).
 
     Returns (piv, nonzero_diag_count_device_tensor)."""
     m, n = a.shape
@@ -433,8 +449,8 @@ def getrf_(a, piv=None):
     cnt = torch.zeros(1, dtype=I64, device=a.device)
     wsb = _native.query("rlra_b200_getrf_workspace", m, n)
     ws = torch.empty(max(wsb, 8), dtype=torch.uint8, device=a.device)
-    _call("rlra_b200_getrf", a.device, ptr(a), ld_of(a), m, n, ptr(piv), ptr(cnt), ptr(ws), wsb,
-                 _stream(a.device))
+    _call("rlra_b200_getrf_ex", a.device, ptr(a), ld_of(a), m, n, ptr(piv), ptr(cnt), ptr(ws), wsb,
+          0 if exact else 1, _stream(a.device))
     return piv, cnt
 
 
