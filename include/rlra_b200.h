@@ -82,14 +82,6 @@ RLRA_B200_API size_t rlra_b200_getrf_workspace(int64_t m, int64_t n);
 /* nonzero_diag (device int64*, nullable) receives count_nonzero(diag(U)) */
 RLRA_B200_API int rlra_b200_getrf(double* a, int64_t lda, int64_t m, int64_t n, int64_t* piv,
                     int64_t* nonzero_diag, void* ws, size_t ws_bytes, void* stream);
-/* Same, with flags: RLRA_B200_GETRF_FAST_UPDATE -- the blocked path's
- * trailing updates on the DMMA GEMM (FMA rounding; same pivot rule, pivots
- * equal the exact kernel's except at rounding-level ties).  The drivers'
- * sketch LUs use it (rlra/rangefinder.py:73-77, rlra/fixedrank.py:144-146);
- * rlra_b200_plu_inplace and flags = 0 stay bit-exact. */
-#define RLRA_B200_GETRF_FAST_UPDATE 1
-RLRA_B200_API int rlra_b200_getrf_ex(double* a, int64_t lda, int64_t m, int64_t n, int64_t* piv,
-                                     int64_t* nonzero_diag, void* ws, size_t ws_bytes, int flags, void* stream);
 RLRA_B200_API int rlra_b200_iota(int64_t* p, int64_t m, void* stream);
 /* count_nonzero(diag(a)) over the leading r x r block -> device int64 *out
  * (rangefinder._check_width, rangefinder.py:55-64) */

@@ -72,8 +72,6 @@ size_t gemm_workspace_bytes(int64_t M, int64_t N, int64_t K);
 size_t getrf_workspace_bytes(int64_t m, int64_t n);
 int getrf(double* a, int64_t lda, int64_t m, int64_t n, int64_t* piv, int64_t* nonzero_diag_dev,
           int* zflag_out, void* ws, size_t ws_bytes, cudaStream_t st);
-int getrf_ex(double* a, int64_t lda, int64_t m, int64_t n, int64_t* piv, int64_t* nonzero_diag_dev,
-             int* zflag_out, void* ws, size_t ws_bytes, int flags, cudaStream_t st);
 int fill_iota(int64_t* p, int64_t m, cudaStream_t st);
 int count_nonzero_diag(const double* a, int64_t lda, int64_t r, int64_t* out_dev, cudaStream_t st);
 int lu_basis(const double* lu, int64_t ldlu, int64_t m, int64_t k, const int64_t* piv,
@@ -234,11 +232,6 @@ int rlra_b200_plu_inplace(double* lu, int64_t m, int64_t n, int64_t* piv) {
 }
 
 size_t rlra_b200_getrf_workspace(int64_t m, int64_t n) { return getrf_workspace_bytes(m, n); }
-
-int rlra_b200_getrf_ex(double* a, int64_t lda, int64_t m, int64_t n, int64_t* piv, int64_t* nonzero_diag,
-                       void* ws, size_t ws_bytes, int flags, void* stream) {
-  return getrf_ex(a, lda, m, n, piv, nonzero_diag, nullptr, ws, ws_bytes, flags, S(stream));
-}
 
 int rlra_b200_getrf(double* a, int64_t lda, int64_t m, int64_t n, int64_t* piv,
                     int64_t* nonzero_diag, void* ws, size_t ws_bytes, void* stream) {

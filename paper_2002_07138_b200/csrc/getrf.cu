@@ -1003,29 +1003,8 @@ static int lu_prepare_kernel(const void* kern) {
 // diagonal and U on/above it, `piv` (caller-preloaded, typically 0..m-1) is
 // permuted like the reference's piv (rlra/_lu_cython.pyx:14, rlra/kernels.py:48),
 // and *nonzero_diag_dev (device int64) receives count_nonzero(diag(U)).
-int gemm(bool ta, bool tb, int64_t M, int64_t N, int64_t K, double alpha, const double* A, int64_t lda,
-         const double* B, int64_t ldb, double beta, double* C, int64_t ldc, void* ws, size_t ws_bytes,
-         cudaStream_t st);
-size_t gemm_workspace_bytes(int64_t M, int64_t N, int64_t K);
-
-// flags: RLRA_B200_GETRF_FAST_UPDATE (1) -- trailing updates A22 -= L21 U12 of
-// the blocked path on the DMMA GEMM (FMA rounding) instead of the bit-exact
-// DMUL-then-DSUB sequence.  Same pivot rule, same panel factorizations and U12
-// (forward substitution); only the rounding of the trailing updates differs,
-// so the pivots agree with the exact kernel except at rounding-level ties
-// (perturbation 1: p / q unchanged on C1-C5).  For the
-// drivers' sketch LUs; the plu_inplace seam stays bit-exact.
-int getrf_ex(double* a, int64_t lda, int64_t m, int64_t n, int64_t* piv, int64_t* nonzero_diag_dev,
-             int* zflag_out, void* ws, size_t ws_bytes, int flags, cudaStream_t st);
-
 int getrf(double* a, int64_t lda, int64_t m, int64_t n, int64_t* piv, int64_t* nonzero_diag_dev,
           int* zflag_out, void* ws, size_t ws_bytes, cudaStream_t st) {
-  return getrf_ex(a, lda, m, n, piv, nonzero_diag_dev, zflag_out, ws, ws_bytes, 0, st);
-}
-
-int getrf_ex(double* a, int64_t lda, int64_t m, int64_t n, int64_t* piv, int64_t* nonzero_diag_dev,
-             int* zflag_out, void* ws, size_t ws_bytes, int flags, cudaStream_t st) {
-  const bool fast_update = (flags & 1) != 0;
   RLRA_REQUIRE(m >= 0 && n >= 0, "getrf: negative dimension");
   RLRA_REQUIRE(lda >= (m > 0 ? m : 1), "getrf: lda < m");
   const int64_t r = m < n ? m : n;
@@ -1084,24 +1063,16 @@ int getrf_ex(double* a, int64_t lda, int64_t m, int64_t n, int64_t* piv, int64_t
     int64_t jo = 0, c0 = 0, ce = 0;
     int nbo = 0;
   } wide;
-  // A(r0:m, c0:c1) -= L(r0:m, j:j+nb) U(j:j+nb, c0:c1): bit-exact kernel, or
-  // the DMMA GEMM in fast mode (zero-pivot steps have zero L columns, so
-  // their terms vanish exactly there too)
-  auto update = [&](int64_t j_, int nb_, int64_t r0_, int64_t c0_, int64_t c1_, cudaStream_t s_) -> int {
-    if (r0_ >= m || c1_ <= c0_) return 0;
-    if (fast_update && gemm_workspace_bytes(m - r0_, c1_ - c0_, nb_) == 0)
-      return gemm(false, false, m - r0_, c1_ - c0_, nb_, -1.0, a + r0_ + j_ * lda, lda, a + j_ + c0_ * lda, lda,
-                  1.0, a + r0_ + c0_ * lda, lda, nullptr, 0, s_);
-    dim3 grid((unsigned)ceil_div(m - r0_, UPD_TM), (unsigned)ceil_div(c1_ - c0_, UPD_TN));
-    lu_update_kernel<<<grid, 256, 0, s_>>>(a, lda, j_, nb_, r0_, m, c0_, c1_, w.zflag);
-    RLRA_LAUNCHED();
-    return 0;
-  };
   auto trailing = [&](int64_t jo_, int nbo_, int64_t ce_, int64_t c0_, int64_t c1_, cudaStream_t s_) -> int {
     int blocks = (int)std::min<int64_t>(ceil_div(c1_ - c0_, 4), 4096);
     lu_trsm_kernel<<<blocks, 128, 0, s_>>>(a, lda, jo_, nbo_, c0_, c1_, w.zflag);
     RLRA_LAUNCHED();
-    return update(jo_, nbo_, ce_, c0_, c1_, s_);
+    if (ce_ < m) {
+      dim3 grid((unsigned)ceil_div(m - ce_, UPD_TM), (unsigned)ceil_div(c1_ - c0_, UPD_TN));
+      lu_update_kernel<<<grid, 256, 0, s_>>>(a, lda, jo_, nbo_, ce_, m, c0_, c1_, w.zflag);
+      RLRA_LAUNCHED();
+    }
+    return 0;
   };
   auto submit_wide = [&]() -> int {
     if (!wide.pending || wide.submitted) return 0;
@@ -1172,7 +1143,11 @@ int getrf_ex(double* a, int64_t lda, int64_t m, int64_t n, int64_t* piv, int64_t
       if (c0 < ce) {  // inner update, restricted to the outer block's columns
         lu_trsm_kernel<<<(unsigned)ceil_div(ce - c0, 4), 128, 0, st>>>(a, lda, j0, nb, c0, ce, w.zflag);
         RLRA_LAUNCHED();
-        if (update(j0, nb, c0, c0, ce, st)) return -1;
+        if (c0 < m) {
+          dim3 grid((unsigned)ceil_div(m - c0, UPD_TM), (unsigned)ceil_div(ce - c0, UPD_TN));
+          lu_update_kernel<<<grid, 256, 0, st>>>(a, lda, j0, nb, c0, m, c0, ce, w.zflag);
+          RLRA_LAUNCHED();
+        }
       }
     }
     if (ce < n) {  // outer trailing update with the whole 32-column block

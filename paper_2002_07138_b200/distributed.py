@@ -114,7 +114,7 @@ class CudaOps:
         return pinv_transpose_apply(g, m_)
 
     def getrf_(self, a):
-        return self.o.getrf_(a, exact=not self.o.DRIVER_GEPP_FAST)
+        return self.o.getrf_(a)
 
     def lu_basis(self, lu, piv):
         return self.o.lu_basis(lu, piv)

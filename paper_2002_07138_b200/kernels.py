@@ -26,7 +26,7 @@ class PivotedLU(NamedTuple):
 def plu_(a, want_l=True, want_u=True):
     """kernels.plu (rlra/kernels.py:37-54) on a device matrix, factoring `a` IN
     PLACE (callers pass a scratch copy when they still need the input)."""
-    piv, cnt = ops.getrf_(a, exact=not ops.DRIVER_GEPP_FAST)
+    piv, cnt = ops.getrf_(a)
     l, u = ops.lu_extract(a, want_l, want_u)
     return PivotedLU(l, u, piv, cnt)
 

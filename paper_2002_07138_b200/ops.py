@@ -432,15 +432,8 @@ def iota(m, device):
     return p
 
 
-# The drivers' sketch LUs: trailing updates of the blocked path on the DMMA
-# GEMM (RLRA_B200_GETRF_FAST_UPDATE); RLRA_B200_GEPP_EXACT=1 keeps them bit-exact.
-DRIVER_GEPP_FAST = os.environ.get("RLRA_B200_GEPP_EXACT", "0") != "1"
-
-
-def getrf_(a, piv=None, exact=True):
-    """In-place packed GEPP of a.  exact=True: bit-exact with
-    rlra/_lu_cython.pyx:14-55; exact=False: same pivot rule, the blocked path's
-    trailing updates on the DMMA GEMM (csrc/getrf.cu getrf_ex).
+def getrf_(a, piv=None):
+    """In-place packed GEPP of a (bit-exact with rlra/_lu_cython.pyx:14-55).
 
     Returns (piv, nonzero_diag_count_device_tensor)."""
     m, n = a.shape
@@ -449,8 +442,8 @@ def getrf_(a, piv=None, exact=True):
     cnt = torch.zeros(1, dtype=I64, device=a.device)
     wsb = _native.query("rlra_b200_getrf_workspace", m, n)
     ws = torch.empty(max(wsb, 8), dtype=torch.uint8, device=a.device)
-    _call("rlra_b200_getrf_ex", a.device, ptr(a), ld_of(a), m, n, ptr(piv), ptr(cnt), ptr(ws), wsb,
-          0 if exact else 1, _stream(a.device))
+    _call("rlra_b200_getrf", a.device, ptr(a), ld_of(a), m, n, ptr(piv), ptr(cnt), ptr(ws), wsb,
+          _stream(a.device))
     return piv, cnt
 
 

@@ -141,7 +141,7 @@ def qr_basis_(x, checks, method="householder"):
 
 def lu_basis_(x, checks):
     """rlra/rangefinder.py:73-77: row-unpermuted L of lu(x) (destroys x)."""
-    piv, cnt = ops.getrf_(x, exact=not ops.DRIVER_GEPP_FAST)
+    piv, cnt = ops.getrf_(x)
     checks.add(cnt, x.shape[1])
     return ops.lu_basis(x, piv)
 
