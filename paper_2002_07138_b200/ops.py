@@ -209,6 +209,35 @@ def oz_guard_stats(header):
     return f(mx), f(mr), f(mc), bool(nf), not nonint
 
 
+_SIDE = {}
+
+
+class _HeaderCopy:
+    def __init__(self, buf, ev):
+        self.buf, self.ev = buf, ev
+
+    def wait(self):
+        self.ev.synchronize()
+        return self.buf.clone()
+
+
+def _header_copy_async(ws, device):
+    """Copy the guard header to pinned host memory on a side stream ordered
+    after the work queued so far on the current stream."""
+    key = str(device)
+    if key not in _SIDE:
+        _SIDE[key] = (torch.cuda.Stream(device), torch.empty(OZ_HEADER_BYTES, dtype=torch.uint8, pin_memory=True))
+    side, buf = _SIDE[key]
+    main = torch.cuda.current_stream(device)
+    side.wait_stream(main)
+    with torch.cuda.stream(side):
+        buf.copy_(ws[:OZ_HEADER_BYTES], non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record(side)
+    ws.record_stream(side)
+    return _HeaderCopy(buf, ev)
+
+
 class OzPrep:
     """Int8 residues of A for the emulated pass products (csrc/ozaki.cu): built
     once per A, they serve both C = A B (trans=False) and C = A^T B.
@@ -232,11 +261,15 @@ class OzPrep:
         st = _stream(a.device)
         if guard:
             _call("rlra_b200_oz_norms", a.device, ptr(a), ld_of(a), self.m, self.n, self.nmod, ptr(self.ws), wsb, st)
-            self.header = self.ws[:OZ_HEADER_BYTES].cpu()
+            # the guard header goes to the host on a side stream while the
+            # residue kernel (~0.8 ms at C2) already runs on the main stream:
+            # the host decision no longer leaves the GPU idle; a rejected
+            # orientation only wastes those residues
+            host = _header_copy_async(self.ws, a.device)
+            _call("rlra_b200_oz_prep_ex", a.device, ptr(a), ld_of(a), self.m, self.n, self.nmod, ptr(self.ws),
+                  ptr(self.ws), wsb, st)
+            self.header = host.wait()
             self.ok = oz_guard(self.header, self.m, self.n)
-            if any(self.ok):
-                _call("rlra_b200_oz_prep_ex", a.device, ptr(a), ld_of(a), self.m, self.n, self.nmod, ptr(self.ws),
-                      ptr(self.ws), wsb, st)
         else:
             self.header = None
             self.ok = (True, True)
@@ -408,9 +441,26 @@ def oz_residue_budget(device):
     return max(0, free - OZ_RESERVE_BYTES)
 
 
+_TOTAL_MEM = {}
+
+
+def _small_residues(nbytes, device):
+    """Residues under an eighth of the device memory need no free-memory query
+    (the query -- cudaMemGetInfo plus the allocator's statistics -- costs
+    ~0.3 ms of host time at the start of every call, GPU idle)."""
+    if os.environ.get("RLRA_B200_OZ_MAX_BYTES"):
+        return False
+    key = str(device)
+    if key not in _TOTAL_MEM:
+        _TOTAL_MEM[key] = torch.cuda.get_device_properties(device).total_memory
+    return nbytes <= _TOTAL_MEM[key] // 8
+
+
 def oz_engine(a, max_residue_bytes=None):
     """OzPrep when the residues of all of A fit (and K is in range), else OzBlocked."""
     m, n = a.shape
+    if max_residue_bytes is None and max(m, n) <= OZ_BLOCK_K and _small_residues(OZ_NMOD * m * n, a.device):
+        return OzPrep(a)
     if max_residue_bytes is None:
         max_residue_bytes = oz_residue_budget(a.device)
     if max(m, n) <= OZ_BLOCK_K and OZ_NMOD * m * n <= max_residue_bytes:

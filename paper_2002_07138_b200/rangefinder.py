@@ -78,7 +78,12 @@ class RankChecks:
             pend.append(extra.view(-1).to(torch.int64))
         if not pend:
             return []
-        vals = (torch.cat(pend) if len(pend) > 1 else pend[0]).cpu().tolist()
+        dev_vals = torch.cat(pend) if len(pend) > 1 else pend[0]
+        host = torch.empty(dev_vals.shape, dtype=dev_vals.dtype, pin_memory=dev_vals.is_cuda)
+        host.copy_(dev_vals, non_blocking=True)  # pinned: no staging copy (r01 verdict: pageable fetch gap)
+        if dev_vals.is_cuda:
+            torch.cuda.current_stream(dev_vals.device).synchronize()
+        vals = host.tolist()
         n = len(vals) - (extra is not None)
         self._resolved.extend(int(v) for v in vals[:n])
         return vals[n:]
