@@ -215,11 +215,13 @@ def roofline_line(w, v, passes, reps, kt, pass_ms, step_ms):
         sw = sweep_width(w.m, 256)
         panels = [min(sw, w.n - j0) for j0 in range(0, w.n, sw)]
         bytes_step = sum(2 * nmod * (w.m * x + (w.m + x) * l_) for x in panels)
+        fp64_bytes_step = sum(2 * 8 * (w.m * x + (w.m + x) * l_) for x in panels)
         i8ops_step = sum(2 * nmod * 2.0 * w.m * x * l_ for x in panels)
     else:
         l_ = FP_WIDTH if w.kind == "powerlu_fp" else w.k + w.q_os
         widths = [l_] * v if w.kind == "powerlu_fp" else [l_] * (v - 1) + [w.k]
         bytes_step = sum(nmod * (w.m * w.n + (w.m + w.n) * x) for x in widths)
+        fp64_bytes_step = sum(8 * (w.m * w.n + (w.m + w.n) * x) for x in widths)
         i8ops_step = sum(nmod * 2.0 * w.m * w.n * x for x in widths)
     g_ms, g_cnt = kt["oz_gemm_i8"]
     hbm_peak = MEASURED.get("hbm_gbs")
@@ -239,7 +241,12 @@ def roofline_line(w, v, passes, reps, kt, pass_ms, step_ms):
             traffic = json.load(open(tpath)).get(f"oz_gemm_i8_{w.name}_v{v}")
         except Exception:
             traffic = None
-    i8_peak = 2.0 * MEASURED.get("bf16_tflops", 1690.0)  # dense int8 = 2x dense bf16 on B200
+    i8_peak, i8_src = 2.0 * MEASURED.get("bf16_tflops", 1690.0), "2 x MEASURED_PEAKS.json bf16_tflops (assumed)"
+    try:  # measured on this pool's B200 (tools/int8_peak.py, cuBLASLt int8 8192^3)
+        i8 = json.load(open(os.path.join(REPO, "profiles", "r02_int8_peak.json")))
+        i8_peak, i8_src = float(i8["int8_tops_burst"]), "profiles/r02_int8_peak.json (torch._int_mm burst, measured)"
+    except (OSError, ValueError, KeyError):
+        pass
     fp64_eq = passes * reps / (pass_ms / 1e3) / 1e12 if pass_ms else None
     other = {nm: {"ms_per_step": t / reps, "launches_per_step": c / reps} for nm, (t, c) in kt.items()}
     return {"bound": "hbm", "kernel": "gemm_i8_kernel (tcgen05 kind::i8 Ozaki-II pass products, csrc/ozaki.cu)",
@@ -249,8 +256,14 @@ def roofline_line(w, v, passes, reps, kt, pass_ms, step_ms):
             "launches_per_step": g_cnt / reps,
             "bytes_per_unit": f"nmod*(m*n + (m+n)*w) per pass of width w, nmod={nmod}",
             "int8_tensor": {"achieved_tops": i8ops_step * reps / (g_ms / 1e3) / 1e12, "peak_tops": i8_peak,
-                            "frac": i8ops_step * reps / (g_ms / 1e3) / 1e12 / i8_peak,
-                            "peak_source": "2 x MEASURED_PEAKS.json bf16_tflops (B200 dense int8 rate)"},
+                            "frac": i8ops_step * reps / (g_ms / 1e3) / 1e12 / i8_peak, "peak_source": i8_src},
+            "fp64_bytes_view": {
+                "algorithmic_bytes_per_launch": fp64_bytes_step * reps / g_cnt,
+                "achieved_gbs": fp64_bytes_step * reps / g_cnt / (per_launch_ms / 1e3) / 1e9,
+                "frac": fp64_bytes_step * reps / g_cnt / (per_launch_ms / 1e3) / 1e9 / hbm_peak,
+                "note": "the same launches against 8 B per element of A + the FP64 skinny operands "
+                        "(the bytes a DGEMM pass would read); the int8 engine must read 14 B/element "
+                        "of residues instead, so this view is capped at ~8/14"},
             "kernel_share_of_step": g_ms / reps / step_ms,
             "fp64_equivalent": {"pass_tflops": fp64_eq, "dmma_peak_tflops": FP64_PEAK_TFLOPS,
                                 "frac_of_dmma_peak": fp64_eq / FP64_PEAK_TFLOPS if fp64_eq else None,
@@ -306,11 +319,35 @@ def reference_arm(args):
         "config": {"workload": desc, "m": w.m, "n": w.n, "k": w.k, "l": w.k + w.q_os, "v": v},
         "cpu_baseline": {"value": val, "unit": "GFLOP/s", "cores": cores, "kind": kind,
                          "sample": f"{sample}, rlra {getattr(mod, '__version__', 'port')} "
-                                   f"backend={getattr(mod, 'BACKEND', 'c-oracle')}, OpenBLAS threads=all"},
+                                   f"backend={getattr(mod, 'BACKEND', 'c-oracle')}, OpenBLAS threads=all",
+                         "host": host_details()},
         "e2e": {"value": val, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
+
+
+def host_details():
+    """CPU model and BLAS build of the box."""
+    model = None
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    blas = None
+    try:
+        import threadpoolctl
+
+        info = [d for d in threadpoolctl.threadpool_info() if d.get("user_api") == "blas"]
+        if info:
+            blas = f"{info[0].get('internal_api')} {info[0].get('version')} ({info[0].get('architecture')}, " \
+                   f"{info[0].get('num_threads')} threads)"
+    except Exception:
+        pass
+    return {"cpu_model": model, "logical_cpus": os.cpu_count(), "blas": blas}
 
 
 def cpu_baseline(a, w, v, flops, budget_s=30.0):
@@ -326,7 +363,7 @@ def cpu_baseline(a, w, v, flops, budget_s=30.0):
     best = min(times)
     return {"value": flops / best / 1e9, "unit": "GFLOP/s", "cores": os.cpu_count(), "kind": kind,
             "sample": f"{len(times)} full {w.name} factorizations (best of), same A and seed; "
-                      f"s/factorization {best:.3f}"}, f
+                      f"s/factorization {best:.3f}", "host": host_details()}, f
 
 
 def cpu_baseline_analogue(w, v):
@@ -356,7 +393,7 @@ def cpu_baseline_analogue(w, v):
     call()
     sec = time.perf_counter() - t0
     return {"value": (p_ + f_) / sec / 1e9, "unit": "GFLOP/s", "cores": os.cpu_count(), "kind": kind,
-            "sample": f"1 call on the {w.name} analogue {m}x{n} (SURVEY Appendix A), {sec:.1f} s"}
+            "sample": f"1 call on the {w.name} analogue {m}x{n} (SURVEY Appendix A), {sec:.1f} s", "host": host_details()}
 
 
 GOLDEN = os.path.join(REPO, "tests", "golden")
