@@ -39,7 +39,7 @@ constexpr int NW = T / 32;    // warps per CTA
 constexpr int CS = 16;        // cluster size
 constexpr int RECD = 2 + W;   // record: {|v|, row bits, row[W]} (<= 144 B)
 constexpr int MAXRPT = 6;     // rows per thread
-constexpr int MAXN = 512;     // widest sketch handled (wider: the blocked path, whose trailing update uses every SM, wins)
+constexpr int MAXN = 1024;    // widest sketch handled (r02: 1024 -- C3 16384 x 1024 / 843; r01 capped it at 512)
 constexpr double ZTOL = 1e-14;  // rlra/_lu_cython.pyx:11
 constexpr unsigned NONE = 0xffffffffu;
 
@@ -880,7 +880,11 @@ bool getrf_full_eligible(int64_t m, int64_t n, int cluster_max) {
     // inside the tool): under a CUDA injection library use the blocked path
     if (getenv("NV_NSIGHT_INJECTION_TRANSPORT_TYPE") || getenv("NV_TPS_LAUNCH_TOKEN")) enabled = 0;
   }
-  return enabled && cluster_max >= lufull::CS && n >= 1 && m >= n && n <= lufull::MAXN &&
+  // widths above 512 only while the far-column work stays small: beyond, the
+  // blocked path's all-SM trailing update wins (profiles/r02_getrf_width.txt:
+  // 4096 x 544 coop 2.12 vs blocked 2.30 ms; 16384 x 1024 coop 8.14 vs 6.25 ms)
+  const bool width_ok = n <= 512 || (n <= lufull::MAXN && m * n <= (int64_t)4500000);
+  return enabled && cluster_max >= lufull::CS && n >= 1 && m >= n && width_ok &&
          m >= (int64_t)lufull::CS * 32 && m <= (int64_t)lufull::CS * lufull::T * lufull::MAXRPT;
 }
 
