@@ -286,9 +286,10 @@ __global__ void __launch_bounds__(256, 3) residue_a_kernel(const double* __restr
 }
 
 // Per-column scale of the skinny operand B (K x ncols): one CTA per (padded)
-// column.  Two passes over the column (it is L1/L2 resident): max |b|, then the
-// sum of squares of b 2^-s (s = exponent of the max) so neither overflow nor
-// underflow of the squares can misplace the scale.  A column holding NaN/Inf
+// column.  One pass: max |b| and the sum of squares; only when that sum left
+// [2^-900, 2^900] (squares that may have over- or underflowed) a second pass
+// sums the squares of b 2^-s (s = exponent of the max), so no over/underflow
+// can misplace the scale.  A column holding NaN/Inf
 // gets kEbNonFinite: its residues are zero and the CRT writes NaN into the
 // output column (every BLAS output touching it is non-finite too).  The scale
 // may exceed 2^1023 (columns of norm < 2^-970): residue_b applies it with
@@ -297,32 +298,55 @@ constexpr int kEbNonFinite = -0x40000000;
 __global__ void __launch_bounds__(256) bscale_kernel(const double* __restrict__ b, int64_t ldb, int64_t k,
                                                      int64_t ncols, int64_t cols_pad, int pb, int* __restrict__ e_b) {
   const int64_t jj = blockIdx.x;
-  __shared__ double red[8];
+  __shared__ double red[8], red2[8];
   __shared__ double s_mx;
   const double* col = b + jj * ldb;
-  double mx = 0.0;
+  // pass 1: max |b|, non-finite flag and the plain sum of squares together;
+  // the scaled second pass runs only when the plain sum left the safe range
+  double mx = 0.0, ss = 0.0;
   bool bad = false;
   if (jj < ncols) {
     for (int64_t i = threadIdx.x; i < k; i += 256) {
-      const double v = fabs(__ldg(col + i));
-      bad |= !(v <= 1.7976931348623157e308);
-      mx = fmax(mx, v);
+      const double v = __ldg(col + i);
+      const double av = fabs(v);
+      bad |= !(av <= 1.7976931348623157e308);
+      mx = fmax(mx, av);
+      ss = fma(v, v, ss);
     }
   }
   bad = __syncthreads_or(bad);
 #pragma unroll
-  for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+  for (int o = 16; o; o >>= 1) {
+    mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    ss += __shfl_xor_sync(0xffffffffu, ss, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    red[threadIdx.x >> 5] = mx;
+    red2[threadIdx.x >> 5] = ss;
+  }
   __syncthreads();
   if (threadIdx.x == 0) {
-    double t = 0.0;
-    for (int w = 0; w < 8; ++w) t = fmax(t, red[w]);
+    double t = 0.0, t2 = 0.0;
+    for (int w = 0; w < 8; ++w) {
+      t = fmax(t, red[w]);
+      t2 += red2[w];
+    }
     s_mx = t;
+    red2[0] = t2;
   }
   __syncthreads();
   mx = s_mx;
+  const double plain = red2[0];
   if (bad || mx == 0.0) {
     if (threadIdx.x == 0) e_b[jj] = bad ? kEbNonFinite : 0;
+    return;
+  }
+  if (plain >= 0x1p-900 && plain <= 0x1p900) {  // no over/underflow could have distorted it
+    if (threadIdx.x == 0) {
+      int ex;
+      frexp(sqrt(plain) * (1.0 + 0x1p-40), &ex);  // ||b_j|| < 2^ex
+      e_b[jj] = pb - ex;
+    }
     return;
   }
   int s;
@@ -336,7 +360,7 @@ __global__ void __launch_bounds__(256) bscale_kernel(const double* __restrict__ 
       s1 = fma(v1, v1, s1);
     }
   }
-  double ss = s0 + s1;
+  ss = s0 + s1;
 #pragma unroll
   for (int o = 16; o; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
   __syncthreads();
