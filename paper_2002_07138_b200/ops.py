@@ -613,8 +613,10 @@ def scholqr3(z):
         # exactly zero column -> flag (diag_ratio_flag sees a zero diagonal of Z^T Z)
         q = z
         for step, limit in enumerate((NO_COND_LIMIT, 1e7, 2.0)):
-            gram, times = _tall_products(q)
-            g = gram()
+            with label("scholqr3_prep"):
+                gram, times = _tall_products(q)
+            with label("scholqr3_gram"):
+                g = gram()
             if step == 0:
                 _call("rlra_b200_diag_ratio_flag", dev, ptr(g), ld_of(g), l, NO_COND_LIMIT, ptr(flag), _stream(dev))
                 _call("rlra_b200_chol_shift_diag", dev, ptr(g), ld_of(g), l,
@@ -622,8 +624,10 @@ def scholqr3(z):
             if step == 2:
                 gram_identity_flag(g, flag)
             rinv = fmat(l, l, dev)
-            chol_inv_blocked(g, rinv, flag, limit)
-            q = times(rinv)
+            with label("scholqr3_chol"):
+                chol_inv_blocked(g, rinv, flag, limit)
+            with label("scholqr3_q"):
+                q = times(rinv)
     return q, flag
 
 
