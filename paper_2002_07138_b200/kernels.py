@@ -80,12 +80,17 @@ def pinv_factor_(l):
         # only when min |R_ii| clears the threshold by PINV_CHOL_MARGIN (Cholesky
         # R is accurate to ~u cond); otherwise -- or when the Cholesky declined
         # -- the Householder path below decides exactly as rlra/kernels.py:64-79.
-        q, flag = ops.cholqr2(l) if n <= ops.cholqr_max_l() else ops.scholqr3(l)
-        _, r = ops.lu_extract(ops.matmul(q, l, ta=True), want_l=False)
-        dmin = ops.diag_absmin(r)
-        vals = torch.cat([dmin, fro2, flag.to(torch.float64)]).cpu()
-        if not int(vals[2]) and float(vals[0]) > PINV_CHOL_MARGIN * PINV_RTOL * float(vals[1]) ** 0.5:
-            return _CholFactor(q, r)
+        # CholeskyQR2 first (two steps, cond(L) up to ~1e7 -- C4's G), shifted
+        # CholeskyQR3 when it declines (cond up to ~u^-1), then Householder
+        for method in (ops.cholqr2, ops.scholqr3):
+            q, flag = method(l)
+            _, r = ops.lu_extract(ops.tn_tall(q, l), want_l=False)
+            dmin = ops.diag_absmin(r)
+            vals = torch.cat([dmin, fro2, flag.to(torch.float64)]).cpu()
+            if not int(vals[2]):
+                if float(vals[0]) > PINV_CHOL_MARGIN * PINV_RTOL * float(vals[1]) ** 0.5:
+                    return _CholFactor(q, r)
+                break  # near the rank threshold: Householder decides, as the reference does
     work = _copy(l)
     qr = ops.QR(work)
     dmin = ops.diag_absmin(qr.r_view())

@@ -541,6 +541,16 @@ def chol_inv(g, out, flag, cond_limit):
     return out
 
 
+def tn_tall(x, y):
+    """x^T y for tall x, y (n x l, n x w): the int8 engine (residues of x, TN
+    product with B = y) when x is large, else the DMMA GEMM."""
+    n, l = x.shape
+    if (os.environ.get("RLRA_B200_PASS_GEMM", "oz") == "oz" and n * l >= CHOLQR_OZ_MIN_ELEMS
+            and n <= OZ_BLOCK_K and y.shape[1] <= 4096):
+        return OzPrep(x).gemm(y, trans=True)
+    return matmul(x, y, ta=True)
+
+
 def _diag_blocks(l, cap):
     nb = max(1, -(-l // cap))
     step = -(-l // nb)
