@@ -135,6 +135,21 @@ RLRA_B200_API int rlra_b200_dgemm(int transa, int transb, int64_t m, int64_t n, 
 RLRA_B200_API int rlra_b200_oz_norms(const double* a, int64_t lda, int64_t m, int64_t n, int nmod, void* prep,
                                      size_t prep_bytes, void* stream);
 RLRA_B200_API double rlra_b200_oz_guard_limit(int64_t k);
+/* Pipelined upload (A arriving in column chunks, the e2e path): norms of
+ * chunk [c0, c1) (c0 a multiple of 256; chunks in ascending order, the first
+ * at 0), a provisional eA after the first chunk (its column norms, row norms
+ * extrapolated), residues of chunk [c0, c1) (multiple of 128) with the
+ * header's eA, then the final norms / guard statistics / ||A||_F^2 with the
+ * final eA in *e_a_final (device int): when it differs from the provisional
+ * one the caller rebuilds the residues (rlra_b200_oz_prep_ex). */
+RLRA_B200_API int rlra_b200_oz_norms_cols(const double* a, int64_t lda, int64_t m, int64_t n, int64_t c0, int64_t c1,
+                                          int nmod, void* prep, size_t prep_bytes, void* stream);
+RLRA_B200_API int rlra_b200_oz_scale_provisional(int64_t m, int64_t n, int64_t c1, int nmod, void* prep,
+                                                 size_t prep_bytes, void* stream);
+RLRA_B200_API int rlra_b200_oz_residue_cols(const double* a, int64_t lda, int64_t m, int64_t n, int64_t c0,
+                                            int64_t c1, int nmod, void* prep, size_t prep_bytes, void* stream);
+RLRA_B200_API int rlra_b200_oz_norms_finish(const double* a, int64_t lda, int64_t m, int64_t n, int nmod, void* prep,
+                                            size_t prep_bytes, int* e_a_final, void* stream);
 RLRA_B200_API int rlra_b200_oz_guard(const void* header, int64_t m, int64_t n, int* ok_nn, int* ok_tn);
 RLRA_B200_API size_t rlra_b200_oz_prep_workspace(int64_t m, int64_t n, int nmod);
 RLRA_B200_API int rlra_b200_oz_prep(const double* a, int64_t lda, int64_t m, int64_t n, int nmod, void* prep,

@@ -52,6 +52,10 @@ SIGNATURES = {
     "rlra_b200_oz_norms": (_c_i, [_c_p, _c_i64, _c_i64, _c_i64, _c_i, _c_p, _c_sz, _c_p]),
     "rlra_b200_oz_guard_limit": (_c_d, [_c_i64]),
     "rlra_b200_oz_guard": (_c_i, [_c_p, _c_i64, _c_i64, _c_p, _c_p]),
+    "rlra_b200_oz_norms_cols": (_c_i, [_c_p, _c_i64, _c_i64, _c_i64, _c_i64, _c_i64, _c_i, _c_p, _c_sz, _c_p]),
+    "rlra_b200_oz_scale_provisional": (_c_i, [_c_i64, _c_i64, _c_i64, _c_i, _c_p, _c_sz, _c_p]),
+    "rlra_b200_oz_residue_cols": (_c_i, [_c_p, _c_i64, _c_i64, _c_i64, _c_i64, _c_i64, _c_i, _c_p, _c_sz, _c_p]),
+    "rlra_b200_oz_norms_finish": (_c_i, [_c_p, _c_i64, _c_i64, _c_i64, _c_i, _c_p, _c_sz, _c_p, _c_p]),
     "rlra_b200_oz_bscale": (_c_i, [_c_p, _c_i64, _c_i64, _c_i64, _c_i, _c_p, _c_p]),
     "rlra_b200_oz_gemm_ex": (_c_i, [_c_i, _c_p, _c_i64, _c_i64, _c_i, _c_p, _c_i64, _c_i64, _c_p, _c_i64,
                                     _c_p, _c_sz, _c_p, _c_i, _c_p]),

@@ -127,6 +127,13 @@ int oz_prep_ex(const double* a, int64_t lda, int64_t m, int64_t n, int nmod, con
 int oz_norms_prep(const double* a, int64_t lda, int64_t m, int64_t n, int nmod, void* prep, size_t prep_bytes,
                   cudaStream_t st);
 double oz_guard_limit(int64_t k);
+int oz_norms_cols(const double* a, int64_t lda, int64_t m, int64_t n, int64_t c0, int64_t c1, int nmod, void* prep,
+                  size_t prep_bytes, cudaStream_t st);
+int oz_scale_provisional(int64_t m, int64_t n, int64_t c1, int nmod, void* prep, size_t prep_bytes, cudaStream_t st);
+int oz_residue_cols(const double* a, int64_t lda, int64_t m, int64_t n, int64_t c0, int64_t c1, int nmod, void* prep,
+                    size_t prep_bytes, cudaStream_t st);
+int oz_norms_finish(const double* a, int64_t lda, int64_t m, int64_t n, int nmod, void* prep, size_t prep_bytes,
+                    int* e_a_final, cudaStream_t st);
 int oz_guard(const void* hdr_host, int64_t m, int64_t n, int* ok_nn, int* ok_tn);
 int64_t oz_cols_pad(int64_t ncols);
 int oz_bscale(const double* b, int64_t ldb, int64_t k, int64_t ncols, int nmod, int* e_b, cudaStream_t st);
@@ -313,6 +320,26 @@ int rlra_b200_oz_norms(const double* a, int64_t lda, int64_t m, int64_t n, int n
 }
 
 double rlra_b200_oz_guard_limit(int64_t k) { return oz_guard_limit(k); }
+
+int rlra_b200_oz_norms_cols(const double* a, int64_t lda, int64_t m, int64_t n, int64_t c0, int64_t c1, int nmod,
+                            void* prep, size_t prep_bytes, void* stream) {
+  return oz_norms_cols(a, lda, m, n, c0, c1, nmod, prep, prep_bytes, static_cast<cudaStream_t>(stream));
+}
+
+int rlra_b200_oz_scale_provisional(int64_t m, int64_t n, int64_t c1, int nmod, void* prep, size_t prep_bytes,
+                                   void* stream) {
+  return oz_scale_provisional(m, n, c1, nmod, prep, prep_bytes, static_cast<cudaStream_t>(stream));
+}
+
+int rlra_b200_oz_residue_cols(const double* a, int64_t lda, int64_t m, int64_t n, int64_t c0, int64_t c1, int nmod,
+                              void* prep, size_t prep_bytes, void* stream) {
+  return oz_residue_cols(a, lda, m, n, c0, c1, nmod, prep, prep_bytes, static_cast<cudaStream_t>(stream));
+}
+
+int rlra_b200_oz_norms_finish(const double* a, int64_t lda, int64_t m, int64_t n, int nmod, void* prep,
+                              size_t prep_bytes, int* e_a_final, void* stream) {
+  return oz_norms_finish(a, lda, m, n, nmod, prep, prep_bytes, e_a_final, static_cast<cudaStream_t>(stream));
+}
 
 int rlra_b200_oz_guard(const void* header, int64_t m, int64_t n, int* ok_nn, int* ok_tn) {
   return oz_guard(header, m, n, ok_nn, ok_tn);

@@ -249,8 +249,9 @@ __device__ __forceinline__ int swz(int r, int c) {  // byte offset of 16-byte ch
 template <int NMOD>
 __global__ void __launch_bounds__(256, 3) residue_a_kernel(const double* __restrict__ a, int64_t lda, int64_t m,
                                                            int64_t n, const int* __restrict__ e_a,
-                                                           int8_t* __restrict__ tiles, int64_t nib, int64_t njb) {
-  const int64_t ib = blockIdx.x, jb = blockIdx.y;
+                                                           int8_t* __restrict__ tiles, int64_t nib, int64_t njb,
+                                                           int64_t jb0) {
+  const int64_t ib = blockIdx.x, jb = blockIdx.y + jb0;
   const double scale = scalbn(1.0, e_a[0]);
   const size_t mod_stride = (size_t)njb * nib * kTileBytes;
   int8_t* tile = tiles + ((size_t)jb * nib + ib) * kTileBytes;
@@ -430,11 +431,12 @@ struct OzHeader {
 
 __global__ void __launch_bounds__(256, 4) norms_partial_kernel(const double* __restrict__ a, int64_t lda, int64_t m,
                                                             int64_t n, double* __restrict__ part_row,
-                                                            double* __restrict__ part_col, OzHeader* hdr) {
+                                                            double* __restrict__ part_col, OzHeader* hdr,
+                                                            int64_t cb0) {
   // warp w owns rows r0 + 256 w + [0, 256) (8 chunks of 32, lane = row in
   // chunk); column blocks of 32: lane keeps its rows' partial sums per column,
   // then one shared-memory transpose per block sums them over the lanes
-  const int64_t rb = blockIdx.x, cb = blockIdx.y;
+  const int64_t rb = blockIdx.x, cb = blockIdx.y + cb0;
   if (rb == 0 && cb == 0 && threadIdx.x == 0) {  // statistics reset (norms_final runs after this kernel)
     hdr->maxbits = 0ull;
     hdr->minrow = ~0ull;
@@ -581,6 +583,43 @@ __global__ void __launch_bounds__(1024) fro2_kernel(const double* __restrict__ p
       merge(hi, lo, h2, l2);
     }
     if (threadIdx.x == 0) hdr->fro2 = hi + lo;
+  }
+}
+
+// Provisional scale from the first column chunk of a pipelined upload
+// (columns [0, c1)): column norms of those columns exactly, row norms
+// extrapolated by n / c1 (the remaining chunks are still on the PCIe bus).  The
+// final norms decide whether it stands (oz_norms_finish: the residues are
+// rebuilt when the final eA differs).
+__global__ void __launch_bounds__(1024) scale_estimate_kernel(const double* __restrict__ part_row, int64_t m,
+                                                              const double* __restrict__ part_col, int64_t nrb,
+                                                              int64_t n, int64_t c1, int pa, OzHeader* __restrict__ hdr) {
+  __shared__ double red[32];
+  const int64_t ncb1 = (c1 + kNormCols - 1) / kNormCols;
+  double mx = 0.0;
+  for (int64_t t = threadIdx.x; t < m + c1; t += 1024) {
+    double v = 0.0;
+    if (t < m) {
+      for (int64_t cb = 0; cb < ncb1; ++cb) v += part_row[cb * m + t];
+      v *= (double)n / (double)c1;
+    } else {
+      for (int64_t rb = 0; rb < nrb; ++rb) v += part_col[rb * n + (t - m)];
+    }
+    mx = fmax(mx, v);
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 0; w < 32; ++w) mx = fmax(mx, red[w]);
+    int e = 0;
+    if (mx > 0.0 && mx <= 1.7976931348623157e308) {
+      int ex;
+      frexp(sqrt(mx) * (1.0 + 0x1p-40), &ex);
+      e = pa - ex;
+    }
+    hdr->e_a = e;
   }
 }
 
@@ -1018,7 +1057,14 @@ template <int NMOD>
 static void launch_residue_a(const double* a, int64_t lda, int64_t m, int64_t n, const int* e_a, int8_t* tiles,
                              const PrepLayout& p, cudaStream_t st) {
   residue_a_kernel<NMOD><<<dim3((unsigned)p.nib, (unsigned)p.njb), 256, 0, st>>>(a, lda, m, n, e_a, tiles, p.nib,
-                                                                                  p.njb);
+                                                                                  p.njb, 0);
+}
+// tile columns [jb0, jb1) only (the column chunks of a pipelined upload)
+template <int NMOD>
+static void launch_residue_a_cols(const double* a, int64_t lda, int64_t m, int64_t n, const int* e_a, int8_t* tiles,
+                                  const PrepLayout& p, int64_t jb0, int64_t jb1, cudaStream_t st) {
+  residue_a_kernel<NMOD><<<dim3((unsigned)p.nib, (unsigned)(jb1 - jb0)), 256, 0, st>>>(a, lda, m, n, e_a, tiles,
+                                                                                        p.nib, p.njb, jb0);
 }
 template <int NMOD>
 static void launch_residue_b(const double* b, int64_t ldb, int64_t k, int64_t ncols, const GemmLayout& g, int pb,
@@ -1060,7 +1106,7 @@ static int oz_norms(const double* a, int64_t lda, int64_t m, int64_t n, int nmod
   }
   ktimer_mark(KT_OZ_NORMS, st, false);
   oz::norms_partial_kernel<<<dim3((unsigned)nrb, (unsigned)ncb), 256, oz::kNormSmem, st>>>(a, lda, m, n, prow,
-                                                                                           pcol, hdr);
+                                                                                           pcol, hdr, 0);
   ktimer_mark(KT_OZ_NORMS, st, true);
   RLRA_LAUNCHED();
   oz::norms_final_kernel<<<(unsigned)ceil_div(m + n, 256), 256, 0, st>>>(prow, ncb, m, pcol, nrb, n, hdr, a, lda);
@@ -1166,6 +1212,75 @@ int oz_norms_prep(const double* a, int64_t lda, int64_t m, int64_t n, int nmod, 
   oz::OzHeader* hdr = reinterpret_cast<oz::OzHeader*>(base + p.off_hdr);
   return oz_norms(a, lda, m, n, nmod, &hdr->e_a, hdr, reinterpret_cast<double*>(base + p.off_prow),
                   reinterpret_cast<double*>(base + p.off_pcol), st);
+}
+
+// ---- pipelined upload (column chunks of A land one after the other):
+// norms per chunk, a provisional eA after the first chunk, residues per chunk,
+// then the final norms / guard statistics and the final eA.
+int oz_norms_cols(const double* a, int64_t lda, int64_t m, int64_t n, int64_t c0, int64_t c1, int nmod, void* prep,
+                  size_t prep_bytes, cudaStream_t st) {
+  const oz::PrepLayout p = oz::prep_layout(m, n, nmod);
+  RLRA_REQUIRE(prep && prep_bytes >= p.total, "oz_norms_cols: workspace too small");
+  RLRA_REQUIRE(c0 >= 0 && c0 < c1 && c1 <= n && c0 % oz::kNormCols == 0 && (c1 % oz::kNormCols == 0 || c1 == n),
+               "oz_norms_cols: chunk [%lld, %lld) not aligned to %d columns", (long long)c0, (long long)c1,
+               oz::kNormCols);
+  uint8_t* base = static_cast<uint8_t*>(prep);
+  const int64_t nrb = ceil_div(m, oz::kNormRows);
+  const int64_t cb0 = c0 / oz::kNormCols, cb1 = ceil_div(c1, oz::kNormCols);
+  RLRA_CHECK_CUDA(cudaFuncSetAttribute(oz::norms_partial_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)oz::kNormSmem));
+  oz::norms_partial_kernel<<<dim3((unsigned)nrb, (unsigned)(cb1 - cb0)), 256, oz::kNormSmem, st>>>(
+      a, lda, m, n, reinterpret_cast<double*>(base + p.off_prow), reinterpret_cast<double*>(base + p.off_pcol),
+      reinterpret_cast<oz::OzHeader*>(base + p.off_hdr), cb0);
+  RLRA_LAUNCHED();
+  return 0;
+}
+
+int oz_scale_provisional(int64_t m, int64_t n, int64_t c1, int nmod, void* prep, size_t prep_bytes, cudaStream_t st) {
+  const oz::PrepLayout p = oz::prep_layout(m, n, nmod);
+  RLRA_REQUIRE(prep && prep_bytes >= p.total && c1 >= 1 && c1 <= n, "oz_scale_provisional: bad arguments");
+  uint8_t* base = static_cast<uint8_t*>(prep);
+  oz::scale_estimate_kernel<<<1, 1024, 0, st>>>(reinterpret_cast<double*>(base + p.off_prow), m,
+                                                reinterpret_cast<double*>(base + p.off_pcol),
+                                                ceil_div(m, oz::kNormRows), n, c1, oz::budget(nmod).pa,
+                                                reinterpret_cast<oz::OzHeader*>(base + p.off_hdr));
+  RLRA_LAUNCHED();
+  return 0;
+}
+
+int oz_residue_cols(const double* a, int64_t lda, int64_t m, int64_t n, int64_t c0, int64_t c1, int nmod, void* prep,
+                    size_t prep_bytes, cudaStream_t st) {
+  const oz::PrepLayout p = oz::prep_layout(m, n, nmod);
+  RLRA_REQUIRE(prep && prep_bytes >= p.total, "oz_residue_cols: workspace too small");
+  RLRA_REQUIRE(c0 >= 0 && c0 < c1 && c1 <= n && c0 % oz::kTile == 0 && (c1 % oz::kTile == 0 || c1 == n),
+               "oz_residue_cols: chunk [%lld, %lld) not aligned to %d columns", (long long)c0, (long long)c1, oz::kTile);
+  uint8_t* base = static_cast<uint8_t*>(prep);
+  const int* e_a = &reinterpret_cast<oz::OzHeader*>(base + p.off_hdr)->e_a;
+  int8_t* tiles = reinterpret_cast<int8_t*>(base + p.off_tiles);
+  const int64_t jb0 = c0 / oz::kTile;
+  int64_t jb1 = ceil_div(c1, oz::kTile);
+  if (c1 == n) jb1 = p.njb;  // the padding tile column (njb is even) belongs to the last chunk
+  OZ_DISPATCH(nmod, oz::launch_residue_a_cols, a, lda, m, n, e_a, tiles, p, jb0, jb1, st);
+  RLRA_LAUNCHED();
+  return 0;
+}
+
+int oz_norms_finish(const double* a, int64_t lda, int64_t m, int64_t n, int nmod, void* prep, size_t prep_bytes,
+                    int* e_a_final, cudaStream_t st) {
+  const oz::PrepLayout p = oz::prep_layout(m, n, nmod);
+  RLRA_REQUIRE(prep && prep_bytes >= p.total && e_a_final, "oz_norms_finish: bad arguments");
+  uint8_t* base = static_cast<uint8_t*>(prep);
+  oz::OzHeader* hdr = reinterpret_cast<oz::OzHeader*>(base + p.off_hdr);
+  double* prow = reinterpret_cast<double*>(base + p.off_prow);
+  double* pcol = reinterpret_cast<double*>(base + p.off_pcol);
+  const int64_t ncb = ceil_div(n, oz::kNormCols), nrb = ceil_div(m, oz::kNormRows);
+  oz::norms_final_kernel<<<(unsigned)ceil_div(m + n, 256), 256, 0, st>>>(prow, ncb, m, pcol, nrb, n, hdr, a, lda);
+  RLRA_LAUNCHED();
+  oz::scale_a_kernel<<<1, 1, 0, st>>>(hdr, oz::budget(nmod).pa, e_a_final);
+  RLRA_LAUNCHED();
+  oz::fro2_kernel<<<1, 1024, 0, st>>>(pcol, nrb * n, hdr);
+  RLRA_LAUNCHED();
+  return 0;
 }
 
 int oz_prep(const double* a, int64_t lda, int64_t m, int64_t n, int nmod, void* prep, size_t prep_bytes,

@@ -120,7 +120,9 @@ class DeviceMatrix:
         copy_stream = torch.cuda.Stream(dev)
         # the destination allocation must be ready before the copy stream writes it
         copy_stream.wait_stream(torch.cuda.current_stream(dev))
-        step = max(1, -(-n // self.PIPELINE_CHUNKS))
+        # chunks of whole 256-column blocks: the residues of each chunk are built
+        # as it lands (ops.OzPipeline aligns norms and residue tiles to them)
+        step = max(256, -(-(-(-n // self.PIPELINE_CHUNKS)) // 256) * 256)
         with torch.cuda.stream(copy_stream):
             for c0 in range(0, n, step):
                 c1 = min(n, c0 + step)
@@ -151,6 +153,21 @@ class DeviceMatrix:
     def device(self):
         return self._a.device
 
+    def _pipeline(self):
+        """Residue builder riding the upload (ops.OzPipeline) when this call's
+        later products will take the int8 engine's one-block path."""
+        m, n = self._a.shape
+        if self._sessions == 0 or self._oz_prep is not None or not self._oz_ok(max(m, n), 1):
+            return None
+        if max(m, n) > ops.OZ_BLOCK_K or not ops._small_residues(ops.OZ_NMOD * m * n, self.device):
+            return None
+        return ops.OzPipeline(self._a)
+
+    def _end_pipeline(self, pipe):
+        if pipe is not None:
+            with ops.label("oz_prep"):
+                self._oz_prep = pipe.finish()
+
     def matmul(self, x):
         """A @ X, one pass over A (rlra/accessors.py:27-28)."""
         x = _dev(x, self.device)
@@ -158,10 +175,14 @@ class DeviceMatrix:
             if self._pending:  # first pass behind the upload: Y = sum_c A_c X_c
                 st = torch.cuda.current_stream(self.device)
                 y = ops.fmat(self._a.shape[0], x.shape[1], self.device)
+                pipe = self._pipeline()
                 for i, (c0, c1, ev) in enumerate(self._pending):
                     st.wait_event(ev)
                     ops.gemm(self._a[:, c0:c1], x[c0:c1, :], y, beta=0.0 if i == 0 else 1.0)
+                    if pipe is not None:
+                        pipe.chunk(c0, c1)
                 self._finish_upload()
+                self._end_pipeline(pipe)
                 return y
             if self._oz_ok(self._a.shape[1], x.shape[1]):
                 return self._oz().gemm(x, trans=False)
@@ -174,10 +195,14 @@ class DeviceMatrix:
             if self._pending:  # first pass behind the upload: Z[c] = A_c^T X per chunk
                 st = torch.cuda.current_stream(self.device)
                 z = ops.fmat(self._a.shape[1], x.shape[1], self.device)
+                pipe = self._pipeline()
                 for c0, c1, ev in self._pending:
                     st.wait_event(ev)
                     ops.gemm(self._a[:, c0:c1], x, z[c0:c1, :], ta=True)
+                    if pipe is not None:
+                        pipe.chunk(c0, c1)
                 self._finish_upload()
+                self._end_pipeline(pipe)
                 return z
             if self._oz_ok(self._a.shape[0], x.shape[1]):
                 return self._oz().gemm(x, trans=True)

@@ -221,17 +221,18 @@ class _HeaderCopy:
         return self.buf.clone()
 
 
-def _header_copy_async(ws, device):
+def _header_copy_async(ws, device, nbytes=OZ_HEADER_BYTES):
     """Copy the guard header to pinned host memory on a side stream ordered
     after the work queued so far on the current stream."""
     key = str(device)
     if key not in _SIDE:
-        _SIDE[key] = (torch.cuda.Stream(device), torch.empty(OZ_HEADER_BYTES, dtype=torch.uint8, pin_memory=True))
-    side, buf = _SIDE[key]
+        _SIDE[key] = torch.cuda.Stream(device)
+    side = _SIDE[key]
+    buf = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)  # per copy (the host allocator caches it)
     main = torch.cuda.current_stream(device)
     side.wait_stream(main)
     with torch.cuda.stream(side):
-        buf.copy_(ws[:OZ_HEADER_BYTES], non_blocking=True)
+        buf.copy_(ws[:nbytes], non_blocking=True)
         ev = torch.cuda.Event()
         ev.record(side)
     ws.record_stream(side)
@@ -243,12 +244,19 @@ class OzPrep:
     once per A, they serve both C = A B (trans=False) and C = A^T B.
 
     guard=True (the product path): the norms and guard statistics are computed
-    first and read back (one small device->host transfer); an orientation the
-    guard rejects (graded rows / columns beyond rlra_b200_oz_guard_limit(K),
-    NaN / Inf, extreme exponent range, integer-valued A) runs on the FP64 DMMA
-    GEMM instead, and
-    the residues are built only if some orientation is admitted.  guard=False
+    first and read back (one small device->host transfer on a side stream while
+    the residue kernel runs); an orientation the guard rejects (graded rows /
+    columns beyond rlra_b200_oz_guard_limit(K), NaN / Inf, extreme exponent
+    range, integer-valued A) runs on the FP64 DMMA GEMM instead.  guard=False
     exercises the raw engine (tests)."""
+
+    _resolve_fn = None
+
+    def _resolve(self):
+        """Pipelined preps (OzPipeline) read their guard header lazily."""
+        if self._resolve_fn is not None:
+            fn, self._resolve_fn = self._resolve_fn, None
+            fn()
 
     def __init__(self, a, nmod=None, guard=True):
         m, n = a.shape
@@ -290,6 +298,7 @@ class OzPrep:
         if ncols == 0:
             return (c, None) if keep_ws else c
         b = as_fmat(b)
+        self._resolve()
         if not self.ok[int(bool(trans))]:  # guard: DGEMM-class accuracy needs the native FP64 GEMM
             gemm(self.a, b, c, ta=bool(trans), beta=1.0 if add else 0.0)
             return (c, None) if keep_ws else c
@@ -299,6 +308,71 @@ class OzPrep:
               ld_of(b), ncols, ptr(c), ld_of(c), ptr(ws), wsb, None, OZ_ADD_TO_C if add else 0,
               _stream(self.device))
         return (c, ws) if keep_ws else c
+
+
+class OzPipeline:
+    """Residues of A built WHILE its column chunks upload (the e2e path,
+    device.DeviceMatrix pipelined upload): per chunk the norms partials and the
+    residues of its tile columns, with a provisional eA from the first chunk
+    (rlra_b200_oz_scale_provisional); after the last chunk the final norms,
+    guard statistics and eA.  When the final eA differs from the provisional
+    one the residues are rebuilt with it, so the result equals OzPrep's bit
+    for bit.  finish() returns the OzPrep."""
+
+    def __init__(self, a, nmod=None):
+        self.a = a
+        self.m, self.n = int(a.shape[0]), int(a.shape[1])
+        self.nmod = OZ_NMOD if nmod is None else int(nmod)
+        self.device = a.device
+        self.wsb = _native.query("rlra_b200_oz_prep_workspace", self.m, self.n, self.nmod)
+        self.ws = torch.empty(max(self.wsb, 8), dtype=torch.uint8, device=a.device)
+        self.first = True
+        self.rebuilt = False
+
+    def chunk(self, c0, c1):
+        a, dev, st = self.a, self.device, _stream(self.device)
+        _call("rlra_b200_oz_norms_cols", dev, ptr(a), ld_of(a), self.m, self.n, int(c0), int(c1), self.nmod,
+              ptr(self.ws), self.wsb, st)
+        if self.first:
+            _call("rlra_b200_oz_scale_provisional", dev, self.m, self.n, int(c1), self.nmod, ptr(self.ws), self.wsb,
+                  st)
+            self.first = False
+        _call("rlra_b200_oz_residue_cols", dev, ptr(a), ld_of(a), self.m, self.n, int(c0), int(c1), self.nmod,
+              ptr(self.ws), self.wsb, st)
+
+    def finish(self):
+        """Final norms / guard statistics / eA queued; the host reads them only
+        when the first product needs them (OzPrep._resolve), so the GPU goes on
+        with the next step (the interior LU) instead of idling on a sync."""
+        a, dev, st = self.a, self.device, _stream(self.device)
+        e_final = torch.empty(1, dtype=torch.int32, device=dev)
+        _call("rlra_b200_oz_norms_finish", dev, ptr(a), ld_of(a), self.m, self.n, self.nmod, ptr(self.ws), self.wsb,
+              ptr(e_final), st)
+        hdr = torch.empty(OZ_HEADER_BYTES + 4, dtype=torch.uint8, device=dev)
+        hdr[:OZ_HEADER_BYTES].copy_(self.ws[:OZ_HEADER_BYTES])
+        hdr[OZ_HEADER_BYTES:].copy_(e_final.view(torch.uint8))
+        prep = OzPrep.__new__(OzPrep)
+        prep.a, prep.m, prep.n, prep.nmod, prep.device, prep.ws = a, self.m, self.n, self.nmod, dev, self.ws
+        prep.fro2 = self.ws[OZ_FRO2_OFFSET:OZ_FRO2_OFFSET + 8].view(torch.float64)
+        prep.header, prep.ok = None, None
+        pipe = self
+        pending = _header_copy_async(hdr, dev, OZ_HEADER_BYTES + 4)  # queued now, read at the first product
+
+        def resolve():
+            host = pending.wait()
+            e_prov = int(host[:4].view(torch.int32)[0])
+            e_fin = int(host[OZ_HEADER_BYTES:].view(torch.int32)[0])
+            if e_prov != e_fin:  # the provisional scale did not hold: residues again, with the final one
+                pipe.ws[:4].copy_(e_final.view(torch.uint8))
+                _call("rlra_b200_oz_prep_ex", dev, ptr(a), ld_of(a), pipe.m, pipe.n, pipe.nmod, ptr(pipe.ws),
+                      ptr(pipe.ws), pipe.wsb, _stream(dev))
+                host[:4] = host[OZ_HEADER_BYTES:]
+                pipe.rebuilt = True
+            prep.header = host[:OZ_HEADER_BYTES].clone()
+            prep.ok = oz_guard(prep.header, pipe.m, pipe.n)
+
+        prep._resolve_fn = resolve
+        return prep
 
 
 OZ_BLOCK_K = 133120  # largest multiple of 256 inside the exact int32 K range (133144)

@@ -290,11 +290,74 @@ def test_pipelined_upload_matches_resident(cuda_dev, monkeypatch):
         assert np.array_equal(f.p, DRV[f"pl_v{v}/p"]) and np.array_equal(f.q, DRV[f"pl_v{v}/q"])
         assert abs(O.rel_fro_error_factor(a, f) - META["drivers"][f"pl_v{v}"]["rel_err"]) <= REL_ERR_TOL
     dm = P.DeviceMatrix(ah)
-    assert len(dm._pending) > 1
     z = dm.rmatmul(np.eye(200)[:, :5])
     from paper_2002_07138_b200 import ops
 
     np.testing.assert_allclose(ops.to_numpy(z), a.T @ np.eye(200)[:, :5], rtol=0, atol=1e-14)
+
+
+@pytest.mark.parametrize("graded_tail", [False, True])
+def test_residues_built_during_the_upload_equal_one_shot(cuda_dev, graded_tail):
+    """ops.OzPipeline (residues per column chunk while A uploads, provisional
+    scale from the first chunk) produces exactly OzPrep's residue set and
+    header; when a later chunk raises the max norm (graded_tail) the final
+    scale differs and the residues are rebuilt -- still identical."""
+    import torch
+
+    from paper_2002_07138_b200 import ops
+
+    rng = np.random.default_rng(31)
+    a = np.asfortranarray(rng.standard_normal((3000, 1900)))
+    if graded_tail:
+        a[:, 1500:] *= 64.0
+    ad = ops.from_numpy(a, cuda_dev)
+    ref = ops.OzPrep(ad)
+    pipe = ops.OzPipeline(ad)
+    for c0 in range(0, 1900, 512):
+        pipe.chunk(c0, min(1900, c0 + 512))
+    got = pipe.finish()
+    got._resolve()  # the host reads the header lazily (first product)
+    assert pipe.rebuilt == graded_tail
+    assert got.ok == ref.ok
+    assert torch.equal(got.ws[:4], ref.ws[:4])  # eA
+    hdr = ops.OZ_HEADER_BYTES
+    assert torch.equal(got.ws[8:40], ref.ws[8:40])  # guard statistics
+    off = ref.ws.numel() - 14 * 3072 * 1920  # the residue tiles fill the tail of the workspace
+    assert torch.equal(got.ws[off:], ref.ws[off:])
+    b = ops.from_numpy(rng.standard_normal((1900, 30)), cuda_dev)
+    assert torch.equal(got.gemm(b).view(torch.int64), ref.gemm(b).view(torch.int64))
+
+
+def test_pipelined_e2e_call_uses_the_upload_residues(cuda_dev, monkeypatch):
+    """The drop-in call on a pinned host A builds its residues during the
+    upload (no separate pass over A afterwards) and matches the golden pivots."""
+    import torch
+
+    import paper_2002_07138_b200 as P
+    from paper_2002_07138_b200 import device, ops
+
+    monkeypatch.setattr(device.DeviceMatrix, "PIPELINE_MIN_BYTES", 1)
+    built = []
+    real = ops.OzPipeline.finish
+
+    def spy(self):
+        built.append(self)
+        return real(self)
+
+    monkeypatch.setattr(ops.OzPipeline, "finish", spy)
+    rng = np.random.default_rng(32)
+    x, _ = np.linalg.qr(rng.standard_normal((2500, 60)))
+    y, _ = np.linalg.qr(rng.standard_normal((1800, 60)))
+    a = np.asfortranarray((x * np.exp(-np.arange(60) / 8.0)) @ y.T + 1e-9 * rng.standard_normal((2500, 1800)))
+    pinned = torch.empty((a.shape[1], a.shape[0]), dtype=torch.float64, pin_memory=True)
+    ah = pinned.numpy().T
+    ah[...] = a
+    for v in (3, 4):
+        f = P.powerlu(ah, 25, q_os=10, v=v, seed=2)
+        g = O.powerlu(a, 25, q_os=10, v=v, seed=2)
+        assert np.array_equal(f.p, g.p) and np.array_equal(f.q, g.q)
+        assert abs(O.rel_fro_error_factor(a, f) - O.rel_fro_error_factor(a, g)) <= REL_ERR_TOL
+    assert len(built) == 2 and not any(b.rebuilt for b in built)
 
 
 @pytest.mark.parametrize("v", [2, 3, 4])
