@@ -83,6 +83,26 @@ RLRA_B200_API size_t rlra_b200_getrf_workspace(int64_t m, int64_t n);
 RLRA_B200_API int rlra_b200_getrf(double* a, int64_t lda, int64_t m, int64_t n, int64_t* piv,
                     int64_t* nonzero_diag, void* ws, size_t ws_bytes, void* stream);
 RLRA_B200_API int rlra_b200_iota(int64_t* p, int64_t m, void* stream);
+/* Row-sharded exact GEPP primitives (distributed.dist_getrf_; bit-identical
+ * to rlra_b200_getrf).  getrf_block factors the 32-column block [j0, j0+nbo)
+ * of an m-row matrix whose VIRTUAL base `a` may be a gathered panel minus
+ * j0*lda (only columns [j0, j0+nbo) are touched); rows < j0 enter the
+ * zero-pivot column maxima only; piv (int64[m]) is permuted; zflag
+ * (int32[>= j0+nbo]) receives the block's zero-pivot flags, ipiv
+ * (int64[>= j0+nbo]) its interchange sequence (row j <-> ipiv[j]); *nonzero
+ * (int64) accumulates count_nonzero(diag(U)).  ws: rlra_b200_getrf_workspace(m, j0+nbo).
+ * lu_trsm_rows: U12 = L11^-1 A12 on rows [j0, j0+nb) of a virtual-row operand.
+ * lu_update_split: A(r0:m, c0:c1) -= L(r0:m, j0:j0+nb) U(j0:j0+nb, c0:c1)
+ * with L in `a` and U in `u`.  All follow the reference's rounding sequence
+ * (rlra/_lu_cython.pyx:14-55). */
+RLRA_B200_API int rlra_b200_getrf_block(double* a, int64_t lda, int64_t m, int64_t j0, int nbo, int64_t* piv,
+                                        int* zflag, int64_t* ipiv, int64_t* nonzero, void* ws, size_t ws_bytes,
+                                        void* stream);
+RLRA_B200_API int rlra_b200_lu_trsm_rows(double* a, int64_t lda, int64_t j0, int nb, int64_t c0, int64_t c1,
+                                         const int* zflag, void* stream);
+RLRA_B200_API int rlra_b200_lu_update_split(double* a, int64_t lda, const double* u, int64_t ldu, int64_t j0, int nb,
+                                            int64_t r0, int64_t m, int64_t c0, int64_t c1, const int* zflag,
+                                            void* stream);
 /* count_nonzero(diag(a)) over the leading r x r block -> device int64 *out
  * (rangefinder._check_width, rangefinder.py:55-64) */
 RLRA_B200_API int rlra_b200_count_nonzero_diag(const double* a, int64_t lda, int64_t r, int64_t* out,

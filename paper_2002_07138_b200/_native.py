@@ -34,6 +34,11 @@ SIGNATURES = {
     "rlra_b200_getrf_workspace": (_c_sz, [_c_i64, _c_i64]),
     "rlra_b200_getrf": (_c_i, [_c_p, _c_i64, _c_i64, _c_i64, _c_p, _c_p, _c_p, _c_sz, _c_p]),
     "rlra_b200_iota": (_c_i, [_c_p, _c_i64, _c_p]),
+    "rlra_b200_getrf_block": (_c_i, [_c_p, _c_i64, _c_i64, _c_i64, _c_i, _c_p, _c_p, _c_p, _c_p, _c_p, _c_sz,
+                                     _c_p]),
+    "rlra_b200_lu_trsm_rows": (_c_i, [_c_p, _c_i64, _c_i64, _c_i, _c_i64, _c_i64, _c_p, _c_p]),
+    "rlra_b200_lu_update_split": (_c_i, [_c_p, _c_i64, _c_p, _c_i64, _c_i64, _c_i, _c_i64, _c_i64, _c_i64, _c_i64,
+                                         _c_p, _c_p]),
     "rlra_b200_count_nonzero_diag": (_c_i, [_c_p, _c_i64, _c_i64, _c_p, _c_p]),
     "rlra_b200_lu_basis": (_c_i, [_c_p, _c_i64, _c_i64, _c_i64, _c_p, _c_p, _c_p, _c_i64, _c_p]),
     "rlra_b200_lu_extract": (_c_i, [_c_p, _c_i64, _c_i64, _c_i64, _c_p, _c_i64, _c_p, _c_i64, _c_p]),

@@ -73,6 +73,12 @@ size_t getrf_workspace_bytes(int64_t m, int64_t n);
 int getrf(double* a, int64_t lda, int64_t m, int64_t n, int64_t* piv, int64_t* nonzero_diag_dev,
           int* zflag_out, void* ws, size_t ws_bytes, cudaStream_t st);
 int fill_iota(int64_t* p, int64_t m, cudaStream_t st);
+int getrf_block(double* a, int64_t lda, int64_t m, int64_t j0, int nbo, int64_t* piv, int* zflag_out,
+                int64_t* ipiv_out, int64_t* nonzero_out, void* ws, size_t ws_bytes, cudaStream_t st);
+int lu_trsm_rows(double* a, int64_t lda, int64_t j0, int nb, int64_t c0, int64_t c1, const int* zflag,
+                 cudaStream_t st);
+int lu_update_split(double* a, int64_t lda, const double* u, int64_t ldu, int64_t j0, int nb, int64_t r0, int64_t m,
+                    int64_t c0, int64_t c1, const int* zflag, cudaStream_t st);
 int count_nonzero_diag(const double* a, int64_t lda, int64_t r, int64_t* out_dev, cudaStream_t st);
 int lu_basis(const double* lu, int64_t ldlu, int64_t m, int64_t k, const int64_t* piv,
              int64_t* pinv_ws, double* w, int64_t ldw, cudaStream_t st);
@@ -239,6 +245,21 @@ int rlra_b200_plu_inplace(double* lu, int64_t m, int64_t n, int64_t* piv) {
 }
 
 size_t rlra_b200_getrf_workspace(int64_t m, int64_t n) { return getrf_workspace_bytes(m, n); }
+
+int rlra_b200_getrf_block(double* a, int64_t lda, int64_t m, int64_t j0, int nbo, int64_t* piv, int* zflag,
+                          int64_t* ipiv, int64_t* nonzero, void* ws, size_t ws_bytes, void* stream) {
+  return getrf_block(a, lda, m, j0, nbo, piv, zflag, ipiv, nonzero, ws, ws_bytes, S(stream));
+}
+
+int rlra_b200_lu_trsm_rows(double* a, int64_t lda, int64_t j0, int nb, int64_t c0, int64_t c1, const int* zflag,
+                           void* stream) {
+  return lu_trsm_rows(a, lda, j0, nb, c0, c1, zflag, S(stream));
+}
+
+int rlra_b200_lu_update_split(double* a, int64_t lda, const double* u, int64_t ldu, int64_t j0, int nb, int64_t r0,
+                              int64_t m, int64_t c0, int64_t c1, const int* zflag, void* stream) {
+  return lu_update_split(a, lda, u, ldu, j0, nb, r0, m, c0, c1, zflag, S(stream));
+}
 
 int rlra_b200_getrf(double* a, int64_t lda, int64_t m, int64_t n, int64_t* piv,
                     int64_t* nonzero_diag, void* ws, size_t ws_bytes, void* stream) {

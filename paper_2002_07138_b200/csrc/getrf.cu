@@ -726,15 +726,15 @@ static constexpr int LU_PANEL_SMEM_BYTES = 200 * 1024;
 // Apply the panel's net row permutation to columns [0, j0) and [j0+nb, n).
 // One warp per column: gather every touched row, then scatter.
 __global__ void lu_laswp_kernel(double* a, int64_t lda, int64_t n, int64_t j0, int nb,
-                                const int64_t* rows, const int64_t* src, const int* cnt_p) {
+                                const int64_t* rows, const int64_t* src, const int* cnt_p, int64_t c_lo = 0) {
   const int cnt = *cnt_p;
   if (cnt == 0) return;
   const int lane = threadIdx.x & 31;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const int64_t ncols = n - nb;
+  const int64_t ncols = n - c_lo - nb;  // columns [c_lo, n) except the panel [j0, j0 + nb)
   for (int64_t w = warp; w < ncols; w += nwarps) {
-    const int64_t c = w < j0 ? w : w + nb;
+    const int64_t c = c_lo + w < j0 ? c_lo + w : c_lo + w + nb;
     double* col = a + cm(0, c, lda);
     double v0 = 0.0, v1 = 0.0;
     if (lane < cnt) v0 = col[src[lane]];
@@ -776,7 +776,11 @@ __global__ void lu_trsm_kernel(double* a, int64_t lda, int64_t j0, int nb, int64
 constexpr int UPD_TM = 64, UPD_TN = 64;
 __global__ void __launch_bounds__(256, 4)
 lu_update_kernel(double* a, int64_t lda, int64_t j0, int nb, int64_t r0, int64_t m, int64_t c0,
-                 int64_t n, const int* zflag) {
+                 int64_t n, const int* zflag, const double* u = nullptr, int64_t ldu = 0) {
+  if (u == nullptr) {  // U12 in the same matrix (rows j0 .. j0 + nb); else a separate (virtual-row) operand
+    u = a;
+    ldu = lda;
+  }
   __shared__ double Ls[LU_NB][UPD_TM];
   __shared__ double Us[LU_NB][UPD_TN + 1];
   __shared__ int z[LU_NB];
@@ -790,7 +794,7 @@ lu_update_kernel(double* a, int64_t lda, int64_t j0, int nb, int64_t r0, int64_t
   for (int e = threadIdx.x; e < nb * UPD_TN; e += blockDim.x) {
     int t = e % nb, c = e / nb;
     int64_t gc = ct + c;
-    Us[t][c] = gc < n ? a[cm(j0 + t, gc, lda)] : 0.0;
+    Us[t][c] = gc < n ? u[cm(j0 + t, gc, ldu)] : 0.0;
   }
   if (threadIdx.x < nb) z[threadIdx.x] = zflag[j0 + threadIdx.x];
   __syncthreads();
@@ -1003,6 +1007,151 @@ static int lu_prepare_kernel(const void* kern) {
 // diagonal and U on/above it, `piv` (caller-preloaded, typically 0..m-1) is
 // permuted like the reference's piv (rlra/_lu_cython.pyx:14, rlra/kernels.py:48),
 // and *nonzero_diag_dev (device int64) receives count_nonzero(diag(U)).
+// ------------------------------------------------------------------ distributed primitives
+// The row-sharded exact GEPP (distributed.dist_getrf_) runs the blocked
+// algorithm with every 32-column block's panel all-gathered: each rank factors
+// the gathered m x 32 panel redundantly (identical pivots everywhere), U12
+// comes from the block's 32 gathered rows, and each rank updates only its own
+// rows.  Every element sees the reference's rounding sequence, exactly as in
+// getrf(): the result is bit-identical to the one-GPU kernel.
+
+__global__ void add_nonzero_diag_kernel(const double* a, int64_t lda, int64_t j0, int r, int64_t* out) {
+  __shared__ int s[32];
+  int cnt = 0;
+  for (int i = threadIdx.x; i < r; i += blockDim.x) cnt += (a[cm(j0 + i, j0 + i, lda)] != 0.0);
+#pragma unroll
+  for (int off = 16; off; off >>= 1) cnt += __shfl_down_sync(0xffffffffu, cnt, off);
+  if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = cnt;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int tot = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); w++) tot += s[w];
+    *out += tot;
+  }
+}
+
+// Factor the 32-column block [j0, j0 + nbo) of an m-row matrix in place: its
+// panels, their interchanges restricted to the block's columns, the inner
+// U12 / updates.  `a` is the VIRTUAL base (only columns [j0, j0 + nbo) are
+// touched -- a gathered panel passed as panel - j0 * lda); rows < j0 are the
+// rows above (they enter the zero-pivot column maxima only); piv (int64[m]) is
+// permuted; zflag_out[j0 .. j0 + nbo) receives the zero-pivot flags,
+// ipiv_out[j0 .. j0 + nbo) the pivot row of each step (the interchange
+// sequence j <-> ipiv[j]) and *nonzero_out accumulates count_nonzero(diag(U)).  ws: a getrf
+// workspace for (m, >= j0 + nbo) columns.
+int getrf_block(double* a, int64_t lda, int64_t m, int64_t j0, int nbo, int64_t* piv, int* zflag_out,
+                int64_t* ipiv_out, int64_t* nonzero_out, void* ws, size_t ws_bytes, cudaStream_t st) {
+  RLRA_REQUIRE(m >= 1 && j0 >= 0 && nbo >= 1 && nbo <= LU_NB && j0 + nbo <= m && lda >= m,
+               "getrf_block: bad block (m=%lld j0=%lld nbo=%d)", (long long)m, (long long)j0, nbo);
+  const int sms = device_info().sm_count;
+  LuLayout L = lu_layout(j0 + nbo, sms);
+  RLRA_REQUIRE(ws != nullptr && ws_bytes >= L.total, "getrf_block: workspace too small (%zu < %zu)", ws_bytes,
+               L.total);
+  LuWork w = lu_work(ws, j0 + nbo, sms);
+  RLRA_CHECK_CUDA(cudaMemsetAsync(w.bar, 0, 2 * sizeof(unsigned), st));
+  auto rows_cap = [](int pw) { return (int64_t)(LU_PANEL_SMEM_BYTES / (pw * 8)); };
+  const int cmax = lu_max_cluster();
+  const bool use_cluster = cmax > 1 && m <= cmax * rows_cap(16);
+  int pw;
+  if (use_cluster) pw = (m <= cmax * rows_cap(32)) ? 32 : 16;
+  else pw = (m <= sms * rows_cap(32)) ? 32 : (m <= sms * rows_cap(16) ? 16 : 8);
+  RLRA_REQUIRE(m <= sms * rows_cap(8), "getrf_block: m = %lld exceeds the panel capacity", (long long)m);
+  const void* kern = use_cluster
+      ? (pw == 32 ? (const void*)lu_panel_cluster_kernel<32, 512> : (const void*)lu_panel_cluster_kernel<16, 512>)
+      : (pw == 32 ? (const void*)lu_panel_smem_kernel<32, 512>
+                  : pw == 16 ? (const void*)lu_panel_smem_kernel<16, 512> : (const void*)lu_panel_smem_kernel<8, 512>);
+  if (lu_prepare_kernel(kern)) return -1;
+  unsigned bar_base = 0;
+  const int64_t ce = j0 + nbo;
+  for (int64_t jp = j0; jp < ce; jp += pw) {
+    const int nb = (int)std::min<int64_t>(pw, ce - jp);
+    const int64_t active = m - jp;
+    PanelArgs pa;
+    pa.a = a; pa.lda = lda; pa.m = m; pa.n = ce; pa.j0 = jp; pa.nb = nb;
+    pa.piv = piv;
+    pa.w = w;
+    pa.bar_base = bar_base;
+    pa.trace = lu_trace_buffer();
+    const int limit = use_cluster ? cmax : sms;
+    const int64_t target = std::min<int64_t>(rows_cap(pw), 512);
+    int G = (int)std::min<int64_t>(limit, ceil_div(active, target));
+    G = (int)std::max<int64_t>(G, ceil_div(active, rows_cap(pw)));
+    pa.rows_per_cta = ceil_div(active, G);
+    pa.rows_per_cta += pa.rows_per_cta & 1;
+    pa.above_per_cta = std::max<int64_t>(1, ceil_div(jp, G));
+    const size_t smem = (size_t)pa.rows_per_cta * nb * sizeof(double);
+    void* args[] = {&pa};
+    if (use_cluster) {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(G);
+      cfg.blockDim = dim3(512);
+      cfg.dynamicSmemBytes = smem;
+      cfg.stream = st;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = G;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      RLRA_CHECK_CUDA(cudaLaunchKernelExC(&cfg, kern, args));
+    } else {
+      RLRA_CHECK_CUDA(cudaLaunchCooperativeKernel(kern, dim3(G), dim3(512), args, smem, st));
+      bar_base += (unsigned)G * nb;
+    }
+    note_launch();
+    if (nbo > nb) {  // the panel's interchanges on the block's other columns only
+      const int64_t ncols = nbo - nb;
+      const int blocks = (int)std::min<int64_t>(ceil_div(ncols * 32, 256), 2048);
+      lu_laswp_kernel<<<blocks, 256, 0, st>>>(a, lda, ce, jp, nb, w.perm_rows, w.perm_src, w.perm_cnt, j0);
+      RLRA_LAUNCHED();
+    }
+    const int64_t c0 = jp + nb;
+    if (c0 < ce) {
+      lu_trsm_kernel<<<(unsigned)ceil_div(ce - c0, 4), 128, 0, st>>>(a, lda, jp, nb, c0, ce, w.zflag);
+      RLRA_LAUNCHED();
+      if (c0 < m) {
+        dim3 grid((unsigned)ceil_div(m - c0, UPD_TM), (unsigned)ceil_div(ce - c0, UPD_TN));
+        lu_update_kernel<<<grid, 256, 0, st>>>(a, lda, jp, nb, c0, m, c0, ce, w.zflag);
+        RLRA_LAUNCHED();
+      }
+    }
+  }
+  if (zflag_out)
+    RLRA_CHECK_CUDA(cudaMemcpyAsync(zflag_out + j0, w.zflag + j0, nbo * sizeof(int), cudaMemcpyDeviceToDevice, st));
+  if (ipiv_out)  // pivot row chosen at each step (== j without a swap): the block's interchange sequence
+    RLRA_CHECK_CUDA(cudaMemcpyAsync(ipiv_out + j0, w.ipiv + j0, nbo * sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
+  if (nonzero_out) {
+    add_nonzero_diag_kernel<<<1, 256, 0, st>>>(a, lda, j0, nbo, nonzero_out);
+    RLRA_LAUNCHED();
+  }
+  return 0;
+}
+
+// U12 = L11^{-1} A12 (bit-exact forward substitution) on rows [j0, j0 + nb) of
+// a virtual-row operand (the block's gathered rows passed as rows - j0).
+int lu_trsm_rows(double* a, int64_t lda, int64_t j0, int nb, int64_t c0, int64_t c1, const int* zflag,
+                 cudaStream_t st) {
+  RLRA_REQUIRE(nb >= 1 && nb <= LU_NB && c1 >= c0, "lu_trsm_rows: bad arguments");
+  if (c1 == c0) return 0;
+  const int blocks = (int)std::min<int64_t>(ceil_div(c1 - c0, 4), 4096);
+  lu_trsm_kernel<<<blocks, 128, 0, st>>>(a, lda, j0, nb, c0, c1, zflag);
+  RLRA_LAUNCHED();
+  return 0;
+}
+
+// A(r0:m, c0:c1) -= L(r0:m, j0:j0+nb) U(j0:j0+nb, c0:c1), L in `a`, U in `u`
+// (virtual rows), bit-exact (rank-1 terms ascending, DMUL then DSUB).
+int lu_update_split(double* a, int64_t lda, const double* u, int64_t ldu, int64_t j0, int nb, int64_t r0, int64_t m,
+                    int64_t c0, int64_t c1, const int* zflag, cudaStream_t st) {
+  RLRA_REQUIRE(nb >= 1 && nb <= LU_NB, "lu_update_split: bad nb");
+  if (r0 >= m || c1 <= c0) return 0;
+  dim3 grid((unsigned)ceil_div(m - r0, UPD_TM), (unsigned)ceil_div(c1 - c0, UPD_TN));
+  lu_update_kernel<<<grid, 256, 0, st>>>(a, lda, j0, nb, r0, m, c0, c1, zflag, u, ldu);
+  RLRA_LAUNCHED();
+  return 0;
+}
+
 int getrf(double* a, int64_t lda, int64_t m, int64_t n, int64_t* piv, int64_t* nonzero_diag_dev,
           int* zflag_out, void* ws, size_t ws_bytes, cudaStream_t st) {
   RLRA_REQUIRE(m >= 0 && n >= 0, "getrf: negative dimension");

@@ -87,6 +87,52 @@ class CudaOps:
     def zeros(self, m, n):
         return self.o.fmat(m, n, self.device, zero=True)
 
+    # ---- row-sharded exact GEPP primitives (dist_getrf_; csrc/getrf.cu)
+    def gepp_state(self, m, n):
+        """piv (iota), zflag, ipiv, nonzero count and the getrf workspace."""
+        o = self.o
+        wsb = o._native.query("rlra_b200_getrf_workspace", m, n)
+        return {"piv": o.iota(m, self.device),
+                "zflag": torch.zeros(max(n, 1), dtype=torch.int32, device=self.device),
+                "ipiv": torch.zeros(max(n, 1), dtype=torch.int64, device=self.device),
+                "cnt": torch.zeros(1, dtype=torch.int64, device=self.device),
+                "ws": torch.empty(max(wsb, 8), dtype=torch.uint8, device=self.device), "wsb": wsb}
+
+    def getrf_block(self, panel, j0, nbo, stt):
+        """Factor the gathered m x nbo panel (global columns [j0, j0+nbo)) in place."""
+        o, m = self.o, panel.shape[0]
+        base = o.ptr(panel) - 8 * j0 * o.ld_of(panel)  # virtual base: column j0 is the panel's first
+        o._call("rlra_b200_getrf_block", self.device, base, o.ld_of(panel), m, j0, nbo, o.ptr(stt["piv"]),
+                o.ptr(stt["zflag"]), o.ptr(stt["ipiv"]), o.ptr(stt["cnt"]), o.ptr(stt["ws"]), stt["wsb"],
+                o._stream(self.device))
+
+    def unit_lower_rows(self, local, pos0):
+        """Rows [pos0, pos0 + rows) of a packed L\\U -> the same rows of the unit
+        lower L (min(m, n) columns): entries left of the diagonal, 1 on it."""
+        rows, n = local.shape
+        out = self.o.fmat(rows, n, self.device)
+        out.copy_(torch.tril(local, diagonal=pos0 - 1))
+        lo, hi = max(0, pos0), min(pos0 + rows, n)
+        if hi > lo:  # rows past the last column (most ranks' shards) have no diagonal entry
+            d = torch.arange(lo, hi, device=self.device)
+            out[d - pos0, d] = 1.0
+        return out
+
+    def ipiv_host(self, stt, j0, nbo):
+        return stt["ipiv"][j0:j0 + nbo].cpu().tolist()
+
+    def lu_trsm_rows(self, blk, j0, nbo, c0, c1, stt):
+        """U12 = L11^-1 A12 in the block's gathered rows (nbo x n, global rows j0..)."""
+        o = self.o
+        o._call("rlra_b200_lu_trsm_rows", self.device, o.ptr(blk) - 8 * j0, o.ld_of(blk), j0, nbo, c0, c1,
+                o.ptr(stt["zflag"]), o._stream(self.device))
+
+    def lu_update_split(self, local, blk, j0, nbo, r_lo, c0, c1, stt):
+        """local[r_lo:, c0:c1] -= local[r_lo:, j0:j0+nbo] U12 (U12 in blk)."""
+        o = self.o
+        o._call("rlra_b200_lu_update_split", self.device, o.ptr(local), o.ld_of(local), o.ptr(blk) - 8 * j0,
+                o.ld_of(blk), j0, nbo, r_lo, local.shape[0], c0, c1, o.ptr(stt["zflag"]), o._stream(self.device))
+
     def sweep_width(self, m, panel):
         from .singlepass import sweep_width
 
@@ -370,6 +416,101 @@ def _check(count, requested):
         raise RankCollapse(achieved, requested)
 
 
+LU_BLOCK = 32  # csrc/getrf.cu LU_NB
+
+
+def _net_perm(j0, seq):
+    """Net row permutation of the interchange sequence (row j0+q <-> seq[q],
+    q ascending) as (touched positions, source positions)."""
+    rows, src = [], {}
+    for q, pr in enumerate(seq):
+        jq = j0 + q
+        if pr == jq:
+            continue
+        for r in (jq, pr):
+            if r not in src:
+                src[r] = r
+                rows.append(r)
+        src[jq], src[pr] = src[pr], src[jq]
+    return rows, [src[r] for r in rows]
+
+
+def _owned_rows(A, buf, positions):
+    """Every rank gets the rows of `buf` (len(positions) x n) that their owners
+    filled: all-gather, then each row from its owner's copy -- a summing
+    all-reduce would turn -0.0 into +0.0 (bit-exactness includes zero signs)."""
+    if A.world == 1:
+        return buf
+    send = buf.t().contiguous()  # column-major (rows, n) == row-major (n, rows)
+    outs = [torch.empty_like(send) for _ in range(A.world)]
+    dist.all_gather(outs, send, group=A.group)
+    res = A.ops.empty(buf.shape[0], buf.shape[1])
+    for t, pos in enumerate(positions):
+        owner = _owner(A.m, A.world, pos)
+        res[t].copy_(outs[owner].t()[t])
+    return res
+
+
+def _owner(m, world, pos):
+    per = -(-m // world)
+    return min(world - 1, pos // per) if per else 0
+
+
+def dist_getrf_(A, local):
+    """Exact GEPP (rlra/_lu_cython.pyx:14-55, bit-identical to the one-GPU
+    kernel) of the row-sharded m x n matrix whose rows [A.r0, A.r1) this rank
+    holds as `local` (factored in place: its rows of the packed L\\U, in the
+    final row order).  Per 32-column block J:
+      1. all-gather the panel's m x 32 columns (positions order);
+      2. every rank factors it redundantly (getrf_block: same pivots everywhere);
+      3. the block's interchanges move <= 64 full rows between ranks (one
+         all-reduce of those rows);
+      4. the block's 32 rows are all-reduced, U12 = L11^-1 A12 on every rank;
+      5. each rank updates only its own rows (bit-exact update kernel).
+    Communication per block: m*32 + 96*n doubles; no m x n gather, no
+    replicated m x n factorization.  Returns (piv replicated int64[m], the
+    n x n block rows of U replicated (rows 0..n of the packed factor), the
+    nonzero-diagonal count)."""
+    ops = A.ops
+    m, n = A.m, local.shape[1]
+    r0, r1 = A.r0, A.r1
+    stt = ops.gepp_state(m, n)
+    urows = ops.zeros(min(m, n), n)
+    for j0 in range(0, min(m, n), LU_BLOCK):
+        nbo = min(LU_BLOCK, min(m, n) - j0)
+        panel = A.gather_rows(local[:, j0:j0 + nbo])
+        ops.getrf_block(panel, j0, nbo, stt)
+        rows, srcs = _net_perm(j0, ops.ipiv_host(stt, j0, nbo))
+        if rows:  # full-row interchanges on the columns outside the block
+            moved = ops.zeros(len(rows), n)
+            for t, sp in enumerate(srcs):
+                if r0 <= sp < r1:
+                    moved[t].copy_(local[sp - r0])
+            moved = _owned_rows(A, moved, srcs)
+            for t, rp in enumerate(rows):
+                if r0 <= rp < r1:
+                    if j0 > 0:
+                        local[rp - r0, :j0].copy_(moved[t, :j0])
+                    if j0 + nbo < n:
+                        local[rp - r0, j0 + nbo:].copy_(moved[t, j0 + nbo:])
+        if r1 > r0:
+            local[:, j0:j0 + nbo].copy_(panel[r0:r1])
+        blk = ops.zeros(nbo, n)  # the block's rows j0..j0+nbo, all columns
+        b0, b1 = max(r0, j0), min(r1, j0 + nbo)
+        if b1 > b0:
+            blk[b0 - j0:b1 - j0].copy_(local[b0 - r0:b1 - r0])
+        blk = _owned_rows(A, blk, range(j0, j0 + nbo))
+        if j0 + nbo < n:
+            ops.lu_trsm_rows(blk, j0, nbo, j0 + nbo, n, stt)
+            if b1 > b0:
+                local[b0 - r0:b1 - r0, j0 + nbo:].copy_(blk[b0 - j0:b1 - j0, j0 + nbo:])
+            lo = max(r0, j0 + nbo) - r0
+            if lo < r1 - r0:
+                ops.lu_update_split(local, blk, j0, nbo, lo, j0 + nbo, n, stt)
+        urows[j0:j0 + nbo].copy_(blk)
+    return stt["piv"], urows, stt["cnt"]
+
+
 def _use_tslu(A, l):
     """Interior LU of a row-sharded sketch: TSLU at 4+ ranks or tall sketches
     (the all-gather of m x l and the replicated m x l GEPP grow with m, the
@@ -470,11 +611,72 @@ def _assemble(A, l1, u2, l2, piv1, piv2, k, cut=None):
     return DistLU(piv1, piv2, big_l, big_u, k, p0, p1, m, A.group, ops)
 
 
+DIST_GEPP = os.environ.get("RLRA_B200_DIST_GEPP", "1") == "1"  # 0: all-gather + replicated exact GEPP
+
+
+def _dist_lu(S, local):
+    """Row-sharded exact GEPP of S (a ShardedMatrix over `local`, factored in a
+    copy): (piv replicated, U (r x r upper, replicated), this rank's rows of the
+    unit-lower L in final row order, nonzero-diagonal count)."""
+    ops = S.ops
+    work = ops.empty(local.shape[0], local.shape[1])
+    work.copy_(local)
+    piv, urows, cnt = dist_getrf_(S, work)
+    _, u = ops.lu_extract(urows)
+    return piv, u, ops.unit_lower_rows(work, S.r0), cnt
+
+
+def _lu_factors_sharded(A, left_local, right_rows, k):
+    """The two exact GEPPs of rlra/fixedrank.py:144-146 / singlepass.py:
+    :134-136 without gathering the tall operand: LU(left) over A's row shards,
+    the right operand (n x k) computed / sliced by row blocks, its LU sharded
+    too; L = L1 U2^T by this rank's rows, U = L2^T (L2 all-gathered)."""
+    piv1, u1, l1_rows, cnt = _dist_lu(A, left_local)
+    n = right_rows.n_total
+    c0, c1 = row_range(n, A.world, A.rank)
+    bt_local = right_rows.rows(u1, c0, c1)
+    B = ShardedMatrix(bt_local, n, c0, c1, A.ops, A.group)
+    piv2, u2, l2_rows, _ = _dist_lu(B, bt_local)
+    big_l = A.ops.matmul(l1_rows, u2, tb=True)
+    l2 = B.gather_rows(l2_rows)
+    big_u = A.ops.transpose(l2)
+    return piv1, piv2, big_l, big_u, cnt
+
+
+class _BtRows:
+    """B^T = V_k U1^T (rlra/fixedrank.py:145) by row blocks."""
+
+    def __init__(self, vk, ops):
+        self.vk, self.ops, self.n_total = vk, ops, vk.shape[0]
+
+    def rows(self, u1, c0, c1):
+        return self.ops.matmul(self.vk[c0:c1], u1, tb=True)
+
+
+class _TRows:
+    """T = (G^T)^+ U1^T (rlra/singlepass.py:135) replicated, sliced by row blocks."""
+
+    def __init__(self, g, ops):
+        self.g, self.ops, self.n_total = g, ops, g.shape[0]
+
+    def rows(self, u1, c0, c1):
+        t = self.ops.pinv_transpose_apply(self.g, self.ops.transpose(u1))
+        out = self.ops.empty(c1 - c0, t.shape[1])
+        out.copy_(t[c0:c1])
+        return out
+
+
 def lu_from_projection(A: ShardedMatrix, g_local, vk):
-    """rlra/fixedrank.py:136-146 with G gathered for the exact GEPP (p, q
-    identical to one GPU); L = L1 U2^T formed by row blocks (DistLU)."""
+    """rlra/fixedrank.py:136-146 over the row shards: the exact GEPP of G and
+    of B^T = V_k U1^T run row-sharded (dist_getrf_: bit-identical to the
+    one-GPU kernel, so p and q are the reference's), L = L1 U2^T by row blocks
+    (DistLU), U = L2^T.  RLRA_B200_DIST_GEPP=0: G all-gathered and factored
+    redundantly on every rank (round 1)."""
     ops = A.ops
     k = g_local.shape[1]
+    if DIST_GEPP and A.world > 1 and hasattr(ops, "gepp_state"):
+        piv1, piv2, big_l, big_u, _ = _lu_factors_sharded(A, g_local, _BtRows(vk, ops), k)
+        return DistLU(piv1, piv2, big_l, big_u, k, A.r0, A.r1, A.m, A.group, ops)
     g = A.gather_rows(g_local)
     piv1, cnt = ops.getrf_(g)
     l1, u1 = ops.lu_extract(g)
@@ -482,7 +684,6 @@ def lu_from_projection(A: ShardedMatrix, g_local, vk):
     piv2, _ = ops.getrf_(bt)
     l2, u2 = ops.lu_extract(bt)
     return _assemble(A, l1, u2, l2, piv1, piv2, k)
-
 
 
 # ---------------------------------------------------------------- sharded factorizations of replicated sketches
@@ -688,6 +889,11 @@ def single_pass_lu(A: ShardedMatrix, k, seed, omega_fn, q_os=0, panel=256):
     l = k + q_os
     ops = A.ops
     g, h_local = stream_sketch(A, l, seed, omega_fn, panel)
+    if DIST_GEPP and A.world > 1 and hasattr(ops, "gepp_state"):
+        piv1, piv2, big_l, big_u, _ = _lu_factors_sharded(A, h_local, _TRows(g, ops), l)
+        if q_os:
+            big_l, big_u = big_l[:, :k], big_u[:k, :]
+        return DistLU(piv1, piv2, big_l, big_u, k, A.r0, A.r1, A.m, A.group, ops)
     h = A.gather_rows(h_local)
     piv1, _ = ops.getrf_(h)
     l1, u1 = ops.lu_extract(h)

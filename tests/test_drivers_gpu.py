@@ -272,6 +272,48 @@ def test_distributed_path_single_rank_nccl(cuda_dev):
         dist.destroy_process_group()
 
 
+@pytest.mark.parametrize("m,n", [(3000, 96), (600, 230), (70000, 64)])
+def test_row_sharded_gepp_primitives_on_device(cuda_dev, m, n):
+    """distributed.dist_getrf_ on the CUDA ops (getrf_block on the gathered
+    panel, lu_trsm_rows, lu_update_split; one rank -- the multi-rank exchanges
+    are the gloo tests): every bit of the packed factor and the pivots equal
+    the one-launch kernel's / the reference's, cooperative and blocked panel
+    paths (70000 rows)."""
+    import os
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2002_07138_b200 import distributed as D, ops
+
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29519")
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=cuda_dev)
+    try:
+        rng = np.random.default_rng(m + n)
+        a = rng.standard_normal((m, n))
+        a[:, 40] = a[:, 7]
+        a[:, 50] = 0.0
+        a = np.asfortranarray(a)
+        loc = ops.from_numpy(a, cuda_dev)
+        S = D.ShardedMatrix(loc, m, 0, m, D.CudaOps(cuda_dev))
+        piv, urows, cnt = D.dist_getrf_(S, loc)
+        lu_ref = a.copy(order="F")
+        piv_ref = np.arange(m, dtype=np.int64)
+        O.plu_inplace(lu_ref, piv_ref)
+        assert np.array_equal(piv.cpu().numpy(), piv_ref)
+        assert np.array_equal(ops.to_numpy(loc).view(np.int64), lu_ref.view(np.int64))
+        assert np.array_equal(ops.to_numpy(urows).view(np.int64), lu_ref[:n].view(np.int64))
+        assert int(cnt.item()) == int(np.count_nonzero(np.diag(lu_ref)))
+        L = np.tril(lu_ref[:, :n], -1)
+        L[np.arange(n), np.arange(n)] = 1.0
+        for r0, r1 in ((0, 50), (40, 300), (400, 600)):  # straddling the last column and past it
+            l_rows = D.CudaOps(cuda_dev).unit_lower_rows(loc[r0:r1], r0)
+            assert np.array_equal(ops.to_numpy(l_rows), L[r0:r1])
+    finally:
+        dist.destroy_process_group()
+
+
 def test_pipelined_upload_matches_resident(cuda_dev, monkeypatch):
     """Pinned host input: column chunks are uploaded on a copy stream and the
     first pass consumes them as they land; results equal the resident run."""
