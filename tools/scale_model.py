@@ -18,7 +18,9 @@ The pieces follow distributed.py exactly (v even, fast_qr):
   TN pass  Z = sum A_i^T W_i            all-reduce n x l
   QR(Z)    sharded sCholQR3 on (n/P) x l blocks, all-reduced l x l Grams, all-gather Q
   NN pass  G_i = A_i V_k
-  LU(G)    all-gather G, exact GEPP m x k (replicated), B^T, GEPP n x k, L_i = L1_i U2^T
+  LU(G)    row-sharded exact GEPP (dist_getrf_: gathered 32-column panels factored
+           redundantly, local updates), B^T by row blocks and its row-sharded GEPP,
+           L_i = L1_i U2^T, L2 all-gathered for U = L2^T
 
 usage: python tools/scale_model.py [C5|C2] [P ...]   -> JSON on stdout
 """
@@ -72,6 +74,41 @@ def gepp_ms(m, n, dev):
         a.copy_(a0)
         ops.getrf_(a)
     return timed(run)
+
+
+def dist_gepp_ms(m, n, p, dev, host_sync_ms=0.03):
+    """Per-rank compute of distributed.dist_getrf_ at P ranks: every 32-column
+    block's gathered m x 32 panel factored (getrf_block, redundant), U12 of the
+    block rows, the update of this rank's m/P rows; the per-block interchange
+    read-back costs host_sync_ms.  Communication is modelled by the caller."""
+    from paper_2002_07138_b200.distributed import CudaOps
+
+    cops = CudaOps(dev)
+    rows = -(-m // p)
+    local = rand(rows, n, dev)
+    panel0 = rand(m, 32, dev)
+    stt = cops.gepp_state(m, n)
+
+    def run():
+        for j0 in range(0, n, 32):
+            nbo = min(32, n - j0)
+            pan = ops.fmat(m, nbo, dev)
+            pan.copy_(panel0[:, :nbo])
+            cops.getrf_block(pan, j0, nbo, stt)
+            blk = ops.fmat(nbo, n, dev)
+            blk.copy_(local[:nbo])
+            if j0 + nbo < n:
+                cops.lu_trsm_rows(blk, j0, nbo, j0 + nbo, n, stt)
+                cops.lu_update_split(local, blk, j0, nbo, 0, j0 + nbo, n, stt)
+    t = timed(run, reps=2)
+    blocks = -(-n // 32)
+    return t + blocks * host_sync_ms
+
+
+def dist_gepp_comm_ms(m, n, p):
+    blocks = -(-n // 32)
+    return sum(allgather_ms(8 * m * min(32, n - 32 * b), p) + 2 * allgather_ms(8 * 32 * n * p, p)
+               for b in range(blocks))
 
 
 def main():
@@ -148,14 +185,24 @@ def main():
             nsteps = 3 if l > ops.cholqr_max_l() else 2
             piece["allreduce_grams"] = nsteps * allreduce_ms(8 * l * l, p)
             piece["allgather_q"] = allgather_ms(8 * n * l, p)
-        # final LU: G all-gathered, exact GEPP m x k and n x k (replicated), L by row blocks
-        piece["allgather_g"] = allgather_ms(8 * m * k, p)
-        piece["lu_g"] = gepp(m, k)
-        piece["lu_bt"] = gepp(n, k)
+        # final LUs: row-sharded exact GEPP (distributed.dist_getrf_) of G (m x k)
+        # and B^T (n x k); at P = 1 the one-GPU kernel
+        if p == 1:
+            piece["lu_g"] = gepp(m, k)
+            piece["lu_bt"] = gepp(n, k)
+        else:
+            piece["lu_g_dist"] = dist_gepp_ms(m, k, p, dev)
+            piece["lu_g_comm"] = dist_gepp_comm_ms(m, k, p)
+            piece["lu_bt_dist"] = dist_gepp_ms(n, k, p, dev)
+            piece["lu_bt_comm"] = dist_gepp_comm_ms(n, k, p)
+            piece["allgather_l2"] = allgather_ms(8 * n * k, p)
+            # the interior m x l LU by the same kernel, for comparison with TSLU (not summed)
+            res.setdefault("alt_interior_dist_gepp_ms", {})[str(p)] = dist_gepp_ms(m, l, p, dev) + \
+                dist_gepp_comm_ms(m, l, p)
         l1 = rand(rows, k, dev)
         u2 = rand(k, k, dev)
         piece["assemble_l"] = timed(lambda: ops.matmul(l1, u2, tb=True))
-        total = sum(piece.values())
+        total = sum(v for kk, v in piece.items())
         res["P"][str(p)] = {"pieces_ms": piece, "total_ms": total}
         print(f"P={p}: {total:8.2f} ms  " + "  ".join(f"{kk}={vv:.2f}" for kk, vv in piece.items()), file=sys.stderr,
               flush=True)
