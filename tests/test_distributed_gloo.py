@@ -321,7 +321,7 @@ def test_sharded_tslu_shards_shorter_than_sketch():
         assert abs(O.rel_fro_error_factor(a, f) - O.rel_fro_error_factor(a, ref)) <= 1e-12
 
 
-@pytest.mark.parametrize("world,panel,q_os", [(2, 16, 0), (2, 7, 10), (3, 64, 5)])
+@pytest.mark.parametrize("world,panel,q_os", [(2, 7, 10), (3, 64, 5)])
 def test_sharded_single_pass_matches_single_process(world, panel, q_os):
     """C4's path (rlra/singlepass.py:99-144) row-sharded: per-panel all-reduce
     of the partial G_J (asynchronous, overlapping the next panel), local H_i,
@@ -359,8 +359,7 @@ def test_reference_signatures_accept_a_sharded_matrix():
         assert np.allclose(np.abs(np.sum(v * ref_v.V, axis=0)), 1.0, atol=1e-10)
 
 
-@pytest.mark.parametrize("v,decline,wide_at", [(4, False, 10 ** 9), (5, False, 16), (4, True, 10 ** 9),
-                                               (6, True, 10 ** 9)])
+@pytest.mark.parametrize("v,decline,wide_at", [(5, False, 16), (4, True, 10 ** 9)])
 def test_sharded_replicated_factorizations_world4(v, decline, wide_at):
     """the n x l sketch factorizations on row blocks of the
     replicated Z (sharded CholeskyQR2 with all-reduced Grams, TSQR when the

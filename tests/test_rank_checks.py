@@ -19,8 +19,13 @@ def test_flag_and_counts_in_one_fetch(monkeypatch):
     c.add(_cnt(10), 10)
     c.defer_cholqr(torch.tensor([0], dtype=torch.int32), "z")
     fetches = []
-    orig = torch.Tensor.cpu
-    monkeypatch.setattr(torch.Tensor, "cpu", lambda t, *a, **k: fetches.append(t.numel()) or orig(t, *a, **k))
+    orig = torch.Tensor.copy_
+
+    def spy(dst, src, *a, **k):  # device -> host transfers of the fetch (into a host buffer)
+        fetches.append(src.numel())
+        return orig(dst, src, *a, **k)
+
+    monkeypatch.setattr(torch.Tensor, "copy_", spy)
     assert c.cholqr_declined() == (False, "z")
     c.raise_if_collapsed()
     assert fetches == [3]  # two counts + the flag, one transfer; nothing left afterwards
