@@ -722,6 +722,13 @@ __global__ void __launch_bounds__(THREADS, 1) lu_panel_cluster_kernel(PanelArgs 
 }
 
 static constexpr int LU_PANEL_SMEM_BYTES = 200 * 1024;
+// the cooperative-grid panel kernels of width 8 / 16 (static smem <= 3.8 KB)
+// may take 223 KB: 148 x 1784 rows of a 16-wide panel cover C5's 262144-row
+// sketches (a 200 KB cap forced 8-wide panels there: twice the launches)
+static constexpr int LU_PANEL_SMEM_BYTES_NARROW = 223 * 1024;
+static int64_t grid_rows_cap(int pw) {
+  return (int64_t)((pw == 32 ? LU_PANEL_SMEM_BYTES : LU_PANEL_SMEM_BYTES_NARROW) / (pw * 8));
+}
 
 // Apply the panel's net row permutation to columns [0, j0) and [j0+nb, n).
 // One warp per column: gather every touched row, then scatter.
@@ -989,14 +996,14 @@ static cudaStream_t lu_aux_stream() {
   return streams[dev & 63];
 }
 
-static int lu_prepare_kernel(const void* kern) {
+static int lu_prepare_kernel(const void* kern, int smem_bytes = LU_PANEL_SMEM_BYTES) {
   static std::mutex mu;
   static std::set<std::pair<int, const void*>> done;
   int dev = 0;
   RLRA_CHECK_CUDA(cudaGetDevice(&dev));
   std::lock_guard<std::mutex> lock(mu);
   if (done.count({dev, kern})) return 0;
-  RLRA_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, LU_PANEL_SMEM_BYTES));
+  RLRA_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes));
   cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   cudaGetLastError();
   done.insert({dev, kern});
@@ -1054,13 +1061,15 @@ int getrf_block(double* a, int64_t lda, int64_t m, int64_t j0, int nbo, int64_t*
   const bool use_cluster = cmax > 1 && m <= cmax * rows_cap(16);
   int pw;
   if (use_cluster) pw = (m <= cmax * rows_cap(32)) ? 32 : 16;
-  else pw = (m <= sms * rows_cap(32)) ? 32 : (m <= sms * rows_cap(16) ? 16 : 8);
-  RLRA_REQUIRE(m <= sms * rows_cap(8), "getrf_block: m = %lld exceeds the panel capacity", (long long)m);
+  else pw = (m <= sms * grid_rows_cap(32)) ? 32 : (m <= sms * grid_rows_cap(16) ? 16 : 8);
+  RLRA_REQUIRE(m <= sms * grid_rows_cap(8), "getrf_block: m = %lld exceeds the panel capacity", (long long)m);
   const void* kern = use_cluster
       ? (pw == 32 ? (const void*)lu_panel_cluster_kernel<32, 512> : (const void*)lu_panel_cluster_kernel<16, 512>)
       : (pw == 32 ? (const void*)lu_panel_smem_kernel<32, 512>
                   : pw == 16 ? (const void*)lu_panel_smem_kernel<16, 512> : (const void*)lu_panel_smem_kernel<8, 512>);
-  if (lu_prepare_kernel(kern)) return -1;
+  const int smem_cap = use_cluster || pw == 32 ? LU_PANEL_SMEM_BYTES : LU_PANEL_SMEM_BYTES_NARROW;
+  auto cap = [&](int w_) { return use_cluster ? rows_cap(w_) : grid_rows_cap(w_); };
+  if (lu_prepare_kernel(kern, smem_cap)) return -1;
   unsigned bar_base = 0;
   const int64_t ce = j0 + nbo;
   for (int64_t jp = j0; jp < ce; jp += pw) {
@@ -1073,9 +1082,9 @@ int getrf_block(double* a, int64_t lda, int64_t m, int64_t j0, int nbo, int64_t*
     pa.bar_base = bar_base;
     pa.trace = lu_trace_buffer();
     const int limit = use_cluster ? cmax : sms;
-    const int64_t target = std::min<int64_t>(rows_cap(pw), 512);
+    const int64_t target = std::min<int64_t>(cap(pw), 512);
     int G = (int)std::min<int64_t>(limit, ceil_div(active, target));
-    G = (int)std::max<int64_t>(G, ceil_div(active, rows_cap(pw)));
+    G = (int)std::max<int64_t>(G, ceil_div(active, cap(pw)));
     pa.rows_per_cta = ceil_div(active, G);
     pa.rows_per_cta += pa.rows_per_cta & 1;
     pa.above_per_cta = std::max<int64_t>(1, ceil_div(jp, G));
@@ -1188,13 +1197,15 @@ int getrf(double* a, int64_t lda, int64_t m, int64_t n, int64_t* piv, int64_t* n
   const bool use_cluster = cmax > 1 && m <= cmax * rows_cap(16);
   int pw;
   if (use_cluster) pw = (m <= cmax * rows_cap(32)) ? 32 : 16;
-  else pw = (m <= sms * rows_cap(32)) ? 32 : (m <= sms * rows_cap(16) ? 16 : 8);
-  RLRA_REQUIRE(m <= sms * rows_cap(8), "getrf: m = %lld exceeds the panel capacity", (long long)m);
+  else pw = (m <= sms * grid_rows_cap(32)) ? 32 : (m <= sms * grid_rows_cap(16) ? 16 : 8);
+  RLRA_REQUIRE(m <= sms * grid_rows_cap(8), "getrf: m = %lld exceeds the panel capacity", (long long)m);
   const void* kern = use_cluster
       ? (pw == 32 ? (const void*)lu_panel_cluster_kernel<32, 512> : (const void*)lu_panel_cluster_kernel<16, 512>)
       : (pw == 32 ? (const void*)lu_panel_smem_kernel<32, 512>
                   : pw == 16 ? (const void*)lu_panel_smem_kernel<16, 512> : (const void*)lu_panel_smem_kernel<8, 512>);
-  if (lu_prepare_kernel(kern)) return -1;
+  const int smem_cap = use_cluster || pw == 32 ? LU_PANEL_SMEM_BYTES : LU_PANEL_SMEM_BYTES_NARROW;
+  auto cap = [&](int w_) { return use_cluster ? rows_cap(w_) : grid_rows_cap(w_); };
+  if (lu_prepare_kernel(kern, smem_cap)) return -1;
   unsigned bar_base = 0;
   // Look-ahead: after block b's panels, only the NEXT block's columns get the
   // trailing update on `st` (narrow); the rest (wide) runs on an auxiliary
@@ -1252,9 +1263,9 @@ int getrf(double* a, int64_t lda, int64_t m, int64_t n, int64_t* piv, int64_t* n
       pa.trace = lu_trace_buffer();
       const int limit = use_cluster ? cmax : sms;
       // about one row per thread, never more rows than shared memory holds
-      const int64_t target = std::min<int64_t>(rows_cap(pw), 512);
+      const int64_t target = std::min<int64_t>(cap(pw), 512);
       int G = (int)std::min<int64_t>(limit, ceil_div(active, target));
-      G = (int)std::max<int64_t>(G, ceil_div(active, rows_cap(pw)));
+      G = (int)std::max<int64_t>(G, ceil_div(active, cap(pw)));
       pa.rows_per_cta = ceil_div(active, G);
       pa.rows_per_cta += pa.rows_per_cta & 1;  // even: 16-byte aligned bulk copies of panel columns
       pa.above_per_cta = std::max<int64_t>(1, ceil_div(j0, G));

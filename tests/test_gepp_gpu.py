@@ -69,7 +69,9 @@ def test_host_seam_plu_inplace_bit_exact(cuda_dev, name):
                                       (24576, 256, 10), (8193, 33, 11), (2000, 60, 12), (520, 256, 13),
                                       (16385, 200, 14), (8192, 300, 15), (24576, 512, 16),
                                       # r02: widths up to 1024 (C3's 16384 x 1024 / 843 sketches)
-                                      (16384, 1024, 17), (12000, 843, 18), (4096, 544, 19), (2000, 1000, 20)])
+                                      (16384, 1024, 17), (12000, 843, 18), (4096, 544, 19), (2000, 1000, 20),
+                                      # r02: 16-wide grid panels up to 148 x 1784 rows (223 KB)
+                                      (262144, 40, 21), (240000, 36, 22)])
 def test_device_gepp_bit_exact_vs_oracle_sketch_shapes(cuda_dev, m, n, seed):
     a = np.random.default_rng(seed).standard_normal((m, n))
     if n > 40:
