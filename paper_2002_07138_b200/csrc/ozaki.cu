@@ -703,6 +703,51 @@ __device__ __forceinline__ void tc_fence_before() {
         "=r"(v[29]), "=r"(v[30]), "=r"(v[31])                                                                 \
       : "r"(taddr))
 
+// 32 accumulators of one TMEM row -> 32 bytes t = (c y) mod m in the warp's
+// staging tile stg[col][lane] (see the epilogue comment in gemm_i8_kernel);
+// ACCUM adds the previous K blocks' bytes staged at stg + 1024.  Straight-line
+// code (no branch per element) so that the 16 pairs' chains interleave: an
+// epilogue warp is alone on its scheduler, instruction-level parallelism is
+// all the latency hiding there is.
+template <bool ACCUM>
+__device__ __forceinline__ void epi_chunk(const unsigned (&v)[32], uint8_t* stg, int lane, f2_t k1f, f2_t ycf,
+                                          f2_t invf, f2_t nmf, float mf) {
+  const f2_t big = f2_dup(12582912.0f), nbig = f2_dup(-12582912.0f), n23 = f2_dup(-8388608.0f);
+  const float fix_neg = mf + 8388608.0f, fix_pos = 8388608.0f;  // exact: m + 2^23 < 2^24
+  unsigned prev[ACCUM ? 32 : 1];
+  if (ACCUM) {
+#pragma unroll
+    for (int e = 0; e < 32; ++e) prev[e] = stg[1024 + e * 32 + lane];
+  }
+#pragma unroll
+  for (int e = 0; e < 32; e += 2) {
+    const unsigned c0 = v[e], c1 = v[e + 1];
+    const f2_t lof = f2_fadd(f2_bits(0x4B000000u | (c0 & 0xFFFFu), 0x4B000000u | (c1 & 0xFFFFu)), n23);
+    const f2_t hif =
+        f2_fadd(f2_bits(0x4B400000u + (unsigned)((int)c0 >> 16), 0x4B400000u + (unsigned)((int)c1 >> 16)), nbig);
+    const f2_t sv = f2_ffma(hif, k1f, f2_ffma(lof, ycf, 0ull));  // exact: |s| < 2^24
+    const f2_t qv = f2_fadd(f2_ffma(sv, invf, big), nbig);       // ~rint(s / m)
+    const f2_t rv = f2_ffma(qv, nmf, sv);                        // exact, |r| <= 125
+    const float r0 = __uint_as_float((unsigned)rv), r1 = __uint_as_float((unsigned)(rv >> 32));
+    unsigned b0, b1;
+    if (ACCUM) {  // exact modular sum with the previous K blocks (bytes in [0, m))
+      float z0 = r0 + __uint_as_float(0x4B000000u | prev[e]);  // 2^23 + (r + prev), r + prev in (-m, 2m)
+      float z1 = r1 + __uint_as_float(0x4B000000u | prev[ACCUM ? e + 1 : 0]);
+      z0 += z0 < 8388608.0f ? mf : 0.0f;
+      z1 += z1 < 8388608.0f ? mf : 0.0f;
+      z0 -= z0 >= fix_neg ? mf : 0.0f;
+      z1 -= z1 >= fix_neg ? mf : 0.0f;
+      b0 = __float_as_uint(z0);
+      b1 = __float_as_uint(z1);
+    } else {
+      b0 = __float_as_uint(r0 + (r0 < 0.0f ? fix_neg : fix_pos));
+      b1 = __float_as_uint(r1 + (r1 < 0.0f ? fix_neg : fix_pos));
+    }
+    stg[e * 32 + lane] = (uint8_t)b0;
+    stg[(e + 1) * 32 + lane] = (uint8_t)b1;
+  }
+}
+
 __global__ void __launch_bounds__(kGemmThreads, 1) gemm_i8_kernel(const GemmArgs g) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-byte alignment of the stage buffers (swizzle atoms)
@@ -809,10 +854,18 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_i8_kernel(const GemmArgs
       }
     }
   } else {
-    // epilogue: warps 2..5 -> TMEM lane quadrant (warp % 4)
+    // epilogue: warps 2..5 -> TMEM lane quadrant (warp % 4).  t = (C_l y_l) mod
+    // m_l on the fp32 pipes (packed FFMA2 / FADD2), every step exact:
+    //   c = hi 2^16 + lo (hi signed, lo in [0, 2^16)); s = hi k1 + lo y' with the
+    //   centred representatives k1 = (2^16 y) mod m, y' = y mod m in [-124, 124],
+    //   so |s| <= 124 (2^15 + 2^16) < 2^24 is an exact fp32 integer = c y (mod m);
+    //   q = rint(s / m) up to +-0.006 (magic-number rounding), r = s - q m exact,
+    //   |r| <= 125 < m; t = r + m (r < 0).  The bytes go through a 32 x 32 staging
+    //   tile per warp so that the global stores are 16-byte rows of t[l][col][row].
     const int q = warp & 3;
     const int64_t rows_pad = g.nmb * 256;
     const int64_t cols_pad = (int64_t)g.ng * g.n_g;
+    uint8_t* stg = smem + (size_t)kStages * stage_bytes + 256 + (size_t)q * 2048;  // [2][32 cols][32 rows]
     unsigned acc_phase = 0;
     for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
       const int gi = (int)(u % g.ng);
@@ -820,36 +873,44 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_i8_kernel(const GemmArgs
       const int l = (int)(u / ((int64_t)g.ng * g.nmb));
       mbar_wait_parity(tmem_full, acc_phase);
       tc_fence_after();
-      const int ml = g.mods[l];
-      const double md = (double)ml, inv = 1.0 / md, yl = (double)g.ys[l];
+      const int ml = g.mods[l], yl = g.ys[l] % ml;
+      int k1 = (int)((65536ll * yl) % ml), yc = yl;
+      if (2 * k1 > ml) k1 -= ml;
+      if (2 * yc > ml) yc -= ml;
+      const float mf = (float)ml;
+      const f2_t k1f = f2_dup((float)k1), ycf = f2_dup((float)yc), invf = f2_dup(1.0f / mf), nmf = f2_dup(-mf);
       for (int t = 0; t < 2; ++t) {
-        const int64_t row = mb * 256 + t * 128 + q * 32 + lane;
-        uint8_t* orow = g.out + ((size_t)l * cols_pad + (size_t)gi * g.n_g) * rows_pad + row;
+        // rows mb*256 + t*128 + q*32 .. +32 of the 32 columns cc.. : 16-byte piece j = lane + 32 i of the
+        // staging tile is rows (j % 2) * 16 .. +16 of column j / 2
+        uint8_t* otile = g.out + ((size_t)l * cols_pad + (size_t)gi * g.n_g) * rows_pad + (mb * 256 + t * 128 + q * 32);
         for (int cc = 0; cc < g.n_g; cc += 32) {
           unsigned v[32];
           const unsigned taddr = tmem_base + ((unsigned)(q * 32) << 16) + (unsigned)(t * g.n_g + cc);
           OZ_LD32(taddr, v);
-          asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+          if (g.accum) {  // previous K blocks' residues of this tile -> staging half 1
 #pragma unroll
-          for (int h = 0; h < 32; h += 16) {
-            unsigned prev[16];  // accumulate: previous K blocks' residues, 16 loads in flight at once
-            if (g.accum) {
-#pragma unroll
-              for (int e = 0; e < 16; ++e) prev[e] = orow[(size_t)(cc + h + e) * rows_pad];
+            for (int i = 0; i < 2; ++i) {
+              const int j = lane + 32 * i;
+              const uint4 pv = *reinterpret_cast<const uint4*>(otile + (size_t)(cc + (j >> 1)) * rows_pad + (j & 1) * 16);
+              *reinterpret_cast<uint4*>(stg + 1024 + j * 16) = pv;
             }
-#pragma unroll
-            for (int e = 0; e < 16; ++e) {
-              const double cv = (double)(int)v[h + e] * yl;  // exact: |c y| < 2^39
-              double r = fma(-floor(cv * inv), md, cv);
-              if (r < 0.0) r += md;
-              if (r >= md) r -= md;
-              if (g.accum) {  // exact modular sum with the previous K blocks
-                r += (double)prev[e];
-                if (r >= md) r -= md;
-              }
-              orow[(size_t)(cc + h + e) * rows_pad] = (uint8_t)(int)r;
-            }
+            __syncwarp();
           }
+          asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#ifdef OZ_EPI_NULL  // probe build: TMEM read only (tools/build_vlib.sh), results are garbage
+          if (v[0] == 0x7fffffffu && v[31] == 0x7ffffffeu) otile[(size_t)cc * rows_pad] = 1;
+          continue;
+#endif
+          if (g.accum) epi_chunk<true>(v, stg, lane, k1f, ycf, invf, nmf, mf);
+          else epi_chunk<false>(v, stg, lane, k1f, ycf, invf, nmf, mf);
+          __syncwarp();
+#pragma unroll
+          for (int i = 0; i < 2; ++i) {
+            const int j = lane + 32 * i;
+            const uint4 ov = *reinterpret_cast<const uint4*>(stg + j * 16);
+            *reinterpret_cast<uint4*>(otile + (size_t)(cc + (j >> 1)) * rows_pad + (j & 1) * 16) = ov;
+          }
+          __syncwarp();
         }
       }
       tc_fence_before();
@@ -1049,8 +1110,8 @@ static GemmLayout gemm_layout(const PrepLayout& p, int trans, int64_t ncols, int
   return g;
 }
 
-static size_t gemm_smem_bytes(int n_g) {
-  return 1024 + (size_t)kStages * (2 * kTileBytes + (size_t)n_g * kTile) + 256;
+static size_t gemm_smem_bytes(int n_g) {  // stages + barriers (256) + the epilogue warps' staging tiles (4 x 2 KB)
+  return 1024 + (size_t)kStages * (2 * kTileBytes + (size_t)n_g * kTile) + 256 + 8192;
 }
 
 template <int NMOD>

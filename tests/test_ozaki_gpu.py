@@ -115,3 +115,29 @@ def test_oz_blocked_bit_identical_to_one_block(cuda_dev, trans, cache_frac):
     for _ in range(2):  # rebuilt blocks reuse the scratch workspace
         c_blk = blk.gemm(bd, trans=trans)
         assert torch.equal(c_full.view(torch.int64), c_blk.view(torch.int64))
+
+
+@pytest.mark.parametrize("trans", [False, True])
+@pytest.mark.parametrize("nmod", [14, 16])
+def test_oz_gemm_exact_on_integer_operands(cuda_dev, trans, nmod):
+    """Integer A (|a| < 2^20) and B (|b| < 2^18) with K = 1500: every product
+    sum is an integer below 2^53, the scalings are exact powers of two, so the
+    emulated product must equal the exact integer product bit for bit -- every
+    residue plane, the fp32 epilogue reduction and the CRT are exercised with
+    accumulators spread over the whole int32 range (raw engine, guard off)."""
+    from paper_2002_07138_b200 import ops
+
+    dev = ops.check_device()
+    rng = np.random.default_rng(11)
+    m, n, l = (1500, 520, 70) if trans else (520, 1500, 70)
+    a = rng.integers(-(2 ** 20) + 1, 2 ** 20, size=(m, n)).astype(np.float64)
+    k = m if trans else n
+    b = rng.integers(-(2 ** 18) + 1, 2 ** 18, size=(k, l)).astype(np.float64)
+    b[:, 3] = 0.0
+    b[:, 5] = 2 ** 17  # constant column: every partial sum has one sign pattern per row
+    opa = a.T if trans else a
+    exact = opa.astype(np.int64) @ b.astype(np.int64)
+    assert np.abs(exact).max() < 2 ** 53
+    prep = ops.OzPrep(ops.from_numpy(a, dev), nmod, guard=False)
+    c = ops.to_numpy(prep.gemm(ops.from_numpy(b, dev), trans=trans))
+    assert np.array_equal(c, exact.astype(np.float64))

@@ -31,20 +31,32 @@ __device__ __forceinline__ void wait_par(uint64_t* b, unsigned par) {
       : "memory");
 }
 
+__device__ __forceinline__ void wait_par_cluster(uint64_t* b, unsigned par) {
+  asm volatile(
+      "{\n.reg .pred P1;\nW_%=:\nmbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n@!P1 bra W_%=;\n}\n" ::"r"(
+          smem_u32(b)),
+      "r"(par)
+      : "memory");
+}
+
 __global__ void __cluster_dims__(16, 1, 1) __launch_bounds__(T, 1) probe(int variant, int iters, double* gstage,
                                                                           unsigned long long* out) {
   cg::cluster_group cluster = cg::this_cluster();
   __shared__ __align__(16) double recv[2][CS][RECD];
   __shared__ __align__(8) uint64_t mbar[2];
+  __shared__ __align__(8) uint64_t mbar2[2];  // variant 4: 16 remote arrivals per phase, no tx bytes
+  __shared__ __align__(16) double stagebuf[RECD + 2];
   __shared__ double red[8];
   const int b = cluster.block_rank(), tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const unsigned tx = CS * RECD * 8;
   if (tid == 0) {
     mbar_init(&mbar[0], 1);
     mbar_init(&mbar[1], 1);
+    mbar_init(&mbar2[0], CS);
+    mbar_init(&mbar2[1], CS);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    expect_tx(&mbar[0], tx);
-    expect_tx(&mbar[1], tx);
+    expect_tx(&mbar[0], variant == 6 ? CS * 16u : tx);
+    expect_tx(&mbar[1], variant == 6 ? CS * 16u : tx);
   }
   cluster.sync();
   double acc = b + tid;
@@ -69,6 +81,33 @@ __global__ void __cluster_dims__(16, 1, 1) __launch_bounds__(T, 1) probe(int var
                        "d"(v + c), "d"(v), "r"(bar)
                        : "memory");
       }
+    } else if (variant == 4) {
+      if (warp == 0 && lane < CS) {
+        const unsigned dst = mapa(smem_u32(&recv[par][b][0]), lane), bar = mapa(smem_u32(&mbar2[par]), lane);
+        for (int c = 0; c < RECD; c += 2)
+          asm volatile("st.shared::cluster.v2.f64 [%0], {%1, %2};" ::"r"(dst + 8 * c), "d"(v + c), "d"(v) : "memory");
+        asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar) : "memory");
+      }
+    } else if (variant == 5) {
+      if (warp == 0) {
+        if (lane < RECD) stagebuf[lane] = v + lane;
+        __syncwarp();
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        if (lane < CS) {
+          const unsigned dst = mapa(smem_u32(&recv[par][b][0]), lane), bar = mapa(smem_u32(&mbar[par]), lane);
+          asm volatile(
+              "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+              "r"(smem_u32(stagebuf)), "r"((unsigned)(RECD * 8)), "r"(bar)
+              : "memory");
+        }
+      }
+    } else if (variant == 6) {
+      if (warp == 0 && lane < CS) {
+        const unsigned dst = mapa(smem_u32(&recv[par][b][0]), lane), bar = mapa(smem_u32(&mbar[par]), lane);
+        asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];" ::"r"(dst),
+                     "d"(v), "d"(v), "r"(bar)
+                     : "memory");
+      }
     } else if (variant == 1) {
       if (tid == 0) {
         double* slot = gstage + ((size_t)par * CS + b) * RECD;
@@ -89,13 +128,16 @@ __global__ void __cluster_dims__(16, 1, 1) __launch_bounds__(T, 1) probe(int var
       asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
     }
     // (c) wait for all records
-    if (variant != 2) {
-      if (variant == 3 || tid == 0) {
+    if (variant == 4) {
+      wait_par_cluster(&mbar2[par], (phase >> par) & 1u);
+      phase ^= 1u << par;
+    } else if (variant != 2) {
+      if (variant == 3 || variant >= 5 || tid == 0) {
         wait_par(&mbar[par], (phase >> par) & 1u);
       }
       phase ^= 1u << par;
-      if (tid == 0) expect_tx(&mbar[par], tx);
-      if (variant != 3) __syncthreads();
+      if (tid == 0) expect_tx(&mbar[par], variant == 6 ? CS * 16u : tx);
+      if (variant == 0 || variant == 1) __syncthreads();
     }
     double s = 0.0;
     if (lane < CS) s = recv[par][lane][1];
@@ -113,9 +155,11 @@ int main() {
   cudaMalloc(&g, 1 << 20);
   cudaMalloc(&o, 64 * 8);
   const char* names[] = {"st.async DSMEM + mbarrier (1 waiter)", "global + TMA multicast + mbarrier",
-                         "DSMEM stores + cluster barrier", "st.async DSMEM + mbarrier (all threads wait)"};
+                         "DSMEM stores + cluster barrier", "st.async DSMEM + mbarrier (all threads wait)",
+                         "remote st + remote mbarrier arrive.release", "smem stage + 16 DSMEM bulk copies",
+                         "st.async key only (16 B per peer)"};
   cudaFuncSetAttribute(probe, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-  for (int v = 0; v < 4; v++) {
+  for (int v = 0; v < 7; v++) {
     probe<<<16, T>>>(v, 2000, g, o);
     cudaError_t e = cudaGetLastError();
     if (e == cudaSuccess) e = cudaDeviceSynchronize();
