@@ -63,6 +63,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-c5", action="store_true", help="skip the C5 (262144 x 32768) sub-record")
+    ap.add_argument("--no-sweep", action="store_true", help="skip the C2 pass sweep v = 2..6 sub-record")
     ap.add_argument("--c5-steps", type=int, default=2)
     return ap.parse_args()
 
@@ -85,6 +86,12 @@ def workload(args):
         desc = (f"{w.name}: single_pass_lu(DeviceColumnStream(A {w.m}x{w.n} float64), k={w.k}, "
                 f"seed={w.seed}, q_os={w.q_os})")
     return w, v, gen, passes, fact, desc
+
+
+def configs_flops(w, v):
+    from paper_2002_07138_b200 import configs
+
+    return configs.powerlu_flops(w.m, w.n, w.k, w.k + w.q_os, v)
 
 
 FP_WIDTH, FP_RANK = 1024, 843  # C3: sketch width and the reference's chosen rank (tests/golden/golden_configs.json)
@@ -579,6 +586,28 @@ def our_arm(args):
         for k2, (t, c) in sorted(summ.items(), key=lambda kv: -kv[1][0]):
             print(f"  {k2:32s} {t / reps:9.3f} ms/step  {c / reps:6.1f} calls/step", file=sys.stderr)
 
+    # ---- BASELINE configs[1] is a sweep over the pass budget: v = 2..6 on the same A
+    sweep = None
+    if w.name == "C2" and w.kind == "powerlu" and not args.no_sweep:
+        sweep = {}
+        for vv in (2, 3, 4, 5, 6):
+            rv = single_runner(w, vv, dm)
+            for _ in range(3):
+                fv = rv()
+            torch.cuda.synchronize()
+            s0 = torch.cuda.Event(enable_timing=True)
+            s1 = torch.cuda.Event(enable_timing=True)
+            s0.record(st)
+            for _ in range(5):
+                fv = rv()
+            s1.record(st)
+            torch.cuda.synchronize()
+            ms_v = s0.elapsed_time(s1) / 5
+            pv, fa = configs_flops(w, vv)
+            fvn = fv.to_numpy()
+            sweep[f"v{vv}"] = dict({"ms_per_step": ms_v, "gflops": (pv + fa) / (ms_v / 1e3) / 1e9},
+                                   **(pq_parity("C2", vv, fvn.p, fvn.q) or {}))
+
     # ---- e2e through the public API with host buffers
     e2e = None
     if not args.no_e2e:
@@ -652,7 +681,7 @@ def our_arm(args):
         "gpu_launches": int(launches), "gpu_launches_per_step": launches / args.steps,
         "clocks": clk, "roofline": roofline, "e2e": e2e, "cpu_baseline": cpu, "parity": parity,
         "host_prep": {"generate_A_s": gen_s, "upload_A_s": upload_s},
-        "comm": None, "C5": c5,
+        "comm": None, "pass_sweep": sweep, "C5": c5,
     }
     print(json.dumps(line), flush=True)
     return 0

@@ -34,10 +34,12 @@ __device__ __forceinline__ void cp_async8(void* dst, const void* src) {
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
-// Blocked (32) right-looking Cholesky in shared memory, one CTA:
+// Blocked (CHOL_NB = 16) right-looking Cholesky in shared memory, one CTA:
 //   diagonal block by warp 0 in registers (shuffles), the block row by a
-//   forward substitution per column (one thread each), the trailing triangle
-//   by a rank-32 update in 4 x 4 register tiles -- 3 barriers per 32 columns.
+//   forward substitution per column (one thread each), the NEXT diagonal block
+//   updated first by warps 0-3 (named barrier 1, 128 threads) so that warp 0
+//   can start on it while the rest of the trailing triangle gets its rank-16
+//   update in 2-D super-tiles of 4 x 4 register tiles.
 // Then X = R^{-1} column by column (one warp each, back substitution, R read
 // only), written straight to global memory.
 constexpr int CHOL_NB = 16;
@@ -156,9 +158,9 @@ __global__ void __launch_bounds__(CHOL_THREADS, 1)
     if (tid == 32) CTRACE(5);
     __syncthreads();
     if (tid == 0) CTRACE(2);
-    // ---- (3) trailing triangle -= R(k0.., :)^T R(k0.., :).  Look-ahead: warp 0
-    // updates the NEXT diagonal block and factors it while warps 1.. update
-    // the rest of the triangle in 4 x 4 tiles.
+    // ---- (3) trailing triangle -= R(k0.., :)^T R(k0.., :).  Look-ahead: warps
+    // 0..3 update the NEXT diagonal block (bar.sync 1, 128), warp 0 then factors
+    // it while the other warps update the rest of the triangle in 4 x 4 tiles.
     const int bn = min(CHOL_NB, m);
     if (warp < 4) {
       // the next diagonal block's update, one entry per thread of warps 0..3
