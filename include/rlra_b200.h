@@ -201,6 +201,16 @@ RLRA_B200_API int rlra_b200_oz_bscale(const double* b, int64_t ldb, int64_t k, i
 RLRA_B200_API int rlra_b200_oz_gemm_ex(int trans, const void* prep, int64_t m, int64_t n, int nmod,
                                        const double* b, int64_t ldb, int64_t ncols, double* c, int64_t ldc,
                                        void* ws, size_t ws_bytes, const int* e_b, int flags, void* stream);
+/* Column energies fused with the product (rlra/fixedprec.py:71-80 takes
+ * sum(G[:, j]**2) of G = A V; north star (d)): with RLRA_B200_OZ_COLSQ the CRT
+ * step of rlra_b200_oz_gemm_ex also leaves double-double partial sums of
+ * squares of the C it writes (per column and 1024-row block) in the workspace;
+ * rlra_b200_oz_colsq -- same trans / m / n / nmod / ncols / ws as that call --
+ * adds them in a fixed order into out[ncols] (device; accumulate != 0: out +=,
+ * for products cut into several output row blocks).  No second read of C. */
+#define RLRA_B200_OZ_COLSQ 8
+RLRA_B200_API int rlra_b200_oz_colsq(int trans, int64_t m, int64_t n, int nmod, int64_t ncols, const void* ws,
+                                     size_t ws_bytes, double* out, int accumulate, void* stream);
 
 /* ---- K4: Householder QR (m >= n) + explicit thin Q --------------------- */
 RLRA_B200_API size_t rlra_b200_geqrf_workspace(int64_t m, int64_t n);

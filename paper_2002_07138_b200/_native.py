@@ -64,6 +64,7 @@ SIGNATURES = {
     "rlra_b200_oz_bscale": (_c_i, [_c_p, _c_i64, _c_i64, _c_i64, _c_i, _c_p, _c_p]),
     "rlra_b200_oz_gemm_ex": (_c_i, [_c_i, _c_p, _c_i64, _c_i64, _c_i, _c_p, _c_i64, _c_i64, _c_p, _c_i64,
                                     _c_p, _c_sz, _c_p, _c_i, _c_p]),
+    "rlra_b200_oz_colsq": (_c_i, [_c_i, _c_i64, _c_i64, _c_i, _c_i64, _c_p, _c_sz, _c_p, _c_i, _c_p]),
     "rlra_b200_geqrf_workspace": (_c_sz, [_c_i64, _c_i64]),
     "rlra_b200_geqrf": (_c_i, [_c_p, _c_i64, _c_i64, _c_i64, _c_p, _c_p, _c_sz, _c_p]),
     "rlra_b200_orgqr": (_c_i, [_c_p, _c_i64, _c_i64, _c_i64, _c_p, _c_i64, _c_p, _c_sz, _c_p]),

@@ -146,6 +146,8 @@ int oz_bscale(const double* b, int64_t ldb, int64_t k, int64_t ncols, int nmod, 
 int oz_gemm_ex(int trans, const void* prep, int64_t m, int64_t n, int nmod, const double* b, int64_t ldb,
                int64_t ncols, double* c, int64_t ldc, void* ws, size_t ws_bytes, const int* e_b_ext, int flags,
                cudaStream_t st);
+int oz_colsq(int trans, int64_t m, int64_t n, int nmod, int64_t ncols, const void* ws, size_t ws_bytes, double* out,
+             int accumulate, cudaStream_t st);
 size_t normal_workspace_bytes(int64_t N);
 int64_t normal_stream_words(int64_t N);
 int64_t normal_tail_cap(int64_t N);
@@ -378,6 +380,11 @@ int rlra_b200_oz_gemm_ex(int trans, const void* prep, int64_t m, int64_t n, int 
                          const int* e_b, int flags, void* stream) {
   return oz_gemm_ex(trans, prep, m, n, nmod, b, ldb, ncols, c, ldc, ws, ws_bytes, e_b, flags,
                     static_cast<cudaStream_t>(stream));
+}
+
+int rlra_b200_oz_colsq(int trans, int64_t m, int64_t n, int nmod, int64_t ncols, const void* ws, size_t ws_bytes,
+                       double* out, int accumulate, void* stream) {
+  return oz_colsq(trans, m, n, nmod, ncols, ws, ws_bytes, out, accumulate, static_cast<cudaStream_t>(stream));
 }
 
 size_t rlra_b200_gemm_workspace(int64_t m, int64_t n, int64_t k) { return gemm_workspace_bytes(m, n, k); }

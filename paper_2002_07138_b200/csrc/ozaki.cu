@@ -1032,34 +1032,103 @@ __device__ __forceinline__ double crt_value(const unsigned (&tv)[kMaxMod], const
   return v;
 }
 
+// Double-double helpers of the fused column energies (same arithmetic as the
+// K8 reduction in misc.cu).
+struct DDv {
+  double hi, lo;
+};
+__device__ __forceinline__ DDv dd_two_sum(double a, double b) {
+  const double s = a + b, bb = s - a;
+  return {s, (a - (s - bb)) + (b - bb)};
+}
+__device__ __forceinline__ DDv dd_plus(DDv x, DDv y) {
+  const DDv s = dd_two_sum(x.hi, y.hi);
+  return dd_two_sum(s.hi, s.lo + x.lo + y.lo);
+}
+__device__ __forceinline__ DDv dd_plus_sq(DDv acc, double x) {
+  const double p = x * x, e = fma(x, x, -p);  // exact square = p + e
+  const DDv s = dd_two_sum(acc.hi, p);
+  return dd_two_sum(s.hi, s.lo + acc.lo + e);
+}
+__device__ __forceinline__ DDv dd_warp_sum(DDv v) {
+#pragma unroll
+  for (int off = 16; off; off >>= 1) {
+    const DDv o{__shfl_down_sync(0xffffffffu, v.hi, off), __shfl_down_sync(0xffffffffu, v.lo, off)};
+    v = dd_plus(v, o);
+  }
+  return v;
+}
+
 // 4 consecutive rows per thread: one 32-bit load per residue plane.
+// colsq != nullptr (RLRA_B200_OZ_COLSQ; rlra/fixedprec.py:71-80, north star (d):
+// the Frobenius-norm reduction fused with the product): the block also leaves
+// the double-double sum of squares of the 1024 values it wrote at
+// colsq[j * nblk + blockIdx.x] (fixed reduction tree: deterministic), so the
+// column energies of G cost no second read of G.
 __global__ void __launch_bounds__(256) crt_kernel(const uint8_t* __restrict__ t, int64_t rows_pad, int64_t cols_pad,
                                                   int64_t mrows, int64_t ncols, const int* __restrict__ e_a,
                                                   const int* __restrict__ e_b, const Crt crt, double* __restrict__ c,
-                                                  int64_t ldc, int add) {
+                                                  int64_t ldc, int add, double2* __restrict__ colsq) {
   const int64_t i0 = 4 * ((int64_t)blockIdx.x * blockDim.x + threadIdx.x);
   const int64_t j = blockIdx.y;
-  if (i0 >= mrows) return;
-  const size_t lstride = (size_t)cols_pad * rows_pad;
-  const uint32_t* tp = reinterpret_cast<const uint32_t*>(t + (size_t)j * rows_pad + i0);  // rows_pad % 256 == 0
-  const int nm = crt.nmod;
-  uint32_t w[kMaxMod];
+  DDv acc{0.0, 0.0};
+  if (i0 < mrows) {
+    const size_t lstride = (size_t)cols_pad * rows_pad;
+    const uint32_t* tp = reinterpret_cast<const uint32_t*>(t + (size_t)j * rows_pad + i0);  // rows_pad % 256 == 0
+    const int nm = crt.nmod;
+    uint32_t w[kMaxMod];
 #pragma unroll
-  for (int l = 0; l < kMaxMod; ++l) w[l] = (l < nm) ? __ldcs(tp + (size_t)l * (lstride / 4)) : 0u;
-  const int eb = e_b[j];
-  const bool dead = eb == kEbNonFinite;  // non-finite column of B: NaN, like every BLAS output it touches
-  const int sc = -(e_a[0] + (dead ? 0 : eb));
+    for (int l = 0; l < kMaxMod; ++l) w[l] = (l < nm) ? __ldcs(tp + (size_t)l * (lstride / 4)) : 0u;
+    const int eb = e_b[j];
+    const bool dead = eb == kEbNonFinite;  // non-finite column of B: NaN, like every BLAS output it touches
+    const int sc = -(e_a[0] + (dead ? 0 : eb));
 #pragma unroll
-  for (int e = 0; e < 4; ++e) {
-    if (i0 + e >= mrows) break;
-    unsigned tv[kMaxMod];
+    for (int e = 0; e < 4; ++e) {
+      if (i0 + e >= mrows) break;
+      unsigned tv[kMaxMod];
 #pragma unroll
-    for (int l = 0; l < kMaxMod; ++l) tv[l] = (w[l] >> (8 * e)) & 0xFFu;
-    bool neg;
-    const double v = crt_value(tv, crt, neg);
-    const double r = dead ? __longlong_as_double(0x7FF8000000000000ll) : scalbn(neg ? -v : v, sc);
-    double* cp = c + (i0 + e) + j * ldc;
-    *cp = add ? *cp + r : r;  // add: C += A B (one rounding of the sum, like beta = 1)
+      for (int l = 0; l < kMaxMod; ++l) tv[l] = (w[l] >> (8 * e)) & 0xFFu;
+      bool neg;
+      const double v = crt_value(tv, crt, neg);
+      double r = dead ? __longlong_as_double(0x7FF8000000000000ll) : scalbn(neg ? -v : v, sc);
+      double* cp = c + (i0 + e) + j * ldc;
+      if (add) r = *cp + r;  // add: C += A B (one rounding of the sum, like beta = 1)
+      *cp = r;
+      acc = dd_plus_sq(acc, r);
+    }
+  }
+  if (colsq == nullptr) return;  // uniform over the grid
+  __shared__ double s_hi[8], s_lo[8];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  acc = dd_warp_sum(acc);
+  if (lane == 0) {
+    s_hi[warp] = acc.hi;
+    s_lo[warp] = acc.lo;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    DDv v = lane < 8 ? DDv{s_hi[lane], s_lo[lane]} : DDv{0.0, 0.0};
+    v = dd_warp_sum(v);
+    if (lane == 0) colsq[(size_t)j * gridDim.x + blockIdx.x] = make_double2(v.hi, v.lo);
+  }
+}
+
+// Column energies from the CRT blocks' partials: one warp per column, partials
+// added in a fixed order in double-double; out[j] = (or +=) the sum.
+__global__ void __launch_bounds__(256) colsq_finish_kernel(const double2* __restrict__ part, int64_t nblk,
+                                                           int64_t ncols, double* __restrict__ out, int accumulate) {
+  const int lane = threadIdx.x & 31;
+  const int64_t j = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (j >= ncols) return;
+  DDv acc{0.0, 0.0};
+  for (int64_t b = lane; b < nblk; b += 32) {
+    const double2 v = part[(size_t)j * nblk + b];
+    acc = dd_plus(acc, DDv{v.x, v.y});
+  }
+  acc = dd_warp_sum(acc);
+  if (lane == 0) {
+    const double v = acc.hi + acc.lo;
+    out[j] = accumulate ? out[j] + v : v;
   }
 }
 
@@ -1087,7 +1156,8 @@ static PrepLayout prep_layout(int64_t m, int64_t n, int nmod) {
 struct GemmLayout {
   int ng, n_g;
   int64_t nkb, nmb, rows_pad, cols_pad;
-  size_t off_eb, off_b, off_t, off_tab, total;
+  size_t off_eb, off_b, off_t, off_tab, off_colsq, total;
+  int64_t nblk;  // CRT blocks (1024 rows) per column: column-energy partials
 };
 static GemmLayout gemm_layout(const PrepLayout& p, int trans, int64_t ncols, int nmod) {
   GemmLayout g;
@@ -1106,7 +1176,9 @@ static GemmLayout gemm_layout(const PrepLayout& p, int trans, int64_t ncols, int
   g.off_t = (((size_t)g.cols_pad * sizeof(int)) + 1023) & ~size_t(1023);
   g.off_b = (g.off_t + (size_t)nmod * g.cols_pad * g.rows_pad + 1023) & ~size_t(1023);
   g.off_tab = g.off_b + (size_t)nmod * g.cols_pad * g.nkb * kTile;
-  g.total = g.off_tab;
+  g.nblk = ceil_div(g.rows_pad, 1024);
+  g.off_colsq = (g.off_tab + 15) & ~size_t(15);
+  g.total = g.off_colsq + (size_t)g.cols_pad * g.nblk * sizeof(double2);
   return g;
 }
 
@@ -1431,9 +1503,28 @@ int oz_gemm_ex(int trans, const void* prep, int64_t m, int64_t n, int nmod, cons
 
   if (flags & 2) return 0;  // RLRA_B200_OZ_NO_CRT: more K blocks follow
   ktimer_mark(KT_OZ_CRT, st, false);
+  RLRA_REQUIRE(ceil_div(mrows, 1024) <= g.nblk, "oz_gemm: CRT grid exceeds the partial buffer");
   oz::crt_kernel<<<dim3((unsigned)ceil_div(mrows, 1024), (unsigned)ncols), 256, 0, st>>>(
-      tout, g.rows_pad, g.cols_pad, mrows, ncols, e_a, e_b, crt, c, ldc, (flags & 4) ? 1 : 0);
+      tout, g.rows_pad, g.cols_pad, mrows, ncols, e_a, e_b, crt, c, ldc, (flags & 4) ? 1 : 0,
+      (flags & 8) ? reinterpret_cast<double2*>(w + g.off_colsq) : nullptr);
   ktimer_mark(KT_OZ_CRT, st, true);
+  RLRA_LAUNCHED();
+  return 0;
+}
+
+// Column energies of the C written by the last oz_gemm_ex call with
+// RLRA_B200_OZ_COLSQ on this workspace (same trans / m / n / nmod / ncols).
+int oz_colsq(int trans, int64_t m, int64_t n, int nmod, int64_t ncols, const void* ws, size_t ws_bytes, double* out,
+             int accumulate, cudaStream_t st) {
+  RLRA_REQUIRE(nmod >= 12 && nmod <= oz::kMaxMod, "oz_colsq: nmod must be in [12, 16], got %d", nmod);
+  if (ncols <= 0) return 0;
+  const oz::PrepLayout p = oz::prep_layout(m, n, nmod);
+  const oz::GemmLayout g = oz::gemm_layout(p, trans, ncols, nmod);
+  RLRA_REQUIRE(ws && ws_bytes >= g.total && out, "oz_colsq: workspace too small (%zu < %zu)", ws_bytes, g.total);
+  const int64_t mrows = trans ? n : m;
+  const double2* part = reinterpret_cast<const double2*>(static_cast<const uint8_t*>(ws) + g.off_colsq);
+  oz::colsq_finish_kernel<<<(unsigned)ceil_div(ncols, 8), 256, 0, st>>>(part, ceil_div(mrows, 1024), ncols, out,
+                                                                        accumulate);
   RLRA_LAUNCHED();
   return 0;
 }

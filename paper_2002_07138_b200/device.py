@@ -168,6 +168,18 @@ class DeviceMatrix:
             with ops.label("oz_prep"):
                 self._oz_prep = pipe.finish()
 
+    def matmul_with_energies(self, x):
+        """(A @ X, column energies sum((A X)[:, j]**2) as a device vector): on
+        the int8 engine the energies are reduced inside the product's CRT step
+        (rlra/fixedprec.py:71-80 without a second read of G); otherwise the K8
+        reduction runs on the product."""
+        x = _dev(x, self.device)
+        if not self._pending and self._oz_ok(self._a.shape[1], x.shape[1]):
+            with ops.label("pass_nn"):
+                return self._oz().gemm(x, trans=False, colsq=True)
+        y = self.matmul(x)
+        return y, ops.colsumsq(y)
+
     def matmul(self, x):
         """A @ X, one pass over A (rlra/accessors.py:27-28)."""
         x = _dev(x, self.device)
@@ -287,6 +299,14 @@ class InstrumentedAccessor:
     def rmatmul(self, x):
         self.product_count += 1
         return self.inner.rmatmul(x)
+
+    def matmul_with_energies(self, x):
+        self.product_count += 1
+        fused = getattr(self.inner, "matmul_with_energies", None)
+        if fused is not None:
+            return fused(x)
+        y = self.inner.matmul(x)
+        return y, ops.colsumsq(y)
 
     def fro_norm(self):
         # a norm query is not a product (rlra/accessors.py:86-88)

@@ -111,6 +111,17 @@ def scan_energies(total, col_energy, eps, b, l):
 POWERLU_FP_QR = os.environ.get("RLRA_B200_POWERLU_FP_QR", "chol")
 
 
+def _g_and_energies(a, v):
+    """G = A V and its column energies (rlra/fixedprec.py:71-80): fused with
+    the product where the accessor offers it (DeviceMatrix: the CRT step of the
+    int8 pass), else the K8 reduction over G."""
+    fused = getattr(a, "matmul_with_energies", None)
+    if fused is not None:
+        return fused(v)
+    g = a.matmul(v)
+    return g, ops.colsumsq(g)
+
+
 def _adaptive(a, params, seed):
     m, n = a.shape
     if params.l > min(m, n):
@@ -119,15 +130,14 @@ def _adaptive(a, params, seed):
     with product_session(a):
         basis = general_power_basis_v(a, params.l, params.v, seed, _checks=checks, _qr=POWERLU_FP_QR)
         V = basis.V
-        g = a.matmul(V)
+        g, energies = _g_and_energies(a, V)
         declined = checks.cholqr_declined()  # one host round trip (the counts ride along)
         if declined is not None and declined[0]:  # rare: Householder basis, then G again
             from .rangefinder import qr_basis_
 
             V = qr_basis_(declined[1], checks, "householder")
-            g = a.matmul(V)
+            g, energies = _g_and_energies(a, V)
         fro2 = a.fro_norm_sq_device()  # inside the session: fused into the pass's norms read
-    energies = ops.colsumsq(g)
     checks.raise_if_collapsed()
     host = torch.cat([fro2, energies]).cpu().numpy()
     # total = fro_norm(a) ** 2 (rlra/fixedprec.py:72): norm then square, as there

@@ -285,9 +285,14 @@ class OzPrep:
         # ||A||_F^2 of the norms pass (header bytes 40..48): device scalar, no extra read of A
         self.fro2 = self.ws[OZ_FRO2_OFFSET:OZ_FRO2_OFFSET + 8].view(torch.float64)
 
-    def gemm(self, b, trans=False, keep_ws=False, out=None, add=False):
+    def gemm(self, b, trans=False, keep_ws=False, out=None, add=False, colsq=False):
         """C = A B (trans=False, b n x l) or A^T B (trans=True, b m x l); with
-        `out`, the product is written into it (add=True: out += A B)."""
+        `out`, the product is written into it (add=True: out += A B).
+        colsq=True also returns the column energies sum(C[:, j]**2) (device
+        vector), reduced inside the product's CRT step -- no second read of C
+        (rlra/fixedprec.py:71-80): the result is (C, energies)."""
+        if colsq and keep_ws:
+            raise ValueError("oz gemm: colsq and keep_ws are exclusive")
         k, rows = (self.m, self.n) if trans else (self.n, self.m)
         if b.shape[0] != k:
             raise ValueError(f"oz gemm shape mismatch: A {(self.m, self.n)} trans={trans}, B {tuple(b.shape)}")
@@ -296,17 +301,26 @@ class OzPrep:
         if tuple(c.shape) != (rows, ncols):
             raise ValueError(f"oz gemm output shape {tuple(c.shape)}, expected {(rows, ncols)}")
         if ncols == 0:
+            if colsq:
+                return c, torch.zeros(0, dtype=F64, device=self.device)
             return (c, None) if keep_ws else c
         b = as_fmat(b)
         self._resolve()
         if not self.ok[int(bool(trans))]:  # guard: DGEMM-class accuracy needs the native FP64 GEMM
             gemm(self.a, b, c, ta=bool(trans), beta=1.0 if add else 0.0)
+            if colsq:
+                return c, colsumsq(c)
             return (c, None) if keep_ws else c
         wsb = _native.query("rlra_b200_oz_gemm_workspace", int(trans), self.m, self.n, ncols, self.nmod)
         ws = torch.empty(max(wsb, 8), dtype=torch.uint8, device=self.device)
+        flags = (OZ_ADD_TO_C if add else 0) | (OZ_COLSQ if colsq else 0)
         _call("rlra_b200_oz_gemm_ex", self.device, int(trans), ptr(self.ws), self.m, self.n, self.nmod, ptr(b),
-              ld_of(b), ncols, ptr(c), ld_of(c), ptr(ws), wsb, None, OZ_ADD_TO_C if add else 0,
-              _stream(self.device))
+              ld_of(b), ncols, ptr(c), ld_of(c), ptr(ws), wsb, None, flags, _stream(self.device))
+        if colsq:
+            energies = torch.empty(ncols, dtype=F64, device=self.device)
+            _call("rlra_b200_oz_colsq", self.device, int(trans), self.m, self.n, self.nmod, ncols, ptr(ws), wsb,
+                  ptr(energies), 0, _stream(self.device))
+            return c, energies
         return (c, ws) if keep_ws else c
 
 
@@ -376,7 +390,7 @@ class OzPipeline:
 
 
 OZ_BLOCK_K = 133120  # largest multiple of 256 inside the exact int32 K range (133144)
-OZ_ACCUMULATE, OZ_NO_CRT, OZ_ADD_TO_C = 1, 2, 4  # include/rlra_b200.h
+OZ_ACCUMULATE, OZ_NO_CRT, OZ_ADD_TO_C, OZ_COLSQ = 1, 2, 4, 8  # include/rlra_b200.h
 
 
 def _split(total, cap):
@@ -468,18 +482,21 @@ class OzBlocked:
         ws = self.cache.get(ij)
         return ws if ws is not None else self._build(ij, self.scratch)
 
-    def gemm(self, b, trans=False):
-        """C = A B (trans=False, b n x l) or A^T B (trans=True, b m x l)."""
+    def gemm(self, b, trans=False, colsq=False):
+        """C = A B (trans=False, b n x l) or A^T B (trans=True, b m x l);
+        colsq=True: (C, column energies of C), reduced in the CRT steps."""
         k, rows = (self.m, self.n) if trans else (self.n, self.m)
         if b.shape[0] != k:
             raise ValueError(f"oz gemm shape mismatch: A {(self.m, self.n)} trans={trans}, B {tuple(b.shape)}")
         ncols = int(b.shape[1])
         c = fmat(rows, ncols, self.device)
         if ncols == 0:
-            return c
+            return (c, torch.zeros(0, dtype=F64, device=self.device)) if colsq else c
         b = as_fmat(b)
         if not self.ok[int(bool(trans))]:  # guard (OzPrep): the native FP64 GEMM
-            return gemm(self.a, b, c, ta=bool(trans))
+            gemm(self.a, b, c, ta=bool(trans))
+            return (c, colsumsq(c)) if colsq else c
+        energies = torch.empty(ncols, dtype=F64, device=self.device) if colsq else None
         dev, st = self.device, _stream(self.device)
         cp = int(_native.load().rlra_b200_oz_cols_pad(ncols))
         e_b = torch.empty(cp, dtype=torch.int32, device=dev)
@@ -493,10 +510,14 @@ class OzBlocked:
             for q, (k0, k1) in enumerate(inner):
                 ij = (q, o) if trans else (o, q)
                 (r0, r1), (c0, c1) = self.rows[ij[0]], self.cols[ij[1]]
-                flags = (OZ_ACCUMULATE if q > 0 else 0) | (OZ_NO_CRT if q + 1 < len(inner) else 0)
+                last = q + 1 == len(inner)
+                flags = (OZ_ACCUMULATE if q > 0 else 0) | (0 if last else OZ_NO_CRT) | (OZ_COLSQ if colsq and last else 0)
                 _call("rlra_b200_oz_gemm_ex", dev, int(trans), ptr(self._prep(ij)), r1 - r0, c1 - c0, self.nmod,
                       ptr(b) + k0 * 8, ld_of(b), ncols, ptr(c) + o0 * 8, ld_of(c), ptr(ws), wsb, ptr(e_b), flags, st)
-        return c
+                if colsq and last:  # this output row block's share of every column's energy
+                    _call("rlra_b200_oz_colsq", dev, int(trans), r1 - r0, c1 - c0, self.nmod, ncols, ptr(ws), wsb,
+                          ptr(energies), 1 if o > 0 else 0, st)
+        return (c, energies) if colsq else c
 
 
 OZ_RESERVE_BYTES = int(os.environ.get("RLRA_B200_OZ_RESERVE_BYTES", str(12 << 30)))

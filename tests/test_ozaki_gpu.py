@@ -141,3 +141,70 @@ def test_oz_gemm_exact_on_integer_operands(cuda_dev, trans, nmod):
     prep = ops.OzPrep(ops.from_numpy(a, dev), nmod, guard=False)
     c = ops.to_numpy(prep.gemm(ops.from_numpy(b, dev), trans=trans))
     assert np.array_equal(c, exact.astype(np.float64))
+
+
+@pytest.mark.parametrize("trans", [False, True])
+def test_oz_gemm_fused_column_energies(cuda_dev, trans):
+    """RLRA_B200_OZ_COLSQ: the column energies reduced inside the CRT step
+    (rlra/fixedprec.py:71-80 without a second read of G) equal the compensated
+    K8 reduction over the product to 4 ulp, the product itself is unchanged
+    bit for bit, repeated calls are bitwise identical, and a block-wise product
+    (several output row blocks, K split) accumulates the same energies."""
+    import torch
+
+    from paper_2002_07138_b200 import ops
+
+    dev = ops.check_device()
+    rng = np.random.default_rng(3)
+    m, n, l = 3100, 2300, 45
+    a = rng.standard_normal((m, n))
+    b = rng.standard_normal((m if trans else n, l)) * np.exp(rng.uniform(-6, 6, size=(1, l)))
+    ad, bd = ops.from_numpy(a, dev), ops.from_numpy(b, dev)
+    prep = ops.OzPrep(ad, guard=False)
+    c0 = prep.gemm(bd, trans=trans)
+    c1, e1 = prep.gemm(bd, trans=trans, colsq=True)
+    c2, e2 = prep.gemm(bd, trans=trans, colsq=True)
+    assert torch.equal(c0.view(torch.int64), c1.view(torch.int64))
+    assert torch.equal(e1.view(torch.int64), e2.view(torch.int64))
+    ref = ops.colsumsq(c0).cpu().numpy()
+    exact = (ops.to_numpy(c0).astype(np.longdouble) ** 2).sum(axis=0).astype(np.float64)
+    got = e1.cpu().numpy()
+    assert np.all(np.abs(got - exact) <= 4 * np.spacing(exact))
+    assert np.all(np.abs(got - ref) <= 4 * np.spacing(exact))
+    blk = ops.OzBlocked(ad, block_bytes=14 * 1024 * 1024, col_cap=1000, cache_bytes=0, guard=False)
+    assert len(blk.rows) >= 2 and len(blk.cols) >= 2
+    cb, eb = blk.gemm(bd, trans=trans, colsq=True)
+    assert torch.equal(cb.view(torch.int64), c0.view(torch.int64))
+    assert np.all(np.abs(eb.cpu().numpy() - exact) <= 4 * np.spacing(exact))
+    # out += A B: the energies are those of the updated C
+    out = c0.clone()
+    c3, e3 = prep.gemm(bd, trans=trans, out=out, add=True, colsq=True)
+    exact3 = (ops.to_numpy(c3).astype(np.longdouble) ** 2).sum(axis=0).astype(np.float64)
+    assert np.all(np.abs(e3.cpu().numpy() - exact3) <= 4 * np.spacing(exact3))
+    # a NaN column of B: NaN energy there, the others untouched
+    b2 = b.copy()
+    b2[5, 7] = np.nan
+    _, e4 = prep.gemm(ops.from_numpy(b2, dev), trans=trans, colsq=True)
+    e4 = e4.cpu().numpy()
+    assert np.isnan(e4[7]) and np.array_equal(np.delete(e4, 7), np.delete(got, 7))
+
+
+def test_device_matrix_matmul_with_energies(cuda_dev):
+    """The accessor seam used by powerlu_fp: fused inside a product session,
+    K8 reduction otherwise; both agree with the energies of the product."""
+    import paper_2002_07138_b200 as P
+    from paper_2002_07138_b200 import ops
+    from paper_2002_07138_b200.device import InstrumentedAccessor, product_session
+
+    rng = np.random.default_rng(8)
+    a = rng.standard_normal((900, 700))
+    v = rng.standard_normal((700, 33))
+    dm = P.DeviceMatrix(a)
+    acc = InstrumentedAccessor(dm)
+    with product_session(dm):
+        g, e = acc.matmul_with_energies(v)
+    assert acc.product_count == 1
+    gn = ops.to_numpy(g)
+    exact = (gn.astype(np.longdouble) ** 2).sum(axis=0).astype(np.float64)
+    assert np.all(np.abs(e.cpu().numpy() - exact) <= 4 * np.spacing(exact))
+    assert np.allclose(gn, a @ v, rtol=0, atol=1e-10)
