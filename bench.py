@@ -406,6 +406,33 @@ def cpu_baseline_analogue(w, v):
 GOLDEN = os.path.join(REPO, "tests", "golden")
 
 
+def pass_sweep(w, dm, st):
+    """C2 over v = 2..6 (BASELINE configs[1]): 3 warm-up + 5 timed factorizations
+    per v (CUDA events), pivots against the reference's goldens."""
+    import torch
+
+    out = {}
+    for vv in (2, 3, 4, 5, 6):
+        rv = single_runner(w, vv, dm)
+        for _ in range(3):
+            fv = rv()
+        torch.cuda.synchronize()
+        s0 = torch.cuda.Event(enable_timing=True)
+        s1 = torch.cuda.Event(enable_timing=True)
+        s0.record(st)
+        for _ in range(5):
+            fv = rv()
+        s1.record(st)
+        torch.cuda.synchronize()
+        ms_v = s0.elapsed_time(s1) / 5
+        pv, fa = configs_flops(w, vv)
+        fvn = fv.to_numpy()
+        out[f"v{vv}"] = dict({"ms_per_step": ms_v, "gflops": (pv + fa) / (ms_v / 1e3) / 1e9},
+                             **(pq_parity("C2", vv, fvn.p, fvn.q) or {}))
+        del rv, fv, fvn
+    return out
+
+
 def golden_pq(name, v):
     """Reference pivots of a config (tests/golden/*_pq.npz, written by the
     unmodified reference; SURVEY.md Appendix A recipes), or None."""
@@ -453,6 +480,7 @@ def c5_record(args, dist_ctx=None):
         import paper_2002_07138_b200 as P
 
         A = P.DeviceMatrix(configs.gen_device("C5", dev), local)
+        torch.cuda.empty_cache()  # the generator's temporaries: the residue cache is sized from the free HBM
         run = lambda: P.powerlu(A, w.k, w.q_os, w.v, w.seed)  # noqa: E731
     else:
         import torch.distributed as dist
@@ -492,6 +520,11 @@ def c5_record(args, dist_ctx=None):
            "ms_per_step": ms, "gflops": flops / (ms / 1e3) / 1e9, "steps": max(1, args.c5_steps), "warmup": 1,
            "algorithmic_gflop": flops / 1e9, "input_build_s": gen_s,
            "parity": pq_parity("C5", 4, p, q)}
+    from paper_2002_07138_b200 import ops as _ops
+
+    if dist_ctx is None and _ops.OzBlocked.last_stats is not None:
+        # 120 GB of residues next to the 68.7 GB A: the blocks that do not fit are rebuilt per product
+        rec["residue_blocks"] = dict(_ops.OzBlocked.last_stats)
     del A, f, run
     core.set_omega_cache(False)
     torch.cuda.empty_cache()
@@ -587,26 +620,7 @@ def our_arm(args):
             print(f"  {k2:32s} {t / reps:9.3f} ms/step  {c / reps:6.1f} calls/step", file=sys.stderr)
 
     # ---- BASELINE configs[1] is a sweep over the pass budget: v = 2..6 on the same A
-    sweep = None
-    if w.name == "C2" and w.kind == "powerlu" and not args.no_sweep:
-        sweep = {}
-        for vv in (2, 3, 4, 5, 6):
-            rv = single_runner(w, vv, dm)
-            for _ in range(3):
-                fv = rv()
-            torch.cuda.synchronize()
-            s0 = torch.cuda.Event(enable_timing=True)
-            s1 = torch.cuda.Event(enable_timing=True)
-            s0.record(st)
-            for _ in range(5):
-                fv = rv()
-            s1.record(st)
-            torch.cuda.synchronize()
-            ms_v = s0.elapsed_time(s1) / 5
-            pv, fa = configs_flops(w, vv)
-            fvn = fv.to_numpy()
-            sweep[f"v{vv}"] = dict({"ms_per_step": ms_v, "gflops": (pv + fa) / (ms_v / 1e3) / 1e9},
-                                   **(pq_parity("C2", vv, fvn.p, fvn.q) or {}))
+    sweep = pass_sweep(w, dm, st) if (w.name == "C2" and w.kind == "powerlu" and not args.no_sweep) else None
 
     # ---- e2e through the public API with host buffers
     e2e = None
@@ -658,9 +672,14 @@ def our_arm(args):
 
     c5 = None
     if not args.no_c5 and w.name != "C5":
-        del dm, f, fd
+        del dm, f, fd, run
         a = None  # the host copy is no longer needed either
+        if e2e is not None:
+            del pinned, ah, fh
         P.set_omega_cache(False)
+        import gc
+
+        gc.collect()  # C5 needs every free byte: its residue cache is sized from the free HBM
         torch.cuda.empty_cache()
         try:
             c5 = c5_record(args)

@@ -1065,6 +1065,7 @@ __device__ __forceinline__ DDv dd_warp_sum(DDv v) {
 // the double-double sum of squares of the 1024 values it wrote at
 // colsq[j * nblk + blockIdx.x] (fixed reduction tree: deterministic), so the
 // column energies of G cost no second read of G.
+template <bool COLSQ>
 __global__ void __launch_bounds__(256) crt_kernel(const uint8_t* __restrict__ t, int64_t rows_pad, int64_t cols_pad,
                                                   int64_t mrows, int64_t ncols, const int* __restrict__ e_a,
                                                   const int* __restrict__ e_b, const Crt crt, double* __restrict__ c,
@@ -1094,10 +1095,10 @@ __global__ void __launch_bounds__(256) crt_kernel(const uint8_t* __restrict__ t,
       double* cp = c + (i0 + e) + j * ldc;
       if (add) r = *cp + r;  // add: C += A B (one rounding of the sum, like beta = 1)
       *cp = r;
-      acc = dd_plus_sq(acc, r);
+      if (COLSQ) acc = dd_plus_sq(acc, r);
     }
   }
-  if (colsq == nullptr) return;  // uniform over the grid
+  if (!COLSQ) return;
   __shared__ double s_hi[8], s_lo[8];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   acc = dd_warp_sum(acc);
@@ -1504,9 +1505,13 @@ int oz_gemm_ex(int trans, const void* prep, int64_t m, int64_t n, int nmod, cons
   if (flags & 2) return 0;  // RLRA_B200_OZ_NO_CRT: more K blocks follow
   ktimer_mark(KT_OZ_CRT, st, false);
   RLRA_REQUIRE(ceil_div(mrows, 1024) <= g.nblk, "oz_gemm: CRT grid exceeds the partial buffer");
-  oz::crt_kernel<<<dim3((unsigned)ceil_div(mrows, 1024), (unsigned)ncols), 256, 0, st>>>(
-      tout, g.rows_pad, g.cols_pad, mrows, ncols, e_a, e_b, crt, c, ldc, (flags & 4) ? 1 : 0,
-      (flags & 8) ? reinterpret_cast<double2*>(w + g.off_colsq) : nullptr);
+  const dim3 cgrid((unsigned)ceil_div(mrows, 1024), (unsigned)ncols);
+  if (flags & 8)
+    oz::crt_kernel<true><<<cgrid, 256, 0, st>>>(tout, g.rows_pad, g.cols_pad, mrows, ncols, e_a, e_b, crt, c, ldc,
+                                                (flags & 4) ? 1 : 0, reinterpret_cast<double2*>(w + g.off_colsq));
+  else
+    oz::crt_kernel<false><<<cgrid, 256, 0, st>>>(tout, g.rows_pad, g.cols_pad, mrows, ncols, e_a, e_b, crt, c, ldc,
+                                                 (flags & 4) ? 1 : 0, nullptr);
   ktimer_mark(KT_OZ_CRT, st, true);
   RLRA_LAUNCHED();
   return 0;

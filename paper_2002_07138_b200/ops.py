@@ -412,6 +412,8 @@ class OzBlocked:
     kept for the product session; the others are rebuilt per product in one
     scratch workspace (8 B read + nmod B written per element)."""
 
+    last_stats = None  # of the most recent engine (bench.py's C5 sub-record reports it)
+
     def __init__(self, a, nmod=None, block_bytes=None, cache_bytes=None, row_cap=OZ_BLOCK_K,
                  col_cap=OZ_BLOCK_K, guard=True):
         m, n = a.shape
@@ -468,6 +470,8 @@ class OzBlocked:
         if self.scratch is not None and len(self.cache) == len(self.blocks):
             self.scratch = None
         self.rebuilt = len(self.blocks) - len(self.cache)
+        OzBlocked.last_stats = {"blocks": len(self.blocks), "cached": len(self.cache), "rebuilt_per_product": self.rebuilt,
+                                "row_blocks": len(self.rows), "col_blocks": len(self.cols)}
 
     def _build(self, ij, into):
         (r0, r1), (c0, c1) = self.rows[ij[0]], self.cols[ij[1]]
