@@ -209,6 +209,11 @@ RLRA_B200_API int rlra_b200_oz_gemm_ex(int trans, const void* prep, int64_t m, i
  * adds them in a fixed order into out[ncols] (device; accumulate != 0: out +=,
  * for products cut into several output row blocks).  No second read of C. */
 #define RLRA_B200_OZ_COLSQ 8
+/* The workspace was last used by a product with the SAME skinny operand b,
+ * trans, m, n, nmod and ncols: its scales and residues of b are still there
+ * and are not rebuilt (the single-pass sweep multiplies every panel^T by the
+ * same Omega, rlra/singlepass.py:112-117). */
+#define RLRA_B200_OZ_REUSE_B 16
 RLRA_B200_API int rlra_b200_oz_colsq(int trans, int64_t m, int64_t n, int nmod, int64_t ncols, const void* ws,
                                      size_t ws_bytes, double* out, int accumulate, void* stream);
 

@@ -1463,11 +1463,13 @@ int oz_gemm_ex(int trans, const void* prep, int64_t m, int64_t n, int nmod, cons
   int8_t* b_tiles = reinterpret_cast<int8_t*>(w + g.off_b);
   uint8_t* tout = w + g.off_t;
   const oz::Budget bud = oz::budget(nmod);
-  ktimer_mark(KT_OZ_RESIDUE_B, st, false);
-  OZ_DISPATCH(nmod, oz::launch_residue_b, b, ldb, K, ncols, g, bud.pb, e_b, b_tiles, e_b_ext == nullptr, st);
-  ktimer_mark(KT_OZ_RESIDUE_B, st, true);
-  RLRA_LAUNCHED();
-  note_launch();  // bscale + residue_b
+  if (!(flags & 16)) {  // RLRA_B200_OZ_REUSE_B: the workspace still holds this B's scales and residues
+    ktimer_mark(KT_OZ_RESIDUE_B, st, false);
+    OZ_DISPATCH(nmod, oz::launch_residue_b, b, ldb, K, ncols, g, bud.pb, e_b, b_tiles, e_b_ext == nullptr, st);
+    ktimer_mark(KT_OZ_RESIDUE_B, st, true);
+    RLRA_LAUNCHED();
+    note_launch();  // bscale + residue_b
+  }
 
   oz::GemmArgs ga;
   ga.a_tiles = a_tiles;

@@ -285,12 +285,16 @@ class OzPrep:
         # ||A||_F^2 of the norms pass (header bytes 40..48): device scalar, no extra read of A
         self.fro2 = self.ws[OZ_FRO2_OFFSET:OZ_FRO2_OFFSET + 8].view(torch.float64)
 
-    def gemm(self, b, trans=False, keep_ws=False, out=None, add=False, colsq=False):
+    def gemm(self, b, trans=False, keep_ws=False, out=None, add=False, colsq=False, b_ws=None):
         """C = A B (trans=False, b n x l) or A^T B (trans=True, b m x l); with
         `out`, the product is written into it (add=True: out += A B).
         colsq=True also returns the column energies sum(C[:, j]**2) (device
         vector), reduced inside the product's CRT step -- no second read of C
-        (rlra/fixedprec.py:71-80): the result is (C, energies)."""
+        (rlra/fixedprec.py:71-80): the result is (C, energies).
+        keep_ws=True returns (C, workspace); passing that workspace back as b_ws
+        to a product of a prep of the SAME shape with the SAME b and trans skips
+        the scales and residues of b (RLRA_B200_OZ_REUSE_B; the single-pass
+        sweep multiplies every panel^T by the same Omega)."""
         if colsq and keep_ws:
             raise ValueError("oz gemm: colsq and keep_ws are exclusive")
         k, rows = (self.m, self.n) if trans else (self.n, self.m)
@@ -312,8 +316,9 @@ class OzPrep:
                 return c, colsumsq(c)
             return (c, None) if keep_ws else c
         wsb = _native.query("rlra_b200_oz_gemm_workspace", int(trans), self.m, self.n, ncols, self.nmod)
-        ws = torch.empty(max(wsb, 8), dtype=torch.uint8, device=self.device)
-        flags = (OZ_ADD_TO_C if add else 0) | (OZ_COLSQ if colsq else 0)
+        reuse = b_ws is not None and b_ws.numel() == max(wsb, 8)
+        ws = b_ws if reuse else torch.empty(max(wsb, 8), dtype=torch.uint8, device=self.device)
+        flags = (OZ_ADD_TO_C if add else 0) | (OZ_COLSQ if colsq else 0) | (OZ_REUSE_B if reuse else 0)
         _call("rlra_b200_oz_gemm_ex", self.device, int(trans), ptr(self.ws), self.m, self.n, self.nmod, ptr(b),
               ld_of(b), ncols, ptr(c), ld_of(c), ptr(ws), wsb, None, flags, _stream(self.device))
         if colsq:
@@ -390,7 +395,7 @@ class OzPipeline:
 
 
 OZ_BLOCK_K = 133120  # largest multiple of 256 inside the exact int32 K range (133144)
-OZ_ACCUMULATE, OZ_NO_CRT, OZ_ADD_TO_C, OZ_COLSQ = 1, 2, 4, 8  # include/rlra_b200.h
+OZ_ACCUMULATE, OZ_NO_CRT, OZ_ADD_TO_C, OZ_COLSQ, OZ_REUSE_B = 1, 2, 4, 8, 16  # include/rlra_b200.h
 
 
 def _split(total, cap):

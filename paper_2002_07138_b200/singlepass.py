@@ -66,6 +66,7 @@ def stream_sketch(stream, k, seed, panel=DEFAULT_PANEL):
     h = ops.fmat(m, k, dev, zero=True)
     oz = PASS_GEMM == "oz" and 0 < m <= ops.OZ_BLOCK_K and k <= 4096 and m * n >= SWEEP_OZ_MIN_ELEMS
     count = 0
+    om_ws, om_w = None, -1  # Omega's residues (the TN product's skinny operand) are the same for every panel
     for j0, block in stream.panels(sweep_width(m, panel) if oz else panel):
         if not isinstance(block, torch.Tensor):
             block = ops.from_numpy(block, dev)
@@ -74,7 +75,10 @@ def stream_sketch(stream, k, seed, panel=DEFAULT_PANEL):
         if oz:
             with ops.label("sweep_oz"):
                 prep = ops.OzPrep(block)  # residues of the panel, read once
-                prep.gemm(om, trans=True, out=gb)  # G(j0:j0+w, :) = panel^T Omega
+                # G(j0:j0+w, :) = panel^T Omega; panels of equal width share one workspace layout
+                _, ws_ = prep.gemm(om, trans=True, out=gb, keep_ws=True, b_ws=om_ws if w == om_w else None)
+                if ws_ is not None:  # None: the guard sent this panel to the FP64 GEMM
+                    om_ws, om_w = ws_, w
                 prep.gemm(gb, out=h, add=True)  # H += panel G_j
         else:
             ops.gemm(block, om, gb, ta=True)  # G(j0:j0+w, :) = panel^T Omega

@@ -208,3 +208,30 @@ def test_device_matrix_matmul_with_energies(cuda_dev):
     exact = (gn.astype(np.longdouble) ** 2).sum(axis=0).astype(np.float64)
     assert np.all(np.abs(e.cpu().numpy() - exact) <= 4 * np.spacing(exact))
     assert np.allclose(gn, a @ v, rtol=0, atol=1e-10)
+
+
+def test_oz_gemm_reuses_the_skinny_operands_residues(cuda_dev):
+    """RLRA_B200_OZ_REUSE_B (the single-pass sweep: every panel^T times the same
+    Omega): a product that reuses the previous product's workspace -- scales
+    and residues of b included -- equals the fresh product bit for bit."""
+    import torch
+
+    from paper_2002_07138_b200 import ops
+
+    dev = ops.check_device()
+    rng = np.random.default_rng(21)
+    m, n, l = 2100, 768, 90
+    b = ops.from_numpy(rng.standard_normal((m, l)) * np.exp(rng.uniform(-4, 4, size=(1, l))), dev)
+    a1 = ops.from_numpy(rng.standard_normal((m, n)), dev)
+    a2 = ops.from_numpy(rng.standard_normal((m, n)) * 3.0, dev)
+    p1, p2 = ops.OzPrep(a1, guard=False), ops.OzPrep(a2, guard=False)
+    _, ws = p1.gemm(b, trans=True, keep_ws=True)
+    fresh = p2.gemm(b, trans=True)
+    reused, ws2 = p2.gemm(b, trans=True, keep_ws=True, b_ws=ws)
+    assert ws2 is ws
+    assert torch.equal(fresh.view(torch.int64), reused.view(torch.int64))
+    # a prep of another shape ignores the offered workspace
+    p3 = ops.OzPrep(ops.from_numpy(rng.standard_normal((m, 512)), dev), guard=False)
+    c3, ws3 = p3.gemm(b, trans=True, keep_ws=True, b_ws=ws)
+    assert ws3 is not ws
+    assert torch.equal(c3.view(torch.int64), p3.gemm(b, trans=True).view(torch.int64))
