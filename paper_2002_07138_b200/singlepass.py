@@ -31,8 +31,12 @@ class SketchPair(NamedTuple):
     H: torch.Tensor  # m x k
 
 
-SWEEP_PANEL = int(os.environ.get("RLRA_B200_SWEEP_PANEL", "8192"))
-SWEEP_PANEL_BYTES = int(os.environ.get("RLRA_B200_SWEEP_BYTES", str(2 << 30)))  # one sweep panel of float64 (host streams keep 3 pinned + 3 device slots)
+# Wider sweep panels amortise the per-panel CRT of H (m x l, read-modify-write)
+# and the panel prologue: C4 (50000^2) 58.4 ms at 2 GB panels, 52.6 at 4 GB,
+# 49.9 at 8 GB (profiles/r02b_c4_sweep_width.txt); 4 GB keeps a host stream's
+# 3 pinned + 3 device slots at 12 GB each side.
+SWEEP_PANEL = int(os.environ.get("RLRA_B200_SWEEP_PANEL", "16384"))
+SWEEP_PANEL_BYTES = int(os.environ.get("RLRA_B200_SWEEP_BYTES", str(4 << 30)))  # one sweep panel of float64 (host streams keep 3 pinned + 3 device slots)
 # The int8 engine's normwise error equals DGEMM's but it is not exact on
 # sparse/identity panels (B is rounded relative to its column norm), which
 # the reference's bitwise identity-stream property (pkg/tests/
