@@ -225,7 +225,9 @@ struct Handoff {
   unsigned long long cmax[MAXN];
   int64_t prow[MAXP][2 * 16], psrc[MAXP][2 * 16];
   int pcnt[MAXP];
-  __align__(16) double stage[2 * CS * (2 + 16) + 2 * 16];  // multicast staging (records, diagonal rows)
+  // multicast staging: records in slots of 2 + 2 * 16 doubles, diagonal rows in slots of 2 * 16 -- the
+  // holder stores its ROTATED registers at slot[jj + i] without a bound check (only 2 + 16 / 16 doubles are sent)
+  __align__(16) double stage[2 * CS * (2 + 2 * 16) + 2 * 2 * 16];
 };
 
 __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
@@ -379,27 +381,31 @@ __device__ __forceinline__ unsigned publish(const Ctx& x, Panel<RPT, W>& P, int 
     }
   }
 #else
-  // the holder thread writes the row from registers (columns >= jj) and sL
-  // (retired columns < jj) to a global staging slot and multicasts it into
-  // every CTA with one bulk copy completing on each peer's mbarrier
-  auto emit = [&](int kk, double* slot) {
-    for (int c = 0; c < jj; c++) slot[c] = x.sL[(size_t)c * RS + kk * T + x.tid];
+  // the holder thread writes the row's live columns (>= jj: registers i <-> column jj + i) to a global
+  // staging slot and multicasts it into every CTA with one bulk copy completing on each peer's
+  // mbarrier.  Columns < jj of a record are never read (rows are relabelled, not moved: the L part
+  // stays with its owner), so they are not staged.  The slot index of the holder's row is made
+  // warp-uniform first: one unpredicated store per column instead of RPT predicated ones.
+  constexpr int SLOT = 2 + 2 * W, DSLOT = 2 * W;
+  auto emit = [&](unsigned bmask, int kk, double* slot) {
+    const int hl = __ffs(bmask) - 1;
+    const int ko = __shfl_sync(0xffffffffu, kk, hl);
+    static_for<0, RPT>([&](auto K) {
+      if (ko == K.value && kk >= 0) {
 #pragma unroll
-    for (int k = 0; k < RPT; k++)
-      if (k == kk)
-#pragma unroll
-        for (int i = 0; i < W; i++)
-          if (jj + i < W) slot[jj + i] = P.a[k][i];
+        for (int i = 0; i < W; i++) slot[jj + i] = P.a[K.value][i];
+      }
+    });
   };
   const unsigned short mask = (unsigned short)0xffffu;
+  double* slot = x.gstage + ((size_t)par * CS + x.b) * SLOT;
+  if (bw != 0u) emit(bw, kw, slot + 2);  // warp-uniform: the warp holding the CTA winner
   if (kw >= 0 || (!has && x.tid == 0)) {
-    double* slot = x.gstage + ((size_t)par * CS + x.b) * RECD;
     const double v = has ? __longlong_as_double((long long)ck) : -1.0;
     const long long gi = has ? (long long)ci : (long long)INT64_MAX;
     slot[0] = v;
     slot[1] = __longlong_as_double(gi);
-    if (has) emit(kw, slot + 2);
-    else
+    if (!has)
       for (int c = 0; c < W; c++) slot[2 + c] = 0.0;
     asm volatile("fence.proxy.async.global;\n" ::: "memory");
     asm volatile(
@@ -408,9 +414,9 @@ __device__ __forceinline__ unsigned publish(const Ctx& x, Panel<RPT, W>& P, int 
         "l"(slot), "r"((unsigned)(RECD * 8)), "r"(bar_l), "h"(mask)
         : "memory");
   }
+  double* dslot = x.gstage + (size_t)2 * CS * SLOT + (size_t)par * DSLOT;
+  if (bd != 0u) emit(bd, kd, dslot);  // warp-uniform: the warp holding row jn
   if (kd >= 0) {
-    double* dslot = x.gstage + (size_t)2 * CS * RECD + (size_t)par * W;
-    emit(kd, dslot);
     asm volatile("fence.proxy.async.global;\n" ::: "memory");
     asm volatile(
         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1], %2, [%3], "
