@@ -81,6 +81,10 @@ struct Args {
   } while (0)
 #endif
 
+// rare operands (zeros, values near the exponent range's ends): out of line, so
+// that the column step's hot path stays short
+__device__ __noinline__ double ieee_div_slow(double x, double d) { return x / d; }
+
 __device__ __forceinline__ double ieee_div(double x, double d, double rcp) {
   const double ax = fabs(x), ad = fabs(d);
   if (ax > 0x1p-960 && ax < 0x1p+960 && ad > 0x1p-960 && ad < 0x1p+960) {
@@ -88,7 +92,7 @@ __device__ __forceinline__ double ieee_div(double x, double d, double rcp) {
     const double rem = fma(-d, q0, x);
     return fma(rem, rcp, q0);  // == RN(x / d) (Markstein)
   }
-  return x / d;
+  return ieee_div_slow(x, d);
 }
 
 // argmax key of |value|: non-negative doubles order like their bit patterns;
