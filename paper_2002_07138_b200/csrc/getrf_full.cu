@@ -160,6 +160,7 @@ struct Shared {
   __align__(16) double recv[2 * CS * RECD];  // every CTA's record, multicast in (by step parity)
   __align__(16) double recv_diag[2 * W];     // current diagonal row (pre-swap), multicast in
   double s_u[2 * 2 * W];                     // local copy of the step's pivot row, zero beyond nb (post-barrier readers)
+  __align__(16) double srow[2 * W], drow[2 * W];  // DSMEM push: staged record / diagonal rows (columns jj + i)
   double l11[W][W + 1];
   unsigned long long wkey[NW];
   unsigned widx[NW];
@@ -253,6 +254,20 @@ __device__ __forceinline__ void wait_geq(const unsigned* p, unsigned target) {
   }
 }
 
+// Bytes every CTA receives for local step jr of a panel (its mbarrier's expected
+// transaction count): CS records + one diagonal row.  The global-staging path
+// always sends whole records; the DSMEM path only the columns >= (jr & ~1).
+template <int W>
+__device__ __forceinline__ unsigned step_tx_bytes(int jr) {
+#ifdef LUF_PUSH_DSMEM
+  const unsigned live = (unsigned)(W - (jr & ~1));
+  return CS * (16u + 8u * live) + 8u * live;
+#else
+  (void)jr;
+  return CS * (2u + W) * 8u + W * 8u;
+#endif
+}
+
 // Per-thread context of the cluster kernel.
 struct Ctx {
   const Args* p;
@@ -284,7 +299,7 @@ __device__ __forceinline__ unsigned publish(const Ctx& x, Panel<RPT, W>& P, int 
                                             const double* su, unsigned par) {
   [[maybe_unused]] const int j0 = SC == 0 ? 1 : jn - 1 - jj;  // for STEP_TRACE (panel 0 steps only)
   constexpr int RECD = 2 + W;
-  constexpr int RS = Plan<RPT, W>::RS;
+  [[maybe_unused]] constexpr int RS = Plan<RPT, W>::RS;
   Shared& S = *x.S;
   unsigned long long bk = 0ull;
   unsigned bi = NONE;
@@ -340,48 +355,42 @@ __device__ __forceinline__ unsigned publish(const Ctx& x, Panel<RPT, W>& P, int 
     }
   }
   // stage a row (registers -> its sL slot, columns >= jj) for the pushing lanes
-  auto stage = [&](int kk) {
-#pragma unroll
-    for (int k = 0; k < RPT; k++)
-      if (k == kk)
-#pragma unroll
-        for (int i = 0; i < W; i++)
-          if (jj + i < W) x.sL[(size_t)(jj + i) * RS + k * T + x.tid] = P.a[k][i];
-  };
 #ifdef LUF_PUSH_DSMEM
-  if (bw != 0u || (!has && x.warp == 0)) {  // this warp publishes the CTA record
-    if (kw >= 0) stage(kw);
+  // The holder's warp stages the row's live columns (registers i <-> column jj + i) in a small
+  // shared row buffer -- one unpredicated store per column after a warp-uniform slot switch --
+  // and lanes q < CS push {|v|, row, columns >= c0} into peer q with DSMEM stores completing on
+  // the peer's mbarrier; c0 = the first even column the receiving step reads (step_tx_bytes).
+  const int c0 = (jj + SC) & ~1;
+  auto stage = [&](unsigned bmask, int kk, double* row) {
+    const int hl = __ffs(bmask) - 1;
+    const int ko = __shfl_sync(0xffffffffu, kk, hl);
+    static_for<0, RPT>([&](auto K) {
+      if (ko == K.value && kk >= 0) {
+#pragma unroll
+        for (int i = 0; i < W; i++) row[jj + i] = P.a[K.value][i];
+      }
+    });
     __syncwarp();
+  };
+  if (bw != 0u || (!has && x.warp == 0)) {  // this warp publishes the CTA record
+    if (bw != 0u) stage(bw, kw, S.srow);
     if (SC) STEP_TRACE(jj, 5);
-    const int ol = bw ? __ffs(bw) - 1 : 0;
-    const int ko = __shfl_sync(0xffffffffu, kw, ol);
     if (x.lane < CS) {
       const unsigned rdst = mapa_u32(smem_u32(S.recv + ((size_t)par * CS + x.b) * RECD), x.lane);
       const unsigned rbar = mapa_u32(bar_l, x.lane);
       const double v = has ? __longlong_as_double((long long)ck) : -1.0;
       const long long gi = has ? (long long)ci : (long long)INT64_MAX;
       st_async2(rdst, v, __longlong_as_double(gi), rbar);
-      const int sl = ko * T + x.warp * 32 + ol;
-#pragma unroll
-      for (int c = 0; c < W; c += 2) {
-        const double x0 = has ? x.sL[(size_t)c * RS + sl] : 0.0;
-        const double x1 = has ? x.sL[(size_t)(c + 1) * RS + sl] : 0.0;
-        st_async2(rdst + 8u * (2 + c), x0, x1, rbar);
-      }
+      for (int c = c0; c < W; c += 2)
+        st_async2(rdst + 8u * (2 + c), has ? S.srow[c] : 0.0, has ? S.srow[c + 1] : 0.0, rbar);
     }
   }
   if (bd != 0u) {  // this warp holds row jn: push the diagonal row
-    if (kd >= 0 && kd != kw) stage(kd);
-    __syncwarp();
-    const int dl = __ffs(bd) - 1;
-    const int kdd = __shfl_sync(0xffffffffu, kd, dl);
+    stage(bd, kd, S.drow);
     if (x.lane < CS) {
       const unsigned rdst = mapa_u32(smem_u32(S.recv_diag + (size_t)par * W), x.lane);
       const unsigned rbar = mapa_u32(bar_l, x.lane);
-      const int sl = kdd * T + x.warp * 32 + dl;
-#pragma unroll
-      for (int c = 0; c < W; c += 2)
-        st_async2(rdst + 8u * c, x.sL[(size_t)c * RS + sl], x.sL[(size_t)(c + 1) * RS + sl], rbar);
+      for (int c = c0; c < W; c += 2) st_async2(rdst + 8u * c, S.drow[c], S.drow[c + 1], rbar);
     }
   }
 #else
@@ -444,7 +453,8 @@ __device__ __forceinline__ void step(const Ctx& x, Panel<RPT, W>& P, double& cm,
   Shared& S = *x.S;
   const int j = j0 + jj;
   const unsigned par = (unsigned)(j & 1);
-  const unsigned tx_bytes = CS * RECD * 8u + W * 8u;
+  // this barrier's next user is local step jj + 2, or step jj + 2 - nb (0 or 1) of the next panel
+  const unsigned tx_bytes = step_tx_bytes<W>(jj + 2 < nb ? jj + 2 : 0);
   STEP_TRACE(jj, 0);
   mbar_wait_bounded(&S.mbar[par], (phase >> par) & 1u);
   phase ^= 1u << par;
@@ -551,7 +561,7 @@ __device__ __forceinline__ void step(const Ctx& x, Panel<RPT, W>& P, double& cm,
 template <int RPT, int W>
 __device__ void panel_role(const Args& p, Handoff* hs, double* dyn) {
   namespace cg = cooperative_groups;
-  constexpr int RECD = 2 + W;
+  [[maybe_unused]] constexpr int RECD = 2 + W;
   constexpr int RS = Plan<RPT, W>::RS;
   cg::cluster_group cluster = cg::this_cluster();
   __shared__ Shared S;
@@ -577,7 +587,7 @@ __device__ void panel_role(const Args& p, Handoff* hs, double* dyn) {
   for (int k = 0; k < RPT; k++)
     if (x.tid + k * T < nloc) x.nk = k + 1;
   const int tid = x.tid, lane = x.lane, warp = x.warp, b = x.b;
-  const unsigned tx_bytes = CS * RECD * 8u + W * 8u;
+  const unsigned tx_bytes = step_tx_bytes<W>(0);  // steps 0 and 1 of panel 0 receive whole records
 
   if (tid == 0) {
     mbar_init(&S.mbar[0], 1);
