@@ -34,7 +34,10 @@ namespace rlra {
 namespace lufull {
 
 constexpr int W = 16;         // widest panel (8 when a thread holds 3 rows)
-constexpr int T = 256;        // threads per CTA (8 warps: the per-step decision is replicated per warp)
+#ifndef LUF_T
+#define LUF_T 256
+#endif
+constexpr int T = LUF_T;      // threads per CTA (8 warps: the per-step decision is replicated per warp)
 constexpr int NW = T / 32;    // warps per CTA
 constexpr int CS = 16;        // cluster size
 constexpr int RECD = 2 + W;   // record: {|v|, row bits, row[W]} (<= 144 B)
