@@ -533,12 +533,15 @@ __device__ __forceinline__ void step(const Ctx& x, Panel<RPT, W>& P, double& cm,
 #endif
       const double* su = S.s_u + par * 2 * W + jj;  // zero beyond nb: padding columns stay inert
       const unsigned bm = below & ~done;
+      double u[W];  // the pivot row once per thread, not once per row slot
+#pragma unroll
+      for (int i = 2; i < W; i++) u[i] = su[i];
 #pragma unroll
       for (int k = 0; k < RPT; k++) {
         if ((bm >> k) & 1u) {
           const double l = P.a[k][0];
 #pragma unroll
-          for (int i = 2; i < W; i++) P.a[k][i] = sub_mul_nofma(P.a[k][i], l, su[i]);
+          for (int i = 2; i < W; i++) P.a[k][i] = sub_mul_nofma(P.a[k][i], l, u[i]);
         }
       }
     }
