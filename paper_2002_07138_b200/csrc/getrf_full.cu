@@ -249,10 +249,13 @@ __device__ __forceinline__ void red_release_add(unsigned* p, unsigned v) {
 __device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
 }
+#ifndef LUF_POLL_NS
+#define LUF_POLL_NS 64
+#endif
 // one thread waits until *p >= target (acquire); bounded: a protocol error traps
 __device__ __forceinline__ void wait_geq(const unsigned* p, unsigned target) {
   for (long long spin = 0; ld_acquire(p) < target; ++spin) {
-    __nanosleep(64);
+    __nanosleep(LUF_POLL_NS);
     if (spin > (1ll << 26)) __trap();
   }
 }
