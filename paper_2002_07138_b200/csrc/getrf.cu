@@ -930,6 +930,9 @@ int fill_iota(int64_t* p, int64_t m, cudaStream_t st) {
 bool getrf_full_eligible(int64_t m, int64_t n, int cluster_max);
 int getrf_full(double* a, int64_t lda, int64_t m, int64_t n, int64_t* piv, int64_t* ipiv, int* zflag, double* recg,
                cudaStream_t st);
+int getrf_full_wide(double* a, int64_t lda, int64_t m, int64_t n, int64_t* piv, int64_t* ipiv, int* zflag, double* recg,
+               cudaStream_t st);  // 384 threads per CTA, m <= getrf_full_wide_rows()
+int64_t getrf_full_wide_rows();
 
 unsigned long long* g_lu_trace = nullptr;  // set by rlra_b200_debug_lu_trace (tools only)
 static unsigned long long* lu_trace_buffer() { return g_lu_trace; }
@@ -1181,7 +1184,8 @@ int getrf(double* a, int64_t lda, int64_t m, int64_t n, int64_t* piv, int64_t* n
   const int cmax = lu_max_cluster();
   if (getrf_full_eligible(m, n, cmax)) {
     // narrow sketch: the whole factorization in one cooperative launch (getrf_full.cu)
-    const int rc = getrf_full(a, lda, m, n, piv, w.ipiv, w.zflag, w.recg, st);
+    const int rc = m <= getrf_full_wide_rows() ? getrf_full_wide(a, lda, m, n, piv, w.ipiv, w.zflag, w.recg, st)
+                                               : getrf_full(a, lda, m, n, piv, w.ipiv, w.zflag, w.recg, st);
     if (rc < 0) return -1;
     if (rc == 0) {
       if (nonzero_diag_dev) {

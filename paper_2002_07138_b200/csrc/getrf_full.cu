@@ -30,6 +30,17 @@
 
 #include "common.cuh"
 
+// The file is compiled twice (csrc/Makefile): the primary build with 256
+// threads per CTA (rows per thread up to 6: m <= 24576) and LUF_WIDE_CTA with
+// 384 threads and at most 2 rows per thread (m <= 12288), measured 8 % faster
+// there (fewer rows per thread on the column step's critical path); beyond 2
+// rows per thread the 12 warps' instruction issue makes it slower than 256.
+#ifdef LUF_WIDE_CTA
+#define LUF_T 384
+#define lufull lufull_wide
+#define getrf_full getrf_full_wide
+#endif
+
 namespace rlra {
 namespace lufull {
 
@@ -899,6 +910,7 @@ __global__ void __launch_bounds__(T, 1) lu_coop_kernel(const Args p) {
 
 }  // namespace lufull
 
+#ifndef LUF_WIDE_CTA
 // Eligibility of the one-launch cluster GEPP (getrf.cu dispatches to it).
 bool getrf_full_eligible(int64_t m, int64_t n, int cluster_max) {
   static int enabled = -1;
@@ -918,6 +930,10 @@ bool getrf_full_eligible(int64_t m, int64_t n, int cluster_max) {
 }
 
 size_t getrf_full_state_bytes() { return sizeof(lufull::Handoff); }
+
+// rows the 384-thread build takes (2 rows per thread)
+int64_t getrf_full_wide_rows() { return (int64_t)lufull::CS * 384 * 2; }
+#endif
 
 // Cooperative launch of the panel cluster + NH helper clusters (returns 1 when
 // the device cannot hold a helper cluster next to the panel cluster: the
@@ -1003,6 +1019,10 @@ int getrf_full(double* a, int64_t lda, int64_t m, int64_t n, int64_t* piv, int64
   const int rpt = (int)ceil_div(args.R, lufull::T);
   RLRA_REQUIRE(rpt >= 1 && rpt <= lufull::MAXRPT, "getrf_full: m = %lld outside the register capacity",
                (long long)m);
+#ifdef LUF_WIDE_CTA
+  RLRA_REQUIRE(rpt <= 2, "getrf_full_wide: m = %lld needs more than 2 rows per thread", (long long)m);
+  return rpt == 1 ? launch_full<1, 16>(args, st) : launch_full<2, 16>(args, st);
+#else
   switch (rpt) {
     case 1: return launch_full<1, 16>(args, st);
     case 2: return launch_full<2, 16>(args, st);
@@ -1011,6 +1031,7 @@ int getrf_full(double* a, int64_t lda, int64_t m, int64_t n, int64_t* piv, int64
     case 5: return launch_full<5, 16>(args, st);
     default: return launch_full<6, 16>(args, st);
   }
+#endif
 }
 
 }  // namespace rlra
