@@ -46,8 +46,10 @@ sys.path.insert(0, REPO)
 FP64_PEAK_TFLOPS = 37.1  # measured DMMA m8n8k4 sustained, profiles/fp64_peak_r01.log
 try:
     MEASURED = json.load(open(os.path.join(REPO, "MEASURED_PEAKS.json")))
+    HBM_PEAK_SRC = "MEASURED_PEAKS.json hbm_gbs (burst copy)"
 except (OSError, ValueError):
     MEASURED = {"hbm_gbs": 7700.0, "bf16_tflops": 2250.0}  # B200_PROFILING.md fallback
+    HBM_PEAK_SRC = "B200_PROFILING.md fallback (7.7 TB/s nominal; MEASURED_PEAKS.json absent)"
 FP64_PEAK_SRC = "measured: tools/fp64_peak.cu on this pool's B200 (profiles/fp64_peak_r01.log); MEASURED_PEAKS.json has no FP64 entry"
 
 
@@ -258,7 +260,7 @@ def roofline_line(w, v, passes, reps, kt, pass_ms, step_ms):
     other = {nm: {"ms_per_step": t / reps, "launches_per_step": c / reps} for nm, (t, c) in kt.items()}
     return {"bound": "hbm", "kernel": "gemm_i8_kernel (tcgen05 kind::i8 Ozaki-II pass products, csrc/ozaki.cu)",
             "achieved": achieved, "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
-            "traffic": traffic, "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)",
+            "traffic": traffic, "peak_source": HBM_PEAK_SRC,
             "algorithmic_bytes_per_launch": per_launch_bytes, "ms_per_launch": per_launch_ms,
             "launches_per_step": g_cnt / reps,
             "bytes_per_unit": f"nmod*(m*n + (m+n)*w) per pass of width w, nmod={nmod}",
