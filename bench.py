@@ -461,6 +461,51 @@ def pq_parity(name, v, p, q):
             "golden": f"tests/golden/{name.lower()}_pq.npz"}
 
 
+def config_record(name, steps=3):
+    """One more BASELINE config on this GPU, device-built input (configs.gen_device):
+    C3 = powerlu_fp (16384^2, rank 843), C4 = single-pass LU (50000^2).  One
+    warm-up, `steps` timed calls (CUDA events), pivots (and C3's rank) against
+    the reference's goldens (tests/golden/c3_pq.npz, c4_pq.npz)."""
+    import torch
+
+    import paper_2002_07138_b200 as P
+    from paper_2002_07138_b200 import configs, core
+
+    w = configs.WORKLOADS[name]
+    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", "0")))
+    core.set_omega_cache(True)
+    t0 = time.perf_counter()
+    dm = P.DeviceMatrix(configs.gen_device(name, dev))
+    torch.cuda.empty_cache()
+    gen_s = time.perf_counter() - t0
+    rank = None
+    if w.kind == "powerlu_fp":
+        call = lambda: P.powerlu_fp(dm, P.PrecisionParams(w.eps, w.b, FP_WIDTH, w.v), w.seed)  # noqa: E731
+    else:
+        call = lambda: (P.single_pass_lu(P.DeviceColumnStream(dm), w.k, w.seed, q_os=w.q_os), None)  # noqa: E731
+    f, out = call()
+    torch.cuda.synchronize()
+    st = torch.cuda.current_stream(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    for _ in range(steps):
+        f, out = call()
+    e1.record(st)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    if out is not None:
+        rank = int(out.rank)
+    rec = {"workload": f"{name}: {w.kind} (A {w.m}x{w.n} float64, device-built)", "ms_per_step": ms, "steps": steps,
+           "warmup": 1, "input_build_s": gen_s, "parity": pq_parity(name, w.v, f.p.cpu().numpy(), f.q.cpu().numpy())}
+    if rank is not None:
+        rec["rank"] = rank
+        rec["rank_reference"] = FP_RANK
+    del dm, f, out, call
+    core.set_omega_cache(False)
+    torch.cuda.empty_cache()
+    return rec
+
+
 def c5_record(args, dist_ctx=None):
     """The north-star config on the same N GPUs: C5 = powerlu(A 262144 x 32768
     (68.7 GB, built in HBM by configs.gen_device), k=512, q_os=32, v=4).  One
@@ -672,6 +717,7 @@ def our_arm(args):
     if gpar is not None:
         parity = dict(parity or {}, **gpar)
 
+    others = None
     c5 = None
     if not args.no_c5 and w.name != "C5":
         del dm, f, fd, run
@@ -683,6 +729,15 @@ def our_arm(args):
 
         gc.collect()  # C5 needs every free byte: its residue cache is sized from the free HBM
         torch.cuda.empty_cache()
+        if w.name == "C2":  # the other single-GPU configs of BASELINE.json, same process, same GPU
+            others = {}
+            for nm in ("C3", "C4"):
+                try:
+                    others[nm] = config_record(nm)
+                except Exception as exc:
+                    others[nm] = {"error": f"{type(exc).__name__}: {exc}"}
+                gc.collect()
+                torch.cuda.empty_cache()
         try:
             c5 = c5_record(args)
         except Exception as exc:  # the sub-record must never cost the headline line
@@ -702,7 +757,7 @@ def our_arm(args):
         "gpu_launches": int(launches), "gpu_launches_per_step": launches / args.steps,
         "clocks": clk, "roofline": roofline, "e2e": e2e, "cpu_baseline": cpu, "parity": parity,
         "host_prep": {"generate_A_s": gen_s, "upload_A_s": upload_s},
-        "comm": None, "pass_sweep": sweep, "C5": c5,
+        "comm": None, "pass_sweep": sweep, "other_configs": others, "C5": c5,
     }
     print(json.dumps(line), flush=True)
     return 0
