@@ -82,10 +82,13 @@ def lu_from_projection_(g, vk, checks=None):
     lu(G) -> (L1, U1, p); lu((U1 V^T)^T) -> (L2, U2, q); L = L1 U2^T, U = L2^T.
     """
     k = g.shape[1]
+    prep_v = ops.tall_prep(vk, k)  # int8 residues of Vk, issued before the GEPP that hides their guard read
     f1 = plu_(g)  # L1 m x k, U1 k x k
-    bt = ops.matmul(vk, f1.U, tb=True)  # (U1 Vk^T)^T = Vk U1^T, n x k
+    prep_l = ops.tall_prep(f1.L, k)
+    bt = ops.tall_times(vk, f1.U, prep_v, ts=True)  # (U1 Vk^T)^T = Vk U1^T, n x k
+    del prep_v
     f2 = plu_(bt)  # L2 n x k, U2 k x k
-    big_l = ops.matmul(f1.L, f2.U, tb=True)  # L1 U2^T
+    big_l = ops.tall_times(f1.L, f2.U, prep_l, ts=True)  # L1 U2^T
     big_u = ops.transpose(f2.L)  # L2^T
     return LowRankLU(p=f1.p, q=f2.p, L=big_l, U=big_u, rank=k)
 

@@ -103,6 +103,8 @@ def pinv_factor_(l):
 def pinv_transpose_apply(l, m_):
     """(L^T)^+ M = Q R^{-T} M (rlra/kernels.py:92-96)."""
     qr = pinv_factor_(l)
+    q = qr.q()
+    prep = ops.tall_prep(q, m_.shape[1])  # Q's residues while the triangular solve runs
     x = _copy(m_)
     ops.trsm_rt_(qr.r_view(), x)
-    return ops.matmul(qr.q(), x)
+    return ops.tall_times(q, x, prep)

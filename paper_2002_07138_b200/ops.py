@@ -276,8 +276,17 @@ class OzPrep:
             host = _header_copy_async(self.ws, a.device)
             _call("rlra_b200_oz_prep_ex", a.device, ptr(a), ld_of(a), self.m, self.n, self.nmod, ptr(self.ws),
                   ptr(self.ws), wsb, st)
-            self.header = host.wait()
-            self.ok = oz_guard(self.header, self.m, self.n)
+            if guard == "lazy":  # read at the first product (tall_prep: issued well before it is needed)
+                self.header, self.ok = None, None
+
+                def resolve():
+                    self.header = host.wait()
+                    self.ok = oz_guard(self.header, self.m, self.n)
+
+                self._resolve_fn = resolve
+            else:
+                self.header = host.wait()
+                self.ok = oz_guard(self.header, self.m, self.n)
         else:
             self.header = None
             self.ok = (True, True)
@@ -694,6 +703,38 @@ def chol_inv_blocked(g, out, flag, cond_limit):
 
 SCHOL_C = 11.0 * 2.0 ** -53  # shift constant of shifted CholeskyQR (Fukaya et al. 2020)
 CHOLQR_OZ_MIN_ELEMS = int(os.environ.get("RLRA_B200_CHOLQR_OZ_MIN", str(1 << 24)))
+
+
+# Tall x small factor products (rlra/fixedrank.py:144-146 L = L1 U2^T and
+# (U1 V^T)^T = V U1^T; rlra/kernels.py:95-96 Q (R^-T M)): 2 rows k^2 flops with a
+# tall operand whose rows are evenly scaled (unit-lower L1, orthonormal V / Q) --
+# on the int8 engine 2-3x the DMMA rate once the product is large enough.  The
+# residues are issued EARLY (before the GEPP that precedes the product), so the
+# guard header has long arrived when the product reads it: no host wait.
+FACTOR_OZ_MIN_WORK = float(os.environ.get("RLRA_B200_FACTOR_OZ_MIN_WORK", "5e9"))   # rows * k * ncols
+FACTOR_OZ_MAX_ELEMS = float(os.environ.get("RLRA_B200_FACTOR_OZ_MAX_ELEMS", "6e7"))  # rows * k (workspace 28 B each)
+
+
+def tall_prep(a, ncols):
+    """Residues of the tall operand `a` (rows x k) for a later a @ s with s
+    k x ncols (tall_times), or None when the FP64 DMMA GEMM is the better engine
+    (small products; C5's 262144 x 512 factor, whose 4 GB of residue workspace
+    would come out of the memory the block-wise pass engine budgets)."""
+    rows, k = a.shape
+    if (os.environ.get("RLRA_B200_PASS_GEMM", "oz") != "oz" or rows * k * ncols < FACTOR_OZ_MIN_WORK
+            or rows * k > FACTOR_OZ_MAX_ELEMS or k > OZ_BLOCK_K or ncols > 4096 or ncols < 1):
+        return None
+    with label("factor_prep"):
+        return OzPrep(as_fmat(a), guard="lazy")
+
+
+def tall_times(a, s, prep=None, ts=False):
+    """a @ s (ts=False) or a @ s^T (ts=True), a tall and s small; `prep` =
+    tall_prep(a, .) issued earlier, else the DMMA GEMM."""
+    if prep is not None:
+        with label("factor_oz"):
+            return prep.gemm(transpose(s) if ts else s, trans=False)
+    return matmul(a, s, tb=ts)
 
 
 def _tall_products(z):

@@ -104,9 +104,10 @@ def single_pass_lu(stream, k, seed, q_os=0, panel=DEFAULT_PANEL):
     l = k + q_os
     g, h = stream_sketch(stream, l, seed, panel=panel)
     f1 = plu_(h)  # L1 m x l, U1 l x l, p
+    prep_l = ops.tall_prep(f1.L, l)  # for L1 U2^T below; the pinv and the second GEPP hide its guard read
     t = pinv_transpose_apply(g, ops.transpose(f1.U))  # (G^T)^+ U1^T
     f2 = plu_(t)  # L2 n x l, U2, q
-    big_l = ops.matmul(f1.L, f2.U, tb=True)
+    big_l = ops.tall_times(f1.L, f2.U, prep_l, ts=True)
     big_u = ops.transpose(f2.L)
     if q_os:
         big_l = big_l[:, :k]
