@@ -235,3 +235,35 @@ def test_oz_gemm_reuses_the_skinny_operands_residues(cuda_dev):
     c3, ws3 = p3.gemm(b, trans=True, keep_ws=True, b_ws=ws)
     assert ws3 is not ws
     assert torch.equal(c3.view(torch.int64), p3.gemm(b, trans=True).view(torch.int64))
+
+
+def test_tall_times_small_factor_products(cuda_dev, monkeypatch):
+    """ops.tall_prep / tall_times (L = L1 U2^T, V U1^T, Q X): the int8 path,
+    forced at a small size, agrees with the float64 product to DGEMM accuracy
+    for s and s^T; small products and guard-rejected operands (integer-valued
+    tall factor) take the DMMA GEMM and equal ops.matmul bit for bit."""
+    import torch
+
+    from paper_2002_07138_b200 import ops
+
+    dev = ops.check_device()
+    rng = np.random.default_rng(17)
+    q, _ = np.linalg.qr(rng.standard_normal((3000, 90)))
+    u = np.triu(rng.standard_normal((90, 90))) * np.exp(-np.arange(90) / 9.0)[:, None]  # graded rows, like U of a sketch
+    qd, ud = ops.from_numpy(q, dev), ops.from_numpy(u, dev)
+    assert ops.tall_prep(qd, 90) is None  # far below the work threshold: DMMA
+    monkeypatch.setattr(ops, "FACTOR_OZ_MIN_WORK", 0.0)
+    prep = ops.tall_prep(qd, 90)
+    assert prep is not None and prep.ok is None  # lazy guard: not read yet
+    got_t = ops.to_numpy(ops.tall_times(qd, ud, prep, ts=True))
+    assert prep.ok == (True, True)
+    got = ops.to_numpy(ops.tall_times(qd, ud, prep))
+    for g, ref in ((got_t, q @ u.T), (got, q @ u)):
+        bound = 1e-15 * np.sqrt(90) * np.linalg.norm(q, axis=1)[:, None] * np.linalg.norm(ref, axis=0)[None, :] + 1e-300
+        assert np.all(np.abs(g - ref) <= 8 * bound + 1e-18)
+    # integer-valued tall operand: the guard sends it to the FP64 GEMM
+    li = ops.from_numpy(rng.integers(-3, 4, size=(3000, 90)).astype(np.float64), dev)
+    pi = ops.tall_prep(li, 90)
+    c = ops.tall_times(li, ud, pi, ts=True)
+    assert pi.ok[0] is False
+    assert torch.equal(c.view(torch.int64), ops.matmul(li, ud, tb=True).view(torch.int64))
