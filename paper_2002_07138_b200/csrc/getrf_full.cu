@@ -924,7 +924,12 @@ bool getrf_full_eligible(int64_t m, int64_t n, int cluster_max) {
   // widths above 512 only while the far-column work stays small: beyond, the
   // blocked path's all-SM trailing update wins (profiles/r02_getrf_width.txt:
   // 4096 x 544 coop 2.12 vs blocked 2.30 ms; 16384 x 1024 coop 8.14 vs 6.25 ms)
-  const bool width_ok = n <= 512 || (n <= lufull::MAXN && m * n <= (int64_t)4500000);
+  static int64_t wide_mn = -1;  // RLRA_B200_LU_FULL_WIDE_MN overrides the measured crossover (experiments)
+  if (wide_mn < 0) {
+    const char* e = getenv("RLRA_B200_LU_FULL_WIDE_MN");
+    wide_mn = (e && atoll(e) > 0) ? atoll(e) : (int64_t)4500000;
+  }
+  const bool width_ok = n <= 512 || (n <= lufull::MAXN && m * n <= wide_mn);
   return enabled && cluster_max >= lufull::CS && n >= 1 && m >= n && width_ok &&
          m >= (int64_t)lufull::CS * 32 && m <= (int64_t)lufull::CS * lufull::T * lufull::MAXRPT;
 }
