@@ -61,6 +61,7 @@ struct PanelArgs {
 // correctly rounded reciprocal rcp = RN(1/d): Markstein's theorem -- q0 = RN(x*rcp),
 // rem = x - d*q0 exactly (FMA), RN(q0 + rem*rcp) == RN(x/d) -- valid away from
 // overflow / underflow; other operands take the hardware division path.
+__device__ __noinline__ double ieee_div_slow_path(double x, double d) { return x / d; }  // rare: keep it out of the column step
 __device__ __forceinline__ double ieee_div_by(double x, double d, double rcp) {
   const double ax = fabs(x), ad = fabs(d);
   if (ax > 0x1p-960 && ax < 0x1p+960 && ad > 0x1p-960 && ad < 0x1p+960) {
@@ -68,7 +69,7 @@ __device__ __forceinline__ double ieee_div_by(double x, double d, double rcp) {
     const double rem = fma(-d, q0, x);
     return fma(rem, rcp, q0);
   }
-  return x / d;
+  return ieee_div_slow_path(x, d);
 }
 
 // strict-greater first-max merge: (v,i) replaces best when v > best or (v == best && i < besti)
